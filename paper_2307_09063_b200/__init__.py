@@ -1,0 +1,21 @@
+"""B200-native Radar-STDA inference engine (drop-in for the reference `stda` model API).
+
+Reference: arXiv 2307.09063, `/root/reference/pkg/stda/src/stda/__init__.py:10-27`.
+The model surface (`StdaConfig`, `StdaNet`, blocks, `concat_frames`,
+`parameter_count`, `load_checkpoint`) mirrors the reference; eval-mode forwards run
+hand-written sm_100a kernels through the C ABI in `include/stda_b200.h`.
+"""
+
+__version__ = "0.1.0"
+
+from .model import (  # noqa: F401
+    EcaBlock,
+    MobileDecoderBlock,
+    MobileEncoderBlock,
+    StdaConfig,
+    StdaNet,
+    concat_frames,
+    load_checkpoint,
+    parameter_count,
+)
+from .fold import fold_state_dict  # noqa: F401

@@ -1,0 +1,607 @@
+// C ABI of the engine (include/stda_b200.h): plans, workspace planning, the forward
+// sequencer, the pipelined host-buffer path, block-level entries and the synthesiser.
+//
+// Forward dataflow (reference model.py:185-199), one launch per row:
+//   stem          conv3x3 s1 + relu                          x        -> s
+//   enc i  s1     reparameterised conv3x3 s1 + relu          cur      -> m
+//          s2     relu(conv3x3s2(m)+b) + conv3x3s2(cur)+b    m, cur   -> e_i, GAP tiles
+//          gate   sigmoid(conv1d(mean))                      GAP      -> g_i      cur = e_i*g_i
+//   dec j  s1     reparameterised conv3x3 s1 + relu          cur      -> m
+//          s2     relu(convT(m)+b) + convT(cur)+b (4 phases) m, cur   -> d_j, GAP tiles
+//          gate                                              GAP      -> g'_j     cur = d_j*g'_j + skip
+//   head   conv3x3 s1                                        cur      -> y
+// Gates and skip adds are applied while the NEXT kernel stages its input tile.
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/stda_b200.h"
+#include "common.cuh"
+#include "simt_conv.cuh"
+
+namespace stda {
+
+void launch_synth(uint64_t seed, int scene, int64_t seq0, int64_t seq_step, int64_t frame0,
+                  int frames_per_seq, int frame_order, int64_t n_out, int H, int W, float* out,
+                  cudaStream_t st);
+
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    STDA_CUDA(cudaGetDevice(&prev));
+    if (prev != dev) STDA_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != prev && prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+constexpr size_t kAlign = 256;
+inline size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
+
+}  // namespace
+}  // namespace stda
+
+using namespace stda;
+
+struct EncLayers {
+  ConvLayer s1, dn, rs;
+  float* eca = nullptr;
+};
+struct DecLayers {
+  ConvLayer s1, up, rs;
+  float* eca = nullptr;
+};
+
+struct stda_plan {
+  int kind = 0;  // 0 = network, 1 = encoder block, 2 = decoder block
+  stda_config cfg{};
+  int device = 0;
+  bool bf16 = false;
+  int block_channels = 0;
+  ConvLayer stem, head;
+  std::vector<EncLayers> enc;
+  std::vector<DecLayers> dec;
+  std::vector<void*> allocations;
+  // host-buffer pipeline resources (created on first use)
+  cudaStream_t copy_in = nullptr, copy_out = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_in[2] = {}, ev_comp[2] = {}, ev_out[2] = {};
+
+  ~stda_plan() {
+    for (void* p : allocations) cudaFree(p);
+    if (copy_in) cudaStreamDestroy(copy_in);
+    if (copy_out) cudaStreamDestroy(copy_out);
+    for (cudaEvent_t e : {ev_start, ev_in[0], ev_in[1], ev_comp[0], ev_comp[1], ev_out[0], ev_out[1]})
+      if (e) cudaEventDestroy(e);
+  }
+
+  float* upload(const std::vector<float>& v) {
+    void* p = nullptr;
+    STDA_CUDA(cudaMalloc(&p, std::max<size_t>(v.size(), 1) * sizeof(float)));
+    allocations.push_back(p);
+    STDA_CUDA(cudaMemcpy(p, v.data(), v.size() * sizeof(float), cudaMemcpyHostToDevice));
+    return static_cast<float*>(p);
+  }
+
+  // canonical weights at `src` -> SIMT layout on device; advances src
+  ConvLayer make_layer(int mode, int cin, int cout, const float*& src) {
+    ConvLayer L;
+    L.mode = mode;
+    L.cin = cin;
+    L.cout = cout;
+    L.cob = simt_cob_for(cout);
+    L.tapsz = simt_tapsz(mode, L.cob);
+    const int nblk = cdiv(cout, L.cob);
+    const size_t wn = (size_t)cout * cin * (mode == CONVT4_S2 ? 16 : 9);
+    std::vector<float> w((size_t)nblk * cin * L.tapsz), b((size_t)nblk * L.cob);
+    simt_pack(mode, cin, cout, src, src + wn, bf16, w.data(), b.data());
+    src += wn + cout;
+    L.w = upload(w);
+    L.b = upload(b);
+    return L;
+  }
+
+  float* make_vec(int n, const float*& src) {
+    std::vector<float> v(src, src + n);
+    src += n;
+    return upload(v);
+  }
+};
+
+namespace {
+
+size_t canonical_floats(const stda_config& c) {
+  const size_t c0 = c.stem_channels, f = c.input_frames, k = c.eca_kernel;
+  size_t n = c0 * f * 9 + c0;
+  for (int i = 0; i < c.stages; ++i) {
+    const size_t ch = c0 << i;
+    n += ch * ch * 9 + ch + 2 * (2 * ch * ch * 9 + 2 * ch) + k;
+  }
+  for (int j = 0; j < c.stages; ++j) {
+    const size_t c2 = c0 << (c.stages - j), ch = c2 / 2;
+    n += c2 * c2 * 9 + c2 + 2 * (ch * c2 * 16 + ch) + k;
+  }
+  return n + c0 * 9 + 1;
+}
+
+void validate(const stda_config& c) {
+  STDA_CHECK(c.input_frames >= 1 && c.stem_channels >= 1 && c.stages >= 1,
+             "config values must be positive");
+  STDA_CHECK(c.eca_kernel >= 1 && c.eca_kernel % 2 == 1, "ECA kernel size must be odd");
+  const int d = 1 << c.stages;
+  STDA_CHECK(c.map_height > 0 && c.map_width > 0 && c.map_height % d == 0 && c.map_width % d == 0,
+             "map size must be divisible by 2^stages");
+  STDA_CHECK(c.precision == STDA_PRECISION_FP32 || c.precision == STDA_PRECISION_BF16,
+             "unknown precision");
+  STDA_CHECK(((int64_t)c.stem_channels << c.stages) <= 4096, "channel count too large");
+}
+
+// Workspace for a batch of B triplets; base == nullptr only sizes it.
+struct NetWs {
+  float* s = nullptr;
+  float* m = nullptr;
+  std::vector<float*> e, ge, pe, d, gd, pd;
+  size_t bytes = 0;
+};
+
+NetWs plan_ws(const stda_plan& p, int64_t B, char* base) {
+  const stda_config& c = p.cfg;
+  const int S = c.stages;
+  NetWs w;
+  size_t off = 0;
+  auto take = [&](size_t nfloat) -> float* {
+    float* r = base ? reinterpret_cast<float*>(base + off) : nullptr;
+    off += align_up(nfloat * sizeof(float));
+    return r;
+  };
+  const size_t HW = (size_t)c.map_height * c.map_width;
+  w.s = take(B * c.stem_channels * HW);
+  // the "mixed" stage-1 buffer is reused by every block: size of the largest
+  size_t mmax = 0;
+  for (int i = 0; i < S; ++i) mmax = std::max(mmax, (size_t)(c.stem_channels << i) * (HW >> (2 * i)));
+  for (int j = 0; j < S; ++j) {
+    const int lvl = S - j;  // decoder input level
+    mmax = std::max(mmax, (size_t)(c.stem_channels << lvl) * (HW >> (2 * lvl)));
+  }
+  w.m = take(B * mmax);
+  for (int i = 0; i < S; ++i) {
+    const int ch = c.stem_channels << (i + 1);
+    const int h = c.map_height >> (i + 1), wd = c.map_width >> (i + 1);
+    w.e.push_back(take(B * ch * (size_t)h * wd));
+    w.pe.push_back(take(B * ch * (size_t)conv_tiles(CONV3_S2, h, wd)));
+    w.ge.push_back(take(B * ch));
+  }
+  for (int j = 0; j < S; ++j) {
+    const int lvl = S - j - 1;  // output level
+    const int ch = c.stem_channels << lvl;
+    const int h = c.map_height >> lvl, wd = c.map_width >> lvl;
+    w.d.push_back(take(B * ch * (size_t)h * wd));
+    w.pd.push_back(take(B * ch * (size_t)conv_tiles(CONVT4_S2, h, wd)));
+    w.gd.push_back(take(B * ch));
+  }
+  w.bytes = off;
+  return w;
+}
+
+// Optional per-launch event marks (stda_forward_profiled): ev[0] before the first
+// launch, ev[i+1] after launch i.
+struct Marks {
+  std::vector<cudaEvent_t>* ev = nullptr;
+  int i = 0;
+  void mark(cudaStream_t st) {
+    if (ev) STDA_CUDA(cudaEventRecord((*ev)[i++], st));
+  }
+};
+
+void run_net(const stda_plan& p, const Src& x, float* y, int64_t B, const NetWs& w, cudaStream_t st,
+             Marks mk = Marks{}) {
+  const stda_config& c = p.cfg;
+  const int S = c.stages, k = c.eca_kernel;
+  const bool bf = p.bf16;
+  int h = c.map_height, wd = c.map_width;
+  mk.mark(st);
+  launch_conv(p.stem, nullptr, x, nullptr, w.s, nullptr, B, h, wd, true, bf, st);
+  mk.mark(st);
+  Src cur = plain_src(w.s, c.stem_channels, h, wd);
+  std::vector<Src> skips{cur};
+  for (int i = 0; i < S; ++i) {
+    const int ch = c.stem_channels << i;
+    const EncLayers& E = p.enc[i];
+    launch_conv(E.s1, nullptr, cur, nullptr, w.m, nullptr, B, h, wd, true, bf, st);
+    mk.mark(st);
+    const Src mixed = plain_src(w.m, ch, h, wd);
+    launch_conv(E.dn, &E.rs, mixed, &cur, w.e[i], w.pe[i], B, h, wd, true, bf, st);
+    mk.mark(st);
+    h /= 2;
+    wd /= 2;
+    launch_gate(w.pe[i], conv_tiles(CONV3_S2, h, wd), E.eca, k, w.ge[i], B, 2 * ch, h * wd, st);
+    mk.mark(st);
+    cur = plain_src(w.e[i], 2 * ch, h, wd);
+    cur.gx = w.ge[i];
+    skips.push_back(cur);
+  }
+  for (int j = 0; j < S; ++j) {
+    const int c2 = c.stem_channels << (S - j), ch = c2 / 2;
+    const DecLayers& D = p.dec[j];
+    launch_conv(D.s1, nullptr, cur, nullptr, w.m, nullptr, B, h, wd, true, bf, st);
+    mk.mark(st);
+    const Src mixed = plain_src(w.m, c2, h, wd);
+    launch_conv(D.up, &D.rs, mixed, &cur, w.d[j], w.pd[j], B, h, wd, true, bf, st);
+    mk.mark(st);
+    h *= 2;
+    wd *= 2;
+    launch_gate(w.pd[j], conv_tiles(CONVT4_S2, h, wd), D.eca, k, w.gd[j], B, ch, h * wd, st);
+    mk.mark(st);
+    Src nxt = plain_src(w.d[j], ch, h, wd);
+    nxt.gx = w.gd[j];
+    const Src& sk = skips[S - 1 - j];
+    nxt.s = sk.x;
+    nxt.sb = sk.xb;
+    nxt.sc = sk.xc;
+    nxt.gs = sk.gx;
+    cur = nxt;
+  }
+  launch_conv(p.head, nullptr, cur, nullptr, y, nullptr, B, h, wd, false, bf, st);
+  mk.mark(st);
+}
+
+std::string launch_names(const stda_config& c) {
+  std::string s = "stem";
+  for (int i = 0; i < c.stages; ++i)
+    s += ";enc" + std::to_string(i) + ".s1;enc" + std::to_string(i) + ".s2;enc" + std::to_string(i) +
+         ".gate";
+  for (int j = 0; j < c.stages; ++j)
+    s += ";dec" + std::to_string(j) + ".s1;dec" + std::to_string(j) + ".s2;dec" + std::to_string(j) +
+         ".gate";
+  return s + ";head";
+}
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const Error& e) {
+    set_error(e.msg);
+  } catch (const std::exception& e) {
+    set_error(e.what());
+  } catch (...) {
+    set_error("unknown error");
+  }
+  return 1;
+}
+
+void check_ws(const stda_plan* p, const void* ws, size_t have, size_t need) {
+  STDA_CHECK(p != nullptr, "null plan");
+  STDA_CHECK(have >= need, "workspace too small: need " + std::to_string(need) + " bytes, got " +
+                               std::to_string(have));
+  STDA_CHECK(need == 0 || ws != nullptr, "null workspace");
+}
+
+}  // namespace
+
+extern "C" {
+
+int stda_abi_version(void) { return STDA_ABI_VERSION; }
+
+const char* stda_last_error(void) { return g_last_error.c_str(); }
+
+size_t stda_blob_floats(const stda_config* cfg) { return cfg ? canonical_floats(*cfg) : 0; }
+
+int stda_plan_create(const stda_config* cfg, const float* blob, size_t n_floats, int device,
+                     stda_plan** out) {
+  return guarded([&] {
+    STDA_CHECK(cfg && blob && out, "null argument");
+    validate(*cfg);
+    STDA_CHECK(n_floats == canonical_floats(*cfg),
+               "blob has " + std::to_string(n_floats) + " floats, config needs " +
+                   std::to_string(canonical_floats(*cfg)));
+    DeviceGuard g(device);
+    auto p = std::make_unique<stda_plan>();
+    p->kind = 0;
+    p->cfg = *cfg;
+    p->device = device;
+    p->bf16 = cfg->precision == STDA_PRECISION_BF16;
+    const float* src = blob;
+    const int c0 = cfg->stem_channels, S = cfg->stages, k = cfg->eca_kernel;
+    p->stem = p->make_layer(CONV3_S1, cfg->input_frames, c0, src);
+    for (int i = 0; i < S; ++i) {
+      const int ch = c0 << i;
+      EncLayers E;
+      E.s1 = p->make_layer(CONV3_S1, ch, ch, src);
+      E.dn = p->make_layer(CONV3_S2, ch, 2 * ch, src);
+      E.rs = p->make_layer(CONV3_S2, ch, 2 * ch, src);
+      E.eca = p->make_vec(k, src);
+      p->enc.push_back(E);
+    }
+    for (int j = 0; j < S; ++j) {
+      const int c2 = c0 << (S - j), ch = c2 / 2;
+      DecLayers D;
+      D.s1 = p->make_layer(CONV3_S1, c2, c2, src);
+      D.up = p->make_layer(CONVT4_S2, c2, ch, src);
+      D.rs = p->make_layer(CONVT4_S2, c2, ch, src);
+      D.eca = p->make_vec(k, src);
+      p->dec.push_back(D);
+    }
+    p->head = p->make_layer(CONV3_S1, c0, 1, src);
+    STDA_CHECK((size_t)(src - blob) == n_floats, "internal: blob parse mismatch");
+    *out = p.release();
+  });
+}
+
+void stda_plan_destroy(stda_plan* plan) {
+  if (!plan) return;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(plan->device);
+  delete plan;
+  if (prev >= 0) cudaSetDevice(prev);
+}
+
+int stda_launches_per_forward(const stda_plan* plan) {
+  if (!plan) return -1;
+  if (plan->kind != 0) return 2;
+  return 2 + 6 * plan->cfg.stages;
+}
+
+size_t stda_workspace_bytes(const stda_plan* plan, int64_t batch) {
+  if (!plan || plan->kind != 0 || batch < 0) return 0;
+  return plan_ws(*plan, batch, nullptr).bytes;
+}
+
+int stda_forward(const stda_plan* plan, const float* x, float* y, int64_t batch, void* ws,
+                 size_t ws_bytes, void* stream) {
+  return guarded([&] {
+    STDA_CHECK(plan && plan->kind == 0, "not a network plan");
+    STDA_CHECK(batch >= 0, "negative batch");
+    if (batch == 0) return;
+    STDA_CHECK(x && y, "null tensor");
+    const NetWs need = plan_ws(*plan, batch, nullptr);
+    check_ws(plan, ws, ws_bytes, need.bytes);
+    DeviceGuard g(plan->device);
+    const stda_config& c = plan->cfg;
+    const Src xs = plain_src(x, c.input_frames, c.map_height, c.map_width);
+    run_net(*plan, xs, y, batch, plan_ws(*plan, batch, static_cast<char*>(ws)),
+            static_cast<cudaStream_t>(stream));
+  });
+}
+
+int stda_forward_profiled(const stda_plan* plan, const float* x, float* y, int64_t batch, void* ws,
+                          size_t ws_bytes, void* stream, float* ms_per_launch, int32_t n) {
+  return guarded([&] {
+    STDA_CHECK(plan && plan->kind == 0, "not a network plan");
+    STDA_CHECK(batch > 0 && x && y, "bad arguments");
+    const int L = stda_launches_per_forward(plan);
+    STDA_CHECK(ms_per_launch && n >= L, "ms_per_launch must hold launches_per_forward floats");
+    const NetWs need = plan_ws(*plan, batch, nullptr);
+    check_ws(plan, ws, ws_bytes, need.bytes);
+    DeviceGuard g(plan->device);
+    const stda_config& c = plan->cfg;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    std::vector<cudaEvent_t> ev(L + 1);
+    for (auto& e : ev) STDA_CUDA(cudaEventCreate(&e));
+    Marks mk;
+    mk.ev = &ev;
+    run_net(*plan, plain_src(x, c.input_frames, c.map_height, c.map_width), y, batch,
+            plan_ws(*plan, batch, static_cast<char*>(ws)), st, mk);
+    STDA_CUDA(cudaEventSynchronize(ev[L]));
+    for (int i = 0; i < L; ++i) STDA_CUDA(cudaEventElapsedTime(&ms_per_launch[i], ev[i], ev[i + 1]));
+    for (auto& e : ev) cudaEventDestroy(e);
+  });
+}
+
+const char* stda_launch_names(const stda_plan* plan) {
+  static thread_local std::string names;
+  names = (plan && plan->kind == 0) ? launch_names(plan->cfg) : std::string();
+  return names.c_str();
+}
+
+int stda_forward_window(const stda_plan* plan, const float* frames, int64_t n_frames, float* y,
+                        void* ws, size_t ws_bytes, void* stream) {
+  return guarded([&] {
+    STDA_CHECK(plan && plan->kind == 0, "not a network plan");
+    const stda_config& c = plan->cfg;
+    const int64_t B = n_frames - (c.input_frames - 1);
+    if (B <= 0) return;
+    STDA_CHECK(frames && y, "null tensor");
+    const NetWs need = plan_ws(*plan, B, nullptr);
+    check_ws(plan, ws, ws_bytes, need.bytes);
+    DeviceGuard g(plan->device);
+    const int64_t HW = (int64_t)c.map_height * c.map_width;
+    // output b <-> t = b + F-1; channel ch reads frame t - ch
+    Src xs;
+    xs.x = frames + (int64_t)(c.input_frames - 1) * HW;
+    xs.xb = HW;
+    xs.xc = -HW;
+    xs.C = c.input_frames;
+    run_net(*plan, xs, y, B, plan_ws(*plan, B, static_cast<char*>(ws)),
+            static_cast<cudaStream_t>(stream));
+  });
+}
+
+int64_t stda_host_chunk(const stda_plan* plan, int64_t batch) {
+  if (!plan || plan->kind != 0 || batch <= 0) return 0;
+  const stda_config& c = plan->cfg;
+  const int64_t per = (int64_t)c.input_frames * c.map_height * c.map_width * 4;
+  const int64_t chunk = std::max<int64_t>(1, (4ll << 20) / per);
+  return std::min(batch, chunk);
+}
+
+size_t stda_host_workspace_bytes(const stda_plan* plan, int64_t chunk) {
+  if (!plan || plan->kind != 0 || chunk <= 0) return 0;
+  const stda_config& c = plan->cfg;
+  const size_t HW = (size_t)c.map_height * c.map_width;
+  return 2 * align_up(chunk * c.input_frames * HW * 4) + 2 * align_up(chunk * HW * 4) +
+         plan_ws(*plan, chunk, nullptr).bytes;
+}
+
+int stda_forward_host(const stda_plan* plan, const float* x_host, float* y_host, int64_t batch,
+                      int64_t chunk, void* ws, size_t ws_bytes, void* stream) {
+  return guarded([&] {
+    STDA_CHECK(plan && plan->kind == 0, "not a network plan");
+    if (batch <= 0) return;
+    STDA_CHECK(x_host && y_host, "null host buffer");
+    STDA_CHECK(chunk >= 1, "chunk must be >= 1");
+    chunk = std::min(chunk, batch);
+    check_ws(plan, ws, ws_bytes, stda_host_workspace_bytes(plan, chunk));
+    DeviceGuard g(plan->device);
+    stda_plan* p = const_cast<stda_plan*>(plan);
+    if (!p->copy_in) {
+      STDA_CUDA(cudaStreamCreateWithFlags(&p->copy_in, cudaStreamNonBlocking));
+      STDA_CUDA(cudaStreamCreateWithFlags(&p->copy_out, cudaStreamNonBlocking));
+      STDA_CUDA(cudaEventCreateWithFlags(&p->ev_start, cudaEventDisableTiming));
+      for (int s = 0; s < 2; ++s) {
+        STDA_CUDA(cudaEventCreateWithFlags(&p->ev_in[s], cudaEventDisableTiming));
+        STDA_CUDA(cudaEventCreateWithFlags(&p->ev_comp[s], cudaEventDisableTiming));
+        STDA_CUDA(cudaEventCreateWithFlags(&p->ev_out[s], cudaEventDisableTiming));
+      }
+    }
+    const stda_config& c = plan->cfg;
+    const size_t HW = (size_t)c.map_height * c.map_width;
+    const size_t in_tri = c.input_frames * HW, in_bytes = align_up(chunk * in_tri * 4),
+                 out_bytes = align_up(chunk * HW * 4);
+    char* base = static_cast<char*>(ws);
+    float* d_in[2] = {reinterpret_cast<float*>(base), reinterpret_cast<float*>(base + in_bytes)};
+    float* d_out[2] = {reinterpret_cast<float*>(base + 2 * in_bytes),
+                       reinterpret_cast<float*>(base + 2 * in_bytes + out_bytes)};
+    const NetWs nw = plan_ws(*plan, chunk, base + 2 * in_bytes + 2 * out_bytes);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    STDA_CUDA(cudaEventRecord(p->ev_start, st));
+    STDA_CUDA(cudaStreamWaitEvent(p->copy_in, p->ev_start, 0));
+    STDA_CUDA(cudaStreamWaitEvent(p->copy_out, p->ev_start, 0));
+    const int64_t n_chunks = (batch + chunk - 1) / chunk;
+    for (int64_t k = 0; k < n_chunks; ++k) {
+      const int s = (int)(k & 1);
+      const int64_t b0 = k * chunk, nb = std::min(chunk, batch - b0);
+      if (k >= 2) STDA_CUDA(cudaStreamWaitEvent(p->copy_in, p->ev_comp[s], 0));
+      STDA_CUDA(cudaMemcpyAsync(d_in[s], x_host + b0 * in_tri, nb * in_tri * 4,
+                                cudaMemcpyHostToDevice, p->copy_in));
+      STDA_CUDA(cudaEventRecord(p->ev_in[s], p->copy_in));
+      STDA_CUDA(cudaStreamWaitEvent(st, p->ev_in[s], 0));
+      if (k >= 2) STDA_CUDA(cudaStreamWaitEvent(st, p->ev_out[s], 0));
+      run_net(*plan, plain_src(d_in[s], c.input_frames, c.map_height, c.map_width), d_out[s], nb, nw,
+              st);
+      STDA_CUDA(cudaEventRecord(p->ev_comp[s], st));
+      STDA_CUDA(cudaStreamWaitEvent(p->copy_out, p->ev_comp[s], 0));
+      STDA_CUDA(cudaMemcpyAsync(y_host + b0 * HW, d_out[s], nb * HW * 4, cudaMemcpyDeviceToHost,
+                                p->copy_out));
+      STDA_CUDA(cudaEventRecord(p->ev_out[s], p->copy_out));
+    }
+    for (int s = 0; s < 2 && s < n_chunks; ++s) STDA_CUDA(cudaStreamWaitEvent(st, p->ev_out[s], 0));
+    STDA_CUDA(cudaStreamSynchronize(p->copy_out));
+  });
+}
+
+// ---- block level ------------------------------------------------------------------
+int stda_block_plan_create(int32_t kind, int32_t channels, const float* blob, size_t n_floats,
+                           int device, stda_plan** out) {
+  return guarded([&] {
+    STDA_CHECK(blob && out, "null argument");
+    STDA_CHECK(kind == 0 || kind == 1, "kind must be 0 (encoder) or 1 (decoder)");
+    STDA_CHECK(channels >= 1 && (kind == 0 || channels % 2 == 0), "bad channel count");
+    const size_t c = channels;
+    const size_t need = kind == 0 ? c * c * 9 + c + 2 * (2 * c * c * 9 + 2 * c)
+                                  : c * c * 9 + c + 2 * ((c / 2) * c * 16 + c / 2);
+    STDA_CHECK(n_floats == need, "block blob size mismatch");
+    DeviceGuard g(device);
+    auto p = std::make_unique<stda_plan>();
+    p->kind = kind + 1;
+    p->device = device;
+    p->block_channels = channels;
+    const float* src = blob;
+    if (kind == 0) {
+      EncLayers E;
+      E.s1 = p->make_layer(CONV3_S1, channels, channels, src);
+      E.dn = p->make_layer(CONV3_S2, channels, 2 * channels, src);
+      E.rs = p->make_layer(CONV3_S2, channels, 2 * channels, src);
+      p->enc.push_back(E);
+    } else {
+      DecLayers D;
+      D.s1 = p->make_layer(CONV3_S1, channels, channels, src);
+      D.up = p->make_layer(CONVT4_S2, channels, channels / 2, src);
+      D.rs = p->make_layer(CONVT4_S2, channels, channels / 2, src);
+      p->dec.push_back(D);
+    }
+    *out = p.release();
+  });
+}
+
+size_t stda_block_workspace_bytes(const stda_plan* b, int64_t batch, int32_t h, int32_t w) {
+  if (!b || b->kind == 0 || batch < 0) return 0;
+  return align_up((size_t)batch * b->block_channels * h * w * sizeof(float));
+}
+
+int stda_block_forward(const stda_plan* b, const float* x, float* y, int64_t batch, int32_t h,
+                       int32_t w, void* ws, size_t ws_bytes, void* stream) {
+  return guarded([&] {
+    STDA_CHECK(b && b->kind != 0, "not a block plan");
+    if (batch == 0) return;
+    STDA_CHECK(x && y, "null tensor");
+    STDA_CHECK(h > 0 && w > 0, "bad spatial size");
+    if (b->kind == 1) STDA_CHECK(h % 2 == 0 && w % 2 == 0, "spatial dims must be even");
+    check_ws(b, ws, ws_bytes, stda_block_workspace_bytes(b, batch, h, w));
+    DeviceGuard g(b->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int C = b->block_channels;
+    float* m = static_cast<float*>(ws);
+    const Src xin = plain_src(x, C, h, w);
+    const Src mixed = plain_src(m, C, h, w);
+    if (b->kind == 1) {
+      const EncLayers& E = b->enc[0];
+      launch_conv(E.s1, nullptr, xin, nullptr, m, nullptr, batch, h, w, true, false, st);
+      launch_conv(E.dn, &E.rs, mixed, &xin, y, nullptr, batch, h, w, true, false, st);
+    } else {
+      const DecLayers& D = b->dec[0];
+      launch_conv(D.s1, nullptr, xin, nullptr, m, nullptr, batch, h, w, true, false, st);
+      launch_conv(D.up, &D.rs, mixed, &xin, y, nullptr, batch, h, w, true, false, st);
+    }
+  });
+}
+
+int stda_eca(const float* w_dev, int32_t k, const float* x, float* gates, float* y, int64_t batch,
+             int32_t channels, int32_t h, int32_t w, void* stream) {
+  return guarded([&] {
+    STDA_CHECK(k >= 1 && k % 2 == 1, "ECA kernel size must be odd");
+    if (batch == 0) return;
+    STDA_CHECK(w_dev && x && gates, "null tensor");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int hw = h * w;
+    launch_channel_sum(x, gates, batch, channels, hw, st);                  // gates <- sums
+    launch_gate(gates, 1, w_dev, k, gates, batch, channels, hw, st);        // in place
+    if (y) launch_scale(x, gates, y, batch, channels, hw, st);
+  });
+}
+
+// ---- synthesiser --------------------------------------------------------------------
+int stda_synth_frames(uint64_t seed, int32_t scene, int64_t seq, int64_t first_frame,
+                      int64_t n_frames, int32_t h, int32_t w, float* out, void* stream) {
+  return guarded([&] {
+    STDA_CHECK(n_frames >= 0 && first_frame >= 0, "bad frame range");
+    if (n_frames == 0) return;
+    STDA_CHECK(out, "null output");
+    STDA_CHECK(n_frames < (1ll << 31), "too many frames");
+    launch_synth(seed, scene, seq, 0, first_frame, (int)n_frames, 0, n_frames, h, w, out,
+                 static_cast<cudaStream_t>(stream));
+  });
+}
+
+int stda_synth_triplets(uint64_t seed, int32_t scene, int64_t first_seq, int64_t batch,
+                        int32_t frames, int32_t h, int32_t w, float* x, void* stream) {
+  return guarded([&] {
+    STDA_CHECK(batch >= 0 && frames >= 1, "bad batch/frames");
+    if (batch == 0) return;
+    STDA_CHECK(x, "null output");
+    launch_synth(seed, scene, first_seq, 1, 0, frames, 1, batch * frames, h, w, x,
+                 static_cast<cudaStream_t>(stream));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,277 @@
+"""Host side of the engine: plan cache on the module, workspace, C-ABI calls.
+
+All device work goes through `libstda_b200.so` (see `_lib.py`); this file only
+folds weights, allocates torch device memory and passes raw pointers plus the
+current CUDA stream.  There is no CPU fallback: every entry point raises if the
+library is missing or the tensor is not on a CUDA device.
+"""
+
+from __future__ import annotations
+
+from typing import Optional
+
+import numpy as np
+import torch
+
+PRECISIONS = ("fp32", "bf16")
+_PREC_ID = {"fp32": 0, "bf16": 1}
+
+
+def _lib():
+    from . import _lib as L
+    return L.lib()
+
+
+def _stream_ptr(device: torch.device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _state_key(module: torch.nn.Module, precision: str, device: torch.device):
+    key = [precision, str(device)]
+    for t in list(module.parameters()) + list(module.buffers()):
+        key.append((t.data_ptr(), t._version))
+    return tuple(key)
+
+
+class _Plan:
+    """Owns one `stda_plan*` (device weights) for a module on one device."""
+
+    def __init__(self, cfg, blob: np.ndarray, precision: str, device: torch.device):
+        from . import _lib as L
+        self.L = L
+        self.cfg = cfg
+        self.device = device
+        self.precision = precision
+        self.handle = L.plan_create(cfg, blob, _PREC_ID[precision], device.index or 0)
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None:
+            try:
+                self.L.plan_destroy(h)
+            except Exception:
+                pass
+            self.handle = None
+
+
+def _device_of(x: torch.Tensor) -> torch.device:
+    if not x.is_cuda:
+        raise RuntimeError("the B200 engine needs CUDA tensors (no CPU inference path)")
+    return x.device
+
+
+def _net_plan(net, device: torch.device) -> _Plan:
+    from .fold import fold_state_dict
+    key = _state_key(net, net.precision, device)
+    cache = getattr(net, "_engine_cache", None)
+    if cache is not None and cache[0] == key:
+        return cache[1]
+    sd = {k: v.detach() for k, v in net.state_dict().items()}
+    blob = fold_state_dict(net.config, sd)
+    plan = _Plan(net.config, blob, net.precision, device)
+    net._engine_cache = (key, plan)
+    return plan
+
+
+def _as_input(x: torch.Tensor) -> torch.Tensor:
+    if x.dtype != torch.float32:
+        raise TypeError(f"the engine computes on float32 inputs, got {x.dtype}")
+    return x.contiguous()
+
+
+def forward(net, x: torch.Tensor) -> torch.Tensor:
+    device = _device_of(x)
+    x = _as_input(x)
+    cfg = net.config
+    B = x.shape[0]
+    y = torch.empty((B, 1, cfg.map_height, cfg.map_width), device=device, dtype=torch.float32)
+    if B == 0:
+        return y
+    plan = _net_plan(net, device)
+    with torch.cuda.device(device):
+        L = plan.L
+        ws = torch.empty(L.workspace_bytes(plan.handle, B), device=device, dtype=torch.uint8)
+        L.forward(plan.handle, x.data_ptr(), y.data_ptr(), B, ws.data_ptr(), ws.numel(),
+                  _stream_ptr(device))
+    return y
+
+
+def forward_window(net, frames: torch.Tensor) -> torch.Tensor:
+    device = _device_of(frames)
+    frames = _as_input(frames)
+    cfg = net.config
+    F = cfg.input_frames
+    if frames.dim() != 3 or tuple(frames.shape[1:]) != (cfg.map_height, cfg.map_width):
+        raise ValueError(f"expected frames [T, {cfg.map_height}, {cfg.map_width}], got {tuple(frames.shape)}")
+    T = frames.shape[0]
+    n_out = max(T - (F - 1), 0)
+    y = torch.empty((n_out, 1, cfg.map_height, cfg.map_width), device=device, dtype=torch.float32)
+    if n_out == 0:
+        return y
+    plan = _net_plan(net, device)
+    with torch.cuda.device(device):
+        L = plan.L
+        ws = torch.empty(L.workspace_bytes(plan.handle, n_out), device=device, dtype=torch.uint8)
+        L.forward_window(plan.handle, frames.data_ptr(), T, y.data_ptr(), ws.data_ptr(),
+                         ws.numel(), _stream_ptr(device))
+    return y
+
+
+def forward_host(net, x: torch.Tensor, out: Optional[torch.Tensor] = None,
+                 device: Optional[torch.device] = None) -> torch.Tensor:
+    if x.is_cuda:
+        raise ValueError("denoise_host takes a host (CPU) tensor; use forward() for device tensors")
+    if x.dtype != torch.float32:
+        raise TypeError(f"the engine computes on float32 inputs, got {x.dtype}")
+    cfg = net.config
+    if tuple(x.shape[1:]) != (cfg.input_frames, cfg.map_height, cfg.map_width) or x.dim() != 4:
+        raise ValueError(f"expected [B, {cfg.input_frames}, {cfg.map_height}, {cfg.map_width}], "
+                         f"got {tuple(x.shape)}")
+    x = x.contiguous()
+    B = x.shape[0]
+    if out is None:
+        out = torch.empty((B, 1, cfg.map_height, cfg.map_width), dtype=torch.float32,
+                          pin_memory=x.is_pinned())
+    if B == 0:
+        return out
+    device = device or torch.device("cuda", torch.cuda.current_device())
+    plan = _net_plan(net, device)
+    with torch.cuda.device(device):
+        L = plan.L
+        chunk = L.host_chunk(plan.handle, B)
+        ws = torch.empty(L.host_workspace_bytes(plan.handle, chunk), device=device, dtype=torch.uint8)
+        L.forward_host(plan.handle, x.data_ptr(), out.data_ptr(), B, chunk, ws.data_ptr(),
+                       ws.numel(), _stream_ptr(device))
+    return out
+
+
+# ---- block-level entry points (reference MobileEncoderBlock / MobileDecoderBlock / EcaBlock)
+class _BlockPlan:
+    def __init__(self, kind: int, channels: int, blob: np.ndarray, device: torch.device):
+        from . import _lib as L
+        self.L = L
+        self.channels = channels
+        self.handle = L.block_plan_create(kind, channels, blob, device.index or 0)
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None:
+            try:
+                self.L.plan_destroy(h)
+            except Exception:
+                pass
+            self.handle = None
+
+
+def _block_plan(block, kind: str, device: torch.device) -> _BlockPlan:
+    from .fold import fold_block
+    key = _state_key(block, "fp32", device)
+    cache = getattr(block, "_engine_cache", None)
+    if cache is not None and cache[0] == key:
+        return cache[1]
+    blob, cin = fold_block(block, kind)
+    plan = _BlockPlan(0 if kind == "enc" else 1, cin, blob, device)
+    block._engine_cache = (key, plan)
+    return plan
+
+
+def _block_forward(block, x: torch.Tensor, kind: str) -> torch.Tensor:
+    device = _device_of(x)
+    x = _as_input(x)
+    B, C, H, W = x.shape
+    plan = _block_plan(block, kind, device)
+    if C != plan.channels:
+        raise RuntimeError(f"{type(block).__name__}({plan.channels}) got {C} input channels")
+    if kind == "enc":
+        y = torch.empty((B, 2 * C, H // 2, W // 2), device=device, dtype=torch.float32)
+    else:
+        y = torch.empty((B, C // 2, 2 * H, 2 * W), device=device, dtype=torch.float32)
+    if B == 0:
+        return y
+    with torch.cuda.device(device):
+        L = plan.L
+        ws = torch.empty(max(L.block_workspace_bytes(plan.handle, B, H, W), 1), device=device,
+                         dtype=torch.uint8)
+        L.block_forward(plan.handle, x.data_ptr(), y.data_ptr(), B, H, W, ws.data_ptr(), ws.numel(),
+                        _stream_ptr(device))
+    return y
+
+
+def encoder_block(block, x: torch.Tensor) -> torch.Tensor:
+    return _block_forward(block, x, "enc")
+
+
+def decoder_block(block, x: torch.Tensor) -> torch.Tensor:
+    return _block_forward(block, x, "dec")
+
+
+def _eca(block, x: torch.Tensor, apply: bool) -> torch.Tensor:
+    from . import _lib as L
+    device = _device_of(x)
+    x = _as_input(x)
+    B, C, H, W = x.shape
+    w = block.conv.weight.detach().to(device=device, dtype=torch.float32).contiguous().view(-1)
+    k = w.numel()
+    g = torch.empty((B, C), device=device, dtype=torch.float32)
+    y = torch.empty_like(x) if apply else None
+    if B == 0:
+        return y if apply else g
+    with torch.cuda.device(device):
+        L.eca(w.data_ptr(), k, x.data_ptr(), g.data_ptr(), y.data_ptr() if apply else None,
+              B, C, H, W, _stream_ptr(device))
+    return y if apply else g
+
+
+def eca_gates(block, x):
+    return _eca(block, x, False)
+
+
+def eca_apply(block, x):
+    return _eca(block, x, True)
+
+
+class CapturedForward:
+    """One engine forward on fixed device buffers, captured as a CUDA graph.
+
+    Serving / benchmark entry point: `replay()` re-runs the whole forward (all
+    kernels of the plan) with a single graph launch, removing host launch overhead.
+    The input buffer `self.x` may be refilled in place between replays.
+    """
+
+    def __init__(self, net, x: torch.Tensor):
+        device = _device_of(x)
+        if net.training:
+            raise RuntimeError("capture an eval-mode network")
+        self.x = _as_input(x)
+        cfg = net.config
+        self.batch = x.shape[0]
+        self.plan = _net_plan(net, device)
+        self.device = device
+        L = self.plan.L
+        with torch.cuda.device(device):
+            self.y = torch.empty((self.batch, 1, cfg.map_height, cfg.map_width), device=device)
+            self.ws = torch.empty(L.workspace_bytes(self.plan.handle, self.batch), device=device,
+                                  dtype=torch.uint8)
+            self._launch()                      # eager run configures kernels before capture
+            torch.cuda.synchronize(device)
+            self.graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.graph):
+                self._launch()
+        self.launches = L.launches_per_forward(self.plan.handle)
+
+    def _launch(self) -> None:
+        self.plan.L.forward(self.plan.handle, self.x.data_ptr(), self.y.data_ptr(), self.batch,
+                            self.ws.data_ptr(), self.ws.numel(), _stream_ptr(self.device))
+
+    def replay(self) -> torch.Tensor:
+        self.graph.replay()
+        return self.y
+
+    def profile(self):
+        """Per-launch device times (ms) of one eager forward + the launch names."""
+        L = self.plan.L
+        with torch.cuda.device(self.device):
+            ms = L.forward_profiled(self.plan.handle, self.x.data_ptr(), self.y.data_ptr(),
+                                    self.batch, self.ws.data_ptr(), self.ws.numel(),
+                                    _stream_ptr(self.device))
+        return L.launch_names(self.plan.handle), ms

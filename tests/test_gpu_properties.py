@@ -1,0 +1,130 @@
+"""GPU mirrors of the reference's property tests (pkg/stda/tests/test_model.py) plus the
+engine's own invariants: bitwise determinism, batch invariance, window equivalence,
+host-buffer path equivalence, error behaviour."""
+
+import pytest
+import torch
+
+from paper_2307_09063_b200 import (
+    EcaBlock,
+    MobileDecoderBlock,
+    MobileEncoderBlock,
+    StdaConfig,
+    StdaNet,
+)
+from paper_2307_09063_b200.synth import synth_frames, synth_triplets
+
+pytestmark = pytest.mark.gpu
+
+
+def test_forward_shape_default_config():                       # test_model.py:130-133
+    net = StdaNet().eval().cuda()
+    assert net(torch.rand(2, 3, 128, 64, device="cuda")).shape == (2, 1, 128, 64)
+
+
+def test_tiny_config():                                         # test_model.py:153-156
+    net = StdaNet(StdaConfig(stem_channels=2, map_height=8, map_width=8)).eval().cuda()
+    assert net(torch.rand(1, 3, 8, 8, device="cuda")).shape == (1, 1, 8, 8)
+
+
+def test_zero_weights_zero_output_blocks():                     # test_model.py:48-55, 68-75
+    for block, x in ((MobileEncoderBlock(4), torch.rand(1, 4, 16, 16)),
+                     (MobileDecoderBlock(8), torch.rand(1, 8, 8, 8))):
+        with torch.no_grad():
+            for p in block.parameters():
+                p.zero_()
+        block = block.eval().cuda()
+        out = block(x.cuda())
+        assert torch.count_nonzero(out) == 0
+
+
+def test_eca_zero_conv_is_half_scale():                         # test_model.py:86-91
+    eca = EcaBlock(3)
+    with torch.no_grad():
+        eca.conv.weight.zero_()
+    eca = eca.eval().cuda()
+    x = torch.rand(2, 8, 16, 16, device="cuda")
+    assert torch.equal(eca(x), 0.5 * x)
+
+
+def test_eca_gates_open_unit_interval():                        # test_model.py:118-122
+    eca = EcaBlock(3).eval().cuda()
+    w = eca.channel_weights(torch.randn(4, 16, 8, 8, device="cuda") * 10)
+    assert w.shape == (4, 16)
+    assert bool((w > 0).all()) and bool((w < 1).all())
+
+
+def test_eval_deterministic_bitwise():                          # test_model.py:144-151
+    net = StdaNet(StdaConfig(map_height=128, map_width=128)).eval().cuda()
+    x = synth_triplets(4, 128, 128, seed=5)
+    assert torch.equal(net(x), net(x))
+
+
+def test_batch_invariance_bitwise():
+    net = StdaNet(StdaConfig(map_height=64, map_width=64)).eval().cuda()
+    x = synth_triplets(6, 64, 64, seed=9)
+    full = net(x)
+    parts = torch.cat([net(x[i:i + 1]) for i in range(6)])
+    assert torch.equal(full, parts)
+    # shard emulation (SURVEY §4 iv): contiguous slices concatenate bitwise
+    assert torch.equal(full, torch.cat([net(x[:2]), net(x[2:5]), net(x[5:])]))
+
+
+def test_stream_window_equals_per_triplet_forward():            # BASELINE config 4 semantics
+    net = StdaNet(StdaConfig(map_height=64, map_width=64)).eval().cuda()
+    frames = synth_frames(12, 64, 64, seed=3)
+    y = net.forward_window(frames)
+    assert y.shape == (10, 1, 64, 64)
+    trip = torch.stack([torch.stack([frames[t], frames[t - 1], frames[t - 2]]) for t in range(2, 12)])
+    assert torch.equal(y, net(trip))
+    # contiguous time chunks with a 2-frame overlap halo reproduce the whole stream
+    y1 = net.forward_window(frames[:7])
+    y2 = net.forward_window(frames[5:])
+    assert torch.equal(torch.cat([y1, y2]), y)
+
+
+def test_host_buffer_path_equals_device_path():
+    net = StdaNet(StdaConfig(map_height=128, map_width=128)).eval().cuda()
+    x = synth_triplets(37, 128, 128, seed=4)
+    ref = net(x).cpu()
+    out = net.denoise_host(x.cpu().pin_memory())
+    assert torch.equal(out, ref)
+
+
+def test_error_behaviour():
+    net = StdaNet(StdaConfig(map_height=32, map_width=32)).eval().cuda()
+    with pytest.raises(ValueError):
+        net(torch.rand(1, 3, 64, 64, device="cuda"))            # wrong map size
+    with pytest.raises(ValueError):
+        net(torch.rand(3, 32, 32, device="cuda"))               # 3-D input (BN ValueError)
+    with pytest.raises(RuntimeError):
+        net(torch.rand(1, 1, 3, 32, 32, device="cuda"))         # 5-D input (conv RuntimeError)
+    with pytest.raises(TypeError):
+        net(torch.rand(1, 3, 32, 32, device="cuda", dtype=torch.float64))
+    assert net(torch.rand(0, 3, 32, 32, device="cuda")).shape == (0, 1, 32, 32)
+
+
+def test_weight_update_invalidates_plan():
+    net = StdaNet(StdaConfig(map_height=32, map_width=32)).eval().cuda()
+    x = torch.rand(2, 3, 32, 32, device="cuda")
+    a = net(x)
+    with torch.no_grad():
+        net.head.bias.add_(1.0)
+    b = net(x)
+    assert torch.allclose(b, a + 1.0, atol=1e-5)
+
+
+def test_synth_properties():
+    x = synth_triplets(8, 128, 128, seed=1)
+    assert x.shape == (8, 3, 128, 128)
+    mins = x.amin(dim=(-2, -1))
+    maxs = x.amax(dim=(-2, -1))
+    assert torch.all(mins == 0) and torch.all(maxs == 1)
+    assert torch.equal(x, synth_triplets(8, 128, 128, seed=1))
+    assert not torch.equal(x, synth_triplets(8, 128, 128, seed=2))
+    # sequence frames == triplet channels (frame F-1-c of sequence b)
+    f = synth_frames(3, 128, 128, seed=1, seq=5)
+    assert torch.equal(x[5, 0], f[2]) and torch.equal(x[5, 2], f[0])
+    # noise floor bulk in 0.4..0.9, targets are the brightest bins
+    med = x.flatten(-2).median(dim=-1).values
+    assert bool(((med > 0.3) & (med < 0.95)).all())

@@ -1,0 +1,52 @@
+"""Pin the CPU oracle and the host folding against the real reference's golden vectors."""
+
+import numpy as np
+import pytest
+import torch
+
+from tests._helpers import folded_forward, golden_index, golden_names, load_golden, nmax_err
+from oracle import np64, port
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_port_matches_reference_golden(name):
+    cfg, sd, x, y, y64 = load_golden(name)
+    out = port.forward(sd, cfg, torch.from_numpy(x)).numpy()
+    # same torch CPU ops in the same order as the reference: identical up to
+    # oneDNN algorithm choice
+    assert nmax_err(out, y) <= 1e-6, nmax_err(out, y)
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_np64_matches_reference_fp64_golden(name):
+    cfg, sd, x, y, y64 = load_golden(name)
+    out = np64.forward(sd, cfg, x)
+    assert nmax_err(out, y64) <= 1e-10, nmax_err(out, y64)
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_reference_fp32_noise_floor(name):
+    _, _, _, y, y64 = load_golden(name)
+    assert nmax_err(y, y64) <= 2e-6
+    assert golden_index()[name]["fp32_vs_fp64"] <= 2e-6
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_folding_is_exact(name):
+    from paper_2307_09063_b200.fold import fold_state_dict
+    from paper_2307_09063_b200.model import StdaConfig
+
+    cfg, sd, x, y, y64 = load_golden(name)
+    blob = fold_state_dict(StdaConfig(**cfg), sd)
+    out = folded_forward(cfg, blob, x)
+    # folded weights are rounded once to fp32; the rest is fp64
+    assert nmax_err(out, y64) <= 2e-6, nmax_err(out, y64)
+
+
+def test_port_eca_and_shape_errors():
+    cfg, sd, x, *_ = load_golden("tiny_c2_8x8")
+    with pytest.raises(ValueError):
+        port.forward(sd, cfg, torch.zeros(1, 3, 8, 16))
+    w = torch.zeros(1, 1, 3)
+    t = torch.rand(2, 8, 4, 4)
+    assert torch.allclose(port.eca(w, t), 0.5 * t)
