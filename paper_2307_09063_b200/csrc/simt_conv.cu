@@ -45,6 +45,7 @@ struct Args {
   const float* b1;
   float* out;
   float* gap;
+  OutLayout ol;
   int64_t b_base;
   int Cin, Cout, Hi, Wi, Ho, Wo;
   int relu0, bf16;
@@ -52,10 +53,10 @@ struct Args {
 };
 
 __device__ __forceinline__ float src_value(const Src& s, int64_t b, int c, int64_t pix) {
-  float v = __ldg(s.x + b * s.xb + (int64_t)c * s.xc + pix);
+  float v = __ldg(s.x + b * s.xb + (int64_t)c * s.xc + pix * s.xp);
   if (s.gx) v = v * __ldg(s.gx + b * s.C + c);
   if (s.s) {
-    float u = __ldg(s.s + b * s.sb + (int64_t)c * s.sc + pix);
+    float u = __ldg(s.s + b * s.sb + (int64_t)c * s.sc + pix * s.sp);
     if (s.gs) u = u * __ldg(s.gs + b * s.C + c);
     v = v + u;
   }
@@ -244,7 +245,7 @@ __global__ void __launch_bounds__(kThreads, 2) conv_simt_kernel(Args a) {
       if (a.relu0) v = fmaxf(v, 0.f);
       if (DUAL) v = v + (acc1[r][q] + bias1);
       if (oy[r] < a.Ho && ox < a.Wo) {
-        a.out[((b * a.Cout + co) * a.Ho + oy[r]) * a.Wo + ox] = v;
+        a.out[b * a.ol.ob + co * a.ol.oc + ((int64_t)oy[r] * a.Wo + ox) * a.ol.op] = v;
         gsum[q] += v;
       }
     }
@@ -394,7 +395,7 @@ void simt_pack(int mode, int cin, int cout, const float* w, const float* bias, b
 
 void launch_conv(const ConvLayer& L0, const ConvLayer* L1, const Src& in0, const Src* in1,
                  float* out, float* gap, int64_t B, int hi, int wi, bool relu0, bool bf16,
-                 cudaStream_t st) {
+                 cudaStream_t st, const OutLayout* out_layout) {
   Args a{};
   a.in0 = in0;
   if (in1) a.in1 = *in1;
@@ -412,6 +413,7 @@ void launch_conv(const ConvLayer& L0, const ConvLayer* L1, const Src& in0, const
   a.Wo = conv_out_h(L0.mode, wi);
   a.relu0 = relu0;
   a.bf16 = bf16;
+  a.ol = out_layout ? *out_layout : OutLayout::nchw(L0.cout, a.Ho, a.Wo);
   a.tiles_x = cdiv(a.Wo, kTileW);
   a.ntiles = conv_tiles(L0.mode, a.Ho, a.Wo);
   const int nblk = cdiv(L0.cout, L0.cob);

@@ -15,12 +15,14 @@ namespace stda {
 enum ConvMode : int { CONV3_S1 = 0, CONV3_S2 = 1, CONVT4_S2 = 2 };
 
 // A logical input tensor [B][C][H][W]: value = x*gx[b][c] (+ s*gs[b][c]).
+// Element (b, c, pixel p = y*W + x) of x lives at x[b*xb + c*xc + p*xp] (NCHW: xp = 1,
+// NHWC: xc = 1, xp = C); the optional skip tensor s has its own strides.
 struct Src {
   const float* x = nullptr;
-  int64_t xb = 0, xc = 0;  // element strides of batch / channel; rows are W-contiguous
+  int64_t xb = 0, xc = 0, xp = 1;
   const float* gx = nullptr;
   const float* s = nullptr;
-  int64_t sb = 0, sc = 0;
+  int64_t sb = 0, sc = 0, sp = 1;
   const float* gs = nullptr;
   int C = 0;
 };
@@ -31,8 +33,28 @@ inline Src plain_src(const float* x, int C, int H, int W) {
   s.C = C;
   s.xc = (int64_t)H * W;
   s.xb = (int64_t)C * H * W;
+  s.xp = 1;
   return s;
 }
+
+inline Src nhwc_src(const float* x, int C, int H, int W) {
+  Src s;
+  s.x = x;
+  s.C = C;
+  s.xc = 1;
+  s.xp = C;
+  s.xb = (int64_t)C * H * W;
+  return s;
+}
+
+// Output addressing of a SIMT conv: out[b*ob + c*oc + (y*Wo + x)*op].
+struct OutLayout {
+  int64_t ob = 0, oc = 0, op = 1;
+  static OutLayout nchw(int C, int H, int W) {
+    return OutLayout{(int64_t)C * H * W, (int64_t)H * W, 1};
+  }
+  static OutLayout nhwc(int C, int H, int W) { return OutLayout{(int64_t)C * H * W, 1, C}; }
+};
 
 // Device weights of one conv layer in the SIMT layout:
 //   w[blk][ci][tapsz], blk = output-channel block of `cob` channels,
@@ -59,7 +81,7 @@ int conv_tiles(int mode, int ho, int wo);
 // [B][tiles][cout] of the final output (deterministic, fixed order).
 void launch_conv(const ConvLayer& L0, const ConvLayer* L1, const Src& in0, const Src* in1,
                  float* out, float* gap, int64_t B, int hi, int wi, bool relu0, bool bf16,
-                 cudaStream_t st);
+                 cudaStream_t st, const OutLayout* out_layout = nullptr);
 
 // gates[b][c] = sigmoid(conv1d_k(sum_t gap[b][t][c] / hw)), zero-padded conv1d.
 void launch_gate(const float* gap, int ntiles, const float* w, int k, float* gates, int64_t B, int C,

@@ -12,6 +12,7 @@
 //   head   conv3x3 s1                                        cur      -> y
 // Gates and skip adds are applied while the NEXT kernel stages its input tile.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -20,6 +21,7 @@
 #include "../../include/stda_b200.h"
 #include "common.cuh"
 #include "simt_conv.cuh"
+#include "tc_conv.cuh"
 
 namespace stda {
 
@@ -54,10 +56,12 @@ using namespace stda;
 
 struct EncLayers {
   ConvLayer s1, dn, rs;
+  tc::TcLayerDesc s1_tc{}, s2_tc{};  // tensor-core versions (dn+rs dual in s2_tc)
   float* eca = nullptr;
 };
 struct DecLayers {
   ConvLayer s1, up, rs;
+  tc::TcLayerDesc s1_tc{}, s2_tc{};
   float* eca = nullptr;
 };
 
@@ -114,6 +118,28 @@ struct stda_plan {
     src += n;
     return upload(v);
   }
+
+  void* upload_bytes(const void* data, size_t bytes) {
+    void* p = nullptr;
+    STDA_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
+    allocations.push_back(p);
+    STDA_CUDA(cudaMemcpy(p, data, bytes, cudaMemcpyHostToDevice));
+    return p;
+  }
+
+  // tensor-core layer from canonical weights w0/b0 (+ w1/b1 for a dual stage)
+  tc::TcLayerDesc make_tc(int mode, int cin, int cout, const float* w0, const float* b0,
+                          const float* w1, const float* b1) {
+    tc::TcLayerDesc d;
+    std::vector<uint16_t> packed;
+    tc::tc_pack_layer(d, mode, cin, cout, w0, w1, bf16, packed);
+    d.w = static_cast<const uint16_t*>(upload_bytes(packed.data(), packed.size() * 2));
+    d.bias0 = upload(std::vector<float>(b0, b0 + cout));
+    d.bias1 = w1 ? upload(std::vector<float>(b1, b1 + cout)) : nullptr;
+    return d;
+  }
+
+  bool use_tc = false;  // every encoder/decoder conv runs on the tcgen05 kernel
 };
 
 namespace {
@@ -176,7 +202,9 @@ NetWs plan_ws(const stda_plan& p, int64_t B, char* base) {
     const int ch = c.stem_channels << (i + 1);
     const int h = c.map_height >> (i + 1), wd = c.map_width >> (i + 1);
     w.e.push_back(take(B * ch * (size_t)h * wd));
-    w.pe.push_back(take(B * ch * (size_t)conv_tiles(CONV3_S2, h, wd)));
+    // GAP partials: SIMT tiles or tensor-core items (<= one per 128 linear positions)
+    const size_t tiles = std::max<size_t>(conv_tiles(CONV3_S2, h, wd), cdiv(h * (wd + 1), 128));
+    w.pe.push_back(take(B * ch * tiles));
     w.ge.push_back(take(B * ch));
   }
   for (int j = 0; j < S; ++j) {
@@ -184,7 +212,9 @@ NetWs plan_ws(const stda_plan& p, int64_t B, char* base) {
     const int ch = c.stem_channels << lvl;
     const int h = c.map_height >> lvl, wd = c.map_width >> lvl;
     w.d.push_back(take(B * ch * (size_t)h * wd));
-    w.pd.push_back(take(B * ch * (size_t)conv_tiles(CONVT4_S2, h, wd)));
+    const size_t tiles =
+        std::max<size_t>(conv_tiles(CONVT4_S2, h, wd), cdiv((h / 2) * (wd / 2 + 1), 128));
+    w.pd.push_back(take(B * ch * tiles));
     w.gd.push_back(take(B * ch));
   }
   w.bytes = off;
@@ -201,8 +231,78 @@ struct Marks {
   }
 };
 
+// Tensor-core forward: stem and head on the SIMT kernel (Cin = 3 / Cout = 1), every
+// encoder/decoder conv on the tcgen05 kernel; intermediates NHWC fp32.
+void run_net_tc(const stda_plan& p, const Src& x, float* y, int64_t B, const NetWs& w,
+                cudaStream_t st, Marks mk) {
+  const stda_config& c = p.cfg;
+  const int S = c.stages, k = c.eca_kernel, c0 = c.stem_channels;
+  const bool bf = p.bf16;
+  int h = c.map_height, wd = c.map_width;
+  mk.mark(st);
+  const OutLayout s_layout = OutLayout::nhwc(c0, h, wd);
+  launch_conv(p.stem, nullptr, x, nullptr, w.s, nullptr, B, h, wd, true, bf, st, &s_layout);
+  mk.mark(st);
+  tc::TcSrc cur;
+  cur.x = w.s;
+  std::vector<tc::TcSrc> skips{cur};
+  for (int i = 0; i < S; ++i) {
+    const EncLayers& E = p.enc[i];
+    tc::TcLayerDesc d1 = E.s1_tc, d2 = E.s2_tc;
+    const tc::TcGeometry g1 = tc::tc_plan(d1, (int)B, h, wd);
+    tc::tc_launch(d1, g1, cur, nullptr, w.m, nullptr, true, st);
+    mk.mark(st);
+    const tc::TcGeometry g2 = tc::tc_plan(d2, (int)B, h, wd);
+    tc::TcSrc mixed;
+    mixed.x = w.m;
+    tc::tc_launch(d2, g2, mixed, &cur, w.e[i], w.pe[i], true, st);
+    mk.mark(st);
+    h /= 2;
+    wd /= 2;
+    launch_gate(w.pe[i], g2.items_per_image, E.eca, k, w.ge[i], B, d2.cout, h * wd, st);
+    mk.mark(st);
+    cur = tc::TcSrc{};
+    cur.x = w.e[i];
+    cur.gx = w.ge[i];
+    skips.push_back(cur);
+  }
+  for (int j = 0; j < S; ++j) {
+    const DecLayers& D = p.dec[j];
+    tc::TcLayerDesc d1 = D.s1_tc, d2 = D.s2_tc;
+    const tc::TcGeometry g1 = tc::tc_plan(d1, (int)B, h, wd);
+    tc::tc_launch(d1, g1, cur, nullptr, w.m, nullptr, true, st);
+    mk.mark(st);
+    const tc::TcGeometry g2 = tc::tc_plan(d2, (int)B, h, wd);
+    tc::TcSrc mixed;
+    mixed.x = w.m;
+    tc::tc_launch(d2, g2, mixed, &cur, w.d[j], w.pd[j], true, st);
+    mk.mark(st);
+    h *= 2;
+    wd *= 2;
+    launch_gate(w.pd[j], g2.items_per_image, D.eca, k, w.gd[j], B, d2.cout, h * wd, st);
+    mk.mark(st);
+    const tc::TcSrc& sk = skips[S - 1 - j];
+    cur = tc::TcSrc{};
+    cur.x = w.d[j];
+    cur.gx = w.gd[j];
+    cur.s = sk.x;
+    cur.gs = sk.gx;
+  }
+  // head reads NHWC d*g + skip through the SIMT source transform
+  Src hs = nhwc_src(cur.x, c0, h, wd);
+  hs.gx = cur.gx;
+  hs.s = cur.s;
+  hs.sb = (int64_t)c0 * h * wd;
+  hs.sc = 1;
+  hs.sp = c0;
+  hs.gs = cur.gs;
+  launch_conv(p.head, nullptr, hs, nullptr, y, nullptr, B, h, wd, false, bf, st);
+  mk.mark(st);
+}
+
 void run_net(const stda_plan& p, const Src& x, float* y, int64_t B, const NetWs& w, cudaStream_t st,
              Marks mk = Marks{}) {
+  if (p.use_tc) return run_net_tc(p, x, y, B, w, st, mk);
   const stda_config& c = p.cfg;
   const int S = c.stages, k = c.eca_kernel;
   const bool bf = p.bf16;
@@ -312,22 +412,50 @@ int stda_plan_create(const stda_config* cfg, const float* blob, size_t n_floats,
     p->bf16 = cfg->precision == STDA_PRECISION_BF16;
     const float* src = blob;
     const int c0 = cfg->stem_channels, S = cfg->stages, k = cfg->eca_kernel;
+    // the tensor-core path needs every encoder/decoder conv in its supported shape set
+    bool tc_ok = true;
+    for (int i = 0; i < S; ++i) {
+      const int ch = c0 << i;
+      tc_ok = tc_ok && tc::tc_supported(CONV3_S1, ch, ch) && tc::tc_supported(CONV3_S2, ch, 2 * ch);
+    }
+    for (int j = 0; j < S; ++j) {
+      const int c2 = c0 << (S - j);
+      tc_ok = tc_ok && tc::tc_supported(CONV3_S1, c2, c2) && tc::tc_supported(CONVT4_S2, c2, c2 / 2);
+    }
+    const char* force = std::getenv("STDA_ENGINE_PATH");  // "simt" forces the generic path
+    p->use_tc = tc_ok && !(force && std::strcmp(force, "simt") == 0);
     p->stem = p->make_layer(CONV3_S1, cfg->input_frames, c0, src);
     for (int i = 0; i < S; ++i) {
       const int ch = c0 << i;
       EncLayers E;
+      const float* w_s1 = src;
       E.s1 = p->make_layer(CONV3_S1, ch, ch, src);
+      const float* w_dn = src;
       E.dn = p->make_layer(CONV3_S2, ch, 2 * ch, src);
+      const float* w_rs = src;
       E.rs = p->make_layer(CONV3_S2, ch, 2 * ch, src);
+      if (p->use_tc) {
+        const size_t n1 = (size_t)ch * ch * 9, n2 = (size_t)2 * ch * ch * 9;
+        E.s1_tc = p->make_tc(CONV3_S1, ch, ch, w_s1, w_s1 + n1, nullptr, nullptr);
+        E.s2_tc = p->make_tc(CONV3_S2, ch, 2 * ch, w_dn, w_dn + n2, w_rs, w_rs + n2);
+      }
       E.eca = p->make_vec(k, src);
       p->enc.push_back(E);
     }
     for (int j = 0; j < S; ++j) {
       const int c2 = c0 << (S - j), ch = c2 / 2;
       DecLayers D;
+      const float* w_s1 = src;
       D.s1 = p->make_layer(CONV3_S1, c2, c2, src);
+      const float* w_up = src;
       D.up = p->make_layer(CONVT4_S2, c2, ch, src);
+      const float* w_rs = src;
       D.rs = p->make_layer(CONVT4_S2, c2, ch, src);
+      if (p->use_tc) {
+        const size_t n1 = (size_t)c2 * c2 * 9, n2 = (size_t)ch * c2 * 16;
+        D.s1_tc = p->make_tc(CONV3_S1, c2, c2, w_s1, w_s1 + n1, nullptr, nullptr);
+        D.s2_tc = p->make_tc(CONVT4_S2, c2, ch, w_up, w_up + n2, w_rs, w_rs + n2);
+      }
       D.eca = p->make_vec(k, src);
       p->dec.push_back(D);
     }

@@ -155,8 +155,10 @@ __global__ void __launch_bounds__(kThreads) synth_kernel(Key key, int scene, int
     vmin = fminf(vmin, red_min[i]);
     vmax = fmaxf(vmax, red_max[i]);
   }
-  const float scale = vmax > vmin ? 1.f / (vmax - vmin) : 0.f;
-  for (int e = threadIdx.x; e < n; e += blockDim.x) dst[e] = (dst[e] - vmin) * scale;
+  // division (not a reciprocal multiply) so the brightest bin maps to exactly 1
+  const float range = vmax - vmin;
+  for (int e = threadIdx.x; e < n; e += blockDim.x)
+    dst[e] = range > 0.f ? (dst[e] - vmin) / range : 0.f;
 }
 
 Key make_key(uint64_t seed, int scene) {

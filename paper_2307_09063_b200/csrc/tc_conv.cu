@@ -1,0 +1,623 @@
+// tcgen05 implicit-GEMM convolution kernel (see tc_conv.cuh for the design).
+#include <algorithm>
+#include <cstring>
+
+#include "tc_conv.cuh"
+
+namespace stda {
+namespace tc {
+
+namespace {
+
+constexpr int kProdWarps = 4;
+constexpr int kEpiWarps = 4;
+constexpr int kMmaWarp = kProdWarps + kEpiWarps;  // warp 8
+constexpr int kThreads = (kProdWarps + kEpiWarps + 1) * 32;
+constexpr int kProdThreads = kProdWarps * 32;
+constexpr int kMaxSmem = 227 * 1024;
+
+struct Params {
+  TcLayerDesc d;
+  TcSrc src[2];
+  float* out;
+  float* gap;
+  int H, W, C;            // input NHWC
+  int Hp, Wp, L, Ho, Wo;
+  int G, stages, slots, items_per_image, total_items;
+  int P_max;
+  uint32_t a_stage_bytes, b_stage_bytes, slot_cols;
+  uint32_t tmem_cols;
+  int relu0;
+};
+
+// ---- PTX helpers -----------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+        "=r"(r[15])
+      : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// UMMA shared-memory descriptor, K-major, SWIZZLE_NONE (canonical ((8,m),(T,2)) layout):
+// core matrix = 8 rows x 16 B contiguous; SBO = byte stride between 8-row groups,
+// LBO = byte stride between the two 8-element K halves.  version = 1 (sm_100).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);
+}
+
+// kind::f16 instruction descriptor: A/B bf16, D f32, both K-major, M = 128.
+__host__ __device__ constexpr uint32_t idesc_bf16(int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((128u >> 4) << 24);
+}
+
+__device__ __forceinline__ int floor_div(int a, int b) {
+  int q = a / b;
+  return (a % b != 0 && ((a < 0) != (b < 0))) ? q - 1 : q;
+}
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+// ---- the kernel ----------------------------------------------------------------------
+template <int N>
+__global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_constant__ Params p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const TcLayerDesc& d = p.d;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_acc = d.n_src * d.n_acc_src;
+  const int cgroups = d.cin / 16;
+  const int n_chunks = d.n_planes * cgroups;
+  const int npassA = d.npass == 3 ? 2 : 1;
+
+  uint8_t* a_base = smem;
+  uint8_t* b_base = smem + (size_t)p.stages * p.a_stage_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(b_base + (size_t)p.stages * p.b_stage_bytes);
+  uint64_t* full = bars;
+  uint64_t* empty = full + p.stages;
+  uint64_t* tfull = empty + p.stages;
+  uint64_t* tempty = tfull + p.slots;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + p.slots);
+  float* red = reinterpret_cast<float*>(tmem_holder + 4);  // [4][N]
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(smem_u32(&full[s]), kProdThreads + 1);
+      mbar_init(smem_u32(&empty[s]), 1);
+    }
+    for (int s = 0; s < p.slots; ++s) {
+      mbar_init(smem_u32(&tfull[s]), 1);
+      mbar_init(smem_u32(&tempty[s]), kEpiWarps * 32);
+    }
+    fence_barrier_init();
+  }
+  if (warp == kMmaWarp) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_holder)),
+                 "r"(p.tmem_cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp < kProdWarps) {
+    // ===================== producers: stage A (and weights via bulk copy) ==============
+    const int tid = threadIdx.x;
+    uint32_t k = 0;
+    for (int item = blockIdx.x; item < p.total_items; item += gridDim.x) {
+      const int b = item / p.items_per_image;
+      const int q0 = (item - b * p.items_per_image) * p.G * 128;
+      for (int c = 0; c < n_chunks; ++c, ++k) {
+        const int stage = k % p.stages;
+        const uint32_t phase = (k / p.stages) & 1;
+        mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+        const int pl = c / cgroups, cgi = c - pl * cgroups;
+        if (tid == 0) {
+          const uint32_t bytes = (uint32_t)(d.chunk_off[c + 1] - d.chunk_off[c]);
+          mbar_arrive_expect_tx(smem_u32(&full[stage]), bytes);
+          bulk_g2s(smem_u32(b_base + (size_t)stage * p.b_stage_bytes),
+                   reinterpret_cast<const uint8_t*>(d.w) + d.chunk_off[c], bytes, smem_u32(&full[stage]));
+        }
+        const PlaneTaps& pt = d.planes[pl];
+        const int P = p.G * 128 + pt.hi - pt.lo;
+        const int py = pl >> 1, px = pl & 1;
+        uint8_t* sa = a_base + (size_t)stage * p.a_stage_bytes;
+        const uint32_t src_bytes = (uint32_t)npassA * 2 * p.P_max * 16;
+        const int total = d.n_src * 2 * P;
+        for (int e = tid; e < total; e += kProdThreads) {
+          const int s = e / (2 * P);
+          const int r = e - s * 2 * P;
+          const int cg8 = r / P;
+          const int qq = r - cg8 * P;
+          const int q = q0 + pt.lo + qq;
+          const int y = floor_div(q, p.L);
+          const int x = q - y * p.L;
+          float v[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) v[i] = 0.f;
+          if (y >= 0 && y < p.Hp && x < p.Wp) {
+            int iy = y, ix = x;
+            if (d.mode == CONV3_S2) {
+              iy = 2 * y + py;
+              ix = 2 * x + px;
+            }
+            const int ch = cgi * 16 + cg8 * 8;
+            const TcSrc& S = p.src[s];
+            const size_t pix = ((size_t)b * p.H + iy) * p.W + ix;
+            const float4* xp = reinterpret_cast<const float4*>(S.x + pix * p.C + ch);
+            float4 a0 = __ldg(xp), a1 = __ldg(xp + 1);
+            v[0] = a0.x; v[1] = a0.y; v[2] = a0.z; v[3] = a0.w;
+            v[4] = a1.x; v[5] = a1.y; v[6] = a1.z; v[7] = a1.w;
+            if (S.gx) {
+              const float4* gp = reinterpret_cast<const float4*>(S.gx + (size_t)b * p.C + ch);
+              const float4 g0 = __ldg(gp), g1 = __ldg(gp + 1);
+              v[0] *= g0.x; v[1] *= g0.y; v[2] *= g0.z; v[3] *= g0.w;
+              v[4] *= g1.x; v[5] *= g1.y; v[6] *= g1.z; v[7] *= g1.w;
+            }
+            if (S.s) {
+              const float4* sp = reinterpret_cast<const float4*>(S.s + pix * p.C + ch);
+              float4 s0 = __ldg(sp), s1 = __ldg(sp + 1);
+              if (S.gs) {
+                const float4* gp = reinterpret_cast<const float4*>(S.gs + (size_t)b * p.C + ch);
+                const float4 g0 = __ldg(gp), g1 = __ldg(gp + 1);
+                s0.x *= g0.x; s0.y *= g0.y; s0.z *= g0.z; s0.w *= g0.w;
+                s1.x *= g1.x; s1.y *= g1.y; s1.z *= g1.z; s1.w *= g1.w;
+              }
+              v[0] += s0.x; v[1] += s0.y; v[2] += s0.z; v[3] += s0.w;
+              v[4] += s1.x; v[5] += s1.y; v[6] += s1.z; v[7] += s1.w;
+            }
+          }
+          float hi[8], lo[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            hi[i] = bf16_round(v[i]);
+            lo[i] = v[i] - hi[i];
+          }
+          uint8_t* dst = sa + (size_t)s * src_bytes + ((size_t)cg8 * p.P_max + qq) * 16;
+          *reinterpret_cast<uint4*>(dst) = make_uint4(pack_bf16x2(hi[0], hi[1]), pack_bf16x2(hi[2], hi[3]),
+                                                      pack_bf16x2(hi[4], hi[5]), pack_bf16x2(hi[6], hi[7]));
+          if (npassA == 2)
+            *reinterpret_cast<uint4*>(dst + (size_t)2 * p.P_max * 16) =
+                make_uint4(pack_bf16x2(lo[0], lo[1]), pack_bf16x2(lo[2], lo[3]),
+                           pack_bf16x2(lo[4], lo[5]), pack_bf16x2(lo[6], lo[7]));
+        }
+        fence_proxy_async_smem();
+        mbar_arrive(smem_u32(&full[stage]));
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    // ===================== MMA issuer (one lane) ========================================
+    if (lane == 0) {
+      const uint32_t idesc = idesc_bf16(N);
+      uint32_t k = 0, ic = 0;
+      const uint32_t src_bytes = (uint32_t)npassA * 2 * p.P_max * 16;
+      const uint32_t lboA = (uint32_t)p.P_max * 16;
+      const uint32_t lboB = (uint32_t)N * 16;
+      const int npassB = d.npass == 3 ? 2 : 1;
+      for (int item = blockIdx.x; item < p.total_items; item += gridDim.x, ++ic) {
+        const int slot = ic % p.slots;
+        const uint32_t sphase = (ic / p.slots) & 1;
+        mbar_wait(smem_u32(&tempty[slot]), sphase ^ 1);
+        tc_fence_after();
+        const uint32_t dslot = tmem_base + (uint32_t)slot * p.slot_cols;
+        uint32_t inited = 0;
+        for (int c = 0; c < n_chunks; ++c, ++k) {
+          const int stage = k % p.stages;
+          const uint32_t phase = (k / p.stages) & 1;
+          mbar_wait(smem_u32(&full[stage]), phase);
+          tc_fence_after();
+          const int pl = c / cgroups;
+          const PlaneTaps& pt = d.planes[pl];
+          const uint32_t sa = smem_u32(a_base + (size_t)stage * p.a_stage_bytes);
+          const uint32_t sb = smem_u32(b_base + (size_t)stage * p.b_stage_bytes);
+          for (int s = 0; s < d.n_src; ++s) {
+            for (int t = 0; t < pt.n; ++t) {
+              const int acc = s * d.n_acc_src + pt.acc[t];
+              const int shift = pt.dy[t] * p.L + pt.dx[t] - pt.lo;
+              const uint32_t b_tap = sb + (uint32_t)((s * pt.n + t) * npassB) * 32u * N;
+              for (int g = 0; g < p.G; ++g) {
+                const uint32_t a_off = sa + s * src_bytes + (uint32_t)(shift + g * 128) * 16u;
+                const uint32_t dcol = dslot + (uint32_t)((g * n_acc + acc) * N);
+                const uint32_t bit = 1u << (g * n_acc + acc);
+                // pass 0: hi*hi
+                tc_mma(dcol, smem_desc(a_off, lboA, 128), smem_desc(b_tap, lboB, 128), idesc,
+                       (inited & bit) ? 1u : 0u);
+                inited |= bit;
+                if (d.npass == 3) {
+                  // pass 1: lo(A)*hi(B); pass 2: hi(A)*lo(B)
+                  tc_mma(dcol, smem_desc(a_off + 2u * lboA, lboA, 128), smem_desc(b_tap, lboB, 128),
+                         idesc, 1u);
+                  tc_mma(dcol, smem_desc(a_off, lboA, 128), smem_desc(b_tap + 32u * N, lboB, 128), idesc,
+                         1u);
+                }
+              }
+            }
+          }
+          tc_commit(smem_u32(&empty[stage]));
+        }
+        tc_commit(smem_u32(&tfull[slot]));
+      }
+    }
+    __syncwarp();
+  } else {
+    // ===================== epilogue warps 4..7 ==========================================
+    const int ew = warp - kProdWarps;  // == warp % 4: TMEM lane quarter
+    const int et = threadIdx.x - kProdThreads;
+    uint32_t ic = 0;
+    const bool dual = d.n_src == 2;
+    for (int item = blockIdx.x; item < p.total_items; item += gridDim.x, ++ic) {
+      const int slot = ic % p.slots;
+      const uint32_t sphase = (ic / p.slots) & 1;
+      const int b = item / p.items_per_image;
+      const int it = item - b * p.items_per_image;
+      const int q0 = it * p.G * 128;
+      mbar_wait(smem_u32(&tfull[slot]), sphase);
+      tc_fence_after();
+      float gsum[N];
+#pragma unroll
+      for (int c = 0; c < N; ++c) gsum[c] = 0.f;
+      const uint32_t trow = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)slot * p.slot_cols;
+      for (int g = 0; g < p.G; ++g) {
+        const int q = q0 + g * 128 + ew * 32 + lane;
+        const int y = q / p.L;
+        const int x = q - y * p.L;
+        const bool valid = y < p.Hp && x < p.Wp;
+        for (int ph = 0; ph < d.n_acc_src; ++ph) {
+          int oy = y, ox = x;
+          if (d.mode == CONVT4_S2) {
+            oy = 2 * y + (ph >> 1);
+            ox = 2 * x + (ph & 1);
+          }
+          float* op = p.out + (((size_t)b * p.Ho + oy) * p.Wo + ox) * N;
+#pragma unroll
+          for (int j = 0; j < N; j += 16) {
+            float a0[16], a1[16];
+            tmem_ld16(trow + (uint32_t)((g * n_acc + ph) * N + j), a0);
+            if (dual) tmem_ld16(trow + (uint32_t)((g * n_acc + d.n_acc_src + ph) * N + j), a1);
+            tmem_wait_ld();
+            float v[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              float t = a0[i] + __ldg(d.bias0 + j + i);
+              if (p.relu0) t = fmaxf(t, 0.f);
+              if (dual) t = t + (a1[i] + __ldg(d.bias1 + j + i));
+              v[i] = t;
+            }
+            if (valid) {
+#pragma unroll
+              for (int i = 0; i < 16; i += 4)
+                *reinterpret_cast<float4*>(op + j + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+#pragma unroll
+              for (int i = 0; i < 16; ++i) gsum[j + i] += v[i];
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(smem_u32(&tempty[slot]));
+      if (p.gap) {
+#pragma unroll
+        for (int c = 0; c < N; ++c) {
+          float s = gsum[c];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+          if (lane == 0) red[ew * N + c] = s;
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+        if (et < N) {
+          const float s = ((red[et] + red[N + et]) + red[2 * N + et]) + red[3 * N + et];
+          p.gap[((size_t)b * p.items_per_image + it) * N + et] = s;
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kMmaWarp) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(p.tmem_cols)
+                 : "memory");
+  }
+}
+
+// ---- host helpers ------------------------------------------------------------------
+uint16_t bf16_bits(float v) {
+  const __nv_bfloat16 h = __float2bfloat16_rn(v);
+  uint16_t r;
+  std::memcpy(&r, &h, 2);
+  return r;
+}
+float bf16_val(float v) { return __bfloat162float(__float2bfloat16_rn(v)); }
+
+// tap tables; wk = index into the canonical per-(co,ci) weight vector
+struct HostTap {
+  int acc, dy, dx, wk;
+};
+
+std::vector<HostTap> plane_taps(int mode, int pl) {
+  std::vector<HostTap> t;
+  if (mode == CONV3_S1) {
+    for (int ky = 0; ky < 3; ++ky)
+      for (int kx = 0; kx < 3; ++kx) t.push_back({0, ky - 1, kx - 1, ky * 3 + kx});
+  } else if (mode == CONV3_S2) {
+    const int py = pl >> 1, px = pl & 1;
+    for (int ky = 0; ky < 3; ++ky)
+      for (int kx = 0; kx < 3; ++kx) {
+        const int dy = ky - 1, dx = kx - 1;
+        const int tpy = dy == 0 ? 0 : 1, tpx = dx == 0 ? 0 : 1;
+        if (tpy != py || tpx != px) continue;
+        t.push_back({0, dy == -1 ? -1 : 0, dx == -1 ? -1 : 0, ky * 3 + kx});
+      }
+  } else {
+    for (int ph = 0; ph < 4; ++ph)
+      for (int a = 0; a < 2; ++a)
+        for (int bb = 0; bb < 2; ++bb) {
+          const int py = ph >> 1, px = ph & 1;
+          t.push_back({ph, py + a - 1, px + bb - 1, ph * 4 + a * 2 + bb});
+        }
+  }
+  return t;
+}
+
+template <int N>
+void launch_n(const Params& p, int grid, size_t smem, cudaStream_t st) {
+  auto kern = tc_conv_kernel<N>;
+  static uint64_t configured = 0;
+  int dev = 0;
+  STDA_CUDA(cudaGetDevice(&dev));
+  if (!(configured >> (dev & 63) & 1)) {
+    STDA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+    configured |= 1ull << (dev & 63);
+  }
+  kern<<<grid, kThreads, smem, st>>>(p);
+  check_launch("tc_conv_kernel");
+}
+
+}  // namespace
+
+bool tc_supported(int mode, int cin, int cout) {
+  (void)mode;
+  return cin % 16 == 0 && cin >= 16 && cin <= 64 && (cout == 16 || cout == 32 || cout == 64);
+}
+
+void tc_pack_layer(TcLayerDesc& d, int mode, int cin, int cout, const float* w0, const float* w1,
+                   bool bf16, std::vector<uint16_t>& packed) {
+  STDA_CHECK(tc_supported(mode, cin, cout), "layer shape not supported by the tensor-core path");
+  std::memset(&d, 0, sizeof(d));
+  d.mode = mode;
+  d.n_src = w1 ? 2 : 1;
+  d.cin = cin;
+  d.cout = cout;
+  d.n_planes = mode == CONV3_S2 ? 4 : 1;
+  d.n_acc_src = mode == CONVT4_S2 ? 4 : 1;
+  d.npass = bf16 ? 1 : 3;
+  const int npassB = bf16 ? 1 : 2;
+  const int wk_per = mode == CONVT4_S2 ? 16 : 9;
+  std::vector<std::vector<HostTap>> taps(d.n_planes);
+  for (int pl = 0; pl < d.n_planes; ++pl) {
+    taps[pl] = plane_taps(mode, pl);
+    PlaneTaps& pt = d.planes[pl];
+    pt.n = (int8_t)taps[pl].size();
+    for (size_t t = 0; t < taps[pl].size(); ++t) {
+      pt.acc[t] = (int8_t)taps[pl][t].acc;
+      pt.dy[t] = (int8_t)taps[pl][t].dy;
+      pt.dx[t] = (int8_t)taps[pl][t].dx;
+    }
+  }
+  const int cgroups = cin / 16;
+  const int n_chunks = d.n_planes * cgroups;
+  STDA_CHECK(n_chunks <= kMaxChunks, "too many K chunks");
+  packed.clear();
+  d.chunk_off[0] = 0;
+  const float* ws[2] = {w0, w1};
+  for (int c = 0; c < n_chunks; ++c) {
+    const int pl = c / cgroups, cgi = c % cgroups;
+    for (int s = 0; s < d.n_src; ++s)
+      for (const HostTap& t : taps[pl])
+        for (int pass = 0; pass < npassB; ++pass)
+          for (int kg = 0; kg < 2; ++kg)
+            for (int n = 0; n < cout; ++n)
+              for (int e = 0; e < 8; ++e) {
+                const int ci = cgi * 16 + kg * 8 + e;
+                const float v = ws[s][((size_t)n * cin + ci) * wk_per + t.wk];
+                const float hi = bf16_val(v);
+                packed.push_back(bf16_bits(pass == 0 ? v : v - hi));
+              }
+    d.chunk_off[c + 1] = (int64_t)packed.size() * 2;
+  }
+}
+
+TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W) {
+  TcGeometry g{};
+  g.B = B;
+  g.H = H;
+  g.W = W;
+  if (d.mode == CONV3_S2) {
+    g.Hp = H / 2;
+    g.Wp = W / 2;
+    g.Ho = H / 2;
+    g.Wo = W / 2;
+  } else if (d.mode == CONVT4_S2) {
+    g.Hp = H;
+    g.Wp = W;
+    g.Ho = 2 * H;
+    g.Wo = 2 * W;
+  } else {
+    g.Hp = H;
+    g.Wp = W;
+    g.Ho = H;
+    g.Wo = W;
+  }
+  g.L = g.Wp + 1;
+  int span = 0;
+  for (int pl = 0; pl < d.n_planes; ++pl) {
+    PlaneTaps& pt = d.planes[pl];
+    int lo = 1 << 30, hi = -(1 << 30);
+    for (int t = 0; t < pt.n; ++t) {
+      const int sft = pt.dy[t] * g.L + pt.dx[t];
+      lo = std::min(lo, sft);
+      hi = std::max(hi, sft);
+    }
+    pt.lo = (int16_t)lo;
+    pt.hi = (int16_t)hi;
+    span = std::max(span, hi - lo);
+  }
+  const int n_acc = d.n_src * d.n_acc_src;
+  const int npassA = d.npass == 3 ? 2 : 1;
+  uint32_t b_stage = 0;
+  for (int c = 0; c < d.n_planes * (d.cin / 16); ++c)
+    b_stage = std::max<uint32_t>(b_stage, (uint32_t)(d.chunk_off[c + 1] - d.chunk_off[c]));
+  const size_t fixed = 1024 + 64 + 4 * 64 * sizeof(float);
+  // largest G (M-tiles per item) with a >= 2-deep smem pipeline; else 1 stage at G = 1
+  bool ok = false;
+  for (int want_stages : {2, 1}) {
+    for (int G : {4, 2, 1}) {
+      const int P8 = (G * 128 + span + 7) / 8 * 8;
+      const uint32_t a_stage = (uint32_t)d.n_src * npassA * 2 * P8 * 16;
+      const int acc_cols = G * n_acc * d.cout;
+      if (acc_cols > 512 || G * n_acc > 32) continue;
+      int stages = 0;
+      for (int st : {3, 2, 1})
+        if ((size_t)st * (a_stage + b_stage) + fixed <= (size_t)kMaxSmem) {
+          stages = st;
+          break;
+        }
+      if (stages < want_stages) continue;
+      g.G = G;
+      g.P_max = P8;
+      g.stages = stages;
+      g.slots = 2 * acc_cols <= 512 ? 2 : 1;
+      g.a_stage_bytes = a_stage;
+      g.b_stage_bytes = b_stage;
+      g.smem_bytes = (size_t)stages * (a_stage + b_stage) + fixed;
+      int cols = 32;
+      while (cols < g.slots * acc_cols) cols *= 2;
+      g.tmem_cols = cols;
+      ok = true;
+      break;
+    }
+    if (ok) break;
+  }
+  STDA_CHECK(ok, "tensor-core conv: no tiling fits shared memory");
+  const int positions = g.Hp * g.L;
+  g.items_per_image = cdiv(positions, g.G * 128);
+  return g;
+}
+
+void tc_launch(const TcLayerDesc& d, const TcGeometry& g, const TcSrc& src0, const TcSrc* src1,
+               float* out, float* gap, bool relu0, cudaStream_t st) {
+  Params p;
+  std::memset(&p, 0, sizeof(p));
+  p.d = d;
+  p.src[0] = src0;
+  if (src1) p.src[1] = *src1;
+  STDA_CHECK((src1 != nullptr) == (d.n_src == 2), "source count mismatch");
+  p.out = out;
+  p.gap = gap;
+  p.H = g.H;
+  p.W = g.W;
+  p.C = d.cin;
+  p.Hp = g.Hp;
+  p.Wp = g.Wp;
+  p.L = g.L;
+  p.Ho = g.Ho;
+  p.Wo = g.Wo;
+  p.G = g.G;
+  p.stages = g.stages;
+  p.slots = g.slots;
+  p.items_per_image = g.items_per_image;
+  p.total_items = g.B * g.items_per_image;
+  p.P_max = g.P_max;
+  p.a_stage_bytes = g.a_stage_bytes;
+  p.b_stage_bytes = g.b_stage_bytes;
+  p.slot_cols = (uint32_t)(g.G * d.n_src * d.n_acc_src * d.cout);
+  p.tmem_cols = (uint32_t)g.tmem_cols;
+  p.relu0 = relu0 ? 1 : 0;
+  if (p.total_items == 0) return;
+  int dev = 0, sms = 148;
+  STDA_CUDA(cudaGetDevice(&dev));
+  STDA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int grid = std::min(p.total_items, sms);
+  switch (d.cout) {
+    case 16: return launch_n<16>(p, grid, g.smem_bytes, st);
+    case 32: return launch_n<32>(p, grid, g.smem_bytes, st);
+    case 64: return launch_n<64>(p, grid, g.smem_bytes, st);
+  }
+  throw Error{"unsupported cout for the tensor-core path"};
+}
+
+}  // namespace tc
+}  // namespace stda
