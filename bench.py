@@ -323,9 +323,10 @@ def run_engine(args, world, rank, local):
             "unit": "TFLOP/s", "frac": achieved / bf16, "traffic": None,
             "peak_kind": f"{peak_kind} dense bf16",
             "flops_per_launch": flops_per_launch, "launch_ms": share[dom],
-            "executed": "fp32 SIMT (FFMA)" if args.precision == "fp32" else "bf16-rounded operands on fp32 SIMT",
-            "fp32_simt_peak_derived_tflops": 74.4,
-            "frac_of_fp32_simt": achieved / 74.4,
+            "executed": ("tcgen05 kind::f16, 3xBF16 split (hi*hi+lo*hi+hi*lo), fp32 accumulate in TMEM"
+                         if args.precision == "fp32" else "tcgen05 kind::f16, bf16 operands, fp32 accumulate"),
+            "mma_passes": 3 if args.precision == "fp32" else 1,
+            "frac_of_split_roof": achieved * (3 if args.precision == "fp32" else 1) / bf16,
             "whole_forward_tflops": total_flops * batch / (ms_per_step * 1e-3) / 1e12,
             "hbm_fraction": (16 * H * W * batch) / (ms_per_step * 1e-3) / (hbm * 1e9),
             "launch_share": {n: m / sum(avg) for n, m in share.items()},

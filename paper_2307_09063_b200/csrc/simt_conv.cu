@@ -68,9 +68,18 @@ __device__ __forceinline__ void stage_tile(float* tile, const Src& s, int64_t b,
                                            int Hi, int Wi, int iy0, int ix0, bool bf16) {
   using G = Geo<MODE>;
   constexpr int PER_CH = G::IH * G::IW;
+  // NCHW sources: x fastest (coalesced rows); NHWC sources: channel fastest (coalesced
+  // pixels).  Both visit every (ci, r, c) of the tile exactly once.
+  const bool chan_fast = s.xc == 1;
   for (int e = threadIdx.x; e < CICH * PER_CH; e += kThreads) {
-    const int ci = e / PER_CH;
-    const int rem = e - ci * PER_CH;
+    int ci, rem;
+    if (chan_fast) {
+      rem = e / CICH;
+      ci = e - rem * CICH;
+    } else {
+      ci = e / PER_CH;
+      rem = e - ci * PER_CH;
+    }
     const int r = rem / G::IW;
     const int c = rem - r * G::IW;
     const int iy = iy0 + r, ix = ix0 + c;
@@ -232,6 +241,8 @@ __global__ void __launch_bounds__(kThreads, 2) conv_simt_kernel(Args a) {
   }
   const int ox = ox0 + lane;
   float gsum[COB];
+  // NHWC output with a full channel block per pixel: contiguous float4 stores
+  const bool vec_store = COB % 4 == 0 && a.ol.oc == 1 && (blk + 1) * COB <= a.Cout;
 #pragma unroll
   for (int q = 0; q < COB; ++q) {
     const int co = blk * COB + q;
@@ -244,10 +255,22 @@ __global__ void __launch_bounds__(kThreads, 2) conv_simt_kernel(Args a) {
       float v = acc0[r][q] + bias0;
       if (a.relu0) v = fmaxf(v, 0.f);
       if (DUAL) v = v + (acc1[r][q] + bias1);
+      acc0[r][q] = v;
       if (oy[r] < a.Ho && ox < a.Wo) {
-        a.out[b * a.ol.ob + co * a.ol.oc + ((int64_t)oy[r] * a.Wo + ox) * a.ol.op] = v;
+        if (!vec_store) a.out[b * a.ol.ob + co * a.ol.oc + ((int64_t)oy[r] * a.Wo + ox) * a.ol.op] = v;
         gsum[q] += v;
       }
+    }
+  }
+  if (vec_store) {
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      if (oy[r] >= a.Ho || ox >= a.Wo) continue;
+      float* op = a.out + b * a.ol.ob + blk * COB + ((int64_t)oy[r] * a.Wo + ox) * a.ol.op;
+#pragma unroll
+      for (int q = 0; q < COB; q += 4)
+        *reinterpret_cast<float4*>(op + q) =
+            make_float4(acc0[r][q], acc0[r][q + 1], acc0[r][q + 2], acc0[r][q + 3]);
     }
   }
   if (a.gap) {

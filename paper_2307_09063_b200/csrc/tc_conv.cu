@@ -9,9 +9,10 @@ namespace tc {
 
 namespace {
 
-constexpr int kProdWarps = 4;
-constexpr int kEpiWarps = 4;
-constexpr int kMmaWarp = kProdWarps + kEpiWarps;  // warp 8
+constexpr int kProdWarps = 8;
+constexpr int kEpiWarps = 4;                      // warps 8..11: warp % 4 = TMEM lane quarter
+constexpr int kMmaWarp = kProdWarps + kEpiWarps;  // warp 12
+constexpr int kUnroll = 4;                        // producer loads in flight per thread
 constexpr int kThreads = (kProdWarps + kEpiWarps + 1) * 32;
 constexpr int kProdThreads = kProdWarps * 32;
 constexpr int kMaxSmem = 227 * 1024;
@@ -117,11 +118,6 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int n) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((128u >> 4) << 24);
 }
 
-__device__ __forceinline__ int floor_div(int a, int b) {
-  int q = a / b;
-  return (a % b != 0 && ((a < 0) != (b < 0))) ? q - 1 : q;
-}
-
 __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
   const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<const uint32_t*>(&h);
@@ -194,63 +190,84 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
         const int py = pl >> 1, px = pl & 1;
         uint8_t* sa = a_base + (size_t)stage * p.a_stage_bytes;
         const uint32_t src_bytes = (uint32_t)npassA * 2 * p.P_max * 16;
-        const int total = d.n_src * 2 * P;
-        for (int e = tid; e < total; e += kProdThreads) {
-          const int s = e / (2 * P);
-          const int r = e - s * 2 * P;
-          const int cg8 = r / P;
-          const int qq = r - cg8 * P;
-          const int q = q0 + pt.lo + qq;
-          const int y = floor_div(q, p.L);
-          const int x = q - y * p.L;
-          float v[8];
+        // each thread owns one (source, 8-channel group) and strides over positions;
+        // kUnroll positions' global loads are issued before any is consumed (MLP)
+        const int groups = d.n_src * 2;
+        const int tpg = kProdThreads / groups;
+        const int grp = tid / tpg, t0 = tid - grp * tpg;
+        const int s = grp >> 1, cg8 = grp & 1;
+        const int ch = cgi * 16 + cg8 * 8;
+        const TcSrc& S = p.src[s];
+        float gx[8], gs[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) v[i] = 0.f;
-          if (y >= 0 && y < p.Hp && x < p.Wp) {
-            int iy = y, ix = x;
-            if (d.mode == CONV3_S2) {
-              iy = 2 * y + py;
-              ix = 2 * x + px;
-            }
-            const int ch = cgi * 16 + cg8 * 8;
-            const TcSrc& S = p.src[s];
-            const size_t pix = ((size_t)b * p.H + iy) * p.W + ix;
-            const float4* xp = reinterpret_cast<const float4*>(S.x + pix * p.C + ch);
-            float4 a0 = __ldg(xp), a1 = __ldg(xp + 1);
-            v[0] = a0.x; v[1] = a0.y; v[2] = a0.z; v[3] = a0.w;
-            v[4] = a1.x; v[5] = a1.y; v[6] = a1.z; v[7] = a1.w;
-            if (S.gx) {
-              const float4* gp = reinterpret_cast<const float4*>(S.gx + (size_t)b * p.C + ch);
-              const float4 g0 = __ldg(gp), g1 = __ldg(gp + 1);
-              v[0] *= g0.x; v[1] *= g0.y; v[2] *= g0.z; v[3] *= g0.w;
-              v[4] *= g1.x; v[5] *= g1.y; v[6] *= g1.z; v[7] *= g1.w;
-            }
-            if (S.s) {
-              const float4* sp = reinterpret_cast<const float4*>(S.s + pix * p.C + ch);
-              float4 s0 = __ldg(sp), s1 = __ldg(sp + 1);
-              if (S.gs) {
-                const float4* gp = reinterpret_cast<const float4*>(S.gs + (size_t)b * p.C + ch);
-                const float4 g0 = __ldg(gp), g1 = __ldg(gp + 1);
-                s0.x *= g0.x; s0.y *= g0.y; s0.z *= g0.z; s0.w *= g0.w;
-                s1.x *= g1.x; s1.y *= g1.y; s1.z *= g1.z; s1.w *= g1.w;
+        for (int i = 0; i < 8; ++i) gx[i] = gs[i] = 1.f;
+        if (S.gx) {
+          const float4 g0 = __ldg(reinterpret_cast<const float4*>(S.gx + (size_t)b * p.C + ch));
+          const float4 g1 = __ldg(reinterpret_cast<const float4*>(S.gx + (size_t)b * p.C + ch) + 1);
+          gx[0] = g0.x; gx[1] = g0.y; gx[2] = g0.z; gx[3] = g0.w;
+          gx[4] = g1.x; gx[5] = g1.y; gx[6] = g1.z; gx[7] = g1.w;
+        }
+        if (S.gs) {
+          const float4 g0 = __ldg(reinterpret_cast<const float4*>(S.gs + (size_t)b * p.C + ch));
+          const float4 g1 = __ldg(reinterpret_cast<const float4*>(S.gs + (size_t)b * p.C + ch) + 1);
+          gs[0] = g0.x; gs[1] = g0.y; gs[2] = g0.z; gs[3] = g0.w;
+          gs[4] = g1.x; gs[5] = g1.y; gs[6] = g1.z; gs[7] = g1.w;
+        }
+        uint8_t* dst_base = sa + (size_t)s * src_bytes + (size_t)cg8 * p.P_max * 16;
+        const size_t img = (size_t)b * p.H;
+        for (int base = t0; base < P; base += kUnroll * tpg) {
+          float4 xa[kUnroll][2], sk[kUnroll][2];
+          bool ok[kUnroll];
+#pragma unroll
+          for (int u = 0; u < kUnroll; ++u) {
+            const int qq = base + u * tpg;
+            const int q = q0 + pt.lo + qq;
+            const int y = (int)((unsigned)(q + p.L) / (unsigned)p.L) - 1;  // q >= -L
+            const int x = q - y * p.L;
+            ok[u] = qq < P && y >= 0 && y < p.Hp && x < p.Wp;
+            xa[u][0] = xa[u][1] = sk[u][0] = sk[u][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (ok[u]) {
+              int iy = y, ix = x;
+              if (d.mode == CONV3_S2) {
+                iy = 2 * y + py;
+                ix = 2 * x + px;
               }
-              v[0] += s0.x; v[1] += s0.y; v[2] += s0.z; v[3] += s0.w;
-              v[4] += s1.x; v[5] += s1.y; v[6] += s1.z; v[7] += s1.w;
+              const size_t off = ((img + iy) * p.W + ix) * p.C + ch;
+              const float4* xp = reinterpret_cast<const float4*>(S.x + off);
+              xa[u][0] = __ldg(xp);
+              xa[u][1] = __ldg(xp + 1);
+              if (S.s) {
+                const float4* sp = reinterpret_cast<const float4*>(S.s + off);
+                sk[u][0] = __ldg(sp);
+                sk[u][1] = __ldg(sp + 1);
+              }
             }
           }
-          float hi[8], lo[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            hi[i] = bf16_round(v[i]);
-            lo[i] = v[i] - hi[i];
+          for (int u = 0; u < kUnroll; ++u) {
+            const int qq = base + u * tpg;
+            if (qq >= P) break;
+            const float xv[8] = {xa[u][0].x, xa[u][0].y, xa[u][0].z, xa[u][0].w,
+                                 xa[u][1].x, xa[u][1].y, xa[u][1].z, xa[u][1].w};
+            const float sv[8] = {sk[u][0].x, sk[u][0].y, sk[u][0].z, sk[u][0].w,
+                                 sk[u][1].x, sk[u][1].y, sk[u][1].z, sk[u][1].w};
+            float hi[8], lo[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              // value = x*gx (+ skip*gs): the reference's eca(x) + skip rounding order
+              float v = xv[i] * gx[i];
+              if (S.s) v = v + sv[i] * gs[i];
+              hi[i] = bf16_round(v);
+              lo[i] = v - hi[i];
+            }
+            uint8_t* dst = dst_base + (size_t)qq * 16;
+            *reinterpret_cast<uint4*>(dst) = make_uint4(pack_bf16x2(hi[0], hi[1]), pack_bf16x2(hi[2], hi[3]),
+                                                        pack_bf16x2(hi[4], hi[5]), pack_bf16x2(hi[6], hi[7]));
+            if (npassA == 2)
+              *reinterpret_cast<uint4*>(dst + (size_t)2 * p.P_max * 16) =
+                  make_uint4(pack_bf16x2(lo[0], lo[1]), pack_bf16x2(lo[2], lo[3]),
+                             pack_bf16x2(lo[4], lo[5]), pack_bf16x2(lo[6], lo[7]));
           }
-          uint8_t* dst = sa + (size_t)s * src_bytes + ((size_t)cg8 * p.P_max + qq) * 16;
-          *reinterpret_cast<uint4*>(dst) = make_uint4(pack_bf16x2(hi[0], hi[1]), pack_bf16x2(hi[2], hi[3]),
-                                                      pack_bf16x2(hi[4], hi[5]), pack_bf16x2(hi[6], hi[7]));
-          if (npassA == 2)
-            *reinterpret_cast<uint4*>(dst + (size_t)2 * p.P_max * 16) =
-                make_uint4(pack_bf16x2(lo[0], lo[1]), pack_bf16x2(lo[2], lo[3]),
-                           pack_bf16x2(lo[4], lo[5]), pack_bf16x2(lo[6], lo[7]));
         }
         fence_proxy_async_smem();
         mbar_arrive(smem_u32(&full[stage]));

@@ -17,10 +17,10 @@
 // fp32 parity: activations and weights are split into bf16 hi + lo parts and each
 // product is formed as hi*hi + lo*hi + hi*lo (3 MMAs, fp32 accumulation in TMEM).
 //
-// Roles (288 threads): warps 0-3 stage A (fp32 NHWC global -> gate/skip transform ->
+// Roles (416 threads): warps 0-7 stage A (fp32 NHWC global -> gate/skip transform ->
 // bf16 hi/lo core-matrix layout in smem) and thread 0 bulk-copies the packed weights
-// (cp.async.bulk + mbarrier tx); warp 8 allocates TMEM and one lane issues every
-// tcgen05.mma; warps 4-7 drain TMEM (tcgen05.ld) into bias/relu/dual epilogues, NHWC
+// (cp.async.bulk + mbarrier tx); warp 12 allocates TMEM and one lane issues every
+// tcgen05.mma; warps 8-11 drain TMEM (tcgen05.ld) into bias/relu/dual epilogues, NHWC
 // stores and per-item channel sums for ECA.  mbarrier pipelines: smem stages
 // (full/empty) and TMEM accumulator slots (full/empty).  Persistent CTAs.
 #pragma once
