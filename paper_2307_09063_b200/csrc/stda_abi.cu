@@ -22,6 +22,7 @@
 #include "common.cuh"
 #include "simt_conv.cuh"
 #include "tc_conv.cuh"
+#include "edge_conv.cuh"
 
 namespace stda {
 
@@ -140,6 +141,7 @@ struct stda_plan {
   }
 
   bool use_tc = false;  // every encoder/decoder conv runs on the tcgen05 kernel
+  float* head_wt = nullptr;  // head weights [9][c0] for the NHWC head kernel
 };
 
 namespace {
@@ -240,8 +242,7 @@ void run_net_tc(const stda_plan& p, const Src& x, float* y, int64_t B, const Net
   const bool bf = p.bf16;
   int h = c.map_height, wd = c.map_width;
   mk.mark(st);
-  const OutLayout s_layout = OutLayout::nhwc(c0, h, wd);
-  launch_conv(p.stem, nullptr, x, nullptr, w.s, nullptr, B, h, wd, true, bf, st, &s_layout);
+  launch_stem_nhwc(p.stem.w, p.stem.b, x, c.input_frames, c0, w.s, B, h, wd, bf, st);
   mk.mark(st);
   tc::TcSrc cur;
   cur.x = w.s;
@@ -288,15 +289,8 @@ void run_net_tc(const stda_plan& p, const Src& x, float* y, int64_t B, const Net
     cur.s = sk.x;
     cur.gs = sk.gx;
   }
-  // head reads NHWC d*g + skip through the SIMT source transform
-  Src hs = nhwc_src(cur.x, c0, h, wd);
-  hs.gx = cur.gx;
-  hs.s = cur.s;
-  hs.sb = (int64_t)c0 * h * wd;
-  hs.sc = 1;
-  hs.sp = c0;
-  hs.gs = cur.gs;
-  launch_conv(p.head, nullptr, hs, nullptr, y, nullptr, B, h, wd, false, bf, st);
+  // head reads the NHWC d*g + skip on the fly
+  launch_head_nhwc(p.head_wt, p.head.b, cur.x, cur.gx, cur.s, cur.gs, c0, y, B, h, wd, bf, st);
   mk.mark(st);
 }
 
@@ -458,6 +452,15 @@ int stda_plan_create(const stda_config* cfg, const float* blob, size_t n_floats,
       }
       D.eca = p->make_vec(k, src);
       p->dec.push_back(D);
+    }
+    if (p->use_tc) {
+      std::vector<float> wt(9 * (size_t)c0);
+      for (int ci = 0; ci < c0; ++ci)
+        for (int t = 0; t < 9; ++t) {
+          const float v = src[(size_t)ci * 9 + t];
+          wt[(size_t)t * c0 + ci] = p->bf16 ? __bfloat162float(__float2bfloat16_rn(v)) : v;
+        }
+      p->head_wt = p->upload(wt);
     }
     p->head = p->make_layer(CONV3_S1, c0, 1, src);
     STDA_CHECK((size_t)(src - blob) == n_floats, "internal: blob parse mismatch");
