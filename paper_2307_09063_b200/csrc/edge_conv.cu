@@ -14,12 +14,13 @@ namespace {
 constexpr int kTH = 8, kTW = 64, kThreads = 256;
 constexpr int kIH = kTH + 2, kIW = kTW + 2;  // staged halo tile
 
-// stem: x (Src: NCHW or window strides) -> s NHWC [B][H][W][C0], relu.
+// stem: x (Src: NCHW or window strides) -> relu(conv) written as operand planes:
+// PL over H x W (stage-1 conv input) and PP phase planes (stage-2 residual input).
 // weights: SIMT layout with cob = 16: [blk][ci][tap][16], bias [C0].
-__global__ void __launch_bounds__(kThreads) stem_nhwc_kernel(const float* __restrict__ w,
-                                                             const float* __restrict__ bias, Src x,
-                                                             int F, int C0, float* __restrict__ out,
-                                                             int H, int W, int bf16, int64_t b_base) {
+__global__ void __launch_bounds__(kThreads) stem_planes_kernel(const float* __restrict__ w,
+                                                               const float* __restrict__ bias, Src x,
+                                                               int F, int C0, PlBuf pl, PlBuf pp,
+                                                               int H, int W, int bf16, int64_t b_base) {
   extern __shared__ __align__(16) float sm[];
   float* xs = sm;                       // [F][kIH][kIW]
   float* ws = xs + F * kIH * kIW;       // [F][9][16]
@@ -79,12 +80,14 @@ __global__ void __launch_bounds__(kThreads) stem_nhwc_kernel(const float* __rest
     for (int pr = 0; pr < 2; ++pr) {
       const int oy = ty0 + r0 + 4 * pr;
       if (oy >= H || ox >= W) continue;
-      float* op = out + (((size_t)b * H + oy) * W + ox) * C0 + blk * 16;
 #pragma unroll
-      for (int q = 0; q < 16; q += 4)
-        *reinterpret_cast<float4*>(op + q) =
-            make_float4(fmaxf(acc[pr][q], 0.f), fmaxf(acc[pr][q + 1], 0.f), fmaxf(acc[pr][q + 2], 0.f),
-                        fmaxf(acc[pr][q + 3], 0.f));
+      for (int h = 0; h < 2; ++h) {
+        float v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = fmaxf(acc[pr][8 * h + i], 0.f);
+        pl_store8(pl, b, 0, 2 * blk + h, oy * pl.L + ox, v);
+        pl_store8(pp, b, (oy & 1) * 2 + (ox & 1), 2 * blk + h, (oy >> 1) * pp.L + (ox >> 1), v);
+      }
     }
   }
 }
@@ -116,8 +119,11 @@ __global__ void __launch_bounds__(kThreads) head_nhwc_kernel(const float* __rest
     if (iy >= 0 && iy < H && ix >= 0 && ix < W) {
       const size_t off = (((size_t)b * H + iy) * W + ix) * C0 + 4 * j;
       const float4 dv = __ldg(reinterpret_cast<const float4*>(d + off));
-      const float4 gv = __ldg(reinterpret_cast<const float4*>(g + (size_t)b * C0 + 4 * j));
-      u = make_float4(dv.x * gv.x, dv.y * gv.y, dv.z * gv.z, dv.w * gv.w);
+      u = dv;
+      if (g) {
+        const float4 gv = __ldg(reinterpret_cast<const float4*>(g + (size_t)b * C0 + 4 * j));
+        u = make_float4(dv.x * gv.x, dv.y * gv.y, dv.z * gv.z, dv.w * gv.w);
+      }
       if (s) {
         float4 sv = __ldg(reinterpret_cast<const float4*>(s + off));
         if (gs) {
@@ -172,15 +178,16 @@ void set_smem(K kern, size_t bytes) {
 
 }  // namespace
 
-void launch_stem_nhwc(const float* w, const float* bias, const Src& x, int F, int C0, float* s,
-                      int64_t B, int H, int W, bool bf16, cudaStream_t st) {
+void launch_stem_planes(const float* w, const float* bias, const Src& x, int F, int C0,
+                        const PlBuf& pl, const PlBuf& pp, int64_t B, int H, int W, bool bf16,
+                        cudaStream_t st) {
   STDA_CHECK(C0 % 16 == 0, "stem kernel needs stem_channels % 16 == 0");
   const size_t smem = sizeof(float) * (F * kIH * kIW + F * 144);
-  set_smem(stem_nhwc_kernel, smem);
+  set_smem(stem_planes_kernel, smem);
   for (int64_t b0 = 0; b0 < B; b0 += 65535) {
     dim3 grid(cdiv(W, kTW), cdiv(H, kTH), (unsigned)std::min<int64_t>(65535, B - b0));
-    stem_nhwc_kernel<<<grid, kThreads, smem, st>>>(w, bias, x, F, C0, s, H, W, bf16, b0);
-    check_launch("stem_nhwc_kernel");
+    stem_planes_kernel<<<grid, kThreads, smem, st>>>(w, bias, x, F, C0, pl, pp, H, W, bf16, b0);
+    check_launch("stem_planes_kernel");
   }
 }
 

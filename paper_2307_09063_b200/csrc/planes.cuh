@@ -1,0 +1,125 @@
+// Operand planes: the HBM layout every tcgen05 convolution reads its A operand from.
+//
+// A tensor of C channels over an Hp x Wp grid is stored, per image, as the grid
+// linearised with row stride L = Wp + 1 (the extra column is an always-zero pad), split
+// into bf16 hi (+ lo) parts, in UMMA K-major core-matrix order:
+//
+//     elem(b, plane, cg16, pass, cg8, q, e) =
+//         base[b*img_stride + plane*plane_stride + (((cg16*np + pass)*2 + cg8)*Q + q + off)*8 + e]
+//
+// q = y*L + x (x = Wp is the pad column), e = channel within the 8-channel group.
+// Because channels of one 8-group are 16 contiguous bytes and positions are contiguous,
+// the A tile of any 128-row M-tile and tap is ONE contiguous byte range per (pass, cg8):
+// the producer is a handful of cp.async.bulk copies, no conversion.
+//   planes = 1 ("PL"): the grid itself (stride-1 convs, transposed convs, skips);
+//   planes = 4 ("PP"): phase planes (py, px) of a 2Hp x 2Wp tensor, plane = py*2 + px,
+//                      (y, x) <-> source pixel (2y+py, 2x+px) (stride-2 conv inputs).
+// Borders that taps can reach — rows -1 and Hp (with margins) and the pad column — are
+// zeroed once per forward (launch_zero_borders); positions past row Hp are only ever read
+// into discarded (junk) output rows.
+#pragma once
+
+#include "common.cuh"
+
+namespace stda {
+
+struct PlBuf {
+  uint16_t* base = nullptr;
+  int planes = 1;
+  int Hp = 0, Wp = 0, L = 0;
+  int C = 0;   // multiple of 16
+  int np = 2;  // 2: hi + lo (fp32 contract), 1: bf16
+  int Q = 0;   // positions per (cg16, pass, cg8) block
+  int off = 0; // position q is stored at index q + off
+  int64_t plane_stride = 0, img_stride = 0;  // in bf16 elements
+
+  __host__ __device__ size_t block_index(int cg16, int pass, int cg8) const {
+    return (size_t)((cg16 * np + pass) * 2 + cg8) * Q;
+  }
+};
+
+// Margins: taps reach q >= -L-1 (kept >= -off), tiles reach q < Hp*L + 4*128 + L + 1.
+inline PlBuf make_plbuf(int planes, int Hp, int Wp, int C, int np) {
+  PlBuf p;
+  p.planes = planes;
+  p.Hp = Hp;
+  p.Wp = Wp;
+  p.L = Wp + 1;
+  p.C = C;
+  p.np = np;
+  p.off = p.L + 8;
+  p.Q = (p.off + Hp * p.L + 4 * 128 + p.L + 16 + 7) / 8 * 8;
+  p.plane_stride = (int64_t)(C / 16) * np * 2 * p.Q * 8;
+  p.img_stride = p.plane_stride * planes;
+  return p;
+}
+
+inline size_t plbuf_bytes(const PlBuf& p, int64_t B) { return (size_t)B * p.img_stride * 2; }
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+// Write 8 channels (one cg8) of position (b, plane, q): hi and, when np == 2, lo.
+__device__ __forceinline__ void pl_store8(const PlBuf& p, int64_t b, int plane, int c8, int q,
+                                          const float (&v)[8]) {
+  const int cg16 = c8 >> 1, cg8 = c8 & 1;
+  uint16_t* img = p.base + b * p.img_stride + (int64_t)plane * p.plane_stride;
+  float hi[8], lo[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    hi[i] = bf16_round(v[i]);
+    lo[i] = v[i] - hi[i];
+  }
+  uint16_t* dh = img + (p.block_index(cg16, 0, cg8) + q + p.off) * 8;
+  *reinterpret_cast<uint4*>(dh) = make_uint4(pack_bf16x2(hi[0], hi[1]), pack_bf16x2(hi[2], hi[3]),
+                                             pack_bf16x2(hi[4], hi[5]), pack_bf16x2(hi[6], hi[7]));
+  if (p.np == 2) {
+    uint16_t* dl = img + (p.block_index(cg16, 1, cg8) + q + p.off) * 8;
+    *reinterpret_cast<uint4*>(dl) = make_uint4(pack_bf16x2(lo[0], lo[1]), pack_bf16x2(lo[2], lo[3]),
+                                               pack_bf16x2(lo[4], lo[5]), pack_bf16x2(lo[6], lo[7]));
+  }
+}
+
+// Read back 8 channels as fp32 (hi + lo).
+__device__ __forceinline__ void pl_load8(const PlBuf& p, int64_t b, int plane, int c8, int q,
+                                         float (&v)[8]) {
+  const int cg16 = c8 >> 1, cg8 = c8 & 1;
+  const uint16_t* img = p.base + b * p.img_stride + (int64_t)plane * p.plane_stride;
+  const uint4 h = __ldg(reinterpret_cast<const uint4*>(img + (p.block_index(cg16, 0, cg8) + q + p.off) * 8));
+  const __nv_bfloat162* hb = reinterpret_cast<const __nv_bfloat162*>(&h);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = __bfloat1622float2(hb[i]);
+    v[2 * i] = f.x;
+    v[2 * i + 1] = f.y;
+  }
+  if (p.np == 2) {
+    const uint4 l = __ldg(reinterpret_cast<const uint4*>(img + (p.block_index(cg16, 1, cg8) + q + p.off) * 8));
+    const __nv_bfloat162* lb = reinterpret_cast<const __nv_bfloat162*>(&l);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __bfloat1622float2(lb[i]);
+      v[2 * i] += f.x;
+      v[2 * i + 1] += f.y;
+    }
+  }
+}
+
+constexpr int kMaxZeroBufs = 16;
+struct ZeroList {
+  PlBuf buf[kMaxZeroBufs];
+  int n = 0;
+};
+// zero every tap-reachable border position of each listed buffer (all images)
+void launch_zero_borders(const ZeroList& zl, int64_t B, cudaStream_t st);
+
+// ECA gate for image b computed from GAP partials, then applied:
+//   v = x * g (+ skip)   x: NHWC fp32 [B][H][W][C]; skip: PL over H x W (or null)
+// written to any of: PL over H x W, PP over (H/2 x W/2) planes, NHWC fp32.
+void launch_gate_apply(const float* gap, int items, const float* eca_w, int k, const float* x,
+                       const PlBuf* skip, const PlBuf* out_pl, const PlBuf* out_pp, float* out_f32,
+                       int64_t B, int C, int H, int W, cudaStream_t st);
+
+}  // namespace stda

@@ -177,6 +177,9 @@ struct NetWs {
   float* s = nullptr;
   float* m = nullptr;
   std::vector<float*> e, ge, pe, d, gd, pd;
+  // tensor-core path: operand planes
+  PlBuf pl_s, pp_s;
+  std::vector<PlBuf> pl_a, pp_a, pl_b, pl_m;
   size_t bytes = 0;
 };
 
@@ -219,6 +222,36 @@ NetWs plan_ws(const stda_plan& p, int64_t B, char* base) {
     w.pd.push_back(take(B * ch * tiles));
     w.gd.push_back(take(B * ch));
   }
+  if (p.use_tc) {
+    // operand planes (planes.cuh) of every tensor a tcgen05 conv reads
+    const int np = p.bf16 ? 1 : 2;
+    const int H = c.map_height, W = c.map_width, c0 = c.stem_channels;
+    auto take_pl = [&](PlBuf b) -> PlBuf {
+      const size_t bytes = plbuf_bytes(b, B);
+      b.base = base ? reinterpret_cast<uint16_t*>(base + off) : nullptr;
+      off += align_up(bytes);
+      return b;
+    };
+    w.pl_s = take_pl(make_plbuf(1, H, W, c0, np));
+    w.pp_s = take_pl(make_plbuf(4, H / 2, W / 2, c0, np));
+    // stage-1 outputs: PP for encoder stride-2 consumers, PL for decoder ConvT consumers
+    // (separate regions, so every border stays zero after the single zeroing pass)
+    for (int i = 0; i < S; ++i)
+      w.pl_m.push_back(take_pl(make_plbuf(4, (H >> i) / 2, (W >> i) / 2, c0 << i, np)));
+    for (int j = 0; j < S; ++j) {
+      const int lvl = S - j;
+      w.pl_m.push_back(take_pl(make_plbuf(1, H >> lvl, W >> lvl, c0 << lvl, np)));
+    }
+    for (int i = 0; i < S; ++i) {
+      const int ch = c0 << (i + 1), h = H >> (i + 1), wd = W >> (i + 1);
+      w.pl_a.push_back(take_pl(make_plbuf(1, h, wd, ch, np)));
+      w.pp_a.push_back(i + 1 < S ? take_pl(make_plbuf(4, h / 2, wd / 2, ch, np)) : PlBuf{});
+    }
+    for (int j = 0; j + 1 < S; ++j) {
+      const int lvl = S - j - 1, ch = c0 << lvl;
+      w.pl_b.push_back(take_pl(make_plbuf(1, H >> lvl, W >> lvl, ch, np)));
+    }
+  }
   w.bytes = off;
   return w;
 }
@@ -241,56 +274,80 @@ void run_net_tc(const stda_plan& p, const Src& x, float* y, int64_t B, const Net
   const int S = c.stages, k = c.eca_kernel, c0 = c.stem_channels;
   const bool bf = p.bf16;
   int h = c.map_height, wd = c.map_width;
+  const int np = bf ? 1 : 2;
   mk.mark(st);
-  launch_stem_nhwc(p.stem.w, p.stem.b, x, c.input_frames, c0, w.s, B, h, wd, bf, st);
+  // zero the tap-reachable borders of every operand plane of this workspace
+  ZeroList zl;
+  auto add = [&](const PlBuf& b) {
+    STDA_CHECK(zl.n < kMaxZeroBufs, "too many operand planes");
+    if (b.base) zl.buf[zl.n++] = b;
+  };
+  add(w.pl_s);
+  add(w.pp_s);
+  for (const PlBuf& b : w.pl_a) add(b);
+  for (const PlBuf& b : w.pp_a) add(b);
+  for (const PlBuf& b : w.pl_b) add(b);
+  // stage-1 outputs: PP for encoder stride-2 consumers, PL for decoder ConvT consumers
+  const std::vector<PlBuf>& mviews = w.pl_m;
+  (void)np;
+  for (const PlBuf& b : mviews) add(b);
+  launch_zero_borders(zl, B, st);
   mk.mark(st);
-  tc::TcSrc cur;
-  cur.x = w.s;
-  std::vector<tc::TcSrc> skips{cur};
+  launch_stem_planes(p.stem.w, p.stem.b, x, c.input_frames, c0, w.pl_s, w.pp_s, B, h, wd, bf, st);
+  mk.mark(st);
+  PlBuf cur_pl = w.pl_s, cur_pp = w.pp_s;
+  std::vector<PlBuf> skips{w.pl_s};
   for (int i = 0; i < S; ++i) {
     const EncLayers& E = p.enc[i];
     tc::TcLayerDesc d1 = E.s1_tc, d2 = E.s2_tc;
     const tc::TcGeometry g1 = tc::tc_plan(d1, (int)B, h, wd);
-    tc::tc_launch(d1, g1, cur, nullptr, w.m, nullptr, true, st);
+    tc::TcOut o1;
+    o1.mode = 2;  // phase planes for the stride-2 consumer
+    o1.pl = mviews[i];
+    tc::tc_launch(d1, g1, cur_pl, nullptr, o1, true, st);
     mk.mark(st);
     const tc::TcGeometry g2 = tc::tc_plan(d2, (int)B, h, wd);
-    tc::TcSrc mixed;
-    mixed.x = w.m;
-    tc::tc_launch(d2, g2, mixed, &cur, w.e[i], w.pe[i], true, st);
+    tc::TcOut o2;
+    o2.f32 = w.e[i];
+    o2.gap = w.pe[i];
+    tc::tc_launch(d2, g2, mviews[i], &cur_pp, o2, true, st);
     mk.mark(st);
     h /= 2;
     wd /= 2;
-    launch_gate(w.pe[i], g2.items_per_image, E.eca, k, w.ge[i], B, d2.cout, h * wd, st);
+    // a_i = e_i * gate_i -> PL (next stage-1 / decoder input / skip) and PP (next stride-2)
+    launch_gate_apply(w.pe[i], g2.items_per_image, E.eca, k, w.e[i], nullptr, &w.pl_a[i],
+                      i + 1 < S ? &w.pp_a[i] : nullptr, nullptr, B, d2.cout, h, wd, st);
     mk.mark(st);
-    cur = tc::TcSrc{};
-    cur.x = w.e[i];
-    cur.gx = w.ge[i];
-    skips.push_back(cur);
+    cur_pl = w.pl_a[i];
+    cur_pp = w.pp_a[i];
+    skips.push_back(cur_pl);
   }
   for (int j = 0; j < S; ++j) {
     const DecLayers& D = p.dec[j];
     tc::TcLayerDesc d1 = D.s1_tc, d2 = D.s2_tc;
     const tc::TcGeometry g1 = tc::tc_plan(d1, (int)B, h, wd);
-    tc::tc_launch(d1, g1, cur, nullptr, w.m, nullptr, true, st);
+    tc::TcOut o1;
+    o1.mode = 1;  // plane for the ConvT consumer
+    o1.pl = mviews[S + j];
+    tc::tc_launch(d1, g1, cur_pl, nullptr, o1, true, st);
     mk.mark(st);
     const tc::TcGeometry g2 = tc::tc_plan(d2, (int)B, h, wd);
-    tc::TcSrc mixed;
-    mixed.x = w.m;
-    tc::tc_launch(d2, g2, mixed, &cur, w.d[j], w.pd[j], true, st);
+    tc::TcOut o2;
+    o2.f32 = w.d[j];
+    o2.gap = w.pd[j];
+    tc::tc_launch(d2, g2, mviews[S + j], &cur_pl, o2, true, st);
     mk.mark(st);
     h *= 2;
     wd *= 2;
-    launch_gate(w.pd[j], g2.items_per_image, D.eca, k, w.gd[j], B, d2.cout, h * wd, st);
+    // b_j = d_j * gate + skip  (model.py:197-198); the last one feeds the head as fp32
+    const PlBuf& sk = skips[S - 1 - j];
+    const bool last = j + 1 == S;
+    launch_gate_apply(w.pd[j], g2.items_per_image, D.eca, k, w.d[j], &sk, last ? nullptr : &w.pl_b[j],
+                      nullptr, last ? w.s : nullptr, B, d2.cout, h, wd, st);
     mk.mark(st);
-    const tc::TcSrc& sk = skips[S - 1 - j];
-    cur = tc::TcSrc{};
-    cur.x = w.d[j];
-    cur.gx = w.gd[j];
-    cur.s = sk.x;
-    cur.gs = sk.gx;
+    if (!last) cur_pl = w.pl_b[j];
   }
-  // head reads the NHWC d*g + skip on the fly
-  launch_head_nhwc(p.head_wt, p.head.b, cur.x, cur.gx, cur.s, cur.gs, c0, y, B, h, wd, bf, st);
+  launch_head_nhwc(p.head_wt, p.head.b, w.s, nullptr, nullptr, nullptr, c0, y, B, h, wd, bf, st);
   mk.mark(st);
 }
 
@@ -347,8 +404,8 @@ void run_net(const stda_plan& p, const Src& x, float* y, int64_t B, const NetWs&
   mk.mark(st);
 }
 
-std::string launch_names(const stda_config& c) {
-  std::string s = "stem";
+std::string launch_names(const stda_config& c, bool tc) {
+  std::string s = tc ? "zero;stem" : "stem";
   for (int i = 0; i < c.stages; ++i)
     s += ";enc" + std::to_string(i) + ".s1;enc" + std::to_string(i) + ".s2;enc" + std::to_string(i) +
          ".gate";
@@ -480,7 +537,7 @@ void stda_plan_destroy(stda_plan* plan) {
 int stda_launches_per_forward(const stda_plan* plan) {
   if (!plan) return -1;
   if (plan->kind != 0) return 2;
-  return 2 + 6 * plan->cfg.stages;
+  return (plan->use_tc ? 3 : 2) + 6 * plan->cfg.stages;
 }
 
 size_t stda_workspace_bytes(const stda_plan* plan, int64_t batch) {
@@ -531,7 +588,7 @@ int stda_forward_profiled(const stda_plan* plan, const float* x, float* y, int64
 
 const char* stda_launch_names(const stda_plan* plan) {
   static thread_local std::string names;
-  names = (plan && plan->kind == 0) ? launch_names(plan->cfg) : std::string();
+  names = (plan && plan->kind == 0) ? launch_names(plan->cfg, plan->use_tc) : std::string();
   return names.c_str();
 }
 

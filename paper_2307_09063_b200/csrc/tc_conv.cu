@@ -9,20 +9,18 @@ namespace tc {
 
 namespace {
 
-constexpr int kProdWarps = 8;
-constexpr int kEpiWarps = 4;                      // warps 8..11: warp % 4 = TMEM lane quarter
-constexpr int kMmaWarp = kProdWarps + kEpiWarps;  // warp 12
-constexpr int kUnroll = 4;                        // producer loads in flight per thread
-constexpr int kThreads = (kProdWarps + kEpiWarps + 1) * 32;
-constexpr int kProdThreads = kProdWarps * 32;
+constexpr int kProdWarp = 0;   // lane 0: cp.async.bulk producer
+constexpr int kMmaWarp = 1;    // TMEM allocator + tcgen05.mma issuer
+constexpr int kEpiWarp0 = 2;   // warps 2..5: epilogue (warp % 4 = TMEM lane quarter)
+constexpr int kEpiWarps = 4;
+constexpr int kThreads = (kEpiWarp0 + kEpiWarps) * 32;
 constexpr int kMaxSmem = 227 * 1024;
 
 struct Params {
   TcLayerDesc d;
-  TcSrc src[2];
-  float* out;
-  float* gap;
-  int H, W, C;            // input NHWC
+  PlBuf src[2];
+  TcOut out;
+  int H, W, C;            // input grid
   int Hp, Wp, L, Ho, Wo;
   int G, stages, slots, items_per_image, total_items;
   int P_max;
@@ -62,9 +60,6 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 }
 __device__ __forceinline__ void fence_barrier_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void fence_proxy_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
   asm volatile(
@@ -118,10 +113,6 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int n) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((128u >> 4) << 24);
 }
 
-__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
-  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-  return *reinterpret_cast<const uint32_t*>(&h);
-}
 
 // ---- the kernel ----------------------------------------------------------------------
 template <int N>
@@ -146,7 +137,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.stages; ++s) {
-      mbar_init(smem_u32(&full[s]), kProdThreads + 1);
+      mbar_init(smem_u32(&full[s]), 1);
       mbar_init(smem_u32(&empty[s]), 1);
     }
     for (int s = 0; s < p.slots; ++s) {
@@ -166,119 +157,49 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  const uint32_t src_bytes = (uint32_t)npassA * 2 * p.P_max * 16;
 
-  if (warp < kProdWarps) {
-    // ===================== producers: stage A (and weights via bulk copy) ==============
-    const int tid = threadIdx.x;
-    uint32_t k = 0;
-    for (int item = blockIdx.x; item < p.total_items; item += gridDim.x) {
-      const int b = item / p.items_per_image;
-      const int q0 = (item - b * p.items_per_image) * p.G * 128;
-      for (int c = 0; c < n_chunks; ++c, ++k) {
-        const int stage = k % p.stages;
-        const uint32_t phase = (k / p.stages) & 1;
-        mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
-        const int pl = c / cgroups, cgi = c - pl * cgroups;
-        if (tid == 0) {
-          const uint32_t bytes = (uint32_t)(d.chunk_off[c + 1] - d.chunk_off[c]);
-          mbar_arrive_expect_tx(smem_u32(&full[stage]), bytes);
+  if (warp == kProdWarp) {
+    // ===================== producer: cp.async.bulk of A ranges + packed weights =========
+    if (lane == 0) {
+      uint32_t k = 0;
+      for (int item = blockIdx.x; item < p.total_items; item += gridDim.x) {
+        const int b = item / p.items_per_image;
+        const int q0 = (item - b * p.items_per_image) * p.G * 128;
+        for (int c = 0; c < n_chunks; ++c, ++k) {
+          const int stage = k % p.stages;
+          const uint32_t phase = (k / p.stages) & 1;
+          mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+          const int pl = c / cgroups, cgi = c - pl * cgroups;
+          const PlaneTaps& pt = d.planes[pl];
+          const int P = p.G * 128 + pt.hi - pt.lo;
+          const uint32_t a_bytes = (uint32_t)P * 16;
+          const uint32_t w_bytes = (uint32_t)(d.chunk_off[c + 1] - d.chunk_off[c]);
+          const uint32_t fb = smem_u32(&full[stage]);
+          mbar_arrive_expect_tx(fb, w_bytes + (uint32_t)d.n_src * npassA * 2 * a_bytes);
           bulk_g2s(smem_u32(b_base + (size_t)stage * p.b_stage_bytes),
-                   reinterpret_cast<const uint8_t*>(d.w) + d.chunk_off[c], bytes, smem_u32(&full[stage]));
-        }
-        const PlaneTaps& pt = d.planes[pl];
-        const int P = p.G * 128 + pt.hi - pt.lo;
-        const int py = pl >> 1, px = pl & 1;
-        uint8_t* sa = a_base + (size_t)stage * p.a_stage_bytes;
-        const uint32_t src_bytes = (uint32_t)npassA * 2 * p.P_max * 16;
-        // each thread owns one (source, 8-channel group) and strides over positions;
-        // kUnroll positions' global loads are issued before any is consumed (MLP)
-        const int groups = d.n_src * 2;
-        const int tpg = kProdThreads / groups;
-        const int grp = tid / tpg, t0 = tid - grp * tpg;
-        const int s = grp >> 1, cg8 = grp & 1;
-        const int ch = cgi * 16 + cg8 * 8;
-        const TcSrc& S = p.src[s];
-        float gx[8], gs[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) gx[i] = gs[i] = 1.f;
-        if (S.gx) {
-          const float4 g0 = __ldg(reinterpret_cast<const float4*>(S.gx + (size_t)b * p.C + ch));
-          const float4 g1 = __ldg(reinterpret_cast<const float4*>(S.gx + (size_t)b * p.C + ch) + 1);
-          gx[0] = g0.x; gx[1] = g0.y; gx[2] = g0.z; gx[3] = g0.w;
-          gx[4] = g1.x; gx[5] = g1.y; gx[6] = g1.z; gx[7] = g1.w;
-        }
-        if (S.gs) {
-          const float4 g0 = __ldg(reinterpret_cast<const float4*>(S.gs + (size_t)b * p.C + ch));
-          const float4 g1 = __ldg(reinterpret_cast<const float4*>(S.gs + (size_t)b * p.C + ch) + 1);
-          gs[0] = g0.x; gs[1] = g0.y; gs[2] = g0.z; gs[3] = g0.w;
-          gs[4] = g1.x; gs[5] = g1.y; gs[6] = g1.z; gs[7] = g1.w;
-        }
-        uint8_t* dst_base = sa + (size_t)s * src_bytes + (size_t)cg8 * p.P_max * 16;
-        const size_t img = (size_t)b * p.H;
-        for (int base = t0; base < P; base += kUnroll * tpg) {
-          float4 xa[kUnroll][2], sk[kUnroll][2];
-          bool ok[kUnroll];
-#pragma unroll
-          for (int u = 0; u < kUnroll; ++u) {
-            const int qq = base + u * tpg;
-            const int q = q0 + pt.lo + qq;
-            const int y = (int)((unsigned)(q + p.L) / (unsigned)p.L) - 1;  // q >= -L
-            const int x = q - y * p.L;
-            ok[u] = qq < P && y >= 0 && y < p.Hp && x < p.Wp;
-            xa[u][0] = xa[u][1] = sk[u][0] = sk[u][1] = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (ok[u]) {
-              int iy = y, ix = x;
-              if (d.mode == CONV3_S2) {
-                iy = 2 * y + py;
-                ix = 2 * x + px;
+                   reinterpret_cast<const uint8_t*>(d.w) + d.chunk_off[c], w_bytes, fb);
+          uint8_t* sa = a_base + (size_t)stage * p.a_stage_bytes;
+          for (int s = 0; s < d.n_src; ++s) {
+            const PlBuf& S = p.src[s];
+            const uint16_t* img =
+                S.base + (int64_t)b * S.img_stride + (int64_t)(S.planes == 4 ? pl : 0) * S.plane_stride;
+            for (int pass = 0; pass < npassA; ++pass)
+              for (int cg8 = 0; cg8 < 2; ++cg8) {
+                const uint16_t* src = img + (S.block_index(cgi, pass, cg8) + q0 + pt.lo + S.off) * 8;
+                bulk_g2s(smem_u32(sa + (size_t)s * src_bytes + (size_t)(pass * 2 + cg8) * p.P_max * 16), src,
+                         a_bytes, fb);
               }
-              const size_t off = ((img + iy) * p.W + ix) * p.C + ch;
-              const float4* xp = reinterpret_cast<const float4*>(S.x + off);
-              xa[u][0] = __ldg(xp);
-              xa[u][1] = __ldg(xp + 1);
-              if (S.s) {
-                const float4* sp = reinterpret_cast<const float4*>(S.s + off);
-                sk[u][0] = __ldg(sp);
-                sk[u][1] = __ldg(sp + 1);
-              }
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < kUnroll; ++u) {
-            const int qq = base + u * tpg;
-            if (qq >= P) break;
-            const float xv[8] = {xa[u][0].x, xa[u][0].y, xa[u][0].z, xa[u][0].w,
-                                 xa[u][1].x, xa[u][1].y, xa[u][1].z, xa[u][1].w};
-            const float sv[8] = {sk[u][0].x, sk[u][0].y, sk[u][0].z, sk[u][0].w,
-                                 sk[u][1].x, sk[u][1].y, sk[u][1].z, sk[u][1].w};
-            float hi[8], lo[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              // value = x*gx (+ skip*gs): the reference's eca(x) + skip rounding order
-              float v = xv[i] * gx[i];
-              if (S.s) v = v + sv[i] * gs[i];
-              hi[i] = bf16_round(v);
-              lo[i] = v - hi[i];
-            }
-            uint8_t* dst = dst_base + (size_t)qq * 16;
-            *reinterpret_cast<uint4*>(dst) = make_uint4(pack_bf16x2(hi[0], hi[1]), pack_bf16x2(hi[2], hi[3]),
-                                                        pack_bf16x2(hi[4], hi[5]), pack_bf16x2(hi[6], hi[7]));
-            if (npassA == 2)
-              *reinterpret_cast<uint4*>(dst + (size_t)2 * p.P_max * 16) =
-                  make_uint4(pack_bf16x2(lo[0], lo[1]), pack_bf16x2(lo[2], lo[3]),
-                             pack_bf16x2(lo[4], lo[5]), pack_bf16x2(lo[6], lo[7]));
           }
         }
-        fence_proxy_async_smem();
-        mbar_arrive(smem_u32(&full[stage]));
       }
     }
+    __syncwarp();
   } else if (warp == kMmaWarp) {
     // ===================== MMA issuer (one lane) ========================================
     if (lane == 0) {
       const uint32_t idesc = idesc_bf16(N);
       uint32_t k = 0, ic = 0;
-      const uint32_t src_bytes = (uint32_t)npassA * 2 * p.P_max * 16;
       const uint32_t lboA = (uint32_t)p.P_max * 16;
       const uint32_t lboB = (uint32_t)N * 16;
       const int npassB = d.npass == 3 ? 2 : 1;
@@ -303,20 +224,18 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
               const int acc = s * d.n_acc_src + pt.acc[t];
               const int shift = pt.dy[t] * p.L + pt.dx[t] - pt.lo;
               const uint32_t b_tap = sb + (uint32_t)((s * pt.n + t) * npassB) * 32u * N;
+              const uint64_t bd_hi = smem_desc(b_tap, lboB, 128);
+              const uint64_t bd_lo = smem_desc(b_tap + 32u * N, lboB, 128);
               for (int g = 0; g < p.G; ++g) {
                 const uint32_t a_off = sa + s * src_bytes + (uint32_t)(shift + g * 128) * 16u;
                 const uint32_t dcol = dslot + (uint32_t)((g * n_acc + acc) * N);
                 const uint32_t bit = 1u << (g * n_acc + acc);
-                // pass 0: hi*hi
-                tc_mma(dcol, smem_desc(a_off, lboA, 128), smem_desc(b_tap, lboB, 128), idesc,
-                       (inited & bit) ? 1u : 0u);
+                const uint64_t ad_hi = smem_desc(a_off, lboA, 128);
+                tc_mma(dcol, ad_hi, bd_hi, idesc, (inited & bit) ? 1u : 0u);  // hi*hi
                 inited |= bit;
                 if (d.npass == 3) {
-                  // pass 1: lo(A)*hi(B); pass 2: hi(A)*lo(B)
-                  tc_mma(dcol, smem_desc(a_off + 2u * lboA, lboA, 128), smem_desc(b_tap, lboB, 128),
-                         idesc, 1u);
-                  tc_mma(dcol, smem_desc(a_off, lboA, 128), smem_desc(b_tap + 32u * N, lboB, 128), idesc,
-                         1u);
+                  tc_mma(dcol, smem_desc(a_off + 2u * lboA, lboA, 128), bd_hi, idesc, 1u);  // lo*hi
+                  tc_mma(dcol, ad_hi, bd_lo, idesc, 1u);                                  // hi*lo
                 }
               }
             }
@@ -328,9 +247,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
     }
     __syncwarp();
   } else {
-    // ===================== epilogue warps 4..7 ==========================================
-    const int ew = warp - kProdWarps;  // == warp % 4: TMEM lane quarter
-    const int et = threadIdx.x - kProdThreads;
+    // ===================== epilogue warps 2..5 ==========================================
+    const int ew = warp & 3;  // TMEM lane quarter accessible to this warp
+    const int et = threadIdx.x - kEpiWarp0 * 32;
     uint32_t ic = 0;
     const bool dual = d.n_src == 2;
     for (int item = blockIdx.x; item < p.total_items; item += gridDim.x, ++ic) {
@@ -356,7 +275,6 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
             oy = 2 * y + (ph >> 1);
             ox = 2 * x + (ph & 1);
           }
-          float* op = p.out + (((size_t)b * p.Ho + oy) * p.Wo + ox) * N;
 #pragma unroll
           for (int j = 0; j < N; j += 16) {
             float a0[16], a1[16];
@@ -371,19 +289,37 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
               if (dual) t = t + (a1[i] + __ldg(d.bias1 + j + i));
               v[i] = t;
             }
-            if (valid) {
+            if (!valid) continue;
+            if (p.out.mode == 0) {
+              float* op = p.out.f32 + (((size_t)b * p.Ho + oy) * p.Wo + ox) * N;
 #pragma unroll
               for (int i = 0; i < 16; i += 4)
                 *reinterpret_cast<float4*>(op + j + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
 #pragma unroll
               for (int i = 0; i < 16; ++i) gsum[j + i] += v[i];
+            } else {
+              int plane = 0, qo;
+              if (p.out.mode == 1) {
+                qo = oy * p.out.pl.L + ox;
+              } else {
+                plane = (oy & 1) * 2 + (ox & 1);
+                qo = (oy >> 1) * p.out.pl.L + (ox >> 1);
+              }
+              float v0[8], v1[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                v0[i] = v[i];
+                v1[i] = v[8 + i];
+              }
+              pl_store8(p.out.pl, b, plane, j / 8, qo, v0);
+              pl_store8(p.out.pl, b, plane, j / 8 + 1, qo, v1);
             }
           }
         }
       }
       tc_fence_before();
       mbar_arrive(smem_u32(&tempty[slot]));
-      if (p.gap) {
+      if (p.out.mode == 0 && p.out.gap) {
 #pragma unroll
         for (int c = 0; c < N; ++c) {
           float s = gsum[c];
@@ -394,7 +330,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
         asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
         if (et < N) {
           const float s = ((red[et] + red[N + et]) + red[2 * N + et]) + red[3 * N + et];
-          p.gap[((size_t)b * p.items_per_image + it) * N + et] = s;
+          p.out.gap[((size_t)b * p.items_per_image + it) * N + et] = s;
         }
         asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
       }
@@ -594,16 +530,18 @@ TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W) {
   return g;
 }
 
-void tc_launch(const TcLayerDesc& d, const TcGeometry& g, const TcSrc& src0, const TcSrc* src1,
-               float* out, float* gap, bool relu0, cudaStream_t st) {
+void tc_launch(const TcLayerDesc& d, const TcGeometry& g, const PlBuf& src0, const PlBuf* src1,
+               const TcOut& out, bool relu0, cudaStream_t st) {
   Params p;
   std::memset(&p, 0, sizeof(p));
   p.d = d;
   p.src[0] = src0;
   if (src1) p.src[1] = *src1;
   STDA_CHECK((src1 != nullptr) == (d.n_src == 2), "source count mismatch");
+  STDA_CHECK(src0.L == g.L && (!src1 || src1->L == g.L), "operand plane geometry mismatch");
+  STDA_CHECK(src0.np == (d.npass == 3 ? 2 : 1), "operand plane precision mismatch");
+  STDA_CHECK((d.mode == CONV3_S2) == (src0.planes == 4), "stride-2 convs read phase planes");
   p.out = out;
-  p.gap = gap;
   p.H = g.H;
   p.W = g.W;
   p.C = d.cin;

@@ -1,33 +1,35 @@
 // tcgen05 implicit-GEMM convolution (sm_100a): the tensor-core path of the engine.
 //
 // GEMM view.  M = output positions, N = output channels (16/32/64), K = taps x Cin.
-// Positions are the image linearised with row stride L = plane_width + 1: the extra
-// column is an always-zero pad, so a 3x3 tap (dy, dx) is a constant shift dy*L + dx of
-// the A rows and every tap of every M-tile is a plain UMMA shared-memory descriptor
-// offset — no im2col copies.  The pad positions are computed and discarded (W/(W+1)
-// efficiency).  Three geometries share one kernel:
-//   S1  3x3 stride 1      A = input grid,             1 plane, 9 taps
-//   S2  3x3 stride 2      A = 4 input phase planes,   tap (dy,dx) -> plane (py,px), shift
-//                         (oy,ox) in {-1,0}^2 (deinterleaved while staging)
-//   T   ConvT 4x4 s2 p1   A = input grid, 4 output phases = 4 accumulators, each a 2x2
-//                         sub-pixel kernel (taps with shifts in {-1,0,1})
-// Stage-2 blocks are dual: a second source (the block input) with its own weights feeds
-// separate TMEM accumulators; the epilogue forms relu(acc0 + b0) + (acc1 + b1).
+// Positions are the image linearised with row stride L = plane_width + 1 (planes.cuh):
+// the extra column is an always-zero pad, so a 3x3 tap (dy, dx) is a constant shift
+// dy*L + dx of the A rows and every tap of every M-tile is a plain UMMA shared-memory
+// descriptor offset — no im2col.  Pad positions are computed and discarded.
+//   S1  3x3 stride 1      A = input plane (PL),                   9 taps
+//   S2  3x3 stride 2      A = 4 phase planes of the input (PP),   tap (dy,dx) -> plane
+//                         (py,px) + shift (oy,ox) in {-1,0}^2
+//   T   ConvT 4x4 s2 p1   A = input plane (PL), 4 output phases = 4 TMEM accumulators,
+//                         each a 2x2 sub-pixel kernel (shifts in {-1,0,1})
+// Stage-2 blocks are dual: the block input (second source, own weights) feeds separate
+// accumulators; the epilogue forms relu(acc0 + b0) + (acc1 + b1).
 //
-// fp32 parity: activations and weights are split into bf16 hi + lo parts and each
-// product is formed as hi*hi + lo*hi + hi*lo (3 MMAs, fp32 accumulation in TMEM).
+// fp32 parity: operands are bf16 hi + lo planes (activations) and hi/lo packed weights;
+// each product is hi*hi + lo*hi + hi*lo (3 MMAs, fp32 accumulation in TMEM).
 //
-// Roles (416 threads): warps 0-7 stage A (fp32 NHWC global -> gate/skip transform ->
-// bf16 hi/lo core-matrix layout in smem) and thread 0 bulk-copies the packed weights
-// (cp.async.bulk + mbarrier tx); warp 12 allocates TMEM and one lane issues every
-// tcgen05.mma; warps 8-11 drain TMEM (tcgen05.ld) into bias/relu/dual epilogues, NHWC
-// stores and per-item channel sums for ECA.  mbarrier pipelines: smem stages
-// (full/empty) and TMEM accumulator slots (full/empty).  Persistent CTAs.
+// Data movement: the operand planes already hold bf16 hi/lo core matrices in HBM, so the
+// producer is ONE thread issuing cp.async.bulk copies (A: one contiguous range per
+// source/pass/8-channel group; B: one packed weight chunk) completing on an mbarrier
+// transaction count.  Roles (192 threads): warp 0 lane 0 = bulk-copy producer; warp 1
+// = TMEM allocator + single-thread tcgen05.mma issuer; warps 2-5 = epilogue (warp % 4 =
+// TMEM lane quarter): tcgen05.ld -> bias/relu/dual -> operand-plane (hi/lo) or NHWC fp32
+// stores + per-item channel sums for ECA.  smem stage ring (full/empty) and TMEM
+// accumulator slots (full/empty); persistent CTAs.
 #pragma once
 
 #include <vector>
 
 #include "common.cuh"
+#include "planes.cuh"
 #include "simt_conv.cuh"
 
 namespace stda {
@@ -37,21 +39,13 @@ constexpr int kMaxChunks = 16;
 constexpr int kMaxTaps = 16;
 constexpr int kMaxPlanes = 4;
 
-// NHWC fp32 logical input: value = x*gx[b][c] + s*gs[b][c] (s, gx, gs optional).
-struct TcSrc {
-  const float* x = nullptr;
-  const float* gx = nullptr;
-  const float* s = nullptr;
-  const float* gs = nullptr;
-};
-
 // Per plane: the taps that read it (position shift = dy*L + dx).
 struct PlaneTaps {
   int8_t n;
   int8_t acc[kMaxTaps];
   int8_t dy[kMaxTaps];
   int8_t dx[kMaxTaps];
-  int16_t lo, hi;  // min / max shift over the taps, in positions (needs L; set by tc_plan)
+  int16_t lo, hi;  // min / max shift over the taps, in positions (set by tc_plan)
 };
 
 struct TcLayerDesc {
@@ -75,9 +69,9 @@ void tc_pack_layer(TcLayerDesc& d, int mode, int cin, int cout, const float* w0,
                    bool bf16, std::vector<uint16_t>& packed);
 
 struct TcGeometry {
-  int B, H, W;            // input tensor (NHWC, cin channels)
+  int B, H, W;            // input grid
   int Hp, Wp, L;          // A plane size and linear stride
-  int Ho, Wo;             // output tensor
+  int Ho, Wo;             // output grid
   int G;                  // M-tiles of 128 positions per work item
   int stages, slots;      // smem pipeline depth, TMEM accumulator slots
   int items_per_image;
@@ -90,9 +84,17 @@ struct TcGeometry {
 bool tc_supported(int mode, int cin, int cout);
 TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W);
 
-// out: NHWC fp32 [B][Ho][Wo][cout]; gap (optional): [B][items_per_image][cout].
-void tc_launch(const TcLayerDesc& d, const TcGeometry& g, const TcSrc& src0, const TcSrc* src1,
-               float* out, float* gap, bool relu0, cudaStream_t st);
+// Output of one launch: either operand planes (PL over the output grid, or PP phase
+// planes of it) or NHWC fp32 with per-item channel sums gap [B][items_per_image][cout].
+struct TcOut {
+  int mode = 0;  // 0 = NHWC fp32 (+gap), 1 = PL, 2 = PP
+  float* f32 = nullptr;
+  float* gap = nullptr;
+  PlBuf pl;
+};
+
+void tc_launch(const TcLayerDesc& d, const TcGeometry& g, const PlBuf& src0, const PlBuf* src1,
+               const TcOut& out, bool relu0, cudaStream_t st);
 
 }  // namespace tc
 }  // namespace stda
