@@ -73,17 +73,22 @@ __device__ __forceinline__ void tc_fence_before() {
 __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
-__device__ __forceinline__ void tc_commit(uint32_t bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-               : "memory");
-}
-__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                       uint32_t accumulate) {
+// Warp-collective: one elected lane issues (the warp must be converged).
+__device__ __forceinline__ void tc_mma_elect(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                             uint32_t idesc, uint32_t accumulate) {
   asm volatile(
-      "{\n\t.reg .pred p;\n\t"
+      "{\n\t.reg .pred p, e;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_elect(uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
       : "memory");
 }
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
@@ -196,54 +201,66 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
     }
     __syncwarp();
   } else if (warp == kMmaWarp) {
-    // ===================== MMA issuer (one lane) ========================================
-    if (lane == 0) {
-      const uint32_t idesc = idesc_bf16(N);
-      uint32_t k = 0, ic = 0;
-      const uint32_t lboA = (uint32_t)p.P_max * 16;
-      const uint32_t lboB = (uint32_t)N * 16;
-      const int npassB = d.npass == 3 ? 2 : 1;
-      for (int item = blockIdx.x; item < p.total_items; item += gridDim.x, ++ic) {
-        const int slot = ic % p.slots;
-        const uint32_t sphase = (ic / p.slots) & 1;
-        mbar_wait(smem_u32(&tempty[slot]), sphase ^ 1);
+    // ===================== MMA issuer ===================================================
+    // The whole warp runs the (uniform) loop so descriptors live in uniform registers;
+    // elect.sync picks the lane that issues each tcgen05.mma / commit.  Descriptors are
+    // advanced by adding 16-byte units to the start-address field (one position = 16 B).
+    // concat: B = [B_hi | B_lo] along N, so A_hi x B is ONE MMA of width 2N producing
+    // hi*hi (cols 0..N) and hi*lo (cols N..2N); A_lo x B_hi accumulates into cols 0..N.
+    const int AW = d.concat ? 2 * N : N;  // TMEM columns per accumulator
+    const uint32_t idesc_n = idesc_bf16(N);
+    const uint32_t idesc_w = idesc_bf16(AW);
+    const uint32_t lboA = (uint32_t)p.P_max * 16;
+    const uint32_t lboB = (uint32_t)(d.concat ? 2 * N : N) * 16;
+    const uint32_t tap_units = (uint32_t)(d.npass == 3 ? 64 * N : 32 * N) >> 4;  // per (src, tap)
+    const uint32_t lo_units = (2 * lboA) >> 4;   // A_lo plane offset
+    const uint32_t blo_units = (32u * N) >> 4;   // B_lo block offset (no concat)
+    uint32_t k = 0, ic = 0;
+    for (int item = blockIdx.x; item < p.total_items; item += gridDim.x, ++ic) {
+      const int slot = ic % p.slots;
+      const uint32_t sphase = (ic / p.slots) & 1;
+      mbar_wait(smem_u32(&tempty[slot]), sphase ^ 1);
+      __syncwarp();
+      tc_fence_after();
+      const uint32_t dslot = tmem_base + (uint32_t)slot * p.slot_cols;
+      uint32_t inited = 0;
+      for (int c = 0; c < n_chunks; ++c, ++k) {
+        const int stage = k % p.stages;
+        const uint32_t phase = (k / p.stages) & 1;
+        mbar_wait(smem_u32(&full[stage]), phase);
+        __syncwarp();
         tc_fence_after();
-        const uint32_t dslot = tmem_base + (uint32_t)slot * p.slot_cols;
-        uint32_t inited = 0;
-        for (int c = 0; c < n_chunks; ++c, ++k) {
-          const int stage = k % p.stages;
-          const uint32_t phase = (k / p.stages) & 1;
-          mbar_wait(smem_u32(&full[stage]), phase);
-          tc_fence_after();
-          const int pl = c / cgroups;
-          const PlaneTaps& pt = d.planes[pl];
-          const uint32_t sa = smem_u32(a_base + (size_t)stage * p.a_stage_bytes);
-          const uint32_t sb = smem_u32(b_base + (size_t)stage * p.b_stage_bytes);
-          for (int s = 0; s < d.n_src; ++s) {
-            for (int t = 0; t < pt.n; ++t) {
-              const int acc = s * d.n_acc_src + pt.acc[t];
-              const int shift = pt.dy[t] * p.L + pt.dx[t] - pt.lo;
-              const uint32_t b_tap = sb + (uint32_t)((s * pt.n + t) * npassB) * 32u * N;
-              const uint64_t bd_hi = smem_desc(b_tap, lboB, 128);
-              const uint64_t bd_lo = smem_desc(b_tap + 32u * N, lboB, 128);
-              for (int g = 0; g < p.G; ++g) {
-                const uint32_t a_off = sa + s * src_bytes + (uint32_t)(shift + g * 128) * 16u;
-                const uint32_t dcol = dslot + (uint32_t)((g * n_acc + acc) * N);
-                const uint32_t bit = 1u << (g * n_acc + acc);
-                const uint64_t ad_hi = smem_desc(a_off, lboA, 128);
-                tc_mma(dcol, ad_hi, bd_hi, idesc, (inited & bit) ? 1u : 0u);  // hi*hi
-                inited |= bit;
-                if (d.npass == 3) {
-                  tc_mma(dcol, smem_desc(a_off + 2u * lboA, lboA, 128), bd_hi, idesc, 1u);  // lo*hi
-                  tc_mma(dcol, ad_hi, bd_lo, idesc, 1u);                                  // hi*lo
-                }
+        const PlaneTaps& pt = d.planes[c / cgroups];
+        const uint64_t a0 = smem_desc(smem_u32(a_base + (size_t)stage * p.a_stage_bytes), lboA, 128);
+        const uint64_t b0 = smem_desc(smem_u32(b_base + (size_t)stage * p.b_stage_bytes), lboB, 128);
+        for (int s = 0; s < d.n_src; ++s) {
+          const uint64_t as = a0 + ((s * src_bytes) >> 4);
+          for (int t = 0; t < pt.n; ++t) {
+            const int acc = s * d.n_acc_src + pt.acc[t];
+            const uint64_t ad_t = as + (uint32_t)(pt.dy[t] * p.L + pt.dx[t] - pt.lo);
+            const uint64_t bd = b0 + (uint32_t)(s * pt.n + t) * tap_units;
+            for (int g = 0; g < p.G; ++g) {
+              const uint64_t ad = ad_t + (uint32_t)(g * 128);
+              const uint32_t dcol = dslot + (uint32_t)((g * n_acc + acc) * AW);
+              const uint32_t bit = 1u << (g * n_acc + acc);
+              const uint32_t accum = (inited & bit) ? 1u : 0u;
+              inited |= bit;
+              if (d.npass == 1) {
+                tc_mma_elect(dcol, ad, bd, idesc_n, accum);
+              } else if (d.concat) {
+                tc_mma_elect(dcol, ad, bd, idesc_w, accum);            // A_hi x [B_hi|B_lo]
+                tc_mma_elect(dcol, ad + lo_units, bd, idesc_n, 1u);    // A_lo x B_hi
+              } else {
+                tc_mma_elect(dcol, ad, bd, idesc_n, accum);            // hi*hi
+                tc_mma_elect(dcol, ad + lo_units, bd, idesc_n, 1u);    // lo*hi
+                tc_mma_elect(dcol, ad, bd + blo_units, idesc_n, 1u);   // hi*lo
               }
             }
           }
-          tc_commit(smem_u32(&empty[stage]));
         }
-        tc_commit(smem_u32(&tfull[slot]));
+        tc_commit_elect(smem_u32(&empty[stage]));
       }
+      tc_commit_elect(smem_u32(&tfull[slot]));
     }
     __syncwarp();
   } else {
@@ -252,6 +269,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
     const int et = threadIdx.x - kEpiWarp0 * 32;
     uint32_t ic = 0;
     const bool dual = d.n_src == 2;
+    const int AW = d.concat ? 2 * N : N;
     for (int item = blockIdx.x; item < p.total_items; item += gridDim.x, ++ic) {
       const int slot = ic % p.slots;
       const uint32_t sphase = (ic / p.slots) & 1;
@@ -278,8 +296,21 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
 #pragma unroll
           for (int j = 0; j < N; j += 16) {
             float a0[16], a1[16];
-            tmem_ld16(trow + (uint32_t)((g * n_acc + ph) * N + j), a0);
-            if (dual) tmem_ld16(trow + (uint32_t)((g * n_acc + d.n_acc_src + ph) * N + j), a1);
+            const uint32_t c0 = (uint32_t)((g * n_acc + ph) * AW + j);
+            const uint32_t c1 = (uint32_t)((g * n_acc + d.n_acc_src + ph) * AW + j);
+            tmem_ld16(trow + c0, a0);
+            if (dual) tmem_ld16(trow + c1, a1);
+            if (d.concat) {  // + the hi*lo half of the concatenated accumulator
+              float h0[16], h1[16];
+              tmem_ld16(trow + c0 + N, h0);
+              if (dual) tmem_ld16(trow + c1 + N, h1);
+              tmem_wait_ld();
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                a0[i] += h0[i];
+                if (dual) a1[i] += h1[i];
+              }
+            }
             tmem_wait_ld();
             float v[16];
 #pragma unroll
@@ -436,19 +467,33 @@ void tc_pack_layer(TcLayerDesc& d, int mode, int cin, int cout, const float* w0,
   packed.clear();
   d.chunk_off[0] = 0;
   const float* ws[2] = {w0, w1};
+  // hi/lo N-concatenation (one A_hi read for hi*hi and hi*lo) when the doubled
+  // accumulators still leave two TMEM slots at one M-tile per item
+  const int n_acc = d.n_src * d.n_acc_src;
+  d.concat = !bf16 && n_acc * 2 * cout * 2 <= 512;
+  // per (src, tap): concat -> [kgrp 2][pass 2][n][8] (kgrp row block = [B_hi; B_lo], 2N rows)
+  //                 else   -> [pass][kgrp 2][n][8]
+  auto put = [&](const float* w, int n, int ci, int wk, int pass) {
+    const float v = w[((size_t)n * cin + ci) * wk_per + wk];
+    const float hi = bf16_val(v);
+    packed.push_back(bf16_bits(pass == 0 ? v : v - hi));
+  };
   for (int c = 0; c < n_chunks; ++c) {
     const int pl = c / cgroups, cgi = c % cgroups;
     for (int s = 0; s < d.n_src; ++s)
-      for (const HostTap& t : taps[pl])
-        for (int pass = 0; pass < npassB; ++pass)
+      for (const HostTap& t : taps[pl]) {
+        if (d.concat) {
           for (int kg = 0; kg < 2; ++kg)
-            for (int n = 0; n < cout; ++n)
-              for (int e = 0; e < 8; ++e) {
-                const int ci = cgi * 16 + kg * 8 + e;
-                const float v = ws[s][((size_t)n * cin + ci) * wk_per + t.wk];
-                const float hi = bf16_val(v);
-                packed.push_back(bf16_bits(pass == 0 ? v : v - hi));
-              }
+            for (int pass = 0; pass < 2; ++pass)
+              for (int n = 0; n < cout; ++n)
+                for (int e = 0; e < 8; ++e) put(ws[s], n, cgi * 16 + kg * 8 + e, t.wk, pass);
+        } else {
+          for (int pass = 0; pass < npassB; ++pass)
+            for (int kg = 0; kg < 2; ++kg)
+              for (int n = 0; n < cout; ++n)
+                for (int e = 0; e < 8; ++e) put(ws[s], n, cgi * 16 + kg * 8 + e, t.wk, pass);
+        }
+      }
     d.chunk_off[c + 1] = (int64_t)packed.size() * 2;
   }
 }
@@ -500,7 +545,7 @@ TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W) {
     for (int G : {4, 2, 1}) {
       const int P8 = (G * 128 + span + 7) / 8 * 8;
       const uint32_t a_stage = (uint32_t)d.n_src * npassA * 2 * P8 * 16;
-      const int acc_cols = G * n_acc * d.cout;
+      const int acc_cols = G * n_acc * d.cout * (d.concat ? 2 : 1);
       if (acc_cols > 512 || G * n_acc > 32) continue;
       int stages = 0;
       for (int st : {3, 2, 1})
@@ -558,7 +603,7 @@ void tc_launch(const TcLayerDesc& d, const TcGeometry& g, const PlBuf& src0, con
   p.P_max = g.P_max;
   p.a_stage_bytes = g.a_stage_bytes;
   p.b_stage_bytes = g.b_stage_bytes;
-  p.slot_cols = (uint32_t)(g.G * d.n_src * d.n_acc_src * d.cout);
+  p.slot_cols = (uint32_t)(g.G * d.n_src * d.n_acc_src * d.cout * (d.concat ? 2 : 1));
   p.tmem_cols = (uint32_t)g.tmem_cols;
   p.relu0 = relu0 ? 1 : 0;
   if (p.total_items == 0) return;

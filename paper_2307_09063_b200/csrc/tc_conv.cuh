@@ -55,6 +55,7 @@ struct TcLayerDesc {
   int n_planes;    // 1 (S1, T) or 4 (S2)
   int n_acc_src;   // accumulators per source: 1 (S1, S2) or 4 (T)
   int npass;       // 3 (fp32 parity) or 1 (bf16)
+  int concat;      // B = [B_hi | B_lo] along N (2 MMAs per tap instead of 3)
   PlaneTaps planes[kMaxPlanes];
   // packed weights: chunk c = plane*(cin/16) + cgroup; inside a chunk for src, tap,
   // weight pass (hi[, lo]): [kgrp 2][n cout][8] bf16.  chunk_off = byte offsets.

@@ -1,0 +1,97 @@
+// Microbenchmark: tcgen05.mma (kind::f16, M=128, SS operands) cycles per instruction
+// vs N and vs the number of distinct accumulators the issue stream round-robins over.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/mma_bench tools/mma_bench.cu
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint64_t desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);
+}
+
+template <bool WARP_UNIFORM>
+__global__ void bench(int n, int naccs, int iters, int a_stride_rows, long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint32_t tmem_holder;
+  __shared__ __align__(8) uint64_t bar;
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_holder)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  for (int i = threadIdx.x; i < 64 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3f803f80u;
+  asm volatile("fence.proxy.async.shared::cta;");
+  __syncthreads();
+  const uint32_t tmem = tmem_holder;
+  if (WARP_UNIFORM ? warp == 0 : threadIdx.x == 0) {
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | (8u << 24);
+    const uint32_t a0 = smem_u32(smem), b0 = smem_u32(smem + 48 * 1024);
+    const uint32_t lboA = 128 * 16 * 2;  // A: 2 K-halves
+    long long t0 = clock64();
+    int acc = 0, arow = 0;
+    for (int i = 0; i < iters; ++i) {
+      const uint32_t a = a0 + (uint32_t)(arow * a_stride_rows) * 16;
+      const uint64_t ad = desc(a, lboA, 128), bd = desc(b0, n * 16, 128);
+      const uint32_t d = tmem + (uint32_t)(acc * n);
+      const uint32_t accum = i >= naccs ? 1u : 0u;
+      if (WARP_UNIFORM)
+        asm volatile("{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                     "elect.sync _|e, 0xffffffff;\n\t"
+                     "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+                     "l"(ad), "l"(bd), "r"(idesc), "r"(accum));
+      else
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                     "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+                     "l"(ad), "l"(bd), "r"(idesc), "r"(accum));
+      if (++acc == naccs) acc = 0;
+      if (++arow == 8) arow = 0;
+    }
+    if (!WARP_UNIFORM || (threadIdx.x & 31) == 0)
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)));
+    uint32_t ok = 0;
+    while (!ok)
+      asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\tselp.u32 %0,1,0,p;\n\t}"
+                   : "=r"(ok) : "r"(smem_u32(&bar)));
+    long long t1 = clock64();
+    if ((threadIdx.x & 31) == 0) out[blockIdx.x] = t1 - t0;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+int main() {
+  long long* d_out;
+  cudaMalloc(&d_out, 148 * sizeof(long long));
+  cudaFuncSetAttribute(bench<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  cudaFuncSetAttribute(bench<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  const int iters = 4096;
+  printf("uniform N  naccs  grid  cycles/mma\n");
+  for (int uni : {0, 1})
+  for (int grid : {1})
+    for (int n : {16, 32, 64, 128, 256})
+      for (int naccs : {1, 2, 4, 8, 16}) {
+        if (naccs * n > 512) continue;
+        if (uni) bench<true><<<grid, 128, 64 * 1024>>>(n, naccs, iters, 16, d_out);
+        else bench<false><<<grid, 128, 64 * 1024>>>(n, naccs, iters, 16, d_out);
+        cudaError_t e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
+        long long h[148];
+        cudaMemcpy(h, d_out, grid * sizeof(long long), cudaMemcpyDeviceToHost);
+        long long mx = 0;
+        for (int i = 0; i < grid; ++i) mx = h[i] > mx ? h[i] : mx;
+        printf("%d %3d %5d %5d %8.1f\n", uni, n, naccs, grid, (double)mx / iters);
+      }
+  return 0;
+}
