@@ -1,4 +1,10 @@
 // tcgen05 implicit-GEMM convolution kernel (see tc_conv.cuh for the design).
+//
+// The kernel is specialised at compile time on (N, geometry, dual, precision scheme):
+// every tap table is constexpr, so the MMA warp's per-chunk issue stream unrolls into a
+// few uniform adds per tcgen05.mma (measured: a runtime-table issue loop spent ~200
+// cycles per MMA; tools/mma_bench.cu shows an M=128 SS-mode MMA completes in 39-48
+// cycles for N = 16..64).
 #include <algorithm>
 #include <cstring>
 
@@ -16,6 +22,11 @@ constexpr int kEpiWarps = 4;
 constexpr int kThreads = (kEpiWarp0 + kEpiWarps) * 32;
 constexpr int kMaxSmem = 227 * 1024;
 
+// precision schemes
+constexpr int kNpmBf16 = 0;    // one pass: A_hi x B_hi
+constexpr int kNpm3 = 1;       // hi*hi + lo*hi + hi*lo, three MMAs of width N
+constexpr int kNpmConcat = 2;  // A_hi x [B_hi | B_lo] (width 2N) + A_lo x B_hi (width N)
+
 struct Params {
   TcLayerDesc d;
   PlBuf src[2];
@@ -28,6 +39,41 @@ struct Params {
   uint32_t tmem_cols;
   int relu0;
 };
+
+// ---- compile-time tap tables (must match plane_taps() on the host) ----------------
+// S1:  t = ky*3+kx, shift (ky-1, kx-1)
+// S2:  plane (py,px) = (dy != 0, dx != 0); shift (dy == -1 ? -1 : 0, dx == -1 ? -1 : 0),
+//      taps of a plane in (ky, kx) order
+// T:   t = ph*4 + a*2 + b, accumulator ph, shift (py + a - 1, px + b - 1)
+__host__ __device__ constexpr int ntaps(int mode, int pl) {
+  return mode == CONV3_S1 ? 9 : mode == CONVT4_S2 ? 16 : (pl == 0 ? 1 : pl == 3 ? 4 : 2);
+}
+__host__ __device__ constexpr int tap_dy(int mode, int pl, int t) {
+  return mode == CONV3_S1    ? t / 3 - 1
+         : mode == CONVT4_S2 ? (t / 4 >> 1) + ((t >> 1) & 1) - 1
+         : pl == 2           ? (t == 0 ? -1 : 0)
+         : pl == 3           ? (t < 2 ? -1 : 0)
+                             : 0;
+}
+__host__ __device__ constexpr int tap_dx(int mode, int pl, int t) {
+  return mode == CONV3_S1    ? t % 3 - 1
+         : mode == CONVT4_S2 ? ((t / 4) & 1) + (t & 1) - 1
+         : pl == 1           ? (t == 0 ? -1 : 0)
+         : pl == 3           ? ((t & 1) == 0 ? -1 : 0)
+                             : 0;
+}
+__host__ __device__ constexpr int tap_acc(int mode, int t) { return mode == CONVT4_S2 ? t / 4 : 0; }
+// first tap touching its accumulator (in chunk 0 = plane 0, channel group 0)
+__host__ __device__ constexpr bool tap_first(int mode, int t) {
+  return mode == CONVT4_S2 ? (t & 3) == 0 : t == 0;
+}
+// minimum shift over a plane's taps, as a*L + b
+__host__ __device__ constexpr int plane_lo_a(int mode, int pl) {
+  return mode == CONV3_S2 ? (pl >= 2 ? -1 : 0) : -1;
+}
+__host__ __device__ constexpr int plane_lo_b(int mode, int pl) {
+  return mode == CONV3_S2 ? ((pl & 1) ? -1 : 0) : -1;
+}
 
 // ---- PTX helpers -----------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -73,23 +119,30 @@ __device__ __forceinline__ void tc_fence_before() {
 __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
-// Warp-collective: one elected lane issues (the warp must be converged).
-__device__ __forceinline__ void tc_mma_elect(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
-                                             uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
+// Issue from one lane of a converged warp: all lanes run the loop, `leader` issues.
+__device__ __forceinline__ void tc_mma(bool leader, uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t idesc, uint32_t accumulate) {
+  if (leader)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
 }
-__device__ __forceinline__ void tc_commit_elect(uint32_t bar) {
+__device__ __forceinline__ void tc_commit(bool leader, uint32_t bar) {
+  if (leader)
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ bool elect_one() {
+  uint32_t e;
   asm volatile(
       "{\n\t.reg .pred e;\n\t"
       "elect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
-      : "memory");
+      "selp.u32 %0, 1, 0, e;\n\t}"
+      : "=r"(e));
+  return e != 0;
 }
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   uint32_t r[16];
@@ -118,17 +171,62 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int n) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((128u >> 4) << 24);
 }
 
+// All MMAs of one staged chunk (plane PL).  Descriptors advance in 16-byte units
+// (one position of one 8-channel group = 16 B).
+template <int N, int MODE, int PL, bool DUAL, int NPM>
+__device__ __forceinline__ void issue_chunk(bool leader, uint64_t a0, uint64_t b0, uint32_t dslot,
+                                            int G, int L, bool first_chunk, uint32_t src_units,
+                                            uint32_t lo_units) {
+  constexpr int NT = ntaps(MODE, PL);
+  constexpr int NACC_SRC = MODE == CONVT4_S2 ? 4 : 1;
+  constexpr int NACC = (DUAL ? 2 : 1) * NACC_SRC;
+  constexpr int AW = NPM == kNpmConcat ? 2 * N : N;
+  constexpr uint32_t TAP_UNITS = (NPM == kNpmBf16 ? 32u * N : 64u * N) / 16u;
+  constexpr uint32_t BLO_UNITS = 32u * N / 16u;
+  constexpr uint32_t IDESC_N = idesc_bf16(N);
+  constexpr uint32_t IDESC_W = idesc_bf16(AW);
+  const int lo = plane_lo_a(MODE, PL) * L + plane_lo_b(MODE, PL);
+#pragma unroll
+  for (int s = 0; s < (DUAL ? 2 : 1); ++s) {
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      const int acc = s * NACC_SRC + tap_acc(MODE, t);
+      const uint64_t ad0 =
+          a0 + (uint32_t)s * src_units + (uint32_t)(tap_dy(MODE, PL, t) * L + tap_dx(MODE, PL, t) - lo);
+      const uint64_t bd = b0 + (uint32_t)(s * NT + t) * TAP_UNITS;
+      const uint32_t accum0 = (first_chunk && tap_first(MODE, t)) ? 0u : 1u;
+      uint64_t ad = ad0;
+      uint32_t dcol = dslot + (uint32_t)(acc * AW);
+      for (int g = 0; g < G; ++g, ad += 128, dcol += NACC * AW) {
+        if (NPM == kNpmBf16) {
+          tc_mma(leader, dcol, ad, bd, IDESC_N, accum0);
+        } else if (NPM == kNpmConcat) {
+          tc_mma(leader, dcol, ad, bd, IDESC_W, accum0);          // A_hi x [B_hi | B_lo]
+          tc_mma(leader, dcol, ad + lo_units, bd, IDESC_N, 1u);   // A_lo x B_hi
+        } else {
+          tc_mma(leader, dcol, ad, bd, IDESC_N, accum0);          // hi*hi
+          tc_mma(leader, dcol, ad + lo_units, bd, IDESC_N, 1u);   // lo*hi
+          tc_mma(leader, dcol, ad, bd + BLO_UNITS, IDESC_N, 1u);  // hi*lo
+        }
+      }
+    }
+  }
+}
 
 // ---- the kernel ----------------------------------------------------------------------
-template <int N>
+template <int N, int MODE, bool DUAL, int NPM>
 __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(1024) uint8_t smem[];
+  constexpr int NSRC = DUAL ? 2 : 1;
+  constexpr int NACC_SRC = MODE == CONVT4_S2 ? 4 : 1;
+  constexpr int NACC = NSRC * NACC_SRC;
+  constexpr int NPLANES = MODE == CONV3_S2 ? 4 : 1;
+  constexpr int NPASS_A = NPM == kNpmBf16 ? 1 : 2;
+  constexpr int AW = NPM == kNpmConcat ? 2 * N : N;  // TMEM columns per accumulator
   const TcLayerDesc& d = p.d;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_acc = d.n_src * d.n_acc_src;
   const int cgroups = d.cin / 16;
-  const int n_chunks = d.n_planes * cgroups;
-  const int npassA = d.npass == 3 ? 2 : 1;
+  const int n_chunks = NPLANES * cgroups;
 
   uint8_t* a_base = smem;
   uint8_t* b_base = smem + (size_t)p.stages * p.a_stage_bytes;
@@ -162,7 +260,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
-  const uint32_t src_bytes = (uint32_t)npassA * 2 * p.P_max * 16;
+  const uint32_t src_bytes = (uint32_t)NPASS_A * 2 * p.P_max * 16;
 
   if (warp == kProdWarp) {
     // ===================== producer: cp.async.bulk of A ranges + packed weights =========
@@ -181,15 +279,18 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
           const uint32_t a_bytes = (uint32_t)P * 16;
           const uint32_t w_bytes = (uint32_t)(d.chunk_off[c + 1] - d.chunk_off[c]);
           const uint32_t fb = smem_u32(&full[stage]);
-          mbar_arrive_expect_tx(fb, w_bytes + (uint32_t)d.n_src * npassA * 2 * a_bytes);
+          mbar_arrive_expect_tx(fb, w_bytes + (uint32_t)NSRC * NPASS_A * 2 * a_bytes);
           bulk_g2s(smem_u32(b_base + (size_t)stage * p.b_stage_bytes),
                    reinterpret_cast<const uint8_t*>(d.w) + d.chunk_off[c], w_bytes, fb);
           uint8_t* sa = a_base + (size_t)stage * p.a_stage_bytes;
-          for (int s = 0; s < d.n_src; ++s) {
+#pragma unroll
+          for (int s = 0; s < NSRC; ++s) {
             const PlBuf& S = p.src[s];
             const uint16_t* img =
-                S.base + (int64_t)b * S.img_stride + (int64_t)(S.planes == 4 ? pl : 0) * S.plane_stride;
-            for (int pass = 0; pass < npassA; ++pass)
+                S.base + (int64_t)b * S.img_stride + (int64_t)(NPLANES == 4 ? pl : 0) * S.plane_stride;
+#pragma unroll
+            for (int pass = 0; pass < NPASS_A; ++pass)
+#pragma unroll
               for (int cg8 = 0; cg8 < 2; ++cg8) {
                 const uint16_t* src = img + (S.block_index(cgi, pass, cg8) + q0 + pt.lo + S.off) * 8;
                 bulk_g2s(smem_u32(sa + (size_t)s * src_bytes + (size_t)(pass * 2 + cg8) * p.P_max * 16), src,
@@ -201,20 +302,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
     }
     __syncwarp();
   } else if (warp == kMmaWarp) {
-    // ===================== MMA issuer ===================================================
-    // The whole warp runs the (uniform) loop so descriptors live in uniform registers;
-    // elect.sync picks the lane that issues each tcgen05.mma / commit.  Descriptors are
-    // advanced by adding 16-byte units to the start-address field (one position = 16 B).
-    // concat: B = [B_hi | B_lo] along N, so A_hi x B is ONE MMA of width 2N producing
-    // hi*hi (cols 0..N) and hi*lo (cols N..2N); A_lo x B_hi accumulates into cols 0..N.
-    const int AW = d.concat ? 2 * N : N;  // TMEM columns per accumulator
-    const uint32_t idesc_n = idesc_bf16(N);
-    const uint32_t idesc_w = idesc_bf16(AW);
+    // ===================== MMA issuer: whole warp runs the loop, one lane issues ========
+    const bool leader = elect_one();
     const uint32_t lboA = (uint32_t)p.P_max * 16;
-    const uint32_t lboB = (uint32_t)(d.concat ? 2 * N : N) * 16;
-    const uint32_t tap_units = (uint32_t)(d.npass == 3 ? 64 * N : 32 * N) >> 4;  // per (src, tap)
-    const uint32_t lo_units = (2 * lboA) >> 4;   // A_lo plane offset
-    const uint32_t blo_units = (32u * N) >> 4;   // B_lo block offset (no concat)
+    const uint32_t lboB = (uint32_t)AW * 16;
+    const uint32_t src_units = src_bytes >> 4;
+    const uint32_t lo_units = (2 * lboA) >> 4;  // A_lo planes follow the A_hi planes
     uint32_t k = 0, ic = 0;
     for (int item = blockIdx.x; item < p.total_items; item += gridDim.x, ++ic) {
       const int slot = ic % p.slots;
@@ -223,44 +316,29 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
       __syncwarp();
       tc_fence_after();
       const uint32_t dslot = tmem_base + (uint32_t)slot * p.slot_cols;
-      uint32_t inited = 0;
       for (int c = 0; c < n_chunks; ++c, ++k) {
         const int stage = k % p.stages;
         const uint32_t phase = (k / p.stages) & 1;
         mbar_wait(smem_u32(&full[stage]), phase);
         __syncwarp();
         tc_fence_after();
-        const PlaneTaps& pt = d.planes[c / cgroups];
         const uint64_t a0 = smem_desc(smem_u32(a_base + (size_t)stage * p.a_stage_bytes), lboA, 128);
         const uint64_t b0 = smem_desc(smem_u32(b_base + (size_t)stage * p.b_stage_bytes), lboB, 128);
-        for (int s = 0; s < d.n_src; ++s) {
-          const uint64_t as = a0 + ((s * src_bytes) >> 4);
-          for (int t = 0; t < pt.n; ++t) {
-            const int acc = s * d.n_acc_src + pt.acc[t];
-            const uint64_t ad_t = as + (uint32_t)(pt.dy[t] * p.L + pt.dx[t] - pt.lo);
-            const uint64_t bd = b0 + (uint32_t)(s * pt.n + t) * tap_units;
-            for (int g = 0; g < p.G; ++g) {
-              const uint64_t ad = ad_t + (uint32_t)(g * 128);
-              const uint32_t dcol = dslot + (uint32_t)((g * n_acc + acc) * AW);
-              const uint32_t bit = 1u << (g * n_acc + acc);
-              const uint32_t accum = (inited & bit) ? 1u : 0u;
-              inited |= bit;
-              if (d.npass == 1) {
-                tc_mma_elect(dcol, ad, bd, idesc_n, accum);
-              } else if (d.concat) {
-                tc_mma_elect(dcol, ad, bd, idesc_w, accum);            // A_hi x [B_hi|B_lo]
-                tc_mma_elect(dcol, ad + lo_units, bd, idesc_n, 1u);    // A_lo x B_hi
-              } else {
-                tc_mma_elect(dcol, ad, bd, idesc_n, accum);            // hi*hi
-                tc_mma_elect(dcol, ad + lo_units, bd, idesc_n, 1u);    // lo*hi
-                tc_mma_elect(dcol, ad, bd + blo_units, idesc_n, 1u);   // hi*lo
-              }
-            }
+        const bool first = c == 0;
+        if constexpr (MODE == CONV3_S2) {
+          switch (c / cgroups) {
+            case 0: issue_chunk<N, MODE, 0, DUAL, NPM>(leader, a0, b0, dslot, p.G, p.L, first, src_units, lo_units); break;
+            case 1: issue_chunk<N, MODE, 1, DUAL, NPM>(leader, a0, b0, dslot, p.G, p.L, first, src_units, lo_units); break;
+            case 2: issue_chunk<N, MODE, 2, DUAL, NPM>(leader, a0, b0, dslot, p.G, p.L, first, src_units, lo_units); break;
+            default: issue_chunk<N, MODE, 3, DUAL, NPM>(leader, a0, b0, dslot, p.G, p.L, first, src_units, lo_units); break;
           }
+        } else {
+          issue_chunk<N, MODE, 0, DUAL, NPM>(leader, a0, b0, dslot, p.G, p.L, first, src_units, lo_units);
         }
-        tc_commit_elect(smem_u32(&empty[stage]));
+        __syncwarp();
+        tc_commit(leader, smem_u32(&empty[stage]));
       }
-      tc_commit_elect(smem_u32(&tfull[slot]));
+      tc_commit(leader, smem_u32(&tfull[slot]));
     }
     __syncwarp();
   } else {
@@ -268,8 +346,6 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
     const int ew = warp & 3;  // TMEM lane quarter accessible to this warp
     const int et = threadIdx.x - kEpiWarp0 * 32;
     uint32_t ic = 0;
-    const bool dual = d.n_src == 2;
-    const int AW = d.concat ? 2 * N : N;
     for (int item = blockIdx.x; item < p.total_items; item += gridDim.x, ++ic) {
       const int slot = ic % p.slots;
       const uint32_t sphase = (ic / p.slots) & 1;
@@ -277,6 +353,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
       const int it = item - b * p.items_per_image;
       const int q0 = it * p.G * 128;
       mbar_wait(smem_u32(&tfull[slot]), sphase);
+      __syncwarp();
       tc_fence_after();
       float gsum[N];
 #pragma unroll
@@ -287,37 +364,39 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
         const int y = q / p.L;
         const int x = q - y * p.L;
         const bool valid = y < p.Hp && x < p.Wp;
-        for (int ph = 0; ph < d.n_acc_src; ++ph) {
+#pragma unroll
+        for (int ph = 0; ph < NACC_SRC; ++ph) {
           int oy = y, ox = x;
-          if (d.mode == CONVT4_S2) {
+          if (MODE == CONVT4_S2) {
             oy = 2 * y + (ph >> 1);
             ox = 2 * x + (ph & 1);
           }
 #pragma unroll
           for (int j = 0; j < N; j += 16) {
             float a0[16], a1[16];
-            const uint32_t c0 = (uint32_t)((g * n_acc + ph) * AW + j);
-            const uint32_t c1 = (uint32_t)((g * n_acc + d.n_acc_src + ph) * AW + j);
+            const uint32_t c0 = (uint32_t)((g * NACC + ph) * AW + j);
+            const uint32_t c1 = (uint32_t)((g * NACC + NACC_SRC + ph) * AW + j);
             tmem_ld16(trow + c0, a0);
-            if (dual) tmem_ld16(trow + c1, a1);
-            if (d.concat) {  // + the hi*lo half of the concatenated accumulator
+            if (DUAL) tmem_ld16(trow + c1, a1);
+            if (NPM == kNpmConcat) {  // + the hi*lo half of the concatenated accumulator
               float h0[16], h1[16];
               tmem_ld16(trow + c0 + N, h0);
-              if (dual) tmem_ld16(trow + c1 + N, h1);
+              if (DUAL) tmem_ld16(trow + c1 + N, h1);
               tmem_wait_ld();
 #pragma unroll
               for (int i = 0; i < 16; ++i) {
                 a0[i] += h0[i];
-                if (dual) a1[i] += h1[i];
+                if (DUAL) a1[i] += h1[i];
               }
+            } else {
+              tmem_wait_ld();
             }
-            tmem_wait_ld();
             float v[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
               float t = a0[i] + __ldg(d.bias0 + j + i);
               if (p.relu0) t = fmaxf(t, 0.f);
-              if (dual) t = t + (a1[i] + __ldg(d.bias1 + j + i));
+              if (DUAL) t = t + (a1[i] + __ldg(d.bias1 + j + i));
               v[i] = t;
             }
             if (!valid) continue;
@@ -413,12 +492,17 @@ std::vector<HostTap> plane_taps(int mode, int pl) {
           t.push_back({ph, py + a - 1, px + bb - 1, ph * 4 + a * 2 + bb});
         }
   }
+  // the device's constexpr tables must agree with this host table
+  for (size_t i = 0; i < t.size(); ++i)
+    STDA_CHECK(t[i].dy == tap_dy(mode, pl, (int)i) && t[i].dx == tap_dx(mode, pl, (int)i) &&
+                   t[i].acc == tap_acc(mode, (int)i) && (int)t.size() == ntaps(mode, pl),
+               "internal: tap table mismatch");
   return t;
 }
 
-template <int N>
-void launch_n(const Params& p, int grid, size_t smem, cudaStream_t st) {
-  auto kern = tc_conv_kernel<N>;
+template <int N, int MODE, bool DUAL, int NPM>
+void launch_k(const Params& p, int grid, size_t smem, cudaStream_t st) {
+  auto kern = tc_conv_kernel<N, MODE, DUAL, NPM>;
   static uint64_t configured = 0;
   int dev = 0;
   STDA_CUDA(cudaGetDevice(&dev));
@@ -428,6 +512,24 @@ void launch_n(const Params& p, int grid, size_t smem, cudaStream_t st) {
   }
   kern<<<grid, kThreads, smem, st>>>(p);
   check_launch("tc_conv_kernel");
+}
+
+template <int N, int MODE, bool DUAL>
+void dispatch_npm(int npm, const Params& p, int grid, size_t smem, cudaStream_t st) {
+  switch (npm) {
+    case kNpmBf16: return launch_k<N, MODE, DUAL, kNpmBf16>(p, grid, smem, st);
+    case kNpm3: return launch_k<N, MODE, DUAL, kNpm3>(p, grid, smem, st);
+    default: return launch_k<N, MODE, DUAL, kNpmConcat>(p, grid, smem, st);
+  }
+}
+
+template <int N>
+void dispatch_mode(int mode, int npm, const Params& p, int grid, size_t smem, cudaStream_t st) {
+  switch (mode) {
+    case CONV3_S1: return dispatch_npm<N, CONV3_S1, false>(npm, p, grid, smem, st);
+    case CONV3_S2: return dispatch_npm<N, CONV3_S2, true>(npm, p, grid, smem, st);
+    default: return dispatch_npm<N, CONVT4_S2, true>(npm, p, grid, smem, st);
+  }
 }
 
 }  // namespace
@@ -440,6 +542,7 @@ bool tc_supported(int mode, int cin, int cout) {
 void tc_pack_layer(TcLayerDesc& d, int mode, int cin, int cout, const float* w0, const float* w1,
                    bool bf16, std::vector<uint16_t>& packed) {
   STDA_CHECK(tc_supported(mode, cin, cout), "layer shape not supported by the tensor-core path");
+  STDA_CHECK((mode == CONV3_S1) == (w1 == nullptr), "S1 layers are single-source, S2/T dual");
   std::memset(&d, 0, sizeof(d));
   d.mode = mode;
   d.n_src = w1 ? 2 : 1;
@@ -529,6 +632,7 @@ TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W) {
       lo = std::min(lo, sft);
       hi = std::max(hi, sft);
     }
+    STDA_CHECK(lo == plane_lo_a(d.mode, pl) * g.L + plane_lo_b(d.mode, pl), "internal: plane lo");
     pt.lo = (int16_t)lo;
     pt.hi = (int16_t)hi;
     span = std::max(span, hi - lo);
@@ -539,14 +643,16 @@ TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W) {
   for (int c = 0; c < d.n_planes * (d.cin / 16); ++c)
     b_stage = std::max<uint32_t>(b_stage, (uint32_t)(d.chunk_off[c + 1] - d.chunk_off[c]));
   const size_t fixed = 1024 + 64 + 4 * 64 * sizeof(float);
-  // largest G (M-tiles per item) with a >= 2-deep smem pipeline; else 1 stage at G = 1
+  // Prefer (1) a >= 2-deep smem pipeline, (2) two TMEM slots (the epilogue of item i
+  // overlaps the MMAs of item i+1), (3) the largest G; fall back step by step.
   bool ok = false;
-  for (int want_stages : {2, 1}) {
+  for (int pass = 0; pass < 3 && !ok; ++pass) {
+    const int want_stages = pass == 2 ? 1 : 2, want_slots = pass == 0 ? 2 : 1;
     for (int G : {4, 2, 1}) {
       const int P8 = (G * 128 + span + 7) / 8 * 8;
       const uint32_t a_stage = (uint32_t)d.n_src * npassA * 2 * P8 * 16;
       const int acc_cols = G * n_acc * d.cout * (d.concat ? 2 : 1);
-      if (acc_cols > 512 || G * n_acc > 32) continue;
+      if (acc_cols * want_slots > 512 || G * n_acc > 32) continue;
       int stages = 0;
       for (int st : {3, 2, 1})
         if ((size_t)st * (a_stage + b_stage) + fixed <= (size_t)kMaxSmem) {
@@ -557,7 +663,7 @@ TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W) {
       g.G = G;
       g.P_max = P8;
       g.stages = stages;
-      g.slots = 2 * acc_cols <= 512 ? 2 : 1;
+      g.slots = want_slots;
       g.a_stage_bytes = a_stage;
       g.b_stage_bytes = b_stage;
       g.smem_bytes = (size_t)stages * (a_stage + b_stage) + fixed;
@@ -567,7 +673,6 @@ TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W) {
       ok = true;
       break;
     }
-    if (ok) break;
   }
   STDA_CHECK(ok, "tensor-core conv: no tiling fits shared memory");
   const int positions = g.Hp * g.L;
@@ -611,10 +716,11 @@ void tc_launch(const TcLayerDesc& d, const TcGeometry& g, const PlBuf& src0, con
   STDA_CUDA(cudaGetDevice(&dev));
   STDA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const int grid = std::min(p.total_items, sms);
+  const int npm = d.npass == 1 ? kNpmBf16 : (d.concat ? kNpmConcat : kNpm3);
   switch (d.cout) {
-    case 16: return launch_n<16>(p, grid, g.smem_bytes, st);
-    case 32: return launch_n<32>(p, grid, g.smem_bytes, st);
-    case 64: return launch_n<64>(p, grid, g.smem_bytes, st);
+    case 16: return dispatch_mode<16>(d.mode, npm, p, grid, g.smem_bytes, st);
+    case 32: return dispatch_mode<32>(d.mode, npm, p, grid, g.smem_bytes, st);
+    case 64: return dispatch_mode<64>(d.mode, npm, p, grid, g.smem_bytes, st);
   }
   throw Error{"unsupported cout for the tensor-core path"};
 }

@@ -77,21 +77,22 @@ int main() {
   cudaFuncSetAttribute(bench<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
   cudaFuncSetAttribute(bench<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
   const int iters = 4096;
-  printf("uniform N  naccs  grid  cycles/mma\n");
-  for (int uni : {0, 1})
+  printf("uniform N  naccs  grid  a_stride_rows  cycles/mma\n");
+  for (int uni : {1})
   for (int grid : {1})
-    for (int n : {16, 32, 64, 128, 256})
-      for (int naccs : {1, 2, 4, 8, 16}) {
+   for (int astr : {16, 8, 4, 1, 3})
+    for (int n : {16, 32, 64})
+      for (int naccs : {1, 4}) {
         if (naccs * n > 512) continue;
-        if (uni) bench<true><<<grid, 128, 64 * 1024>>>(n, naccs, iters, 16, d_out);
-        else bench<false><<<grid, 128, 64 * 1024>>>(n, naccs, iters, 16, d_out);
+        if (uni) bench<true><<<grid, 128, 64 * 1024>>>(n, naccs, iters, astr, d_out);
+        else bench<false><<<grid, 128, 64 * 1024>>>(n, naccs, iters, astr, d_out);
         cudaError_t e = cudaDeviceSynchronize();
         if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
         long long h[148];
         cudaMemcpy(h, d_out, grid * sizeof(long long), cudaMemcpyDeviceToHost);
         long long mx = 0;
         for (int i = 0; i < grid; ++i) mx = h[i] > mx ? h[i] : mx;
-        printf("%d %3d %5d %5d %8.1f\n", uni, n, naccs, grid, (double)mx / iters);
+        printf("%d %3d %5d %5d %4d %8.1f\n", uni, n, naccs, grid, astr, (double)mx / iters);
       }
   return 0;
 }
