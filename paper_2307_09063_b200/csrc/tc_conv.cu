@@ -173,11 +173,13 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int n) {
 
 // All MMAs of one staged chunk (plane PL).  Descriptors advance in 16-byte units
 // (one position of one 8-channel group = 16 B).
-template <int N, int MODE, int PL, bool DUAL, int NPM>
-__device__ __forceinline__ void issue_chunk(bool leader, uint64_t a0, uint64_t b0, uint32_t dslot,
-                                            int G, int L, bool first_chunk, uint32_t src_units,
-                                            uint32_t lo_units) {
-  constexpr int NT = ntaps(MODE, PL);
+// The tap loop is NOT unrolled: the transposed-conv stream fully unrolled is ~60 KB of
+// SASS and thrashes the instruction cache (ncu: stall_no_inst); tap geometry is a few
+// uniform integer ops instead.
+template <int N, int MODE, bool DUAL, int NPM>
+__device__ __forceinline__ void issue_chunk(bool leader, int pl, uint64_t a0, uint64_t b0,
+                                            uint32_t dslot, int G, int L, bool first_chunk,
+                                            uint32_t src_units, uint32_t lo_units) {
   constexpr int NACC_SRC = MODE == CONVT4_S2 ? 4 : 1;
   constexpr int NACC = (DUAL ? 2 : 1) * NACC_SRC;
   constexpr int AW = NPM == kNpmConcat ? 2 * N : N;
@@ -185,18 +187,20 @@ __device__ __forceinline__ void issue_chunk(bool leader, uint64_t a0, uint64_t b
   constexpr uint32_t BLO_UNITS = 32u * N / 16u;
   constexpr uint32_t IDESC_N = idesc_bf16(N);
   constexpr uint32_t IDESC_W = idesc_bf16(AW);
-  const int lo = plane_lo_a(MODE, PL) * L + plane_lo_b(MODE, PL);
-#pragma unroll
+  const int nt = ntaps(MODE, pl);
+  const int lo = plane_lo_a(MODE, pl) * L + plane_lo_b(MODE, pl);
+#pragma unroll 1
   for (int s = 0; s < (DUAL ? 2 : 1); ++s) {
-#pragma unroll
-    for (int t = 0; t < NT; ++t) {
+#pragma unroll 1
+    for (int t = 0; t < nt; ++t) {
       const int acc = s * NACC_SRC + tap_acc(MODE, t);
       const uint64_t ad0 =
-          a0 + (uint32_t)s * src_units + (uint32_t)(tap_dy(MODE, PL, t) * L + tap_dx(MODE, PL, t) - lo);
-      const uint64_t bd = b0 + (uint32_t)(s * NT + t) * TAP_UNITS;
+          a0 + (uint32_t)s * src_units + (uint32_t)(tap_dy(MODE, pl, t) * L + tap_dx(MODE, pl, t) - lo);
+      const uint64_t bd = b0 + (uint32_t)(s * nt + t) * TAP_UNITS;
       const uint32_t accum0 = (first_chunk && tap_first(MODE, t)) ? 0u : 1u;
       uint64_t ad = ad0;
       uint32_t dcol = dslot + (uint32_t)(acc * AW);
+#pragma unroll 1
       for (int g = 0; g < G; ++g, ad += 128, dcol += NACC * AW) {
         if (NPM == kNpmBf16) {
           tc_mma(leader, dcol, ad, bd, IDESC_N, accum0);
@@ -324,17 +328,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
         tc_fence_after();
         const uint64_t a0 = smem_desc(smem_u32(a_base + (size_t)stage * p.a_stage_bytes), lboA, 128);
         const uint64_t b0 = smem_desc(smem_u32(b_base + (size_t)stage * p.b_stage_bytes), lboB, 128);
-        const bool first = c == 0;
-        if constexpr (MODE == CONV3_S2) {
-          switch (c / cgroups) {
-            case 0: issue_chunk<N, MODE, 0, DUAL, NPM>(leader, a0, b0, dslot, p.G, p.L, first, src_units, lo_units); break;
-            case 1: issue_chunk<N, MODE, 1, DUAL, NPM>(leader, a0, b0, dslot, p.G, p.L, first, src_units, lo_units); break;
-            case 2: issue_chunk<N, MODE, 2, DUAL, NPM>(leader, a0, b0, dslot, p.G, p.L, first, src_units, lo_units); break;
-            default: issue_chunk<N, MODE, 3, DUAL, NPM>(leader, a0, b0, dslot, p.G, p.L, first, src_units, lo_units); break;
-          }
-        } else {
-          issue_chunk<N, MODE, 0, DUAL, NPM>(leader, a0, b0, dslot, p.G, p.L, first, src_units, lo_units);
-        }
+        issue_chunk<N, MODE, DUAL, NPM>(leader, c / cgroups, a0, b0, dslot, p.G, p.L, c == 0, src_units,
+                                        lo_units);
         __syncwarp();
         tc_commit(leader, smem_u32(&empty[stage]));
       }
