@@ -36,6 +36,8 @@ struct Params {
   int G, stages, slots, items_per_image, total_items;
   int P_max;
   uint32_t a_stage_bytes, b_stage_bytes, slot_cols;
+  int resident;       // all packed weights loaded once into smem (else one chunk per stage)
+  uint32_t w_total;   // packed weight bytes of the layer
   uint32_t tmem_cols;
   int relu0;
 };
@@ -234,12 +236,15 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
 
   uint8_t* a_base = smem;
   uint8_t* b_base = smem + (size_t)p.stages * p.a_stage_bytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(b_base + (size_t)p.stages * p.b_stage_bytes);
+  const size_t b_region = p.resident ? (size_t)(p.w_total + 127) / 128 * 128
+                                     : (size_t)p.stages * p.b_stage_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(b_base + b_region);
   uint64_t* full = bars;
   uint64_t* empty = full + p.stages;
   uint64_t* tfull = empty + p.stages;
   uint64_t* tempty = tfull + p.slots;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + p.slots);
+  uint64_t* wbar = tempty + p.slots;  // resident weights landed
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(wbar + 1);
   float* red = reinterpret_cast<float*>(tmem_holder + 4);  // [4][N]
 
   if (threadIdx.x == 0) {
@@ -251,6 +256,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
       mbar_init(smem_u32(&tfull[s]), 1);
       mbar_init(smem_u32(&tempty[s]), kEpiWarps * 32);
     }
+    mbar_init(smem_u32(wbar), 1);
     fence_barrier_init();
   }
   if (warp == kMmaWarp) {
@@ -269,6 +275,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
   if (warp == kProdWarp) {
     // ===================== producer: cp.async.bulk of A ranges + packed weights =========
     if (lane == 0) {
+      if (p.resident) {
+        mbar_arrive_expect_tx(smem_u32(wbar), p.w_total);
+        bulk_g2s(smem_u32(b_base), d.w, p.w_total, smem_u32(wbar));
+      }
       uint32_t k = 0;
       for (int item = blockIdx.x; item < p.total_items; item += gridDim.x) {
         const int b = item / p.items_per_image;
@@ -281,11 +291,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
           const PlaneTaps& pt = d.planes[pl];
           const int P = p.G * 128 + pt.hi - pt.lo;
           const uint32_t a_bytes = (uint32_t)P * 16;
-          const uint32_t w_bytes = (uint32_t)(d.chunk_off[c + 1] - d.chunk_off[c]);
+          const uint32_t w_bytes = p.resident ? 0u : (uint32_t)(d.chunk_off[c + 1] - d.chunk_off[c]);
           const uint32_t fb = smem_u32(&full[stage]);
           mbar_arrive_expect_tx(fb, w_bytes + (uint32_t)NSRC * NPASS_A * 2 * a_bytes);
-          bulk_g2s(smem_u32(b_base + (size_t)stage * p.b_stage_bytes),
-                   reinterpret_cast<const uint8_t*>(d.w) + d.chunk_off[c], w_bytes, fb);
+          if (!p.resident)
+            bulk_g2s(smem_u32(b_base + (size_t)stage * p.b_stage_bytes),
+                     reinterpret_cast<const uint8_t*>(d.w) + d.chunk_off[c], w_bytes, fb);
           uint8_t* sa = a_base + (size_t)stage * p.a_stage_bytes;
 #pragma unroll
           for (int s = 0; s < NSRC; ++s) {
@@ -313,6 +324,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
     const uint32_t src_units = src_bytes >> 4;
     const uint32_t lo_units = (2 * lboA) >> 4;  // A_lo planes follow the A_hi planes
     uint32_t k = 0, ic = 0;
+    if (p.resident) {
+      mbar_wait(smem_u32(wbar), 0);
+      __syncwarp();
+    }
     for (int item = blockIdx.x; item < p.total_items; item += gridDim.x, ++ic) {
       const int slot = ic % p.slots;
       const uint32_t sphase = (ic / p.slots) & 1;
@@ -327,7 +342,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
         __syncwarp();
         tc_fence_after();
         const uint64_t a0 = smem_desc(smem_u32(a_base + (size_t)stage * p.a_stage_bytes), lboA, 128);
-        const uint64_t b0 = smem_desc(smem_u32(b_base + (size_t)stage * p.b_stage_bytes), lboB, 128);
+        const uint64_t b0 = smem_desc(
+            smem_u32(b_base + (p.resident ? (size_t)d.chunk_off[c] : (size_t)stage * p.b_stage_bytes)), lboB,
+            128);
         issue_chunk<N, MODE, DUAL, NPM>(leader, c / cgroups, a0, b0, dslot, p.G, p.L, c == 0, src_units,
                                         lo_units);
         __syncwarp();
@@ -637,9 +654,12 @@ TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W) {
   uint32_t b_stage = 0;
   for (int c = 0; c < d.n_planes * (d.cin / 16); ++c)
     b_stage = std::max<uint32_t>(b_stage, (uint32_t)(d.chunk_off[c + 1] - d.chunk_off[c]));
-  const size_t fixed = 1024 + 64 + 4 * 64 * sizeof(float);
+  const size_t fixed = 1024 + 80 + 4 * 64 * sizeof(float);
+  const uint32_t w_total = (uint32_t)d.chunk_off[d.n_planes * (d.cin / 16)];
+  const size_t w_res = (w_total + 127) / 128 * 128;
   // Prefer (1) a >= 2-deep smem pipeline, (2) two TMEM slots (the epilogue of item i
-  // overlaps the MMAs of item i+1), (3) the largest G; fall back step by step.
+  // overlaps the MMAs of item i+1), (3) the largest G, (4) resident weights (loaded once
+  // per CTA instead of once per work item); fall back step by step.
   bool ok = false;
   for (int pass = 0; pass < 3 && !ok; ++pass) {
     const int want_stages = pass == 2 ? 1 : 2, want_slots = pass == 0 ? 2 : 1;
@@ -648,25 +668,33 @@ TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W) {
       const uint32_t a_stage = (uint32_t)d.n_src * npassA * 2 * P8 * 16;
       const int acc_cols = G * n_acc * d.cout * (d.concat ? 2 : 1);
       if (acc_cols * want_slots > 512 || G * n_acc > 32) continue;
-      int stages = 0;
-      for (int st : {3, 2, 1})
-        if ((size_t)st * (a_stage + b_stage) + fixed <= (size_t)kMaxSmem) {
-          stages = st;
-          break;
+      for (bool resident : {true, false}) {
+        int stages = 0;
+        for (int st : {3, 2, 1}) {
+          const size_t need = resident ? (size_t)st * a_stage + w_res : (size_t)st * (a_stage + b_stage);
+          if (need + fixed <= (size_t)kMaxSmem) {
+            stages = st;
+            break;
+          }
         }
-      if (stages < want_stages) continue;
-      g.G = G;
-      g.P_max = P8;
-      g.stages = stages;
-      g.slots = want_slots;
-      g.a_stage_bytes = a_stage;
-      g.b_stage_bytes = b_stage;
-      g.smem_bytes = (size_t)stages * (a_stage + b_stage) + fixed;
-      int cols = 32;
-      while (cols < g.slots * acc_cols) cols *= 2;
-      g.tmem_cols = cols;
-      ok = true;
-      break;
+        if (stages < want_stages) continue;
+        g.G = G;
+        g.P_max = P8;
+        g.stages = stages;
+        g.slots = want_slots;
+        g.a_stage_bytes = a_stage;
+        g.b_stage_bytes = resident ? 0 : b_stage;
+        g.resident = resident;
+        g.w_total = w_total;
+        g.smem_bytes =
+            (resident ? (size_t)stages * a_stage + w_res : (size_t)stages * (a_stage + b_stage)) + fixed;
+        int cols = 32;
+        while (cols < g.slots * acc_cols) cols *= 2;
+        g.tmem_cols = cols;
+        ok = true;
+        break;
+      }
+      if (ok) break;
     }
   }
   STDA_CHECK(ok, "tensor-core conv: no tiling fits shared memory");
@@ -703,6 +731,8 @@ void tc_launch(const TcLayerDesc& d, const TcGeometry& g, const PlBuf& src0, con
   p.P_max = g.P_max;
   p.a_stage_bytes = g.a_stage_bytes;
   p.b_stage_bytes = g.b_stage_bytes;
+  p.resident = g.resident ? 1 : 0;
+  p.w_total = g.w_total;
   p.slot_cols = (uint32_t)(g.G * d.n_src * d.n_acc_src * d.cout * (d.concat ? 2 : 1));
   p.tmem_cols = (uint32_t)g.tmem_cols;
   p.relu0 = relu0 ? 1 : 0;
