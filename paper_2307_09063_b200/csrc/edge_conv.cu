@@ -1,9 +1,12 @@
 // Edge layers of the tensor-core path: the stem (F frames -> c0 channels, temporal
 // fusion, reference model.py:144-147) and the head (c0 -> 1, model.py:158,199).  Both
 // are too narrow for the tensor cores (Cin = 3 / Cout = 1) and bandwidth-shaped, so
-// they are dedicated FP32 SIMT kernels around the NHWC layout of the tcgen05 layers.
+// they are dedicated FP32 SIMT kernels.  The head is fused with the last ECA gate and
+// skip add (model.py:197-199): it reduces the GAP partials itself and stages
+// u = d * gate + skip straight from the decoder output and the stem's operand plane.
 //
 // Tile = 8 rows x 64 columns, 256 threads, 2 output pixels (rows r and r+4) per thread.
+// Staging loops issue kBatch independent loads per thread before consuming them.
 #include <algorithm>
 
 #include "edge_conv.cuh"
@@ -13,6 +16,7 @@ namespace {
 
 constexpr int kTH = 8, kTW = 64, kThreads = 256;
 constexpr int kIH = kTH + 2, kIW = kTW + 2;  // staged halo tile
+constexpr int kBatch = 8;
 
 // stem: x (Src: NCHW or window strides) -> relu(conv) written as operand planes:
 // PL over H x W (stage-1 conv input) and PP phase planes (stage-2 residual input).
@@ -27,17 +31,27 @@ __global__ void __launch_bounds__(kThreads) stem_planes_kernel(const float* __re
   const int tid = threadIdx.x;
   const int ty0 = blockIdx.y * kTH, tx0 = blockIdx.x * kTW;
   const int64_t b = b_base + blockIdx.z;
-  for (int e = tid; e < F * kIH * kIW; e += kThreads) {
-    const int ci = e / (kIH * kIW);
-    const int rem = e - ci * kIH * kIW;
-    const int r = rem / kIW, c = rem - r * kIW;
-    const int iy = ty0 - 1 + r, ix = tx0 - 1 + c;
-    float v = 0.f;
-    if (iy >= 0 && iy < H && ix >= 0 && ix < W) {
-      v = __ldg(x.x + b * x.xb + (int64_t)ci * x.xc + ((int64_t)iy * W + ix) * x.xp);
-      if (bf16) v = bf16_round(v);
+  const int n = F * kIH * kIW;
+  for (int e0 = tid; e0 < n; e0 += kBatch * kThreads) {
+    float v[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const int e = e0 + u * kThreads;
+      v[u] = 0.f;
+      if (e < n) {
+        const int ci = e / (kIH * kIW);
+        const int rem = e - ci * kIH * kIW;
+        const int r = rem / kIW, c = rem - r * kIW;
+        const int iy = ty0 - 1 + r, ix = tx0 - 1 + c;
+        if (iy >= 0 && iy < H && ix >= 0 && ix < W)
+          v[u] = __ldg(x.x + b * x.xb + (int64_t)ci * x.xc + ((int64_t)iy * W + ix) * x.xp);
+      }
     }
-    xs[e] = v;
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const int e = e0 + u * kThreads;
+      if (e < n) xs[e] = bf16 ? bf16_round(v[u]) : v[u];
+    }
   }
   const int c = tid & (kTW - 1), r0 = tid / kTW;  // rows r0 and r0 + 4
   const int ox = tx0 + c;
@@ -92,50 +106,80 @@ __global__ void __launch_bounds__(kThreads) stem_planes_kernel(const float* __re
   }
 }
 
-// head: u = d*g (+ s*gs) over NHWC C0 channels -> y [B][H][W] (one output channel).
+// head fused with the last ECA gate and skip add:
+//   y = bias + conv3x3(d * gate(d) + skip) over C0 channels, one output channel.
+// d: NHWC fp32 [B][H][W][C0] (decoder output); gap: its per-item channel sums
+// [B][items][C0]; skip: operand plane (PL over H x W) of the stem output.
 // weights [9][C0] (tap-major, channel fastest), bias[1].
-__global__ void __launch_bounds__(kThreads) head_nhwc_kernel(const float* __restrict__ w,
-                                                             const float* __restrict__ bias,
-                                                             const float* __restrict__ d,
-                                                             const float* __restrict__ g,
-                                                             const float* __restrict__ s,
-                                                             const float* __restrict__ gs, int C0,
-                                                             float* __restrict__ y, int H, int W,
-                                                             int bf16, int64_t b_base) {
+__global__ void __launch_bounds__(kThreads) head_fused_kernel(
+    const float* __restrict__ w, const float* __restrict__ bias, const float* __restrict__ gap, int items,
+    const float* __restrict__ eca_w, int k, const float* __restrict__ d, PlBuf skip, int C0,
+    float* __restrict__ y, int H, int W, int bf16, int64_t b_base) {
   extern __shared__ __align__(16) float sm[];
   const int CP = C0 + 4;                 // padded pixel stride: conflict-free float4 reads
-  const int Q = C0 / 4;
+  const int G8 = C0 / 8;
   float* us = sm;                        // [kIH*kIW][CP]
   float* ws = us + kIH * kIW * CP;       // [9][C0]
+  float* gate = ws + 9 * C0;             // [C0]
+  float* mean = gate + C0;               // [C0]
   const int tid = threadIdx.x;
   const int ty0 = blockIdx.y * kTH, tx0 = blockIdx.x * kTW;
   const int64_t b = b_base + blockIdx.z;
   for (int e = tid; e < 9 * C0; e += kThreads) ws[e] = __ldg(w + e);
-  for (int e = tid; e < kIH * kIW * Q; e += kThreads) {
-    const int pix = e / Q, j = e - pix * Q;
-    const int r = pix / kIW, c = pix - r * kIW;
-    const int iy = ty0 - 1 + r, ix = tx0 - 1 + c;
-    float4 u = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (iy >= 0 && iy < H && ix >= 0 && ix < W) {
-      const size_t off = (((size_t)b * H + iy) * W + ix) * C0 + 4 * j;
-      const float4 dv = __ldg(reinterpret_cast<const float4*>(d + off));
-      u = dv;
-      if (g) {
-        const float4 gv = __ldg(reinterpret_cast<const float4*>(g + (size_t)b * C0 + 4 * j));
-        u = make_float4(dv.x * gv.x, dv.y * gv.y, dv.z * gv.z, dv.w * gv.w);
-      }
-      if (s) {
-        float4 sv = __ldg(reinterpret_cast<const float4*>(s + off));
-        if (gs) {
-          const float4 h = __ldg(reinterpret_cast<const float4*>(gs + (size_t)b * C0 + 4 * j));
-          sv = make_float4(sv.x * h.x, sv.y * h.y, sv.z * h.z, sv.w * h.w);
-        }
-        u = make_float4(u.x + sv.x, u.y + sv.y, u.z + sv.z, u.w + sv.w);
-      }
-      if (bf16)
-        u = make_float4(bf16_round(u.x), bf16_round(u.y), bf16_round(u.z), bf16_round(u.w));
+  // ECA gate of this image (fixed-order reduction: identical in every CTA)
+  for (int ch = tid; ch < C0; ch += kThreads) {
+    float s = 0.f;
+    for (int t = 0; t < items; ++t) s += __ldg(gap + (b * items + t) * C0 + ch);
+    mean[ch] = s / (float)(H * W);
+  }
+  __syncthreads();
+  for (int ch = tid; ch < C0; ch += kThreads) {
+    float z = 0.f;
+    for (int j = 0; j < k; ++j) {
+      const int cc = ch + j - k / 2;
+      if (cc >= 0 && cc < C0) z = fmaf(__ldg(eca_w + j), mean[cc], z);
     }
-    *reinterpret_cast<float4*>(us + pix * CP + 4 * j) = u;
+    gate[ch] = 1.f / (1.f + expf(-z));
+  }
+  __syncthreads();
+  const int n = kIH * kIW * G8;
+  for (int e0 = tid; e0 < n; e0 += 4 * kThreads) {
+    float4 dv[4][2];
+    float sv[4][8];
+    bool ok[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + u * kThreads;
+      const int pix = e / G8, c8 = e - pix * G8;
+      const int r = pix / kIW, cc = pix - r * kIW;
+      const int iy = ty0 - 1 + r, ix = tx0 - 1 + cc;
+      ok[u] = e < n && iy >= 0 && iy < H && ix >= 0 && ix < W;
+      if (ok[u]) {
+        const float4* dp = reinterpret_cast<const float4*>(d + (((size_t)b * H + iy) * W + ix) * C0 + c8 * 8);
+        dv[u][0] = __ldg(dp);
+        dv[u][1] = __ldg(dp + 1);
+        pl_load8(skip, b, 0, c8, iy * skip.L + ix, sv[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + u * kThreads;
+      if (e >= n) break;
+      const int pix = e / G8, c8 = e - pix * G8;
+      float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      if (ok[u]) {
+        const float dd[8] = {dv[u][0].x, dv[u][0].y, dv[u][0].z, dv[u][0].w,
+                             dv[u][1].x, dv[u][1].y, dv[u][1].z, dv[u][1].w};
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          v[i] = dd[i] * gate[c8 * 8 + i] + sv[u][i];  // eca(d) + skip (model.py:197-198)
+          if (bf16) v[i] = bf16_round(v[i]);
+        }
+      }
+      float* dst = us + pix * CP + c8 * 8;
+      *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
+      *reinterpret_cast<float4*>(dst + 4) = make_float4(v[4], v[5], v[6], v[7]);
+    }
   }
   __syncthreads();
   const int c = tid & (kTW - 1), r0 = tid / kTW;
@@ -165,7 +209,7 @@ __global__ void __launch_bounds__(kThreads) head_nhwc_kernel(const float* __rest
 }
 
 template <typename K>
-void set_smem(K kern, size_t bytes) {
+void set_smem(K kern) {
   static uint64_t configured = 0;
   int dev = 0;
   STDA_CUDA(cudaGetDevice(&dev));
@@ -173,7 +217,6 @@ void set_smem(K kern, size_t bytes) {
     STDA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     configured |= 1ull << (dev & 63);
   }
-  (void)bytes;
 }
 
 }  // namespace
@@ -183,7 +226,7 @@ void launch_stem_planes(const float* w, const float* bias, const Src& x, int F, 
                         cudaStream_t st) {
   STDA_CHECK(C0 % 16 == 0, "stem kernel needs stem_channels % 16 == 0");
   const size_t smem = sizeof(float) * (F * kIH * kIW + F * 144);
-  set_smem(stem_planes_kernel, smem);
+  set_smem(stem_planes_kernel);
   for (int64_t b0 = 0; b0 < B; b0 += 65535) {
     dim3 grid(cdiv(W, kTW), cdiv(H, kTH), (unsigned)std::min<int64_t>(65535, B - b0));
     stem_planes_kernel<<<grid, kThreads, smem, st>>>(w, bias, x, F, C0, pl, pp, H, W, bf16, b0);
@@ -191,16 +234,17 @@ void launch_stem_planes(const float* w, const float* bias, const Src& x, int F, 
   }
 }
 
-void launch_head_nhwc(const float* w, const float* bias, const float* d, const float* g,
-                      const float* s, const float* gs, int C0, float* y, int64_t B, int H, int W,
-                      bool bf16, cudaStream_t st) {
-  STDA_CHECK(C0 % 4 == 0, "head kernel needs stem_channels % 4 == 0");
-  const size_t smem = sizeof(float) * ((size_t)kIH * kIW * (C0 + 4) + 9 * C0);
-  set_smem(head_nhwc_kernel, smem);
+void launch_head_fused(const float* w, const float* bias, const float* gap, int items,
+                       const float* eca_w, int k, const float* d, const PlBuf& skip, int C0, float* y,
+                       int64_t B, int H, int W, bool bf16, cudaStream_t st) {
+  STDA_CHECK(C0 % 8 == 0, "head kernel needs stem_channels % 8 == 0");
+  const size_t smem = sizeof(float) * ((size_t)kIH * kIW * (C0 + 4) + 9 * C0 + 2 * C0);
+  set_smem(head_fused_kernel);
   for (int64_t b0 = 0; b0 < B; b0 += 65535) {
     dim3 grid(cdiv(W, kTW), cdiv(H, kTH), (unsigned)std::min<int64_t>(65535, B - b0));
-    head_nhwc_kernel<<<grid, kThreads, smem, st>>>(w, bias, d, g, s, gs, C0, y, H, W, bf16, b0);
-    check_launch("head_nhwc_kernel");
+    head_fused_kernel<<<grid, kThreads, smem, st>>>(w, bias, gap, items, eca_w, k, d, skip, C0, y, H, W, bf16,
+                                                    b0);
+    check_launch("head_fused_kernel");
   }
 }
 

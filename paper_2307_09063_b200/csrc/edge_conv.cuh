@@ -14,10 +14,11 @@ void launch_stem_planes(const float* w, const float* bias, const Src& x, int F, 
                         const PlBuf& pl, const PlBuf& pp, int64_t B, int H, int W, bool bf16,
                         cudaStream_t st);
 
-// y[b][h][w] = bias + conv3x3(d*g + s*gs) over C0 NHWC channels; w [9][C0].
-// g == nullptr: d is already the combined input.
-void launch_head_nhwc(const float* w, const float* bias, const float* d, const float* g,
-                      const float* s, const float* gs, int C0, float* y, int64_t B, int H, int W,
-                      bool bf16, cudaStream_t st);
+// y[b][h][w] = bias + conv3x3(d * gate + skip) over C0 channels, gate = ECA of d computed
+// from its per-item channel sums gap [B][items][C0]; d NHWC fp32, skip a PL plane.
+// w [9][C0].
+void launch_head_fused(const float* w, const float* bias, const float* gap, int items,
+                       const float* eca_w, int k, const float* d, const PlBuf& skip, int C0, float* y,
+                       int64_t B, int H, int W, bool bf16, cudaStream_t st);
 
 }  // namespace stda

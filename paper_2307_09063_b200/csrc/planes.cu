@@ -6,29 +6,23 @@
 namespace stda {
 namespace {
 
-__global__ void zero_borders_kernel(ZeroList zl, int64_t B) {
-  // unit = one 16-byte position slot of one (image, plane, cg16, pass, cg8) block
-  for (int i = 0; i < zl.n; ++i) {
-    const PlBuf& p = zl.buf[i];
-    const int per_block = 2 * (p.L + 8) + p.Hp;  // top margin, bottom margin, pad column
-    const int blocks = p.planes * (p.C / 16) * p.np * 2;
-    const int64_t total = B * blocks * (int64_t)per_block;
-    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < total;
-         u += (int64_t)gridDim.x * blockDim.x) {
-      const int64_t bb = u / per_block;
-      const int r = (int)(u - bb * per_block);
-      const int64_t b = bb / blocks;
-      const int blk = (int)(bb - b * blocks);
-      const int plane = blk / ((p.C / 16) * p.np * 2);
-      const int inner = blk - plane * ((p.C / 16) * p.np * 2);
-      int q;
-      if (r < p.L + 8) q = -(p.L + 8) + r;                    // rows -2/-1 region
-      else if (r < 2 * (p.L + 8)) q = p.Hp * p.L + (r - (p.L + 8));  // row Hp (+ margin)
-      else q = (r - 2 * (p.L + 8)) * p.L + p.Wp;              // pad column of row y
-      uint16_t* dst = p.base + b * p.img_stride + (int64_t)plane * p.plane_stride +
-                      ((size_t)inner * p.Q + q + p.off) * 8;
-      *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
-    }
+// One CTA per (buffer, image, plane, cg16/pass/cg8 block); its threads zero the border
+// positions of that block: the top margin (rows -2/-1), the bottom margin (row Hp) and
+// the pad column of every row.  blocks_before[i] = first CTA index of buffer i.
+__global__ void zero_borders_kernel(ZeroList zl, ZeroOffsets zo) {
+  int i = 0;
+  while (i + 1 < zl.n && (int64_t)blockIdx.x >= zo.blocks_before[i + 1]) ++i;
+  const PlBuf& p = zl.buf[i];
+  const int64_t blk = blockIdx.x - zo.blocks_before[i];  // b * blocks_per_img + inner
+  uint16_t* base = p.base + blk * (int64_t)p.Q * 8;      // blocks are contiguous per image
+  const int margin = p.L + 8;
+  const int per_block = 2 * margin + p.Hp;
+  for (int r = threadIdx.x; r < per_block; r += blockDim.x) {
+    int q;
+    if (r < margin) q = -margin + r;                       // rows -2/-1 region
+    else if (r < 2 * margin) q = p.Hp * p.L + (r - margin);  // row Hp (+ margin)
+    else q = (r - 2 * margin) * p.L + p.Wp;                // pad column of row y
+    *reinterpret_cast<uint4*>(base + (size_t)(q + p.off) * 8) = make_uint4(0, 0, 0, 0);
   }
 }
 
@@ -61,28 +55,46 @@ __global__ void __launch_bounds__(kGateThreads) gate_apply_kernel(
   const int G8 = C / 8;
   const int pix0 = blockIdx.x * kPixPerCta;
   const int npix = min(kPixPerCta, H * W - pix0);
-  for (int u = threadIdx.x; u < npix * G8; u += blockDim.x) {
-    const int pl = u / G8, c8 = u - pl * G8;
-    const int pix = pix0 + pl;
-    const int y = pix / W, xx = pix - y * W;
-    const float* xp = x + ((size_t)b * H * W + pix) * C + c8 * 8;
-    const float4 a0 = __ldg(reinterpret_cast<const float4*>(xp));
-    const float4 a1 = __ldg(reinterpret_cast<const float4*>(xp) + 1);
-    float v[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+  constexpr int kB = 4;  // units whose loads are issued before any is consumed
+  const int n = npix * G8;
+  for (int u0 = threadIdx.x; u0 < n; u0 += kB * blockDim.x) {
+    float4 xa[kB][2];
+    float sk[kB][8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = v[i] * gate[c8 * 8 + i];  // eca(x) = x * gate
-    if (has_skip) {
-      float s[8];
-      pl_load8(skip, b, 0, c8, y * skip.L + xx, s);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] = v[i] + s[i];             // + skip (model.py:197-198)
+    for (int j = 0; j < kB; ++j) {
+      const int u = u0 + j * blockDim.x;
+      if (u >= n) break;
+      const int pl = u / G8, c8 = u - pl * G8;
+      const int pix = pix0 + pl;
+      const float* xp = x + ((size_t)b * H * W + pix) * C + c8 * 8;
+      xa[j][0] = __ldg(reinterpret_cast<const float4*>(xp));
+      xa[j][1] = __ldg(reinterpret_cast<const float4*>(xp) + 1);
+      if (has_skip) {
+        const int y = pix / W, xx = pix - y * W;
+        pl_load8(skip, b, 0, c8, y * skip.L + xx, sk[j]);
+      }
     }
-    if (has_pl) pl_store8(out_pl, b, 0, c8, y * out_pl.L + xx, v);
-    if (has_pp) pl_store8(out_pp, b, (y & 1) * 2 + (xx & 1), c8, (y >> 1) * out_pp.L + (xx >> 1), v);
-    if (out_f32) {
-      float* op = out_f32 + ((size_t)b * H * W + pix) * C + c8 * 8;
-      *reinterpret_cast<float4*>(op) = make_float4(v[0], v[1], v[2], v[3]);
-      *reinterpret_cast<float4*>(op + 4) = make_float4(v[4], v[5], v[6], v[7]);
+#pragma unroll
+    for (int j = 0; j < kB; ++j) {
+      const int u = u0 + j * blockDim.x;
+      if (u >= n) break;
+      const int pl = u / G8, c8 = u - pl * G8;
+      const int pix = pix0 + pl;
+      const int y = pix / W, xx = pix - y * W;
+      float v[8] = {xa[j][0].x, xa[j][0].y, xa[j][0].z, xa[j][0].w,
+                    xa[j][1].x, xa[j][1].y, xa[j][1].z, xa[j][1].w};
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        v[i] = v[i] * gate[c8 * 8 + i];                 // eca(x) = x * gate
+        if (has_skip) v[i] = v[i] + sk[j][i];           // + skip (model.py:197-198)
+      }
+      if (has_pl) pl_store8(out_pl, b, 0, c8, y * out_pl.L + xx, v);
+      if (has_pp) pl_store8(out_pp, b, (y & 1) * 2 + (xx & 1), c8, (y >> 1) * out_pp.L + (xx >> 1), v);
+      if (out_f32) {
+        float* op = out_f32 + ((size_t)b * H * W + pix) * C + c8 * 8;
+        *reinterpret_cast<float4*>(op) = make_float4(v[0], v[1], v[2], v[3]);
+        *reinterpret_cast<float4*>(op + 4) = make_float4(v[4], v[5], v[6], v[7]);
+      }
     }
   }
 }
@@ -91,7 +103,17 @@ __global__ void __launch_bounds__(kGateThreads) gate_apply_kernel(
 
 void launch_zero_borders(const ZeroList& zl, int64_t B, cudaStream_t st) {
   if (zl.n == 0 || B == 0) return;
-  zero_borders_kernel<<<148 * 4, 256, 0, st>>>(zl, B);
+  // (b, plane, cg16, pass, cg8) blocks of an image buffer are contiguous Q*8-element
+  // blocks: img_stride = planes * blocks_per_plane * Q * 8
+  ZeroOffsets zo;
+  int64_t total = 0;
+  for (int i = 0; i < zl.n; ++i) {
+    const PlBuf& p = zl.buf[i];
+    zo.blocks_before[i] = total;
+    total += B * (int64_t)p.planes * (p.C / 16) * p.np * 2;
+  }
+  STDA_CHECK(total < (1ll << 31), "zero_borders: too many blocks");
+  zero_borders_kernel<<<(unsigned)total, 128, 0, st>>>(zl, zo);
   check_launch("zero_borders_kernel");
 }
 

@@ -112,6 +112,9 @@ struct ZeroList {
   PlBuf buf[kMaxZeroBufs];
   int n = 0;
 };
+struct ZeroOffsets {
+  int64_t blocks_before[kMaxZeroBufs];
+};
 // zero every tap-reachable border position of each listed buffer (all images)
 void launch_zero_borders(const ZeroList& zl, int64_t B, cudaStream_t st);
 

@@ -339,16 +339,19 @@ void run_net_tc(const stda_plan& p, const Src& x, float* y, int64_t B, const Net
     mk.mark(st);
     h *= 2;
     wd *= 2;
-    // b_j = d_j * gate + skip  (model.py:197-198); the last one feeds the head as fp32
+    // b_j = d_j * gate + skip  (model.py:197-198); the last one is fused into the head
     const PlBuf& sk = skips[S - 1 - j];
-    const bool last = j + 1 == S;
-    launch_gate_apply(w.pd[j], g2.items_per_image, D.eca, k, w.d[j], &sk, last ? nullptr : &w.pl_b[j],
-                      nullptr, last ? w.s : nullptr, B, d2.cout, h, wd, st);
-    mk.mark(st);
-    if (!last) cur_pl = w.pl_b[j];
+    if (j + 1 < S) {
+      launch_gate_apply(w.pd[j], g2.items_per_image, D.eca, k, w.d[j], &sk, &w.pl_b[j], nullptr, nullptr, B,
+                        d2.cout, h, wd, st);
+      mk.mark(st);
+      cur_pl = w.pl_b[j];
+    } else {
+      launch_head_fused(p.head_wt, p.head.b, w.pd[j], g2.items_per_image, D.eca, k, w.d[j], sk, c0, y, B, h,
+                        wd, bf, st);
+      mk.mark(st);
+    }
   }
-  launch_head_nhwc(p.head_wt, p.head.b, w.s, nullptr, nullptr, nullptr, c0, y, B, h, wd, bf, st);
-  mk.mark(st);
 }
 
 void run_net(const stda_plan& p, const Src& x, float* y, int64_t B, const NetWs& w, cudaStream_t st,
@@ -409,9 +412,10 @@ std::string launch_names(const stda_config& c, bool tc) {
   for (int i = 0; i < c.stages; ++i)
     s += ";enc" + std::to_string(i) + ".s1;enc" + std::to_string(i) + ".s2;enc" + std::to_string(i) +
          ".gate";
-  for (int j = 0; j < c.stages; ++j)
-    s += ";dec" + std::to_string(j) + ".s1;dec" + std::to_string(j) + ".s2;dec" + std::to_string(j) +
-         ".gate";
+  for (int j = 0; j < c.stages; ++j) {
+    s += ";dec" + std::to_string(j) + ".s1;dec" + std::to_string(j) + ".s2";
+    if (!tc || j + 1 < c.stages) s += ";dec" + std::to_string(j) + ".gate";  // tc: last gate fused into head
+  }
   return s + ";head";
 }
 
@@ -537,7 +541,7 @@ void stda_plan_destroy(stda_plan* plan) {
 int stda_launches_per_forward(const stda_plan* plan) {
   if (!plan) return -1;
   if (plan->kind != 0) return 2;
-  return (plan->use_tc ? 3 : 2) + 6 * plan->cfg.stages;
+  return 2 + 6 * plan->cfg.stages;  // tensor-core path: +1 border zeroing, -1 gate fused in head
 }
 
 size_t stda_workspace_bytes(const stda_plan* plan, int64_t batch) {
