@@ -17,6 +17,7 @@ namespace {
 constexpr int kTH = 8, kTW = 64, kThreads = 256;
 constexpr int kIH = kTH + 2, kIW = kTW + 2;  // staged halo tile
 constexpr int kBatch = 8;
+constexpr int kHeadTH = 16;  // head tile rows (4 per thread x 4 thread rows)
 
 // stem: x (Src: NCHW or window strides) -> relu(conv) written as operand planes:
 // PL over H x W (stage-1 conv input) and PP phase planes (stage-2 residual input).
@@ -102,7 +103,16 @@ __global__ void __launch_bounds__(kThreads) stem_planes_kernel(const float* __re
         pl_store8(pl, b, 0, 2 * blk + h, oy * pl.L + ox, v);
         pl_store8(pp, b, (oy & 1) * 2 + (ox & 1), 2 * blk + h, (oy >> 1) * pp.L + (ox >> 1), v);
       }
+      // pad columns of the rows this thread ends (planes.cuh border contract)
+      if (blk == 0 && ox >= W - 2) {
+        if (ox == W - 1) pl_zero_pos(pl, b, 0, oy * pl.L + W);
+        pl_zero_pos(pp, b, (oy & 1) * 2 + (ox & 1), (oy >> 1) * pp.L + W / 2);
+      }
     }
+  }
+  if (blockIdx.x == 0 && blockIdx.y == 0) {  // top / bottom margins, once per image
+    pl_zero_margins(pl, b, tid, kThreads);
+    pl_zero_margins(pp, b, tid, kThreads);
   }
 }
 
@@ -116,6 +126,7 @@ __global__ void __launch_bounds__(kThreads) head_fused_kernel(
     const float* __restrict__ eca_w, int k, const float* __restrict__ d, PlBuf skip, int C0,
     float* __restrict__ y, int H, int W, int bf16, int64_t b_base) {
   extern __shared__ __align__(16) float sm[];
+  constexpr int kIH = kHeadTH + 2;       // head tile: 16 rows x 64 columns
   const int CP = C0 + 4;                 // padded pixel stride: conflict-free float4 reads
   const int G8 = C0 / 8;
   float* us = sm;                        // [kIH*kIW][CP]
@@ -123,7 +134,7 @@ __global__ void __launch_bounds__(kThreads) head_fused_kernel(
   float* gate = ws + 9 * C0;             // [C0]
   float* mean = gate + C0;               // [C0]
   const int tid = threadIdx.x;
-  const int ty0 = blockIdx.y * kTH, tx0 = blockIdx.x * kTW;
+  const int ty0 = blockIdx.y * kHeadTH, tx0 = blockIdx.x * kTW;
   const int64_t b = b_base + blockIdx.z;
   for (int e = tid; e < 9 * C0; e += kThreads) ws[e] = __ldg(w + e);
   // ECA gate of this image (fixed-order reduction: identical in every CTA)
@@ -182,29 +193,39 @@ __global__ void __launch_bounds__(kThreads) head_fused_kernel(
     }
   }
   __syncthreads();
-  const int c = tid & (kTW - 1), r0 = tid / kTW;
-  float a0 = 0.f, a1 = 0.f;
-  for (int t = 0; t < 9; ++t) {
-    const int ky = t / 3, kx = t % 3;
-    const float* p0 = us + ((r0 + ky) * kIW + c + kx) * CP;
-    const float* p1 = p0 + 4 * kIW * CP;
-    const float* wt = ws + t * C0;
-    for (int j = 0; j < C0; j += 4) {
-      const float4 w4 = *reinterpret_cast<const float4*>(wt + j);
-      const float4 u0 = *reinterpret_cast<const float4*>(p0 + j);
-      const float4 u1 = *reinterpret_cast<const float4*>(p1 + j);
-      a0 = fmaf(u0.x, w4.x, a0); a0 = fmaf(u0.y, w4.y, a0);
-      a0 = fmaf(u0.z, w4.z, a0); a0 = fmaf(u0.w, w4.w, a0);
-      a1 = fmaf(u1.x, w4.x, a1); a1 = fmaf(u1.y, w4.y, a1);
-      a1 = fmaf(u1.z, w4.z, a1); a1 = fmaf(u1.w, w4.w, a1);
+  // 4 consecutive output rows per thread: the 6 staged rows they need are read once
+  // per (column tap, channel quad) and reused by every row tap
+  const int c = tid & (kTW - 1), r0 = (tid / kTW) * 4;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int j = 0; j < C0; j += 4) {
+#pragma unroll
+    for (int kx = 0; kx < 3; ++kx) {
+      float4 u[6];
+#pragma unroll
+      for (int rr = 0; rr < 6; ++rr)
+        u[rr] = *reinterpret_cast<const float4*>(us + ((r0 + rr) * kIW + c + kx) * CP + j);
+#pragma unroll
+      for (int ky = 0; ky < 3; ++ky) {
+        const float4 w4 = *reinterpret_cast<const float4*>(ws + (ky * 3 + kx) * C0 + j);
+#pragma unroll
+        for (int o = 0; o < 4; ++o) {
+          const float4 v = u[o + ky];
+          acc[o] = fmaf(v.x, w4.x, acc[o]);
+          acc[o] = fmaf(v.y, w4.y, acc[o]);
+          acc[o] = fmaf(v.z, w4.z, acc[o]);
+          acc[o] = fmaf(v.w, w4.w, acc[o]);
+        }
+      }
     }
   }
   const float bv = __ldg(bias);
   const int ox = tx0 + c;
   if (ox < W) {
-    const int oy0 = ty0 + r0, oy1 = oy0 + 4;
-    if (oy0 < H) y[((size_t)b * H + oy0) * W + ox] = a0 + bv;
-    if (oy1 < H) y[((size_t)b * H + oy1) * W + ox] = a1 + bv;
+#pragma unroll
+    for (int o = 0; o < 4; ++o) {
+      const int oy = ty0 + r0 + o;
+      if (oy < H) y[((size_t)b * H + oy) * W + ox] = acc[o] + bv;
+    }
   }
 }
 
@@ -238,10 +259,11 @@ void launch_head_fused(const float* w, const float* bias, const float* gap, int 
                        const float* eca_w, int k, const float* d, const PlBuf& skip, int C0, float* y,
                        int64_t B, int H, int W, bool bf16, cudaStream_t st) {
   STDA_CHECK(C0 % 8 == 0, "head kernel needs stem_channels % 8 == 0");
-  const size_t smem = sizeof(float) * ((size_t)kIH * kIW * (C0 + 4) + 9 * C0 + 2 * C0);
+  const size_t smem = sizeof(float) * ((size_t)(kHeadTH + 2) * kIW * (C0 + 4) + 9 * C0 + 2 * C0);
+  STDA_CHECK(smem <= 200 * 1024, "head kernel: stem_channels too large for the smem tile");
   set_smem(head_fused_kernel);
   for (int64_t b0 = 0; b0 < B; b0 += 65535) {
-    dim3 grid(cdiv(W, kTW), cdiv(H, kTH), (unsigned)std::min<int64_t>(65535, B - b0));
+    dim3 grid(cdiv(W, kTW), cdiv(H, kHeadTH), (unsigned)std::min<int64_t>(65535, B - b0));
     head_fused_kernel<<<grid, kThreads, smem, st>>>(w, bias, gap, items, eca_w, k, d, skip, C0, y, H, W, bf16,
                                                     b0);
     check_launch("head_fused_kernel");

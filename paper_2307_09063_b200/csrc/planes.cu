@@ -27,7 +27,7 @@ __global__ void zero_borders_kernel(ZeroList zl, ZeroOffsets zo) {
 }
 
 constexpr int kGateThreads = 256;
-constexpr int kPixPerCta = 512;
+constexpr int kPixPerCta = 128;
 
 __global__ void __launch_bounds__(kGateThreads) gate_apply_kernel(
     const float* __restrict__ gap, int items, const float* __restrict__ eca_w, int k,
@@ -55,6 +55,10 @@ __global__ void __launch_bounds__(kGateThreads) gate_apply_kernel(
   const int G8 = C / 8;
   const int pix0 = blockIdx.x * kPixPerCta;
   const int npix = min(kPixPerCta, H * W - pix0);
+  if (blockIdx.x == 0) {  // top / bottom margins of the output planes, once per image
+    if (has_pl) pl_zero_margins(out_pl, b, threadIdx.x, blockDim.x);
+    if (has_pp) pl_zero_margins(out_pp, b, threadIdx.x, blockDim.x);
+  }
   constexpr int kB = 4;  // units whose loads are issued before any is consumed
   const int n = npix * G8;
   for (int u0 = threadIdx.x; u0 < n; u0 += kB * blockDim.x) {
@@ -90,6 +94,10 @@ __global__ void __launch_bounds__(kGateThreads) gate_apply_kernel(
       }
       if (has_pl) pl_store8(out_pl, b, 0, c8, y * out_pl.L + xx, v);
       if (has_pp) pl_store8(out_pp, b, (y & 1) * 2 + (xx & 1), c8, (y >> 1) * out_pp.L + (xx >> 1), v);
+      if (c8 == 0 && xx >= W - 2) {  // pad columns of the rows ending here
+        if (has_pl && xx == W - 1) pl_zero_pos(out_pl, b, 0, y * out_pl.L + W);
+        if (has_pp) pl_zero_pos(out_pp, b, (y & 1) * 2 + (xx & 1), (y >> 1) * out_pp.L + W / 2);
+      }
       if (out_f32) {
         float* op = out_f32 + ((size_t)b * H * W + pix) * C + c8 * 8;
         *reinterpret_cast<float4*>(op) = make_float4(v[0], v[1], v[2], v[3]);

@@ -107,6 +107,31 @@ __device__ __forceinline__ void pl_load8(const PlBuf& p, int64_t b, int plane, i
   }
 }
 
+// Border maintenance by the writers themselves (no separate zeroing pass):
+// the pad column of a row is zeroed by whichever thread writes that row's last column,
+// the top / bottom margins of an image by one CTA (or warp group) per image.
+__device__ __forceinline__ void pl_zero16(uint16_t* p) {
+  *reinterpret_cast<uint4*>(p) = make_uint4(0, 0, 0, 0);
+}
+// zero position q of every (cg16, pass, cg8) block of (b, plane)
+__device__ __forceinline__ void pl_zero_pos(const PlBuf& p, int64_t b, int plane, int q) {
+  uint16_t* img = p.base + b * p.img_stride + (int64_t)plane * p.plane_stride;
+  const int nblk = (p.C / 16) * p.np * 2;
+  for (int k = 0; k < nblk; ++k) pl_zero16(img + ((size_t)k * p.Q + q + p.off) * 8);
+}
+// top margin [-L-8, 0) and bottom margin [Hp*L, Hp*L+L+8) of all planes/blocks of image b,
+// split over `nthr` cooperating threads
+__device__ __forceinline__ void pl_zero_margins(const PlBuf& p, int64_t b, int tid, int nthr) {
+  const int margin = p.L + 8;
+  const int nblk = p.planes * (p.C / 16) * p.np * 2;
+  uint16_t* img = p.base + b * p.img_stride;  // blocks of one image are contiguous
+  for (int u = tid; u < nblk * 2 * margin; u += nthr) {
+    const int k = u / (2 * margin), r = u - k * 2 * margin;
+    const int q = r < margin ? -margin + r : p.Hp * p.L + (r - margin);
+    pl_zero16(img + ((size_t)k * p.Q + q + p.off) * 8);
+  }
+}
+
 constexpr int kMaxZeroBufs = 16;
 struct ZeroList {
   PlBuf buf[kMaxZeroBufs];

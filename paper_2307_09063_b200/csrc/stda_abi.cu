@@ -276,23 +276,11 @@ void run_net_tc(const stda_plan& p, const Src& x, float* y, int64_t B, const Net
   int h = c.map_height, wd = c.map_width;
   const int np = bf ? 1 : 2;
   mk.mark(st);
-  // zero the tap-reachable borders of every operand plane of this workspace
-  ZeroList zl;
-  auto add = [&](const PlBuf& b) {
-    STDA_CHECK(zl.n < kMaxZeroBufs, "too many operand planes");
-    if (b.base) zl.buf[zl.n++] = b;
-  };
-  add(w.pl_s);
-  add(w.pp_s);
-  for (const PlBuf& b : w.pl_a) add(b);
-  for (const PlBuf& b : w.pp_a) add(b);
-  for (const PlBuf& b : w.pl_b) add(b);
+  // Every operand plane is fully rewritten each forward by its writer, including the
+  // tap-reachable borders (pad column, top/bottom margins): no zeroing pass is needed.
   // stage-1 outputs: PP for encoder stride-2 consumers, PL for decoder ConvT consumers
   const std::vector<PlBuf>& mviews = w.pl_m;
   (void)np;
-  for (const PlBuf& b : mviews) add(b);
-  launch_zero_borders(zl, B, st);
-  mk.mark(st);
   launch_stem_planes(p.stem.w, p.stem.b, x, c.input_frames, c0, w.pl_s, w.pp_s, B, h, wd, bf, st);
   mk.mark(st);
   PlBuf cur_pl = w.pl_s, cur_pp = w.pp_s;
@@ -408,7 +396,7 @@ void run_net(const stda_plan& p, const Src& x, float* y, int64_t B, const NetWs&
 }
 
 std::string launch_names(const stda_config& c, bool tc) {
-  std::string s = tc ? "zero;stem" : "stem";
+  std::string s = "stem";
   for (int i = 0; i < c.stages; ++i)
     s += ";enc" + std::to_string(i) + ".s1;enc" + std::to_string(i) + ".s2;enc" + std::to_string(i) +
          ".gate";
@@ -541,7 +529,7 @@ void stda_plan_destroy(stda_plan* plan) {
 int stda_launches_per_forward(const stda_plan* plan) {
   if (!plan) return -1;
   if (plan->kind != 0) return 2;
-  return 2 + 6 * plan->cfg.stages;  // tensor-core path: +1 border zeroing, -1 gate fused in head
+  return (plan->use_tc ? 1 : 2) + 6 * plan->cfg.stages;  // tensor-core path: last gate fused in head
 }
 
 size_t stda_workspace_bytes(const stda_plan* plan, int64_t batch) {

@@ -376,6 +376,16 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
         const int y = q / p.L;
         const int x = q - y * p.L;
         const bool valid = y < p.Hp && x < p.Wp;
+        if (p.out.mode != 0 && y < p.Hp && x == p.Wp) {
+          // this position is a pad of the output grid: keep the operand plane's pad
+          // column zero (planes.cuh border contract)
+          if (p.out.mode == 1) {
+            pl_zero_pos(p.out.pl, b, 0, y * p.out.pl.L + p.Wp);
+          } else {
+            pl_zero_pos(p.out.pl, b, (y & 1) * 2, (y >> 1) * p.out.pl.L + p.Wp / 2);
+            pl_zero_pos(p.out.pl, b, (y & 1) * 2 + 1, (y >> 1) * p.out.pl.L + p.Wp / 2);
+          }
+        }
 #pragma unroll
         for (int ph = 0; ph < NACC_SRC; ++ph) {
           int oy = y, ox = x;
@@ -441,6 +451,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
       }
       tc_fence_before();
       mbar_arrive(smem_u32(&tempty[slot]));
+      if (p.out.mode != 0 && it == 0) pl_zero_margins(p.out.pl, b, et, kEpiWarps * 32);
       if (p.out.mode == 0 && p.out.gap) {
 #pragma unroll
         for (int c = 0; c < N; ++c) {
