@@ -1,0 +1,266 @@
+// tcgen05 implicit-GEMM convolution: host side (weight packing, tiling plan, launch).
+#include <algorithm>
+#include <cstring>
+
+#include "tc_kernel.cuh"
+
+namespace stda {
+namespace tc {
+
+using namespace detail;
+
+namespace {
+
+// ---- host helpers ------------------------------------------------------------------
+uint16_t bf16_bits(float v) {
+  const __nv_bfloat16 h = __float2bfloat16_rn(v);
+  uint16_t r;
+  std::memcpy(&r, &h, 2);
+  return r;
+}
+float bf16_val(float v) { return __bfloat162float(__float2bfloat16_rn(v)); }
+
+// tap tables; wk = index into the canonical per-(co,ci) weight vector
+struct HostTap {
+  int acc, dy, dx, wk;
+};
+
+std::vector<HostTap> plane_taps(int mode, int pl) {
+  std::vector<HostTap> t;
+  if (mode == CONV3_S1) {
+    for (int ky = 0; ky < 3; ++ky)
+      for (int kx = 0; kx < 3; ++kx) t.push_back({0, ky - 1, kx - 1, ky * 3 + kx});
+  } else if (mode == CONV3_S2) {
+    const int py = pl >> 1, px = pl & 1;
+    for (int ky = 0; ky < 3; ++ky)
+      for (int kx = 0; kx < 3; ++kx) {
+        const int dy = ky - 1, dx = kx - 1;
+        const int tpy = dy == 0 ? 0 : 1, tpx = dx == 0 ? 0 : 1;
+        if (tpy != py || tpx != px) continue;
+        t.push_back({0, dy == -1 ? -1 : 0, dx == -1 ? -1 : 0, ky * 3 + kx});
+      }
+  } else {
+    for (int ph = 0; ph < 4; ++ph)
+      for (int a = 0; a < 2; ++a)
+        for (int bb = 0; bb < 2; ++bb) {
+          const int py = ph >> 1, px = ph & 1;
+          t.push_back({ph, py + a - 1, px + bb - 1, ph * 4 + a * 2 + bb});
+        }
+  }
+  // the device's constexpr tables must agree with this host table
+  for (size_t i = 0; i < t.size(); ++i)
+    STDA_CHECK(t[i].dy == tap_dy(mode, pl, (int)i) && t[i].dx == tap_dx(mode, pl, (int)i) &&
+                   t[i].acc == tap_acc(mode, (int)i) && (int)t.size() == ntaps(mode, pl),
+               "internal: tap table mismatch");
+  return t;
+}
+
+}  // namespace
+
+bool tc_supported(int mode, int cin, int cout) {
+  (void)mode;
+  return cin % 16 == 0 && cin >= 16 && cin <= 64 && (cout == 16 || cout == 32 || cout == 64);
+}
+
+void tc_pack_layer(TcLayerDesc& d, int mode, int cin, int cout, const float* w0, const float* w1,
+                   bool bf16, std::vector<uint16_t>& packed) {
+  STDA_CHECK(tc_supported(mode, cin, cout), "layer shape not supported by the tensor-core path");
+  STDA_CHECK((mode == CONV3_S1) == (w1 == nullptr), "S1 layers are single-source, S2/T dual");
+  std::memset(&d, 0, sizeof(d));
+  d.mode = mode;
+  d.n_src = w1 ? 2 : 1;
+  d.cin = cin;
+  d.cout = cout;
+  d.n_planes = mode == CONV3_S2 ? 4 : 1;
+  d.n_acc_src = mode == CONVT4_S2 ? 4 : 1;
+  d.npass = bf16 ? 1 : 3;
+  const int npassB = bf16 ? 1 : 2;
+  const int wk_per = mode == CONVT4_S2 ? 16 : 9;
+  std::vector<std::vector<HostTap>> taps(d.n_planes);
+  for (int pl = 0; pl < d.n_planes; ++pl) {
+    taps[pl] = plane_taps(mode, pl);
+    PlaneTaps& pt = d.planes[pl];
+    pt.n = (int8_t)taps[pl].size();
+    for (size_t t = 0; t < taps[pl].size(); ++t) {
+      pt.acc[t] = (int8_t)taps[pl][t].acc;
+      pt.dy[t] = (int8_t)taps[pl][t].dy;
+      pt.dx[t] = (int8_t)taps[pl][t].dx;
+    }
+  }
+  const int cgroups = cin / 16;
+  const int n_chunks = d.n_planes * cgroups;
+  STDA_CHECK(n_chunks <= kMaxChunks, "too many K chunks");
+  packed.clear();
+  d.chunk_off[0] = 0;
+  const float* ws[2] = {w0, w1};
+  // hi/lo N-concatenation (one A_hi read for hi*hi and hi*lo) when the doubled
+  // accumulators still leave two TMEM slots at one M-tile per item
+  const int n_acc = d.n_src * d.n_acc_src;
+  d.concat = !bf16 && n_acc * 2 * cout * 2 <= 512;
+  // per (src, tap): concat -> [kgrp 2][pass 2][n][8] (kgrp row block = [B_hi; B_lo], 2N rows)
+  //                 else   -> [pass][kgrp 2][n][8]
+  auto put = [&](const float* w, int n, int ci, int wk, int pass) {
+    const float v = w[((size_t)n * cin + ci) * wk_per + wk];
+    const float hi = bf16_val(v);
+    packed.push_back(bf16_bits(pass == 0 ? v : v - hi));
+  };
+  for (int c = 0; c < n_chunks; ++c) {
+    const int pl = c / cgroups, cgi = c % cgroups;
+    for (int s = 0; s < d.n_src; ++s)
+      for (const HostTap& t : taps[pl]) {
+        if (d.concat) {
+          for (int kg = 0; kg < 2; ++kg)
+            for (int pass = 0; pass < 2; ++pass)
+              for (int n = 0; n < cout; ++n)
+                for (int e = 0; e < 8; ++e) put(ws[s], n, cgi * 16 + kg * 8 + e, t.wk, pass);
+        } else {
+          for (int pass = 0; pass < npassB; ++pass)
+            for (int kg = 0; kg < 2; ++kg)
+              for (int n = 0; n < cout; ++n)
+                for (int e = 0; e < 8; ++e) put(ws[s], n, cgi * 16 + kg * 8 + e, t.wk, pass);
+        }
+      }
+    d.chunk_off[c + 1] = (int64_t)packed.size() * 2;
+  }
+}
+
+TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W) {
+  TcGeometry g{};
+  g.B = B;
+  g.H = H;
+  g.W = W;
+  if (d.mode == CONV3_S2) {
+    g.Hp = H / 2;
+    g.Wp = W / 2;
+    g.Ho = H / 2;
+    g.Wo = W / 2;
+  } else if (d.mode == CONVT4_S2) {
+    g.Hp = H;
+    g.Wp = W;
+    g.Ho = 2 * H;
+    g.Wo = 2 * W;
+  } else {
+    g.Hp = H;
+    g.Wp = W;
+    g.Ho = H;
+    g.Wo = W;
+  }
+  g.L = g.Wp + 1;
+  int span = 0;
+  for (int pl = 0; pl < d.n_planes; ++pl) {
+    PlaneTaps& pt = d.planes[pl];
+    int lo = 1 << 30, hi = -(1 << 30);
+    for (int t = 0; t < pt.n; ++t) {
+      const int sft = pt.dy[t] * g.L + pt.dx[t];
+      lo = std::min(lo, sft);
+      hi = std::max(hi, sft);
+    }
+    STDA_CHECK(lo == plane_lo_a(d.mode, pl) * g.L + plane_lo_b(d.mode, pl), "internal: plane lo");
+    pt.lo = (int16_t)lo;
+    pt.hi = (int16_t)hi;
+    span = std::max(span, hi - lo);
+  }
+  const int n_acc = d.n_src * d.n_acc_src;
+  const int npassA = d.npass == 3 ? 2 : 1;
+  uint32_t b_stage = 0;
+  for (int c = 0; c < d.n_planes * (d.cin / 16); ++c)
+    b_stage = std::max<uint32_t>(b_stage, (uint32_t)(d.chunk_off[c + 1] - d.chunk_off[c]));
+  const size_t fixed = 1024 + 80 + 4 * 64 * sizeof(float);
+  const uint32_t w_total = (uint32_t)d.chunk_off[d.n_planes * (d.cin / 16)];
+  const size_t w_res = (w_total + 127) / 128 * 128;
+  // Prefer (1) a >= 2-deep smem pipeline, (2) two TMEM slots (the epilogue of item i
+  // overlaps the MMAs of item i+1), (3) the largest G, (4) resident weights (loaded once
+  // per CTA instead of once per work item); fall back step by step.
+  bool ok = false;
+  for (int pass = 0; pass < 3 && !ok; ++pass) {
+    const int want_stages = pass == 2 ? 1 : 2, want_slots = pass == 0 ? 2 : 1;
+    for (int G : {4, 2, 1}) {
+      const int P8 = (G * 128 + span + 7) / 8 * 8;
+      const uint32_t a_stage = (uint32_t)d.n_src * npassA * 2 * P8 * 16;
+      const int acc_cols = G * n_acc * d.cout * (d.concat ? 2 : 1);
+      if (acc_cols * want_slots > 512 || G * n_acc > 32) continue;
+      for (bool resident : {true, false}) {
+        int stages = 0;
+        for (int st : {3, 2, 1}) {
+          const size_t need = resident ? (size_t)st * a_stage + w_res : (size_t)st * (a_stage + b_stage);
+          if (need + fixed <= (size_t)kMaxSmem) {
+            stages = st;
+            break;
+          }
+        }
+        if (stages < want_stages) continue;
+        g.G = G;
+        g.P_max = P8;
+        g.stages = stages;
+        g.slots = want_slots;
+        g.a_stage_bytes = a_stage;
+        g.b_stage_bytes = resident ? 0 : b_stage;
+        g.resident = resident;
+        g.w_total = w_total;
+        g.smem_bytes =
+            (resident ? (size_t)stages * a_stage + w_res : (size_t)stages * (a_stage + b_stage)) + fixed;
+        int cols = 32;
+        while (cols < g.slots * acc_cols) cols *= 2;
+        g.tmem_cols = cols;
+        ok = true;
+        break;
+      }
+      if (ok) break;
+    }
+  }
+  STDA_CHECK(ok, "tensor-core conv: no tiling fits shared memory");
+  const int positions = g.Hp * g.L;
+  g.items_per_image = cdiv(positions, g.G * 128);
+  return g;
+}
+
+void tc_launch(const TcLayerDesc& d, const TcGeometry& g, const PlBuf& src0, const PlBuf* src1,
+               const TcOut& out, bool relu0, cudaStream_t st) {
+  Params p;
+  std::memset(&p, 0, sizeof(p));
+  p.d = d;
+  p.src[0] = src0;
+  if (src1) p.src[1] = *src1;
+  STDA_CHECK((src1 != nullptr) == (d.n_src == 2), "source count mismatch");
+  STDA_CHECK(src0.L == g.L && (!src1 || src1->L == g.L), "operand plane geometry mismatch");
+  STDA_CHECK(src0.np == (d.npass == 3 ? 2 : 1), "operand plane precision mismatch");
+  STDA_CHECK((d.mode == CONV3_S2) == (src0.planes == 4), "stride-2 convs read phase planes");
+  p.out = out;
+  p.H = g.H;
+  p.W = g.W;
+  p.C = d.cin;
+  p.Hp = g.Hp;
+  p.Wp = g.Wp;
+  p.L = g.L;
+  p.Ho = g.Ho;
+  p.Wo = g.Wo;
+  p.G = g.G;
+  p.stages = g.stages;
+  p.slots = g.slots;
+  p.items_per_image = g.items_per_image;
+  p.total_items = g.B * g.items_per_image;
+  p.P_max = g.P_max;
+  p.a_stage_bytes = g.a_stage_bytes;
+  p.b_stage_bytes = g.b_stage_bytes;
+  p.resident = g.resident ? 1 : 0;
+  p.w_total = g.w_total;
+  p.slot_cols = (uint32_t)(g.G * d.n_src * d.n_acc_src * d.cout * (d.concat ? 2 : 1));
+  p.tmem_cols = (uint32_t)g.tmem_cols;
+  p.relu0 = relu0 ? 1 : 0;
+  if (p.total_items == 0) return;
+  int dev = 0, sms = 148;
+  STDA_CUDA(cudaGetDevice(&dev));
+  STDA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int grid = std::min(p.total_items, sms);
+  const int npm = d.npass == 1 ? kNpmBf16 : (d.concat ? kNpmConcat : kNpm3);
+  STDA_CHECK(d.cout == 16 || d.cout == 32 || d.cout == 64, "unsupported cout for the tensor-core path");
+  STDA_CHECK(g.G == 1 || g.G == 2 || g.G == 4, "unsupported tile count per item");
+  switch (d.mode) {
+    case CONV3_S1: return dispatch_s1(d.cout, npm, g.G, p, grid, g.smem_bytes, st);
+    case CONV3_S2: return dispatch_s2(d.cout, npm, g.G, p, grid, g.smem_bytes, st);
+    default: return dispatch_t(d.cout, npm, g.G, p, grid, g.smem_bytes, st);
+  }
+}
+
+}  // namespace tc
+}  // namespace stda

@@ -1,19 +1,21 @@
-// tcgen05 implicit-GEMM convolution kernel (see tc_conv.cuh for the design).
+// tcgen05 implicit-GEMM convolution: device code (internal header of tc_conv_*.cu).
 //
-// The kernel is specialised at compile time on (N, geometry, dual, precision scheme):
-// every tap table is constexpr, so the MMA warp's per-chunk issue stream unrolls into a
-// few uniform adds per tcgen05.mma (measured: a runtime-table issue loop spent ~200
-// cycles per MMA; tools/mma_bench.cu shows an M=128 SS-mode MMA completes in 39-48
-// cycles for N = 16..64).
+// The kernel is specialised at compile time on (N, geometry, dual, precision scheme, G):
+// tap tables are constexpr and the per-chunk MMA stream is fully unrolled, so each
+// tcgen05.mma costs a few uniform adds to issue (tools/mma_bench.cu: an M=128 SS-mode
+// MMA executes in 39-48 cycles for N = 16..64, i.e. (A + B bytes) / 128 B/clk).
+// Instantiations are split by geometry over tc_conv_s1.cu / _s2.cu / _t.cu.
+#pragma once
+
 #include <algorithm>
 #include <cstring>
+#include <type_traits>
 
 #include "tc_conv.cuh"
 
 namespace stda {
 namespace tc {
-
-namespace {
+namespace detail {
 
 constexpr int kProdWarp = 0;   // lane 0: cp.async.bulk producer
 constexpr int kMmaWarp = 1;    // TMEM allocator + tcgen05.mma issuer
@@ -175,13 +177,15 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int n) {
 
 // All MMAs of one staged chunk (plane PL).  Descriptors advance in 16-byte units
 // (one position of one 8-channel group = 16 B).
-// The tap loop is NOT unrolled: the transposed-conv stream fully unrolled is ~60 KB of
-// SASS and thrashes the instruction cache (ncu: stall_no_inst); tap geometry is a few
-// uniform integer ops instead.
-template <int N, int MODE, bool DUAL, int NPM>
-__device__ __forceinline__ void issue_chunk(bool leader, int pl, uint64_t a0, uint64_t b0,
-                                            uint32_t dslot, int G, int L, bool first_chunk,
-                                            uint32_t src_units, uint32_t lo_units) {
+// All MMAs of one staged chunk (plane PL), fully unrolled over sources, taps and the G
+// M-tiles of the item (G is a template parameter): ~2-3 uniform ops per tcgen05.mma.
+// (A runtime tap/tile loop spent ~55 uniform instructions per tap, ~110 cycles per MMA;
+// the unrolled stream is a few hundred instructions per chunk and stays in the I-cache.)
+template <int N, int MODE, int PL, bool DUAL, int NPM, int G>
+__device__ __forceinline__ void issue_chunk(bool leader, uint64_t a0, uint64_t b0, uint32_t dslot,
+                                            int L, bool first_chunk, uint32_t src_units,
+                                            uint32_t lo_units) {
+  constexpr int NT = ntaps(MODE, PL);
   constexpr int NACC_SRC = MODE == CONVT4_S2 ? 4 : 1;
   constexpr int NACC = (DUAL ? 2 : 1) * NACC_SRC;
   constexpr int AW = NPM == kNpmConcat ? 2 * N : N;
@@ -189,21 +193,20 @@ __device__ __forceinline__ void issue_chunk(bool leader, int pl, uint64_t a0, ui
   constexpr uint32_t BLO_UNITS = 32u * N / 16u;
   constexpr uint32_t IDESC_N = idesc_bf16(N);
   constexpr uint32_t IDESC_W = idesc_bf16(AW);
-  const int nt = ntaps(MODE, pl);
-  const int lo = plane_lo_a(MODE, pl) * L + plane_lo_b(MODE, pl);
-#pragma unroll 1
+  const int lo = plane_lo_a(MODE, PL) * L + plane_lo_b(MODE, PL);
+#pragma unroll
   for (int s = 0; s < (DUAL ? 2 : 1); ++s) {
-#pragma unroll 1
-    for (int t = 0; t < nt; ++t) {
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
       const int acc = s * NACC_SRC + tap_acc(MODE, t);
       const uint64_t ad0 =
-          a0 + (uint32_t)s * src_units + (uint32_t)(tap_dy(MODE, pl, t) * L + tap_dx(MODE, pl, t) - lo);
-      const uint64_t bd = b0 + (uint32_t)(s * nt + t) * TAP_UNITS;
+          a0 + (uint32_t)s * src_units + (uint32_t)(tap_dy(MODE, PL, t) * L + tap_dx(MODE, PL, t) - lo);
+      const uint64_t bd = b0 + (uint32_t)(s * NT + t) * TAP_UNITS;
       const uint32_t accum0 = (first_chunk && tap_first(MODE, t)) ? 0u : 1u;
-      uint64_t ad = ad0;
-      uint32_t dcol = dslot + (uint32_t)(acc * AW);
-#pragma unroll 1
-      for (int g = 0; g < G; ++g, ad += 128, dcol += NACC * AW) {
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const uint64_t ad = ad0 + (uint32_t)(g * 128);
+        const uint32_t dcol = dslot + (uint32_t)((g * NACC + acc) * AW);
         if (NPM == kNpmBf16) {
           tc_mma(leader, dcol, ad, bd, IDESC_N, accum0);
         } else if (NPM == kNpmConcat) {
@@ -220,7 +223,7 @@ __device__ __forceinline__ void issue_chunk(bool leader, int pl, uint64_t a0, ui
 }
 
 // ---- the kernel ----------------------------------------------------------------------
-template <int N, int MODE, bool DUAL, int NPM>
+template <int N, int MODE, bool DUAL, int NPM, int G>
 __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int NSRC = DUAL ? 2 : 1;
@@ -345,8 +348,16 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
         const uint64_t b0 = smem_desc(
             smem_u32(b_base + (p.resident ? (size_t)d.chunk_off[c] : (size_t)stage * p.b_stage_bytes)), lboB,
             128);
-        issue_chunk<N, MODE, DUAL, NPM>(leader, c / cgroups, a0, b0, dslot, p.G, p.L, c == 0, src_units,
-                                        lo_units);
+        if constexpr (MODE == CONV3_S2) {
+          switch (c / cgroups) {
+            case 0: issue_chunk<N, MODE, 0, DUAL, NPM, G>(leader, a0, b0, dslot, p.L, c == 0, src_units, lo_units); break;
+            case 1: issue_chunk<N, MODE, 1, DUAL, NPM, G>(leader, a0, b0, dslot, p.L, c == 0, src_units, lo_units); break;
+            case 2: issue_chunk<N, MODE, 2, DUAL, NPM, G>(leader, a0, b0, dslot, p.L, c == 0, src_units, lo_units); break;
+            default: issue_chunk<N, MODE, 3, DUAL, NPM, G>(leader, a0, b0, dslot, p.L, c == 0, src_units, lo_units); break;
+          }
+        } else {
+          issue_chunk<N, MODE, 0, DUAL, NPM, G>(leader, a0, b0, dslot, p.L, c == 0, src_units, lo_units);
+        }
         __syncwarp();
         tc_commit(leader, smem_u32(&empty[stage]));
       }
@@ -371,7 +382,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
 #pragma unroll
       for (int c = 0; c < N; ++c) gsum[c] = 0.f;
       const uint32_t trow = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)slot * p.slot_cols;
-      for (int g = 0; g < p.G; ++g) {
+      for (int g = 0; g < G; ++g) {
         const int q = q0 + g * 128 + ew * 32 + lane;
         const int y = q / p.L;
         const int x = q - y * p.L;
@@ -479,53 +490,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
   }
 }
 
-// ---- host helpers ------------------------------------------------------------------
-uint16_t bf16_bits(float v) {
-  const __nv_bfloat16 h = __float2bfloat16_rn(v);
-  uint16_t r;
-  std::memcpy(&r, &h, 2);
-  return r;
-}
-float bf16_val(float v) { return __bfloat162float(__float2bfloat16_rn(v)); }
-
-// tap tables; wk = index into the canonical per-(co,ci) weight vector
-struct HostTap {
-  int acc, dy, dx, wk;
-};
-
-std::vector<HostTap> plane_taps(int mode, int pl) {
-  std::vector<HostTap> t;
-  if (mode == CONV3_S1) {
-    for (int ky = 0; ky < 3; ++ky)
-      for (int kx = 0; kx < 3; ++kx) t.push_back({0, ky - 1, kx - 1, ky * 3 + kx});
-  } else if (mode == CONV3_S2) {
-    const int py = pl >> 1, px = pl & 1;
-    for (int ky = 0; ky < 3; ++ky)
-      for (int kx = 0; kx < 3; ++kx) {
-        const int dy = ky - 1, dx = kx - 1;
-        const int tpy = dy == 0 ? 0 : 1, tpx = dx == 0 ? 0 : 1;
-        if (tpy != py || tpx != px) continue;
-        t.push_back({0, dy == -1 ? -1 : 0, dx == -1 ? -1 : 0, ky * 3 + kx});
-      }
-  } else {
-    for (int ph = 0; ph < 4; ++ph)
-      for (int a = 0; a < 2; ++a)
-        for (int bb = 0; bb < 2; ++bb) {
-          const int py = ph >> 1, px = ph & 1;
-          t.push_back({ph, py + a - 1, px + bb - 1, ph * 4 + a * 2 + bb});
-        }
-  }
-  // the device's constexpr tables must agree with this host table
-  for (size_t i = 0; i < t.size(); ++i)
-    STDA_CHECK(t[i].dy == tap_dy(mode, pl, (int)i) && t[i].dx == tap_dx(mode, pl, (int)i) &&
-                   t[i].acc == tap_acc(mode, (int)i) && (int)t.size() == ntaps(mode, pl),
-               "internal: tap table mismatch");
-  return t;
-}
-
-template <int N, int MODE, bool DUAL, int NPM>
+template <int N, int MODE, bool DUAL, int NPM, int G>
 void launch_k(const Params& p, int grid, size_t smem, cudaStream_t st) {
-  auto kern = tc_conv_kernel<N, MODE, DUAL, NPM>;
+  auto kern = tc_conv_kernel<N, MODE, DUAL, NPM, G>;
   static uint64_t configured = 0;
   int dev = 0;
   STDA_CUDA(cudaGetDevice(&dev));
@@ -537,229 +504,34 @@ void launch_k(const Params& p, int grid, size_t smem, cudaStream_t st) {
   check_launch("tc_conv_kernel");
 }
 
-template <int N, int MODE, bool DUAL>
-void dispatch_npm(int npm, const Params& p, int grid, size_t smem, cudaStream_t st) {
-  switch (npm) {
-    case kNpmBf16: return launch_k<N, MODE, DUAL, kNpmBf16>(p, grid, smem, st);
-    case kNpm3: return launch_k<N, MODE, DUAL, kNpm3>(p, grid, smem, st);
-    default: return launch_k<N, MODE, DUAL, kNpmConcat>(p, grid, smem, st);
-  }
-}
-
-template <int N>
-void dispatch_mode(int mode, int npm, const Params& p, int grid, size_t smem, cudaStream_t st) {
-  switch (mode) {
-    case CONV3_S1: return dispatch_npm<N, CONV3_S1, false>(npm, p, grid, smem, st);
-    case CONV3_S2: return dispatch_npm<N, CONV3_S2, true>(npm, p, grid, smem, st);
-    default: return dispatch_npm<N, CONVT4_S2, true>(npm, p, grid, smem, st);
-  }
-}
-
-}  // namespace
-
-bool tc_supported(int mode, int cin, int cout) {
-  (void)mode;
-  return cin % 16 == 0 && cin >= 16 && cin <= 64 && (cout == 16 || cout == 32 || cout == 64);
-}
-
-void tc_pack_layer(TcLayerDesc& d, int mode, int cin, int cout, const float* w0, const float* w1,
-                   bool bf16, std::vector<uint16_t>& packed) {
-  STDA_CHECK(tc_supported(mode, cin, cout), "layer shape not supported by the tensor-core path");
-  STDA_CHECK((mode == CONV3_S1) == (w1 == nullptr), "S1 layers are single-source, S2/T dual");
-  std::memset(&d, 0, sizeof(d));
-  d.mode = mode;
-  d.n_src = w1 ? 2 : 1;
-  d.cin = cin;
-  d.cout = cout;
-  d.n_planes = mode == CONV3_S2 ? 4 : 1;
-  d.n_acc_src = mode == CONVT4_S2 ? 4 : 1;
-  d.npass = bf16 ? 1 : 3;
-  const int npassB = bf16 ? 1 : 2;
-  const int wk_per = mode == CONVT4_S2 ? 16 : 9;
-  std::vector<std::vector<HostTap>> taps(d.n_planes);
-  for (int pl = 0; pl < d.n_planes; ++pl) {
-    taps[pl] = plane_taps(mode, pl);
-    PlaneTaps& pt = d.planes[pl];
-    pt.n = (int8_t)taps[pl].size();
-    for (size_t t = 0; t < taps[pl].size(); ++t) {
-      pt.acc[t] = (int8_t)taps[pl][t].acc;
-      pt.dy[t] = (int8_t)taps[pl][t].dy;
-      pt.dx[t] = (int8_t)taps[pl][t].dx;
+template <int MODE, bool DUAL>
+void dispatch_mode(int n, int npm, int G, const Params& p, int grid, size_t smem, cudaStream_t st) {
+  auto by_g = [&](auto n_c, auto npm_c) {
+    constexpr int NN = decltype(n_c)::value, PM = decltype(npm_c)::value;
+    switch (G) {
+      case 1: return launch_k<NN, MODE, DUAL, PM, 1>(p, grid, smem, st);
+      case 2: return launch_k<NN, MODE, DUAL, PM, 2>(p, grid, smem, st);
+      default: return launch_k<NN, MODE, DUAL, PM, 4>(p, grid, smem, st);
     }
-  }
-  const int cgroups = cin / 16;
-  const int n_chunks = d.n_planes * cgroups;
-  STDA_CHECK(n_chunks <= kMaxChunks, "too many K chunks");
-  packed.clear();
-  d.chunk_off[0] = 0;
-  const float* ws[2] = {w0, w1};
-  // hi/lo N-concatenation (one A_hi read for hi*hi and hi*lo) when the doubled
-  // accumulators still leave two TMEM slots at one M-tile per item
-  const int n_acc = d.n_src * d.n_acc_src;
-  d.concat = !bf16 && n_acc * 2 * cout * 2 <= 512;
-  // per (src, tap): concat -> [kgrp 2][pass 2][n][8] (kgrp row block = [B_hi; B_lo], 2N rows)
-  //                 else   -> [pass][kgrp 2][n][8]
-  auto put = [&](const float* w, int n, int ci, int wk, int pass) {
-    const float v = w[((size_t)n * cin + ci) * wk_per + wk];
-    const float hi = bf16_val(v);
-    packed.push_back(bf16_bits(pass == 0 ? v : v - hi));
   };
-  for (int c = 0; c < n_chunks; ++c) {
-    const int pl = c / cgroups, cgi = c % cgroups;
-    for (int s = 0; s < d.n_src; ++s)
-      for (const HostTap& t : taps[pl]) {
-        if (d.concat) {
-          for (int kg = 0; kg < 2; ++kg)
-            for (int pass = 0; pass < 2; ++pass)
-              for (int n = 0; n < cout; ++n)
-                for (int e = 0; e < 8; ++e) put(ws[s], n, cgi * 16 + kg * 8 + e, t.wk, pass);
-        } else {
-          for (int pass = 0; pass < npassB; ++pass)
-            for (int kg = 0; kg < 2; ++kg)
-              for (int n = 0; n < cout; ++n)
-                for (int e = 0; e < 8; ++e) put(ws[s], n, cgi * 16 + kg * 8 + e, t.wk, pass);
-        }
-      }
-    d.chunk_off[c + 1] = (int64_t)packed.size() * 2;
-  }
-}
-
-TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W) {
-  TcGeometry g{};
-  g.B = B;
-  g.H = H;
-  g.W = W;
-  if (d.mode == CONV3_S2) {
-    g.Hp = H / 2;
-    g.Wp = W / 2;
-    g.Ho = H / 2;
-    g.Wo = W / 2;
-  } else if (d.mode == CONVT4_S2) {
-    g.Hp = H;
-    g.Wp = W;
-    g.Ho = 2 * H;
-    g.Wo = 2 * W;
-  } else {
-    g.Hp = H;
-    g.Wp = W;
-    g.Ho = H;
-    g.Wo = W;
-  }
-  g.L = g.Wp + 1;
-  int span = 0;
-  for (int pl = 0; pl < d.n_planes; ++pl) {
-    PlaneTaps& pt = d.planes[pl];
-    int lo = 1 << 30, hi = -(1 << 30);
-    for (int t = 0; t < pt.n; ++t) {
-      const int sft = pt.dy[t] * g.L + pt.dx[t];
-      lo = std::min(lo, sft);
-      hi = std::max(hi, sft);
+  auto by_npm = [&](auto n_c) {
+    switch (npm) {
+      case kNpmBf16: return by_g(n_c, std::integral_constant<int, kNpmBf16>{});
+      case kNpm3: return by_g(n_c, std::integral_constant<int, kNpm3>{});
+      default: return by_g(n_c, std::integral_constant<int, kNpmConcat>{});
     }
-    STDA_CHECK(lo == plane_lo_a(d.mode, pl) * g.L + plane_lo_b(d.mode, pl), "internal: plane lo");
-    pt.lo = (int16_t)lo;
-    pt.hi = (int16_t)hi;
-    span = std::max(span, hi - lo);
+  };
+  switch (n) {
+    case 16: return by_npm(std::integral_constant<int, 16>{});
+    case 32: return by_npm(std::integral_constant<int, 32>{});
+    default: return by_npm(std::integral_constant<int, 64>{});
   }
-  const int n_acc = d.n_src * d.n_acc_src;
-  const int npassA = d.npass == 3 ? 2 : 1;
-  uint32_t b_stage = 0;
-  for (int c = 0; c < d.n_planes * (d.cin / 16); ++c)
-    b_stage = std::max<uint32_t>(b_stage, (uint32_t)(d.chunk_off[c + 1] - d.chunk_off[c]));
-  const size_t fixed = 1024 + 80 + 4 * 64 * sizeof(float);
-  const uint32_t w_total = (uint32_t)d.chunk_off[d.n_planes * (d.cin / 16)];
-  const size_t w_res = (w_total + 127) / 128 * 128;
-  // Prefer (1) a >= 2-deep smem pipeline, (2) two TMEM slots (the epilogue of item i
-  // overlaps the MMAs of item i+1), (3) the largest G, (4) resident weights (loaded once
-  // per CTA instead of once per work item); fall back step by step.
-  bool ok = false;
-  for (int pass = 0; pass < 3 && !ok; ++pass) {
-    const int want_stages = pass == 2 ? 1 : 2, want_slots = pass == 0 ? 2 : 1;
-    for (int G : {4, 2, 1}) {
-      const int P8 = (G * 128 + span + 7) / 8 * 8;
-      const uint32_t a_stage = (uint32_t)d.n_src * npassA * 2 * P8 * 16;
-      const int acc_cols = G * n_acc * d.cout * (d.concat ? 2 : 1);
-      if (acc_cols * want_slots > 512 || G * n_acc > 32) continue;
-      for (bool resident : {true, false}) {
-        int stages = 0;
-        for (int st : {3, 2, 1}) {
-          const size_t need = resident ? (size_t)st * a_stage + w_res : (size_t)st * (a_stage + b_stage);
-          if (need + fixed <= (size_t)kMaxSmem) {
-            stages = st;
-            break;
-          }
-        }
-        if (stages < want_stages) continue;
-        g.G = G;
-        g.P_max = P8;
-        g.stages = stages;
-        g.slots = want_slots;
-        g.a_stage_bytes = a_stage;
-        g.b_stage_bytes = resident ? 0 : b_stage;
-        g.resident = resident;
-        g.w_total = w_total;
-        g.smem_bytes =
-            (resident ? (size_t)stages * a_stage + w_res : (size_t)stages * (a_stage + b_stage)) + fixed;
-        int cols = 32;
-        while (cols < g.slots * acc_cols) cols *= 2;
-        g.tmem_cols = cols;
-        ok = true;
-        break;
-      }
-      if (ok) break;
-    }
-  }
-  STDA_CHECK(ok, "tensor-core conv: no tiling fits shared memory");
-  const int positions = g.Hp * g.L;
-  g.items_per_image = cdiv(positions, g.G * 128);
-  return g;
 }
 
-void tc_launch(const TcLayerDesc& d, const TcGeometry& g, const PlBuf& src0, const PlBuf* src1,
-               const TcOut& out, bool relu0, cudaStream_t st) {
-  Params p;
-  std::memset(&p, 0, sizeof(p));
-  p.d = d;
-  p.src[0] = src0;
-  if (src1) p.src[1] = *src1;
-  STDA_CHECK((src1 != nullptr) == (d.n_src == 2), "source count mismatch");
-  STDA_CHECK(src0.L == g.L && (!src1 || src1->L == g.L), "operand plane geometry mismatch");
-  STDA_CHECK(src0.np == (d.npass == 3 ? 2 : 1), "operand plane precision mismatch");
-  STDA_CHECK((d.mode == CONV3_S2) == (src0.planes == 4), "stride-2 convs read phase planes");
-  p.out = out;
-  p.H = g.H;
-  p.W = g.W;
-  p.C = d.cin;
-  p.Hp = g.Hp;
-  p.Wp = g.Wp;
-  p.L = g.L;
-  p.Ho = g.Ho;
-  p.Wo = g.Wo;
-  p.G = g.G;
-  p.stages = g.stages;
-  p.slots = g.slots;
-  p.items_per_image = g.items_per_image;
-  p.total_items = g.B * g.items_per_image;
-  p.P_max = g.P_max;
-  p.a_stage_bytes = g.a_stage_bytes;
-  p.b_stage_bytes = g.b_stage_bytes;
-  p.resident = g.resident ? 1 : 0;
-  p.w_total = g.w_total;
-  p.slot_cols = (uint32_t)(g.G * d.n_src * d.n_acc_src * d.cout * (d.concat ? 2 : 1));
-  p.tmem_cols = (uint32_t)g.tmem_cols;
-  p.relu0 = relu0 ? 1 : 0;
-  if (p.total_items == 0) return;
-  int dev = 0, sms = 148;
-  STDA_CUDA(cudaGetDevice(&dev));
-  STDA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const int grid = std::min(p.total_items, sms);
-  const int npm = d.npass == 1 ? kNpmBf16 : (d.concat ? kNpmConcat : kNpm3);
-  switch (d.cout) {
-    case 16: return dispatch_mode<16>(d.mode, npm, p, grid, g.smem_bytes, st);
-    case 32: return dispatch_mode<32>(d.mode, npm, p, grid, g.smem_bytes, st);
-    case 64: return dispatch_mode<64>(d.mode, npm, p, grid, g.smem_bytes, st);
-  }
-  throw Error{"unsupported cout for the tensor-core path"};
-}
+void dispatch_s1(int n, int npm, int G, const Params& p, int grid, size_t smem, cudaStream_t st);
+void dispatch_s2(int n, int npm, int G, const Params& p, int grid, size_t smem, cudaStream_t st);
+void dispatch_t(int n, int npm, int G, const Params& p, int grid, size_t smem, cudaStream_t st);
 
+}  // namespace detail
 }  // namespace tc
 }  // namespace stda
