@@ -10,6 +10,7 @@
 #include <algorithm>
 
 #include "edge_conv.cuh"
+#include "ptx.cuh"
 
 namespace stda {
 namespace {
@@ -229,6 +230,136 @@ __global__ void __launch_bounds__(kThreads) head_fused_kernel(
   }
 }
 
+// ---- row-block versions on the bulk-copy (TMA) engine --------------------------------
+// One CTA = R rows of one image; inputs are bulk-loaded contiguous row ranges, outputs of
+// the stem are staged as operand-plane row images and bulk-stored (pad columns included).
+constexpr int kRowThreads = 256;
+
+__device__ __forceinline__ void split_store(uint8_t* dst_hi, uint8_t* dst_lo, const float (&v)[8], int np) {
+  float hi[8], lo[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    hi[i] = bf16_round(v[i]);
+    lo[i] = v[i] - hi[i];
+  }
+  *reinterpret_cast<uint4*>(dst_hi) = make_uint4(pack_bf16x2(hi[0], hi[1]), pack_bf16x2(hi[2], hi[3]),
+                                                 pack_bf16x2(hi[4], hi[5]), pack_bf16x2(hi[6], hi[7]));
+  if (np == 2)
+    *reinterpret_cast<uint4*>(dst_lo) = make_uint4(pack_bf16x2(lo[0], lo[1]), pack_bf16x2(lo[2], lo[3]),
+                                                   pack_bf16x2(lo[4], lo[5]), pack_bf16x2(lo[6], lo[7]));
+}
+
+// stem: rows [y0, y0+R) of relu(conv3x3(x)) -> PL rows (H x W grid) and PP rows (planes).
+// x rows must be contiguous (x.xp == 1): frame ci row iy at x.x + b*xb + ci*xc + iy*W.
+__global__ void __launch_bounds__(kRowThreads) stem_rows_kernel(const float* __restrict__ w,
+                                                                const float* __restrict__ bias, Src x, int F,
+                                                                int C0, PlBuf pl, PlBuf pp, int H, int W, int R,
+                                                                int bf16, int64_t b_base) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t bar;
+  const int tid = threadIdx.x;
+  const int64_t b = b_base + blockIdx.y;
+  const int y0 = blockIdx.x * R;
+  const int np = pl.np, nblk = (C0 / 16) * np * 2, L = W + 1, Lp = W / 2 + 1;
+  auto al = [](size_t v) { return (v + 127) / 128 * 128; };
+  float* xs = reinterpret_cast<float*>(smem_raw);                 // [F][R+2][W]
+  float* ws = reinterpret_cast<float*>(smem_raw + al((size_t)F * (R + 2) * W * 4));  // [C0/16][F][9][16]
+  uint8_t* po = reinterpret_cast<uint8_t*>(ws) + al((size_t)C0 * F * 9 * 4);
+  const size_t po_blk = (size_t)R * L * 16;
+  uint8_t* pp_s = po + al(nblk * po_blk);
+  const size_t pp_blk = (size_t)(R / 2) * Lp * 16;
+  const int r_lo = max(y0 - 1, 0), r_hi = min(y0 + R + 1, H);  // rows present in the image
+  if (tid == 0) {
+    ptx::mbar_init(ptx::smem_u32(&bar), 1);
+    ptx::fence_barrier_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const uint32_t rb = (uint32_t)(r_hi - r_lo) * W * 4;
+    ptx::mbar_arrive_expect_tx(ptx::smem_u32(&bar), rb * F);
+    for (int ci = 0; ci < F; ++ci)
+      ptx::bulk_g2s(ptx::smem_u32(xs + ((size_t)ci * (R + 2) + (r_lo - (y0 - 1))) * W),
+                    x.x + b * x.xb + (int64_t)ci * x.xc + (int64_t)r_lo * W, rb, ptx::smem_u32(&bar));
+  }
+  for (int e = tid; e < C0 * F * 9; e += kRowThreads) ws[e] = __ldg(w + e);
+  // rows outside the image are zero (bulk copies only cover the present rows)
+  for (int ci = 0; ci < F; ++ci)
+    for (int e = tid; e < W; e += kRowThreads) {
+      if (y0 - 1 < 0) xs[((size_t)ci * (R + 2)) * W + e] = 0.f;
+      if (y0 + R >= H) xs[((size_t)ci * (R + 2) + R + 1) * W + e] = 0.f;
+    }
+  if (blockIdx.x == 0) {  // top / bottom margins of the output planes, once per image
+    pl_zero_margins(pl, b, tid, kRowThreads);
+    pl_zero_margins(pp, b, tid, kRowThreads);
+  }
+  ptx::mbar_wait(ptx::smem_u32(&bar), 0);
+  __syncthreads();
+  for (int pix = tid; pix < R * W; pix += kRowThreads) {
+    const int r = pix / W, xx = pix - r * W;
+    for (int blk = 0; blk < C0 / 16; ++blk) {
+      float acc[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) acc[q] = __ldg(bias + blk * 16 + q);
+      for (int ci = 0; ci < F; ++ci) {
+        const float* xc = xs + (size_t)ci * (R + 2) * W;
+        const float4* wc = reinterpret_cast<const float4*>(ws + ((size_t)blk * F + ci) * 144);
+#pragma unroll
+        for (int ky = 0; ky < 3; ++ky)
+#pragma unroll
+          for (int kx = 0; kx < 3; ++kx) {
+            const int ix = xx + kx - 1;
+            float v = (ix >= 0 && ix < W) ? xc[(r + ky) * W + ix] : 0.f;
+            if (bf16) v = bf16_round(v);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float4 w4 = wc[(ky * 3 + kx) * 4 + q];
+              acc[4 * q + 0] = fmaf(v, w4.x, acc[4 * q + 0]);
+              acc[4 * q + 1] = fmaf(v, w4.y, acc[4 * q + 1]);
+              acc[4 * q + 2] = fmaf(v, w4.z, acc[4 * q + 2]);
+              acc[4 * q + 3] = fmaf(v, w4.w, acc[4 * q + 3]);
+            }
+          }
+      }
+      const int plane = ((y0 + r) & 1) * 2 + (xx & 1);
+      const size_t pos_pl = (size_t)(r * L + xx) * 16, pos_pp = (size_t)((r >> 1) * Lp + (xx >> 1)) * 16;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = fmaxf(acc[8 * h + i], 0.f);
+        const int kh = (blk * np) * 2 + h;  // hi block of channel group 2*blk+h
+        split_store(po + kh * po_blk + pos_pl, po + (kh + 2) * po_blk + pos_pl, v, np);
+        uint8_t* ppl = pp_s + (size_t)plane * nblk * pp_blk;
+        split_store(ppl + kh * pp_blk + pos_pp, ppl + (kh + 2) * pp_blk + pos_pp, v, np);
+      }
+    }
+  }
+  for (int u = tid; u < R * nblk; u += kRowThreads) {  // pad columns of the staged rows
+    const int r = u / nblk, kb = u - r * nblk;
+    *reinterpret_cast<uint4*>(po + kb * po_blk + (size_t)(r * L + W) * 16) = make_uint4(0, 0, 0, 0);
+    if ((r & 1) == 0)
+      for (int plane = 0; plane < 4; ++plane)
+        *reinterpret_cast<uint4*>(pp_s + ((size_t)plane * nblk + kb) * pp_blk + (size_t)((r >> 1) * Lp + W / 2) * 16) =
+            make_uint4(0, 0, 0, 0);
+  }
+  ptx::fence_proxy_async();
+  __syncthreads();
+  if (tid == 0) {
+    uint16_t* img = pl.base + b * pl.img_stride;
+    for (int kb = 0; kb < nblk; ++kb)
+      ptx::bulk_s2g(img + ((size_t)kb * pl.Q + y0 * L + pl.off) * 8, ptx::smem_u32(po + kb * po_blk),
+                    (uint32_t)po_blk);
+    for (int plane = 0; plane < 4; ++plane) {
+      uint16_t* pimg = pp.base + b * pp.img_stride + (int64_t)plane * pp.plane_stride;
+      for (int kb = 0; kb < nblk; ++kb)
+        ptx::bulk_s2g(pimg + ((size_t)kb * pp.Q + (y0 / 2) * Lp + pp.off) * 8,
+                      ptx::smem_u32(pp_s + ((size_t)plane * nblk + kb) * pp_blk), (uint32_t)pp_blk);
+    }
+    ptx::bulk_commit();
+    ptx::bulk_wait_read();
+  }
+}
+
 template <typename K>
 void set_smem(K kern) {
   static uint64_t configured = 0;
@@ -246,6 +377,23 @@ void launch_stem_planes(const float* w, const float* bias, const Src& x, int F, 
                         const PlBuf& pl, const PlBuf& pp, int64_t B, int H, int W, bool bf16,
                         cudaStream_t st) {
   STDA_CHECK(C0 % 16 == 0, "stem kernel needs stem_channels % 16 == 0");
+  if (x.xp == 1 && H % 2 == 0 && W % 2 == 0 && W <= 1024) {
+    // bulk-copy row-block path: R rows (even, dividing H) with R*W ~ 256 pixels
+    int R = 2;
+    while (R * 2 * W <= 256 && H % (R * 2) == 0) R *= 2;
+    const int np = pl.np, nblk = (C0 / 16) * np * 2, L = W + 1, Lp = W / 2 + 1;
+    auto al = [](size_t v) { return (v + 127) / 128 * 128; };
+    const size_t smem = al((size_t)F * (R + 2) * W * 4) + al((size_t)C0 * F * 9 * 4) +
+                        al((size_t)nblk * R * L * 16) + al((size_t)4 * nblk * (R / 2) * Lp * 16);
+    STDA_CHECK(smem <= 200 * 1024, "stem: rows do not fit shared memory");
+    set_smem(stem_rows_kernel);
+    for (int64_t b0 = 0; b0 < B; b0 += 65535) {
+      dim3 grid(H / R, (unsigned)std::min<int64_t>(65535, B - b0));
+      stem_rows_kernel<<<grid, kRowThreads, smem, st>>>(w, bias, x, F, C0, pl, pp, H, W, R, bf16, b0);
+      check_launch("stem_rows_kernel");
+    }
+    return;
+  }
   const size_t smem = sizeof(float) * (F * kIH * kIW + F * 144);
   set_smem(stem_planes_kernel);
   for (int64_t b0 = 0; b0 < B; b0 += 65535) {

@@ -2,6 +2,7 @@
 #include <algorithm>
 
 #include "planes.cuh"
+#include "ptx.cuh"
 
 namespace stda {
 namespace {
@@ -107,6 +108,162 @@ __global__ void __launch_bounds__(kGateThreads) gate_apply_kernel(
   }
 }
 
+// Row-block gate + apply on the bulk-copy (TMA) engine: one CTA = R rows of one image.
+// Inputs are contiguous row ranges — x rows (NHWC fp32) and, per (cg16, pass, cg8) block,
+// the skip plane's positions [y0*L, (y0+R)*L) — bulk-loaded on an mbarrier; threads form
+// v = x*gate (+ skip), split hi/lo into shared-memory images of the output plane rows
+// (pad column included), and the row ranges go back with bulk stores.
+__global__ void __launch_bounds__(kGateThreads) gate_apply_rows_kernel(
+    const float* __restrict__ gap, int items, const float* __restrict__ eca_w, int k,
+    const float* __restrict__ x, PlBuf skip, int has_skip, PlBuf out_pl, int has_pl, PlBuf out_pp,
+    int has_pp, int C, int H, int W, int R) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  __shared__ float gate[1024];
+  __shared__ float mean[1024];
+  __shared__ __align__(8) uint64_t bar;
+  const int tid = threadIdx.x;
+  const int64_t b = blockIdx.y;
+  const int y0 = blockIdx.x * R;
+  const int G8 = C / 8;
+  const int nblk = (C / 16) * out_pl.np * 2;  // (cg16, pass, cg8) blocks per plane
+  const int L = W + 1, Lp = W / 2 + 1;
+  // shared-memory carve-up (all 128-byte aligned)
+  auto al = [](size_t v) { return (v + 127) / 128 * 128; };
+  float* xs = reinterpret_cast<float*>(smem_raw);
+  uint8_t* sk = smem_raw + al((size_t)R * W * C * 4);
+  const size_t sk_blk = (size_t)R * L * 16;
+  uint8_t* po = sk + (has_skip ? al(nblk * sk_blk) : 0);
+  const size_t po_blk = (size_t)R * L * 16;
+  uint8_t* pp = po + (has_pl ? al(nblk * po_blk) : 0);
+  const size_t pp_blk = (size_t)(R / 2) * Lp * 16;
+
+  if (tid == 0) {
+    ptx::mbar_init(ptx::smem_u32(&bar), 1);
+    ptx::fence_barrier_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const uint32_t xb = (uint32_t)R * W * C * 4;
+    const uint32_t sb = has_skip ? (uint32_t)(nblk * sk_blk) : 0u;
+    ptx::mbar_arrive_expect_tx(ptx::smem_u32(&bar), xb + sb);
+    ptx::bulk_g2s(ptx::smem_u32(xs), x + ((size_t)b * H + y0) * W * C, xb, ptx::smem_u32(&bar));
+    if (has_skip) {
+      const uint16_t* img = skip.base + b * skip.img_stride;
+      for (int kb = 0; kb < nblk; ++kb)
+        ptx::bulk_g2s(ptx::smem_u32(sk + kb * sk_blk), img + ((size_t)kb * skip.Q + y0 * L + skip.off) * 8,
+                      (uint32_t)sk_blk, ptx::smem_u32(&bar));
+    }
+  }
+  // ECA gate of this image while the copies fly (fixed order: identical in every CTA)
+  for (int c = tid; c < C; c += blockDim.x) {
+    float s = 0.f;
+    for (int t = 0; t < items; ++t) s += __ldg(gap + (b * items + t) * C + c);
+    mean[c] = s / (float)(H * W);
+  }
+  __syncthreads();
+  for (int c = tid; c < C; c += blockDim.x) {
+    float z = 0.f;
+    for (int j = 0; j < k; ++j) {
+      const int cc = c + j - k / 2;
+      if (cc >= 0 && cc < C) z = fmaf(__ldg(eca_w + j), mean[cc], z);
+    }
+    gate[c] = 1.f / (1.f + expf(-z));
+  }
+  if (blockIdx.x == 0) {  // top / bottom margins of the output planes, once per image
+    if (has_pl) pl_zero_margins(out_pl, b, tid, blockDim.x);
+    if (has_pp) pl_zero_margins(out_pp, b, tid, blockDim.x);
+  }
+  __syncthreads();
+  ptx::mbar_wait(ptx::smem_u32(&bar), 0);
+
+  const int np = out_pl.np;
+  const int n = R * W * G8;
+  for (int u = tid; u < n; u += blockDim.x) {
+    const int c8 = u % G8, pix = u / G8;
+    const int r = pix / W, xx = pix - r * W;
+    const float4 a0 = *reinterpret_cast<const float4*>(xs + (size_t)pix * C + c8 * 8);
+    const float4 a1 = *reinterpret_cast<const float4*>(xs + (size_t)pix * C + c8 * 8 + 4);
+    float v[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = v[i] * gate[c8 * 8 + i];  // eca(x) = x * gate
+    if (has_skip) {                                              // + skip (model.py:197-198)
+      const int kh = ((c8 >> 1) * np) * 2 + (c8 & 1);
+      const uint4 h = *reinterpret_cast<const uint4*>(sk + kh * sk_blk + (size_t)(r * L + xx) * 16);
+      const __nv_bfloat162* hb = reinterpret_cast<const __nv_bfloat162*>(&h);
+      float s[8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 f = __bfloat1622float2(hb[i]);
+        s[2 * i] = f.x;
+        s[2 * i + 1] = f.y;
+      }
+      if (np == 2) {
+        const uint4 l = *reinterpret_cast<const uint4*>(sk + (kh + 2) * sk_blk + (size_t)(r * L + xx) * 16);
+        const __nv_bfloat162* lb = reinterpret_cast<const __nv_bfloat162*>(&l);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 f = __bfloat1622float2(lb[i]);
+          s[2 * i] += f.x;
+          s[2 * i + 1] += f.y;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = v[i] + s[i];
+    }
+    float hi[8], lo[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      hi[i] = bf16_round(v[i]);
+      lo[i] = v[i] - hi[i];
+    }
+    const uint4 hv = make_uint4(pack_bf16x2(hi[0], hi[1]), pack_bf16x2(hi[2], hi[3]), pack_bf16x2(hi[4], hi[5]),
+                                pack_bf16x2(hi[6], hi[7]));
+    const uint4 lv = make_uint4(pack_bf16x2(lo[0], lo[1]), pack_bf16x2(lo[2], lo[3]), pack_bf16x2(lo[4], lo[5]),
+                                pack_bf16x2(lo[6], lo[7]));
+    const int kh = ((c8 >> 1) * np) * 2 + (c8 & 1);  // hi block of this 8-channel group
+    if (has_pl) {
+      *reinterpret_cast<uint4*>(po + kh * po_blk + (size_t)(r * L + xx) * 16) = hv;
+      if (np == 2) *reinterpret_cast<uint4*>(po + (kh + 2) * po_blk + (size_t)(r * L + xx) * 16) = lv;
+    }
+    if (has_pp) {
+      const int plane = ((y0 + r) & 1) * 2 + (xx & 1);
+      uint8_t* ppl = pp + (size_t)plane * nblk * pp_blk;
+      const size_t pos = (size_t)((r >> 1) * Lp + (xx >> 1)) * 16;
+      *reinterpret_cast<uint4*>(ppl + kh * pp_blk + pos) = hv;
+      if (np == 2) *reinterpret_cast<uint4*>(ppl + (kh + 2) * pp_blk + pos) = lv;
+    }
+  }
+  // pad columns of the staged rows
+  for (int u = tid; u < R * nblk; u += blockDim.x) {
+    const int r = u / nblk, kb = u - r * nblk;
+    if (has_pl) *reinterpret_cast<uint4*>(po + kb * po_blk + (size_t)(r * L + W) * 16) = make_uint4(0, 0, 0, 0);
+    if (has_pp && (r & 1) == 0)
+      for (int plane = 0; plane < 4; ++plane)
+        *reinterpret_cast<uint4*>(pp + ((size_t)plane * nblk + kb) * pp_blk + (size_t)((r >> 1) * Lp + W / 2) * 16) =
+            make_uint4(0, 0, 0, 0);
+  }
+  ptx::fence_proxy_async();
+  __syncthreads();
+  if (tid == 0) {
+    if (has_pl) {
+      uint16_t* img = out_pl.base + b * out_pl.img_stride;
+      for (int kb = 0; kb < nblk; ++kb)
+        ptx::bulk_s2g(img + ((size_t)kb * out_pl.Q + y0 * L + out_pl.off) * 8, ptx::smem_u32(po + kb * po_blk),
+                      (uint32_t)po_blk);
+    }
+    if (has_pp) {
+      for (int plane = 0; plane < 4; ++plane) {
+        uint16_t* img = out_pp.base + b * out_pp.img_stride + (int64_t)plane * out_pp.plane_stride;
+        for (int kb = 0; kb < nblk; ++kb)
+          ptx::bulk_s2g(img + ((size_t)kb * out_pp.Q + (y0 / 2) * Lp + out_pp.off) * 8,
+                        ptx::smem_u32(pp + ((size_t)plane * nblk + kb) * pp_blk), (uint32_t)pp_blk);
+      }
+    }
+    ptx::bulk_commit();
+    ptx::bulk_wait_read();
+  }
+}
+
 }  // namespace
 
 void launch_zero_borders(const ZeroList& zl, int64_t B, cudaStream_t st) {
@@ -130,6 +287,34 @@ void launch_gate_apply(const float* gap, int items, const float* eca_w, int k, c
                        int64_t B, int C, int H, int W, cudaStream_t st) {
   STDA_CHECK(C % 8 == 0 && C <= 1024, "gate_apply: channel count");
   STDA_CHECK(B <= 65535, "gate_apply: batch too large for one launch");
+  if (out_f32 == nullptr && out_pl != nullptr && C % 16 == 0 && H % 2 == 0 && W % 2 == 0) {
+    // bulk-copy row-block path: R rows per CTA, shared memory sized for the buffers used
+    const int np = out_pl->np, nblk = (C / 16) * np * 2, L = W + 1, Lp = W / 2 + 1;
+    auto al = [](size_t v) { return (v + 127) / 128 * 128; };
+    int R = 2;
+    auto bytes = [&](int r) {
+      return al((size_t)r * W * C * 4) + (skip ? al((size_t)nblk * r * L * 16) : 0) +
+             al((size_t)nblk * r * L * 16) + (out_pp ? al((size_t)4 * nblk * (r / 2) * Lp * 16) : 0);
+    };
+    while (R * 2 <= 8 && H % (R * 2) == 0 && (size_t)R * 2 * W <= 512 && bytes(R * 2) <= 96 * 1024) R *= 2;
+    const size_t smem = bytes(R);
+    STDA_CHECK(smem <= 200 * 1024, "gate_apply: rows do not fit shared memory");
+    static uint64_t configured = 0;
+    int dev = 0;
+    STDA_CUDA(cudaGetDevice(&dev));
+    if (!(configured >> (dev & 63) & 1)) {
+      STDA_CUDA(cudaFuncSetAttribute(gate_apply_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     200 * 1024));
+      configured |= 1ull << (dev & 63);
+    }
+    dim3 grid(H / R, (unsigned)B);
+    gate_apply_rows_kernel<<<grid, kGateThreads, smem, st>>>(gap, items, eca_w, k, x, skip ? *skip : PlBuf{},
+                                                             skip != nullptr, *out_pl, 1,
+                                                             out_pp ? *out_pp : PlBuf{}, out_pp != nullptr, C,
+                                                             H, W, R);
+    check_launch("gate_apply_rows_kernel");
+    return;
+  }
   dim3 grid(cdiv(H * W, kPixPerCta), (unsigned)B);
   gate_apply_kernel<<<grid, kGateThreads, 0, st>>>(
       gap, items, eca_w, k, x, skip ? *skip : PlBuf{}, skip != nullptr, out_pl ? *out_pl : PlBuf{},
