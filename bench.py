@@ -294,18 +294,22 @@ def run_engine(args, world, rank, local):
     achieved = flops_per_launch / (share[dom] * 1e-3) / 1e12
     total_flops = sum(fl.values())
 
-    # end-to-end through the public host-buffer API
-    x_host = x.cpu().pin_memory()
-    y_host = torch.empty((batch, 1, H, W), dtype=torch.float32).pin_memory()
-    for _ in range(2):
-        net.denoise_host(x_host, y_host)
+    # end-to-end through the public host-buffer API: a stream of e2e_steps batches in
+    # pinned host memory goes through ONE StdaNet.denoise_host call, which pipelines
+    # H2D / forward / D2H per batch-sized chunk on separate streams.  Every step's H2D of
+    # its inputs and D2H of its result are inside the timed region.
+    e2e_steps = max(3, min(32, args.steps // 4))
+    x_host = torch.empty((e2e_steps * batch, 3, H, W), dtype=torch.float32).pin_memory()
+    for s in range(e2e_steps):
+        x_host[s * batch:(s + 1) * batch].copy_(x)
+    y_host = torch.empty((e2e_steps * batch, 1, H, W), dtype=torch.float32).pin_memory()
+    net.denoise_host(x_host, y_host)                            # warm-up (plans, streams)
     barrier(world)
     t0 = time.perf_counter()
-    for _ in range(max(3, args.steps // 4)):
-        net.denoise_host(x_host, y_host)
+    net.denoise_host(x_host, y_host)
     e2e_s = max_over_ranks(time.perf_counter() - t0, world)
-    e2e_steps = max(3, args.steps // 4)
     e2e_rate = batch * world * e2e_steps / e2e_s
+    assert torch.equal(y_host[:batch], cap.replay().cpu()), "host path differs from device path"
 
     line = {
         "metric": METRIC, "value": value, "unit": "triplets/s", "n_gpus": world,
@@ -332,7 +336,8 @@ def run_engine(args, world, rank, local):
             "launch_share": {n: m / sum(avg) for n, m in share.items()},
         },
         "e2e": {"value": e2e_rate, "unit": "triplets/s",
-                "h2d_bytes_per_step": batch * 3 * H * W * 4, "d2h_bytes_per_step": batch * H * W * 4},
+                "h2d_bytes_per_step": batch * 3 * H * W * 4, "d2h_bytes_per_step": batch * H * W * 4,
+                "steps": e2e_steps, "api": "StdaNet.denoise_host (pinned host in/out, pipelined chunks)"},
         "clocks": clocks.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu:

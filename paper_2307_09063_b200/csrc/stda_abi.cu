@@ -611,7 +611,9 @@ int64_t stda_host_chunk(const stda_plan* plan, int64_t batch) {
   if (!plan || plan->kind != 0 || batch <= 0) return 0;
   const stda_config& c = plan->cfg;
   const int64_t per = (int64_t)c.input_frames * c.map_height * c.map_width * 4;
-  const int64_t chunk = std::max<int64_t>(1, (4ll << 20) / per);
+  // ~16 MB of input per chunk (64 triplets at 128x128): big enough for full-efficiency
+  // forwards, small enough that H2D / forward / D2H of neighbouring chunks overlap
+  const int64_t chunk = std::max<int64_t>(1, (16ll << 20) / per);
   return std::min(batch, chunk);
 }
 
