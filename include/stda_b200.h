@@ -128,6 +128,11 @@ int stda_synth_frames(uint64_t seed, int32_t scene, int64_t seq, int64_t first_f
 int stda_synth_triplets(uint64_t seed, int32_t scene, int64_t first_seq, int64_t batch,
                         int32_t frames, int32_t h, int32_t w, float* x, void* stream);
 
+/* ---- debug (no reference counterpart) ----
+ * Arm a one-shot clock64 timeline of CTA 0 for the launch_index-th following tensor-core
+ * conv launch; dev_buf holds 5 x 8192 uint64 (layout in csrc/tc_kernel.cuh, trace_at). */
+int stda_debug_trace(void* dev_buf, int32_t launch_index);
+
 #ifdef __cplusplus
 }
 #endif

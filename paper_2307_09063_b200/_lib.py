@@ -46,6 +46,7 @@ SIGNATURES = {
     "stda_eca": (C.c_int, [_vp, _i32, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp]),
     "stda_synth_frames": (C.c_int, [_u64, _i32, _i64, _i64, _i64, _i32, _i32, _vp, _vp]),
     "stda_synth_triplets": (C.c_int, [_u64, _i32, _i64, _i64, _i32, _i32, _i32, _vp, _vp]),
+    "stda_debug_trace": (C.c_int, [_vp, _i32]),
 }
 
 ABI_VERSION = 1

@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 
 namespace stda {
 
@@ -38,6 +39,37 @@ __host__ __device__ inline int cdiv(int a, int b) { return (a + b - 1) / b; }
 
 __device__ __forceinline__ float bf16_round(float v) {
   return __bfloat162float(__float2bfloat16_rn(v));
+}
+
+// ---- programmatic dependent launch (PDL) -------------------------------------------
+// Forward kernels are launched with launch_pdl: a kernel may become resident while the
+// previous kernel of the stream drains, run its prologue (barrier init, TMEM alloc,
+// weight loads), and block in grid_dep_wait() until the previous grid has completed and
+// its writes are visible.  Every kernel calls grid_dep_wait() before it reads or writes
+// activation memory.  Without a programmatic edge grid_dep_wait() returns immediately.
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// let the next kernel of the stream start launching (its CTAs still wait in grid_dep_wait)
+__device__ __forceinline__ void grid_dep_launch() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+bool pdl_enabled();  // env STDA_PDL=0 disables the programmatic edges (A/B timing)
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                const char* what, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+  if (e != cudaSuccess) throw Error{std::string(what) + ": " + cudaGetErrorString(e)};
 }
 
 }  // namespace stda

@@ -8,6 +8,9 @@
 // Tile = 8 rows x 64 columns, 256 threads, 2 output pixels (rows r and r+4) per thread.
 // Staging loops issue kBatch independent loads per thread before consuming them.
 #include <algorithm>
+#include <cstdlib>
+#include <string>
+#include <type_traits>
 
 #include "edge_conv.cuh"
 #include "ptx.cuh"
@@ -27,6 +30,7 @@ __global__ void __launch_bounds__(kThreads) stem_planes_kernel(const float* __re
                                                                const float* __restrict__ bias, Src x,
                                                                int F, int C0, PlBuf pl, PlBuf pp,
                                                                int H, int W, int bf16, int64_t b_base) {
+  grid_dep_wait();  // PDL: previous kernel complete (common.cuh)
   extern __shared__ __align__(16) float sm[];
   float* xs = sm;                       // [F][kIH][kIW]
   float* ws = xs + F * kIH * kIW;       // [F][9][16]
@@ -126,6 +130,7 @@ __global__ void __launch_bounds__(kThreads) head_fused_kernel(
     const float* __restrict__ w, const float* __restrict__ bias, const float* __restrict__ gap, int items,
     const float* __restrict__ eca_w, int k, const float* __restrict__ d, PlBuf skip, int C0,
     float* __restrict__ y, int H, int W, int bf16, int64_t b_base) {
+  grid_dep_wait();  // PDL: previous kernel complete (common.cuh)
   extern __shared__ __align__(16) float sm[];
   constexpr int kIH = kHeadTH + 2;       // head tile: 16 rows x 64 columns
   const int CP = C0 + 4;                 // padded pixel stride: conflict-free float4 reads
@@ -255,6 +260,7 @@ __global__ void __launch_bounds__(kRowThreads) stem_rows_kernel(const float* __r
                                                                 const float* __restrict__ bias, Src x, int F,
                                                                 int C0, PlBuf pl, PlBuf pp, int H, int W, int R,
                                                                 int bf16, int64_t b_base) {
+  grid_dep_wait();  // PDL: previous kernel complete (common.cuh)
   extern __shared__ __align__(128) uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t bar;
   const int tid = threadIdx.x;
@@ -360,6 +366,223 @@ __global__ void __launch_bounds__(kRowThreads) stem_rows_kernel(const float* __r
   }
 }
 
+// ---- persistent strip head (C0 = 16, W in {32, 64, 128}) ------------------------------
+// One CTA per SM walks a contiguous range of strips (R = 512 / W rows x W columns; an
+// image's ECA gate is computed once per CTA-image, halo rows of neighbouring strips hit
+// L2).  A producer warp bulk-copies rows y0-1 .. y0+R of d (NHWC fp32: one contiguous
+// range) and of the skip plane (per (pass, cg8) block one contiguous range of rows with
+// their zero pad column) into a 2-stage ring, so strip i+1 is in flight while the 8
+// compute warps transform and convolve strip i.  u = d * gate + skip is formed in place
+// over d, channel quad j of stage pixel p stored at quad slot j ^ ((p >> 1) & 3): the
+// conv's float4 reads of 8 consecutive pixels then hit 8 distinct 16-byte bank groups.
+// Each compute thread produces 2 output rows of one column.
+constexpr int kHsCompute = 256;              // 8 compute warps
+constexpr int kHsThreads = kHsCompute + 32;  // + producer warp
+constexpr int kHsC = 16;
+
+struct HeadStrips {
+  int R, SR, L, dbytes, sblk, stage;  // rows, staged rows, plane row stride, d / skip-block / stage bytes
+  size_t smem;
+};
+
+__host__ __device__ constexpr HeadStrips head_strips_geom(int W) {
+  HeadStrips g{};
+  g.R = 2 * kHsCompute / W;
+  g.SR = g.R + 2;
+  g.L = W + 1;
+  g.dbytes = g.SR * W * kHsC * 4;
+  g.sblk = g.SR * g.L * 16;
+  g.stage = g.dbytes + 4 * g.sblk;
+  g.smem = 2 * (size_t)g.stage + (9 * kHsC + kHsC + 16 * kHsC + kHsC) * 4 + 4 * 8;
+  return g;
+}
+
+__device__ __forceinline__ int hs_swz(int p) { return (p >> 1) & 3; }
+
+template <int W>
+__global__ void __launch_bounds__(kHsThreads, 1) head_strips_kernel(
+    const float* __restrict__ w, const float* __restrict__ bias, const float* __restrict__ gap, int items,
+    const float* __restrict__ eca_w, int k, const float* __restrict__ d, PlBuf skip, float* __restrict__ y,
+    int64_t B, int H, int bf16) {
+  using namespace ptx;
+  extern __shared__ __align__(128) uint8_t hsm[];
+  constexpr HeadStrips g = head_strips_geom(W);
+  constexpr int R = g.R, SR = g.SR, L = g.L;
+  float* ws = reinterpret_cast<float*>(hsm + 2 * (size_t)g.stage);  // [9][16]
+  float* gate = ws + 9 * kHsC;                                       // [16]
+  float* part = gate + kHsC;                                         // [16 groups][16]
+  float* mean = part + 16 * kHsC;                                    // [16]
+  uint64_t* full = reinterpret_cast<uint64_t*>(mean + kHsC);         // [2]
+  uint64_t* empty = full + 2;                                        // [2]
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int spi = H / R;  // strips per image
+  const int64_t n_strips = B * spi;
+  const int64_t s_begin = blockIdx.x * n_strips / gridDim.x;
+  const int64_t s_end = (blockIdx.x + 1) * n_strips / gridDim.x;
+  const int np = skip.np;
+
+  if (tid == 0) {
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&empty[s]), kHsCompute / 32);
+    }
+    fence_barrier_init();
+  }
+  for (int e = tid; e < 9 * kHsC; e += kHsThreads) ws[e] = __ldg(w + e);
+  __syncthreads();
+  grid_dep_wait();  // d, gap and skip come from the previous kernels
+
+  if (warp == kHsCompute / 32) {
+    // ===== producer warp: one bulk copy per tensor (and skip block) per strip =====
+    if ((tid & 31) == 0) {
+      int i = 0;
+      for (int64_t s = s_begin; s < s_end; ++s, ++i) {
+        const int st = i & 1;
+        mbar_wait(smem_u32(&empty[st]), ((i >> 1) & 1) ^ 1);
+        const int64_t b = s / spi;
+        const int y0 = (int)(s - b * spi) * R;
+        const int r0 = y0 == 0 ? 1 : 0;                // first staged row inside the image
+        const int r1 = y0 + R == H ? SR - 1 : SR;      // one past the last
+        const int nr = r1 - r0, iy0 = y0 - 1 + r0;
+        const uint32_t bar = smem_u32(&full[st]);
+        uint8_t* base = hsm + (size_t)st * g.stage;
+        mbar_arrive_expect_tx(bar, (uint32_t)(nr * W * kHsC * 4 + np * 2 * nr * L * 16));
+        bulk_g2s(smem_u32(base + (size_t)r0 * W * kHsC * 4), d + ((size_t)b * H + iy0) * W * kHsC,
+                 (uint32_t)(nr * W * kHsC * 4), bar);
+        const uint16_t* simg = skip.base + b * skip.img_stride;
+        for (int pass = 0; pass < np; ++pass)
+          for (int cg8 = 0; cg8 < 2; ++cg8)
+            bulk_g2s(smem_u32(base + g.dbytes + (size_t)(pass * 2 + cg8) * g.sblk + (size_t)r0 * L * 16),
+                     simg + (skip.block_index(0, pass, cg8) + skip.off + (size_t)iy0 * L) * 8,
+                     (uint32_t)(nr * L * 16), bar);
+      }
+    }
+    return;
+  }
+
+  // ===== 8 compute warps =====
+  const float bv = __ldg(bias);
+  const int cx = tid % W, rp = tid / W;  // conv: column, row pair
+  int64_t cur_b = -1;
+  int i = 0;
+  for (int64_t s = s_begin; s < s_end; ++s, ++i) {
+    const int st = i & 1;
+    const int64_t b = s / spi;
+    const int y0 = (int)(s - b * spi) * R;
+    if (b != cur_b) {
+      // ECA gate of image b (model.py:128-135); fixed-order two-level reduction
+      {
+        const int c = tid & 15, grp = tid >> 4;
+        float a = 0.f;
+        for (int t = grp; t < items; t += 16) a += __ldg(gap + ((size_t)b * items + t) * kHsC + c);
+        part[grp * kHsC + c] = a;
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(kHsCompute) : "memory");
+      if (tid < kHsC) {
+        float a = 0.f;
+        for (int grp = 0; grp < 16; ++grp) a += part[grp * kHsC + tid];
+        mean[tid] = a / (float)(H * W);
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(kHsCompute) : "memory");
+      if (tid < kHsC) {
+        float z = 0.f;
+        for (int j = 0; j < k; ++j) {
+          const int cc = tid + j - k / 2;
+          if (cc >= 0 && cc < kHsC) z = fmaf(__ldg(eca_w + j), mean[cc], z);
+        }
+        gate[tid] = 1.f / (1.f + expf(-z));
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(kHsCompute) : "memory");
+      cur_b = b;
+    }
+    mbar_wait(smem_u32(&full[st]), (i >> 1) & 1);
+    float* ubase = reinterpret_cast<float*>(hsm + (size_t)st * g.stage);
+    const uint8_t* sbase = hsm + (size_t)st * g.stage + g.dbytes;
+    // transform: one (stage pixel, channel quad) per thread step
+#pragma unroll
+    for (int e0 = 0; e0 < SR * W * 4; e0 += kHsCompute) {
+      const int e = e0 + tid;
+      const int q = e & 3, p = e >> 2;
+      const int r = p / W, x = p - r * W;
+      const int iy = y0 - 1 + r;
+      float4 u = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (iy >= 0 && iy < H) {
+        const float4 dv = *reinterpret_cast<const float4*>(ubase + p * kHsC + q * 4);
+        // channels 4q..4q+3: cg8 block (q >> 1), bytes (q & 1) * 8 of position r*L + x
+        const size_t so = (size_t)(r * L + x) * 16 + (q & 1) * 8;
+        const uint2 hv = *reinterpret_cast<const uint2*>(sbase + (size_t)(q >> 1) * g.sblk + so);
+        float s4[4];
+        s4[0] = __uint_as_float(hv.x << 16);
+        s4[1] = __uint_as_float(hv.x & 0xFFFF0000u);
+        s4[2] = __uint_as_float(hv.y << 16);
+        s4[3] = __uint_as_float(hv.y & 0xFFFF0000u);
+        if (np == 2) {
+          const uint2 lv = *reinterpret_cast<const uint2*>(sbase + (size_t)(2 + (q >> 1)) * g.sblk + so);
+          s4[0] += __uint_as_float(lv.x << 16);
+          s4[1] += __uint_as_float(lv.x & 0xFFFF0000u);
+          s4[2] += __uint_as_float(lv.y << 16);
+          s4[3] += __uint_as_float(lv.y & 0xFFFF0000u);
+        }
+        const float4 g4 = *reinterpret_cast<const float4*>(gate + q * 4);
+        u.x = fmaf(dv.x, g4.x, s4[0]);  // eca(d) + skip (model.py:197-198)
+        u.y = fmaf(dv.y, g4.y, s4[1]);
+        u.z = fmaf(dv.z, g4.z, s4[2]);
+        u.w = fmaf(dv.w, g4.w, s4[3]);
+        if (bf16) {
+          u.x = bf16_round(u.x);
+          u.y = bf16_round(u.y);
+          u.z = bf16_round(u.z);
+          u.w = bf16_round(u.w);
+        }
+      }
+      __syncwarp();  // the 4 quads of a pixel are lanes of one warp: all read before any write
+      *reinterpret_cast<float4*>(ubase + p * kHsC + (q ^ hs_swz(p)) * 4) = u;
+    }
+    fence_proxy_async();  // generic writes of this stage before its next async refill
+    asm volatile("bar.sync 1, %0;" ::"n"(kHsCompute) : "memory");
+    // conv3x3 (model.py:158,199): rows 2rp, 2rp+1 of the strip at column cx
+    float acc0 = 0.f, acc1 = 0.f;
+#pragma unroll
+    for (int kx = 0; kx < 3; ++kx) {
+      const int xx = cx + kx - 1;
+      const bool in = xx >= 0 && xx < W;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float4 u[4];
+#pragma unroll
+        for (int rr = 0; rr < 4; ++rr) {
+          const int p = (2 * rp + rr) * W + (in ? xx : 0);
+          u[rr] = *reinterpret_cast<const float4*>(ubase + p * kHsC + (j ^ hs_swz(p)) * 4);
+          if (!in) u[rr] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int ky = 0; ky < 3; ++ky) {
+          const float4 w4 = *reinterpret_cast<const float4*>(ws + (ky * 3 + kx) * kHsC + j * 4);
+          acc0 = fmaf(u[ky].x, w4.x, acc0);
+          acc0 = fmaf(u[ky].y, w4.y, acc0);
+          acc0 = fmaf(u[ky].z, w4.z, acc0);
+          acc0 = fmaf(u[ky].w, w4.w, acc0);
+          acc1 = fmaf(u[ky + 1].x, w4.x, acc1);
+          acc1 = fmaf(u[ky + 1].y, w4.y, acc1);
+          acc1 = fmaf(u[ky + 1].z, w4.z, acc1);
+          acc1 = fmaf(u[ky + 1].w, w4.w, acc1);
+        }
+      }
+    }
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive(smem_u32(&empty[st]));  // this warp is done with stage st
+    float* yo = y + ((size_t)b * H + y0 + 2 * rp) * W + cx;
+    yo[0] = acc0 + bv;
+    yo[W] = acc1 + bv;
+  }
+}
+
+bool head_strips_ok(int C0, int64_t B, int H, int W) {
+  if (C0 != kHsC || (W != 32 && W != 64 && W != 128) || B <= 0) return false;
+  const HeadStrips g = head_strips_geom(W);
+  return H % g.R == 0 && g.smem <= 227 * 1024;
+}
+
 template <typename K>
 void set_smem(K kern) {
   static uint64_t configured = 0;
@@ -389,8 +612,8 @@ void launch_stem_planes(const float* w, const float* bias, const Src& x, int F, 
     set_smem(stem_rows_kernel);
     for (int64_t b0 = 0; b0 < B; b0 += 65535) {
       dim3 grid(H / R, (unsigned)std::min<int64_t>(65535, B - b0));
-      stem_rows_kernel<<<grid, kRowThreads, smem, st>>>(w, bias, x, F, C0, pl, pp, H, W, R, bf16, b0);
-      check_launch("stem_rows_kernel");
+      launch_pdl(stem_rows_kernel, grid, dim3(kRowThreads), smem, st, "stem_rows_kernel", w, bias, x, F, C0,
+                 pl, pp, H, W, R, (int)bf16, b0);
     }
     return;
   }
@@ -398,8 +621,8 @@ void launch_stem_planes(const float* w, const float* bias, const Src& x, int F, 
   set_smem(stem_planes_kernel);
   for (int64_t b0 = 0; b0 < B; b0 += 65535) {
     dim3 grid(cdiv(W, kTW), cdiv(H, kTH), (unsigned)std::min<int64_t>(65535, B - b0));
-    stem_planes_kernel<<<grid, kThreads, smem, st>>>(w, bias, x, F, C0, pl, pp, H, W, bf16, b0);
-    check_launch("stem_planes_kernel");
+    launch_pdl(stem_planes_kernel, grid, dim3(kThreads), smem, st, "stem_planes_kernel", w, bias, x, F, C0, pl,
+               pp, H, W, (int)bf16, b0);
   }
 }
 
@@ -407,14 +630,39 @@ void launch_head_fused(const float* w, const float* bias, const float* gap, int 
                        const float* eca_w, int k, const float* d, const PlBuf& skip, int C0, float* y,
                        int64_t B, int H, int W, bool bf16, cudaStream_t st) {
   STDA_CHECK(C0 % 8 == 0, "head kernel needs stem_channels % 8 == 0");
+  static const bool strips_off = [] {
+    const char* e = std::getenv("STDA_HEAD");
+    return e && std::string(e) == "tiles";
+  }();
+  if (!strips_off && head_strips_ok(C0, B, H, W)) {
+    int dev = 0, sms = 148;
+    STDA_CUDA(cudaGetDevice(&dev));
+    STDA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const HeadStrips g = head_strips_geom(W);
+    const int64_t n_strips = B * (H / g.R);
+    const unsigned grid = (unsigned)std::min<int64_t>(n_strips, sms);
+    auto go = [&](auto wc) {
+      const auto kern = head_strips_kernel<decltype(wc)::value>;
+      static uint64_t configured = 0;  // per instantiation of this generic lambda (per W)
+      if (!(configured >> (dev & 63) & 1)) {
+        STDA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        configured |= 1ull << (dev & 63);
+      }
+      launch_pdl(kern, dim3(grid), dim3(kHsThreads), g.smem, st, "head_strips_kernel", w, bias, gap, items, eca_w,
+                 k, d, skip, y, B, H, (int)bf16);
+    };
+    if (W == 32) go(std::integral_constant<int, 32>{});
+    else if (W == 64) go(std::integral_constant<int, 64>{});
+    else go(std::integral_constant<int, 128>{});
+    return;
+  }
   const size_t smem = sizeof(float) * ((size_t)(kHeadTH + 2) * kIW * (C0 + 4) + 9 * C0 + 2 * C0);
   STDA_CHECK(smem <= 200 * 1024, "head kernel: stem_channels too large for the smem tile");
   set_smem(head_fused_kernel);
   for (int64_t b0 = 0; b0 < B; b0 += 65535) {
     dim3 grid(cdiv(W, kTW), cdiv(H, kHeadTH), (unsigned)std::min<int64_t>(65535, B - b0));
-    head_fused_kernel<<<grid, kThreads, smem, st>>>(w, bias, gap, items, eca_w, k, d, skip, C0, y, H, W, bf16,
-                                                    b0);
-    check_launch("head_fused_kernel");
+    launch_pdl(head_fused_kernel, grid, dim3(kThreads), smem, st, "head_fused_kernel", w, bias, gap, items,
+               eca_w, k, d, skip, C0, y, H, W, (int)bf16, b0);
   }
 }
 

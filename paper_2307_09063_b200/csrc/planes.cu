@@ -34,6 +34,7 @@ __global__ void __launch_bounds__(kGateThreads) gate_apply_kernel(
     const float* __restrict__ gap, int items, const float* __restrict__ eca_w, int k,
     const float* __restrict__ x, PlBuf skip, int has_skip, PlBuf out_pl, int has_pl, PlBuf out_pp,
     int has_pp, float* __restrict__ out_f32, int C, int H, int W) {
+  grid_dep_wait();  // PDL: previous kernel complete (common.cuh)
   __shared__ float mean[1024];
   __shared__ float gate[1024];
   const int64_t b = blockIdx.y;
@@ -117,6 +118,7 @@ __global__ void __launch_bounds__(kGateThreads) gate_apply_rows_kernel(
     const float* __restrict__ gap, int items, const float* __restrict__ eca_w, int k,
     const float* __restrict__ x, PlBuf skip, int has_skip, PlBuf out_pl, int has_pl, PlBuf out_pp,
     int has_pp, int C, int H, int W, int R) {
+  grid_dep_wait();  // PDL: previous kernel complete (common.cuh)
   extern __shared__ __align__(128) uint8_t smem_raw[];
   __shared__ float gate[1024];
   __shared__ float mean[1024];
@@ -308,18 +310,15 @@ void launch_gate_apply(const float* gap, int items, const float* eca_w, int k, c
       configured |= 1ull << (dev & 63);
     }
     dim3 grid(H / R, (unsigned)B);
-    gate_apply_rows_kernel<<<grid, kGateThreads, smem, st>>>(gap, items, eca_w, k, x, skip ? *skip : PlBuf{},
-                                                             skip != nullptr, *out_pl, 1,
-                                                             out_pp ? *out_pp : PlBuf{}, out_pp != nullptr, C,
-                                                             H, W, R);
-    check_launch("gate_apply_rows_kernel");
+    launch_pdl(gate_apply_rows_kernel, grid, dim3(kGateThreads), smem, st, "gate_apply_rows_kernel", gap, items,
+               eca_w, k, x, skip ? *skip : PlBuf{}, (int)(skip != nullptr), *out_pl, 1,
+               out_pp ? *out_pp : PlBuf{}, (int)(out_pp != nullptr), C, H, W, R);
     return;
   }
   dim3 grid(cdiv(H * W, kPixPerCta), (unsigned)B);
-  gate_apply_kernel<<<grid, kGateThreads, 0, st>>>(
-      gap, items, eca_w, k, x, skip ? *skip : PlBuf{}, skip != nullptr, out_pl ? *out_pl : PlBuf{},
-      out_pl != nullptr, out_pp ? *out_pp : PlBuf{}, out_pp != nullptr, out_f32, C, H, W);
-  check_launch("gate_apply_kernel");
+  launch_pdl(gate_apply_kernel, grid, dim3(kGateThreads), 0, st, "gate_apply_kernel", gap, items, eca_w, k, x,
+             skip ? *skip : PlBuf{}, (int)(skip != nullptr), out_pl ? *out_pl : PlBuf{}, (int)(out_pl != nullptr),
+             out_pp ? *out_pp : PlBuf{}, (int)(out_pp != nullptr), out_f32, C, H, W);
 }
 
 }  // namespace stda

@@ -33,6 +33,14 @@ void launch_synth(uint64_t seed, int scene, int64_t seq0, int64_t seq_step, int6
 static thread_local std::string g_last_error;
 void set_error(const std::string& msg) { g_last_error = msg; }
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("STDA_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 namespace {
 
 struct DeviceGuard {
@@ -746,6 +754,10 @@ int stda_block_forward(const stda_plan* b, const float* x, float* y, int64_t bat
       launch_conv(D.up, &D.rs, mixed, &xin, y, nullptr, batch, h, w, true, false, st);
     }
   });
+}
+
+int stda_debug_trace(void* dev_buf, int32_t launch_index) {
+  return guarded([&] { tc::tc_debug_trace(dev_buf, launch_index); });
 }
 
 int stda_eca(const float* w_dev, int32_t k, const float* x, float* gates, float* y, int64_t batch,

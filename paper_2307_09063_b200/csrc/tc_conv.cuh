@@ -99,5 +99,9 @@ struct TcOut {
 void tc_launch(const TcLayerDesc& d, const TcGeometry& g, const PlBuf& src0, const PlBuf* src1,
                const TcOut& out, bool relu0, cudaStream_t st);
 
+// Debug: record a clock64 timeline of CTA 0 (see tc_kernel.cuh trace_at) into dev_buf
+// during the launch_index-th following tc_launch.
+void tc_debug_trace(void* dev_buf, int launch_index);
+
 }  // namespace tc
 }  // namespace stda

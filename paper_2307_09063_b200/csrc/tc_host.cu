@@ -1,5 +1,6 @@
 // tcgen05 implicit-GEMM convolution: host side (weight packing, tiling plan, launch).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "tc_kernel.cuh"
@@ -165,7 +166,7 @@ TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W) {
   uint32_t b_stage = 0;
   for (int c = 0; c < d.n_planes * (d.cin / 16); ++c)
     b_stage = std::max<uint32_t>(b_stage, (uint32_t)(d.chunk_off[c + 1] - d.chunk_off[c]));
-  const size_t fixed = 1024 + 80 + 4 * 64 * sizeof(float);
+  const size_t fixed = 1024 + 80 + kEpiWarps * 64 * sizeof(float);
   const uint32_t w_total = (uint32_t)d.chunk_off[d.n_planes * (d.cin / 16)];
   const size_t w_res = (w_total + 127) / 128 * 128;
   // Prefer (1) a >= 2-deep smem pipeline, (2) two TMEM slots (the epilogue of item i
@@ -214,6 +215,16 @@ TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W) {
   return g;
 }
 
+namespace {
+unsigned long long* g_trace_buf = nullptr;  // armed by tc_debug_trace, consumed by one launch
+int g_trace_countdown = 0;
+}  // namespace
+
+void tc_debug_trace(void* dev_buf, int launch_index) {
+  g_trace_buf = static_cast<unsigned long long*>(dev_buf);
+  g_trace_countdown = launch_index;
+}
+
 void tc_launch(const TcLayerDesc& d, const TcGeometry& g, const PlBuf& src0, const PlBuf* src1,
                const TcOut& out, bool relu0, cudaStream_t st) {
   Params p;
@@ -232,6 +243,9 @@ void tc_launch(const TcLayerDesc& d, const TcGeometry& g, const PlBuf& src0, con
   p.Hp = g.Hp;
   p.Wp = g.Wp;
   p.L = g.L;
+  p.L_mul = (uint32_t)((((uint64_t)1 << 32) + (uint64_t)g.L - 1) / (uint64_t)g.L);
+  STDA_CHECK((uint64_t)g.items_per_image * g.G * 128 * (uint64_t)g.L < ((uint64_t)1 << 32),
+             "tensor-core conv: map too large for the position decode");
   p.Ho = g.Ho;
   p.Wo = g.Wo;
   p.G = g.G;
@@ -247,6 +261,18 @@ void tc_launch(const TcLayerDesc& d, const TcGeometry& g, const PlBuf& src0, con
   p.slot_cols = (uint32_t)(g.G * d.n_src * d.n_acc_src * d.cout * (d.concat ? 2 : 1));
   p.tmem_cols = (uint32_t)g.tmem_cols;
   p.relu0 = relu0 ? 1 : 0;
+  {
+    static const int early = [] {
+      const char* e = std::getenv("STDA_PDL_EARLY");
+      return e ? std::atoi(e) : 0;  // measured: early trigger costs ~1% (co-resident waiters)
+    }();
+    p.early_trigger = early;
+  }
+  if (g_trace_buf != nullptr && g_trace_countdown-- == 0) {
+    p.trace = g_trace_buf;
+    g_trace_buf = nullptr;
+    if (const char* e = std::getenv("STDA_TC_DBG")) p.dbg = std::atoi(e);  // traced launch only
+  }
   if (p.total_items == 0) return;
   int dev = 0, sms = 148;
   STDA_CUDA(cudaGetDevice(&dev));

@@ -19,8 +19,8 @@ namespace detail {
 
 constexpr int kProdWarp = 0;   // lane 0: cp.async.bulk producer
 constexpr int kMmaWarp = 1;    // TMEM allocator + tcgen05.mma issuer
-constexpr int kEpiWarp0 = 2;   // warps 2..5: epilogue (warp % 4 = TMEM lane quarter)
-constexpr int kEpiWarps = 4;
+constexpr int kEpiWarp0 = 2;   // warps 2..9: epilogue (warp % 4 = TMEM lane quarter)
+constexpr int kEpiWarps = 8;
 constexpr int kThreads = (kEpiWarp0 + kEpiWarps) * 32;
 constexpr int kMaxSmem = 227 * 1024;
 
@@ -35,6 +35,7 @@ struct Params {
   TcOut out;
   int H, W, C;            // input grid
   int Hp, Wp, L, Ho, Wo;
+  uint32_t L_mul;          // ceil(2^32 / L): q / L == umulhi(q, L_mul) for q * L < 2^32
   int G, stages, slots, items_per_image, total_items;
   int P_max;
   uint32_t a_stage_bytes, b_stage_bytes, slot_cols;
@@ -42,7 +43,24 @@ struct Params {
   uint32_t w_total;   // packed weight bytes of the layer
   uint32_t tmem_cols;
   int relu0;
+  unsigned long long* trace;  // debug timeline of CTA 0 (null in normal runs)
+  int early_trigger;          // griddepcontrol.launch_dependents at kernel start
+  int dbg;                    // debug ablations (env STDA_TC_DBG; 0 in normal runs):
+                              // 1 no epilogue stores, 2 no TMEM loads, 4 no A copies after
+                              // the first fill, 8 epilogue only releases the slot
 };
+
+// ---- debug timeline (stda_debug_trace): clock64 stamps of CTA 0, one region per role ---
+// region 0: producer  [k*2 + {empty acquired, chunk issued}]
+// region 1: MMA warp  [k*2 + {full acquired, chunk issued}]
+// region 2: MMA warp  [ic]  TMEM slot acquired
+// region 3: epilogue  [ic*2 + {TMEM full acquired, slot released}]
+// region 4: [0] kernel start, [1] kernel end
+constexpr int kTraceRegion = 8192;
+__device__ __forceinline__ void trace_at(unsigned long long* tr, int region, int idx) {
+  if (tr != nullptr && blockIdx.x == 0 && idx < kTraceRegion)
+    tr[region * kTraceRegion + idx] = clock64();
+}
 
 // ---- compile-time tap tables (must match plane_taps() on the host) ----------------
 // S1:  t = ky*3+kx, shift (ky-1, kx-1)
@@ -248,9 +266,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
   uint64_t* tempty = tfull + p.slots;
   uint64_t* wbar = tempty + p.slots;  // resident weights landed
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(wbar + 1);
-  float* red = reinterpret_cast<float*>(tmem_holder + 4);  // [4][N]
+  float* red = reinterpret_cast<float*>(tmem_holder + 4);  // [kEpiWarps][N]
 
   if (threadIdx.x == 0) {
+    trace_at(p.trace, 4, 0);
     for (int s = 0; s < p.stages; ++s) {
       mbar_init(smem_u32(&full[s]), 1);
       mbar_init(smem_u32(&empty[s]), 1);
@@ -274,6 +293,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
   const uint32_t src_bytes = (uint32_t)NPASS_A * 2 * p.P_max * 16;
+  // single-wave persistent grid: let the next kernel's CTAs take SMs as ours retire
+  if (p.early_trigger) grid_dep_launch();
 
   if (warp == kProdWarp) {
     // ===================== producer: cp.async.bulk of A ranges + packed weights =========
@@ -282,6 +303,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
         mbar_arrive_expect_tx(smem_u32(wbar), p.w_total);
         bulk_g2s(smem_u32(b_base), d.w, p.w_total, smem_u32(wbar));
       }
+      grid_dep_wait();  // weights are static; activations come from the previous kernel
       uint32_t k = 0;
       for (int item = blockIdx.x; item < p.total_items; item += gridDim.x) {
         const int b = item / p.items_per_image;
@@ -290,12 +312,17 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
           const int stage = k % p.stages;
           const uint32_t phase = (k / p.stages) & 1;
           mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+          trace_at(p.trace, 0, 2 * k);
           const int pl = c / cgroups, cgi = c - pl * cgroups;
           const PlaneTaps& pt = d.planes[pl];
           const int P = p.G * 128 + pt.hi - pt.lo;
           const uint32_t a_bytes = (uint32_t)P * 16;
           const uint32_t w_bytes = p.resident ? 0u : (uint32_t)(d.chunk_off[c + 1] - d.chunk_off[c]);
           const uint32_t fb = smem_u32(&full[stage]);
+          if ((p.dbg & 4) && k >= (uint32_t)p.stages) {
+            mbar_arrive(fb);
+            continue;
+          }
           mbar_arrive_expect_tx(fb, w_bytes + (uint32_t)NSRC * NPASS_A * 2 * a_bytes);
           if (!p.resident)
             bulk_g2s(smem_u32(b_base + (size_t)stage * p.b_stage_bytes),
@@ -315,6 +342,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
                          a_bytes, fb);
               }
           }
+          trace_at(p.trace, 0, 2 * k + 1);
         }
       }
     }
@@ -337,6 +365,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
       mbar_wait(smem_u32(&tempty[slot]), sphase ^ 1);
       __syncwarp();
       tc_fence_after();
+      if (leader) trace_at(p.trace, 2, ic);
       const uint32_t dslot = tmem_base + (uint32_t)slot * p.slot_cols;
       for (int c = 0; c < n_chunks; ++c, ++k) {
         const int stage = k % p.stages;
@@ -344,6 +373,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
         mbar_wait(smem_u32(&full[stage]), phase);
         __syncwarp();
         tc_fence_after();
+        if (leader) trace_at(p.trace, 1, 2 * k);
         const uint64_t a0 = smem_desc(smem_u32(a_base + (size_t)stage * p.a_stage_bytes), lboA, 128);
         const uint64_t b0 = smem_desc(
             smem_u32(b_base + (p.resident ? (size_t)d.chunk_off[c] : (size_t)stage * p.b_stage_bytes)), lboB,
@@ -360,14 +390,22 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
         }
         __syncwarp();
         tc_commit(leader, smem_u32(&empty[stage]));
+        if (leader) trace_at(p.trace, 1, 2 * k + 1);
       }
       tc_commit(leader, smem_u32(&tfull[slot]));
     }
     __syncwarp();
   } else {
-    // ===================== epilogue warps 2..5 ==========================================
-    const int ew = warp & 3;  // TMEM lane quarter accessible to this warp
+    // ===================== epilogue warps 2..9 ==========================================
+    // Two warps per TMEM lane quarter; the (tile, phase, 16-channel) units of an item
+    // alternate between them so each SM sub-partition has two independent epilogue
+    // streams to interleave (one warp alone is latency-bound on the LDTM -> convert ->
+    // store chain).
+    constexpr int NJ = N / 16;
+    const int ew = warp & 3;                               // TMEM lane quarter of this warp
+    const int half = (warp - kEpiWarp0) / 4;               // which units of the item
     const int et = threadIdx.x - kEpiWarp0 * 32;
+    grid_dep_wait();  // outputs may still be read by the previous kernel
     uint32_t ic = 0;
     for (int item = blockIdx.x; item < p.total_items; item += gridDim.x, ++ic) {
       const int slot = ic % p.slots;
@@ -378,16 +416,22 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
       mbar_wait(smem_u32(&tfull[slot]), sphase);
       __syncwarp();
       tc_fence_after();
+      if (et == 0) trace_at(p.trace, 3, 2 * ic);
+      if (p.dbg & 8) {
+        tc_fence_before();
+        mbar_arrive(smem_u32(&tempty[slot]));
+        continue;
+      }
       float gsum[N];
 #pragma unroll
       for (int c = 0; c < N; ++c) gsum[c] = 0.f;
       const uint32_t trow = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)slot * p.slot_cols;
       for (int g = 0; g < G; ++g) {
         const int q = q0 + g * 128 + ew * 32 + lane;
-        const int y = q / p.L;
+        const int y = (int)__umulhi((uint32_t)q, p.L_mul);  // q / L (host-checked exact)
         const int x = q - y * p.L;
         const bool valid = y < p.Hp && x < p.Wp;
-        if (p.out.mode != 0 && y < p.Hp && x == p.Wp) {
+        if (p.out.mode != 0 && ((g * NACC_SRC * NJ) & 1) == half && y < p.Hp && x == p.Wp) {
           // this position is a pad of the output grid: keep the operand plane's pad
           // column zero (planes.cuh border contract)
           if (p.out.mode == 1) {
@@ -406,15 +450,24 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
           }
 #pragma unroll
           for (int j = 0; j < N; j += 16) {
+            if ((((g * NACC_SRC + ph) * NJ + j / 16) & 1) != half) continue;  // warp-uniform
             float a0[16], a1[16];
             const uint32_t c0 = (uint32_t)((g * NACC + ph) * AW + j);
             const uint32_t c1 = (uint32_t)((g * NACC + NACC_SRC + ph) * AW + j);
-            tmem_ld16(trow + c0, a0);
-            if (DUAL) tmem_ld16(trow + c1, a1);
+            auto ld = [&](uint32_t a, float(&v)[16]) {
+              if (p.dbg & 2) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) v[i] = 0.f;
+              } else {
+                tmem_ld16(a, v);
+              }
+            };
+            ld(trow + c0, a0);
+            if (DUAL) ld(trow + c1, a1);
             if (NPM == kNpmConcat) {  // + the hi*lo half of the concatenated accumulator
               float h0[16], h1[16];
-              tmem_ld16(trow + c0 + N, h0);
-              if (DUAL) tmem_ld16(trow + c1 + N, h1);
+              ld(trow + c0 + N, h0);
+              if (DUAL) ld(trow + c1 + N, h1);
               tmem_wait_ld();
 #pragma unroll
               for (int i = 0; i < 16; ++i) {
@@ -432,7 +485,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
               if (DUAL) t = t + (a1[i] + __ldg(d.bias1 + j + i));
               v[i] = t;
             }
-            if (!valid) continue;
+            if (!valid || (p.dbg & 1)) continue;
             if (p.out.mode == 0) {
               float* op = p.out.f32 + (((size_t)b * p.Ho + oy) * p.Wo + ox) * N;
 #pragma unroll
@@ -462,18 +515,22 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
       }
       tc_fence_before();
       mbar_arrive(smem_u32(&tempty[slot]));
+      if (et == 0) trace_at(p.trace, 3, 2 * ic + 1);
       if (p.out.mode != 0 && it == 0) pl_zero_margins(p.out.pl, b, et, kEpiWarps * 32);
       if (p.out.mode == 0 && p.out.gap) {
+        // deterministic: fixed-order sum of the 8 warp partials
 #pragma unroll
         for (int c = 0; c < N; ++c) {
           float s = gsum[c];
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-          if (lane == 0) red[ew * N + c] = s;
+          if (lane == 0) red[(warp - kEpiWarp0) * N + c] = s;
         }
         asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
         if (et < N) {
-          const float s = ((red[et] + red[N + et]) + red[2 * N + et]) + red[3 * N + et];
+          float s = red[et];
+#pragma unroll
+          for (int w = 1; w < kEpiWarps; ++w) s += red[w * N + et];
           p.out.gap[((size_t)b * p.items_per_image + it) * N + et] = s;
         }
         asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
@@ -483,6 +540,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
 
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) trace_at(p.trace, 4, 1);
   if (warp == kMmaWarp) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(p.tmem_cols)
@@ -500,8 +558,7 @@ void launch_k(const Params& p, int grid, size_t smem, cudaStream_t st) {
     STDA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
     configured |= 1ull << (dev & 63);
   }
-  kern<<<grid, kThreads, smem, st>>>(p);
-  check_launch("tc_conv_kernel");
+  launch_pdl(kern, dim3(grid), dim3(kThreads), smem, st, "tc_conv_kernel", p);
 }
 
 template <int MODE, bool DUAL>
