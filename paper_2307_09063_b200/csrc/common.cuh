@@ -41,6 +41,20 @@ __device__ __forceinline__ float bf16_round(float v) {
   return __bfloat162float(__float2bfloat16_rn(v));
 }
 
+// ---- packed fp32 (sm_100 FFMA2): two independent round-to-nearest fp32 FMAs per instruction,
+// bit-identical to two fmaf() calls; halves the issue slots of FMA-bound SIMT loops.
+__device__ __forceinline__ unsigned long long f2_pack(float lo, float hi) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2_unpack(unsigned long long v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ void f2_fma(unsigned long long& acc, unsigned long long a, unsigned long long b) {
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(a), "l"(b));
+}
+
 // ---- programmatic dependent launch (PDL) -------------------------------------------
 // Forward kernels are launched with launch_pdl: a kernel may become resident while the
 // previous kernel of the stream drains, run its prologue (barrier init, TMEM alloc,

@@ -256,10 +256,10 @@ __device__ __forceinline__ void split_store(uint8_t* dst_hi, uint8_t* dst_lo, co
 
 // stem: rows [y0, y0+R) of relu(conv3x3(x)) -> PL rows (H x W grid) and PP rows (planes).
 // x rows must be contiguous (x.xp == 1): frame ci row iy at x.x + b*xb + ci*xc + iy*W.
-__global__ void __launch_bounds__(kRowThreads) stem_rows_kernel(const float* __restrict__ w,
+__global__ void __launch_bounds__(kRowThreads, 4) stem_rows_kernel(const float* __restrict__ w,
                                                                 const float* __restrict__ bias, Src x, int F,
                                                                 int C0, PlBuf pl, PlBuf pp, int H, int W, int R,
-                                                                int bf16, int64_t b_base) {
+                                                                int bf16, int64_t b_base, int direct) {
   grid_dep_wait();  // PDL: previous kernel complete (common.cuh)
   extern __shared__ __align__(128) uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t bar;
@@ -300,32 +300,47 @@ __global__ void __launch_bounds__(kRowThreads) stem_rows_kernel(const float* __r
   }
   ptx::mbar_wait(ptx::smem_u32(&bar), 0);
   __syncthreads();
-  for (int pix = tid; pix < R * W; pix += kRowThreads) {
-    const int r = pix / W, xx = pix - r * W;
+  // two vertically adjacent pixels per thread: every weight read from smem feeds both
+  // (the kernel is bound by shared-memory wavefronts, not FMA issue)
+  for (int it = tid; it < (R / 2) * W; it += kRowThreads) {
+    const int r0 = (it / W) * 2, xx = it - (it / W) * W;
     for (int blk = 0; blk < C0 / 16; ++blk) {
-      float acc[16];
+      // channel pairs packed for FFMA2 (same per-channel fmaf sequence, half the issues)
+      unsigned long long acc2[2][8];
 #pragma unroll
-      for (int q = 0; q < 16; ++q) acc[q] = __ldg(bias + blk * 16 + q);
+      for (int q = 0; q < 8; ++q)
+        acc2[0][q] = acc2[1][q] = f2_pack(__ldg(bias + blk * 16 + 2 * q), __ldg(bias + blk * 16 + 2 * q + 1));
       for (int ci = 0; ci < F; ++ci) {
         const float* xc = xs + (size_t)ci * (R + 2) * W;
-        const float4* wc = reinterpret_cast<const float4*>(ws + ((size_t)blk * F + ci) * 144);
+        const ulonglong2* wc = reinterpret_cast<const ulonglong2*>(ws + ((size_t)blk * F + ci) * 144);
 #pragma unroll
-        for (int ky = 0; ky < 3; ++ky)
+        for (int kx = 0; kx < 3; ++kx) {
+          const int ix = xx + kx - 1;
+          unsigned long long vv[4];
 #pragma unroll
-          for (int kx = 0; kx < 3; ++kx) {
-            const int ix = xx + kx - 1;
-            float v = (ix >= 0 && ix < W) ? xc[(r + ky) * W + ix] : 0.f;
+          for (int k = 0; k < 4; ++k) {
+            float v = (ix >= 0 && ix < W) ? xc[(r0 + k) * W + ix] : 0.f;
             if (bf16) v = bf16_round(v);
+            vv[k] = f2_pack(v, v);
+          }
+#pragma unroll
+          for (int ky = 0; ky < 3; ++ky)
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-              const float4 w4 = wc[(ky * 3 + kx) * 4 + q];
-              acc[4 * q + 0] = fmaf(v, w4.x, acc[4 * q + 0]);
-              acc[4 * q + 1] = fmaf(v, w4.y, acc[4 * q + 1]);
-              acc[4 * q + 2] = fmaf(v, w4.z, acc[4 * q + 2]);
-              acc[4 * q + 3] = fmaf(v, w4.w, acc[4 * q + 3]);
+              const ulonglong2 w4 = wc[(ky * 3 + kx) * 4 + q];
+              f2_fma(acc2[0][2 * q], vv[ky], w4.x);
+              f2_fma(acc2[0][2 * q + 1], vv[ky], w4.y);
+              f2_fma(acc2[1][2 * q], vv[ky + 1], w4.x);
+              f2_fma(acc2[1][2 * q + 1], vv[ky + 1], w4.y);
             }
-          }
+        }
       }
+#pragma unroll
+      for (int o = 0; o < 2; ++o) {
+      const int r = r0 + o;
+      float acc[16];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) f2_unpack(acc2[o][q], acc[2 * q], acc[2 * q + 1]);
       const int plane = ((y0 + r) & 1) * 2 + (xx & 1);
       const size_t pos_pl = (size_t)(r * L + xx) * 16, pos_pp = (size_t)((r >> 1) * Lp + (xx >> 1)) * 16;
 #pragma unroll
@@ -333,13 +348,26 @@ __global__ void __launch_bounds__(kRowThreads) stem_rows_kernel(const float* __r
         float v[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) v[i] = fmaxf(acc[8 * h + i], 0.f);
+        if (direct) {  // coalesced 16-byte stores straight to the planes
+          const int oy = y0 + r;
+          pl_store8(pl, b, 0, 2 * blk + h, oy * L + xx, v);
+          pl_store8(pp, b, plane, 2 * blk + h, (oy >> 1) * Lp + (xx >> 1), v);
+          continue;
+        }
         const int kh = (blk * np) * 2 + h;  // hi block of channel group 2*blk+h
         split_store(po + kh * po_blk + pos_pl, po + (kh + 2) * po_blk + pos_pl, v, np);
         uint8_t* ppl = pp_s + (size_t)plane * nblk * pp_blk;
         split_store(ppl + kh * pp_blk + pos_pp, ppl + (kh + 2) * pp_blk + pos_pp, v, np);
       }
+      if (direct && blk == 0 && xx >= W - 2) {  // pad columns (planes.cuh border contract)
+        const int oy = y0 + r;
+        if (xx == W - 1) pl_zero_pos(pl, b, 0, oy * L + W);
+        pl_zero_pos(pp, b, plane, (oy >> 1) * Lp + W / 2);
+      }
+      }
     }
   }
+  if (direct) return;
   for (int u = tid; u < R * nblk; u += kRowThreads) {  // pad columns of the staged rows
     const int r = u / nblk, kb = u - r * nblk;
     *reinterpret_cast<uint4*>(po + kb * po_blk + (size_t)(r * L + W) * 16) = make_uint4(0, 0, 0, 0);
@@ -601,19 +629,24 @@ void launch_stem_planes(const float* w, const float* bias, const Src& x, int F, 
                         cudaStream_t st) {
   STDA_CHECK(C0 % 16 == 0, "stem kernel needs stem_channels % 16 == 0");
   if (x.xp == 1 && H % 2 == 0 && W % 2 == 0 && W <= 1024) {
-    // bulk-copy row-block path: R rows (even, dividing H) with R*W ~ 256 pixels
+    // bulk-copy row-block path: R rows (even, dividing H) with R*W ~ 512 pixels
+    // (256 threads x 2 vertically adjacent pixels)
     int R = 2;
-    while (R * 2 * W <= 256 && H % (R * 2) == 0) R *= 2;
+    while (R * 2 * W <= 512 && H % (R * 2) == 0) R *= 2;
     const int np = pl.np, nblk = (C0 / 16) * np * 2, L = W + 1, Lp = W / 2 + 1;
     auto al = [](size_t v) { return (v + 127) / 128 * 128; };
+    static const int direct = [] {
+      const char* e = std::getenv("STDA_STEM_STORE");
+      return e && std::string(e) == "bulk" ? 0 : 1;
+    }();
     const size_t smem = al((size_t)F * (R + 2) * W * 4) + al((size_t)C0 * F * 9 * 4) +
-                        al((size_t)nblk * R * L * 16) + al((size_t)4 * nblk * (R / 2) * Lp * 16);
+                        (direct ? 0 : al((size_t)nblk * R * L * 16) + al((size_t)4 * nblk * (R / 2) * Lp * 16));
     STDA_CHECK(smem <= 200 * 1024, "stem: rows do not fit shared memory");
     set_smem(stem_rows_kernel);
     for (int64_t b0 = 0; b0 < B; b0 += 65535) {
       dim3 grid(H / R, (unsigned)std::min<int64_t>(65535, B - b0));
       launch_pdl(stem_rows_kernel, grid, dim3(kRowThreads), smem, st, "stem_rows_kernel", w, bias, x, F, C0,
-                 pl, pp, H, W, R, (int)bf16, b0);
+                 pl, pp, H, W, R, (int)bf16, b0, direct);
     }
     return;
   }

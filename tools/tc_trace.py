@@ -70,6 +70,12 @@ for li in range(n_tc):
     ea, er = epi[0 : 2 * ni : 2], epi[1 : 2 * ni : 2]
     ew = ea - np.concatenate([[t0], er[:-1]])
     print(f"  epilogue  wait-full  {stats(ew)} | busy {stats(er - ea)}")
+    if f"--chunks={names[li]}" in sys.argv:
+        print("   k  prod.empty  prod.issued  mma.full  mma.issued   (cycles from kernel start)")
+        for c in range(min(nk, 40)):
+            print(f"  {c:3d} {prod[2*c]-t0:10d} {prod[2*c+1]-t0:11d} {mma[2*c]-t0:9d} {mma[2*c+1]-t0:10d}")
+        for i in range(min(ni, 20)):
+            print(f"   item {i}: epi {ea[i]-t0}..{er[i]-t0}")
     if li == 0 or "--verbose" in sys.argv:
         for i in range(min(ni, 6)):
             c0 = i * cpi
