@@ -76,6 +76,69 @@ def layer_flops(cfg) -> dict:
     return out
 
 
+def layer_bytes(cfg) -> dict:
+    """Algorithmic HBM bytes per triplet of each launch: every input and output tensor once
+    at 4 B per value (the fp32 contract; hi + lo bf16 operand planes are also 4 B per value)."""
+    H, W, c0, F, S = cfg.map_height, cfg.map_width, cfg.stem_channels, cfg.input_frames, cfg.stages
+    HW = H * W
+    out = {"stem": 4 * (F + c0) * HW}
+    for i in range(S):
+        c, hw = c0 << i, (H >> i) * (W >> i)
+        out[f"enc{i}.s1"] = 4 * (c + c) * hw
+        out[f"enc{i}.s2"] = 4 * (2 * c * hw + 2 * c * hw // 4)
+        out[f"enc{i}.gate"] = 4 * 2 * (2 * c * hw // 4)
+    for j in range(S):
+        c2 = c0 << (S - j)
+        c, hw = c2 // 2, (H >> (S - j)) * (W >> (S - j))
+        out[f"dec{j}.s1"] = 4 * 2 * c2 * hw
+        out[f"dec{j}.s2"] = 4 * (2 * c2 * hw + c * 4 * hw)
+        out[f"dec{j}.gate"] = 4 * 3 * c * 4 * hw
+    out["head"] = 4 * (2 * c0 + 1) * HW
+    return out
+
+
+def layer_operand_bytes(cfg, precision: str) -> dict:
+    """Shared-memory operand bytes the tensor cores read per triplet for each tcgen05 launch
+    (csrc/tc_kernel.cuh issue_chunk): M=128 tiles over the padded grid (row stride W+1), per
+    tap and 16-channel chunk A = 4 KB per MMA plus B = width x 32 B.  SS-mode M=128 MMAs are
+    bound by these reads at ~128 B/clk/SM (profiles/r1_tcgen05_microbench.md)."""
+    H, W, c0, S = cfg.map_height, cfg.map_width, cfg.stem_channels, cfg.stages
+
+    def per_tap(n_src, n_acc_src, cout):
+        if precision == "bf16":
+            return 4096 + 32 * cout
+        if n_src * n_acc_src * 2 * cout * 2 <= 512:      # hi/lo N-concat: 2 MMAs
+            return 2 * 4096 + 32 * 3 * cout
+        return 3 * 4096 + 3 * 32 * cout                   # 3 MMAs of width N
+
+    def tiles(hp, wp):
+        return -(-(hp * (wp + 1)) // 128)
+
+    out = {}
+    for i in range(S):
+        c, h, w = c0 << i, H >> i, W >> i
+        out[f"enc{i}.s1"] = tiles(h, w) * (c // 16) * 9 * per_tap(1, 1, c)
+        out[f"enc{i}.s2"] = tiles(h // 2, w // 2) * (c // 16) * 9 * 2 * per_tap(2, 1, 2 * c)
+    for j in range(S):
+        c2 = c0 << (S - j)
+        h, w = H >> (S - j), W >> (S - j)
+        out[f"dec{j}.s1"] = tiles(h, w) * (c2 // 16) * 9 * per_tap(1, 1, c2)
+        out[f"dec{j}.s2"] = tiles(h, w) * (c2 // 16) * 16 * 2 * per_tap(2, 4, c2 // 2)
+    return out
+
+
+def ncu_traffic(kernel: str, batch: int, H: int, W: int, precision: str):
+    """DRAM bytes per launch of `kernel` from a committed ncu --set full capture
+    (profiles/ncu_traffic.json, written from the capture's raw page), or None."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if not p.exists():
+        return None
+    for e in json.loads(p.read_text()):
+        if (e["launch"], e["batch"], e["map"], e["precision"]) == (kernel, batch, [H, W], precision):
+            return e["dram_bytes"]
+    return None
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
@@ -293,6 +356,25 @@ def run_engine(args, world, rank, local):
     flops_per_launch = fl[dom] * batch
     achieved = flops_per_launch / (share[dom] * 1e-3) / 1e12
     total_flops = sum(fl.values())
+    byt = layer_bytes(cfg)
+    opb = layer_operand_bytes(cfg, args.precision)
+    sm_ghz = (clocks.summary().get("sm_max_mhz") or 1965.0) / 1000.0
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    floor_us = {n: b * batch / (128.0 * n_sm * sm_ghz * 1e3) for n, b in opb.items()}
+    if dom in opb:   # tcgen05 conv: FLOP roofline + the operand-feed floor that binds it
+        roof = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": bf16, "unit": "TFLOP/s",
+                "frac": achieved / bf16, "peak_kind": f"{peak_kind} dense bf16",
+                "flops_per_launch": flops_per_launch,
+                "operand_floor_us": floor_us[dom],
+                "frac_of_operand_floor": floor_us[dom] / (share[dom] * 1e3),
+                "hbm_floor_us": byt[dom] * batch / (hbm * 1e3),
+                "frac_of_binding_floor": max(floor_us[dom], byt[dom] * batch / (hbm * 1e3)) / (share[dom] * 1e3)}
+    else:            # SIMT edge / gate kernel: HBM roofline on algorithmic bytes
+        gbs = byt[dom] * batch / (share[dom] * 1e-3) / 1e9
+        roof = {"bound": "hbm", "kernel": dom, "achieved": gbs, "peak": hbm, "unit": "GB/s",
+                "frac": gbs / hbm, "peak_kind": f"{peak_kind} HBM copy bandwidth",
+                "bytes_per_launch": byt[dom] * batch}
+    roof["traffic"] = ncu_traffic(dom, batch, H, W, args.precision)
 
     # end-to-end through the public host-buffer API: a stream of e2e_steps batches in
     # pinned host memory goes through ONE StdaNet.denoise_host call, which pipelines
@@ -323,16 +405,12 @@ def run_engine(args, world, rank, local):
                    "timing": "CUDA-graph replay of the whole forward, CUDA events per step"},
         "gpu_launches": cap.launches * args.steps,
         "roofline": {
-            "bound": "tensor", "kernel": dom, "achieved": achieved, "peak": bf16,
-            "unit": "TFLOP/s", "frac": achieved / bf16, "traffic": None,
-            "peak_kind": f"{peak_kind} dense bf16",
-            "flops_per_launch": flops_per_launch, "launch_ms": share[dom],
-            "executed": ("tcgen05 kind::f16, 3xBF16 split (hi*hi+lo*hi+hi*lo), fp32 accumulate in TMEM"
+            **roof, "launch_ms": share[dom],
+            "executed": ("tcgen05 kind::f16, 3xBF16 split (A_hi x [B_hi|B_lo] + A_lo x B_hi), fp32 accumulate in TMEM"
                          if args.precision == "fp32" else "tcgen05 kind::f16, bf16 operands, fp32 accumulate"),
-            "mma_passes": 3 if args.precision == "fp32" else 1,
-            "frac_of_split_roof": achieved * (3 if args.precision == "fp32" else 1) / bf16,
             "whole_forward_tflops": total_flops * batch / (ms_per_step * 1e-3) / 1e12,
-            "hbm_fraction": (16 * H * W * batch) / (ms_per_step * 1e-3) / (hbm * 1e9),
+            "forward_operand_floor_us": sum(floor_us.values()),
+            "launch_us": {n: m * 1e3 for n, m in share.items()},
             "launch_share": {n: m / sum(avg) for n, m in share.items()},
         },
         "e2e": {"value": e2e_rate, "unit": "triplets/s",
