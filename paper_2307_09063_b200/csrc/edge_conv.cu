@@ -144,20 +144,9 @@ __global__ void __launch_bounds__(kThreads) head_fused_kernel(
   const int64_t b = b_base + blockIdx.z;
   for (int e = tid; e < 9 * C0; e += kThreads) ws[e] = __ldg(w + e);
   // ECA gate of this image (fixed-order reduction: identical in every CTA)
-  for (int ch = tid; ch < C0; ch += kThreads) {
-    float s = 0.f;
-    for (int t = 0; t < items; ++t) s += __ldg(gap + (b * items + t) * C0 + ch);
-    mean[ch] = s / (float)(H * W);
-  }
+  for (int ch = tid; ch < C0; ch += kThreads) mean[ch] = eca_channel_sum(gap, items, C0, b, ch) / (float)(H * W);
   __syncthreads();
-  for (int ch = tid; ch < C0; ch += kThreads) {
-    float z = 0.f;
-    for (int j = 0; j < k; ++j) {
-      const int cc = ch + j - k / 2;
-      if (cc >= 0 && cc < C0) z = fmaf(__ldg(eca_w + j), mean[cc], z);
-    }
-    gate[ch] = 1.f / (1.f + expf(-z));
-  }
+  for (int ch = tid; ch < C0; ch += kThreads) gate[ch] = eca_gate_of(mean, C0, ch, eca_w, k);
   __syncthreads();
   const int n = kIH * kIW * G8;
   for (int e0 = tid; e0 < n; e0 += 4 * kThreads) {
@@ -498,28 +487,17 @@ __global__ void __launch_bounds__(kHsThreads, 1) head_strips_kernel(
     const int64_t b = s / spi;
     const int y0 = (int)(s - b * spi) * R;
     if (b != cur_b) {
-      // ECA gate of image b (model.py:128-135); fixed-order two-level reduction
-      {
-        const int c = tid & 15, grp = tid >> 4;
-        float a = 0.f;
-        for (int t = grp; t < items; t += 16) a += __ldg(gap + ((size_t)b * items + t) * kHsC + c);
-        part[grp * kHsC + c] = a;
-      }
+      // ECA gate of image b (model.py:128-135): kEcaGroups group sums in parallel, added
+      // in group order (planes.cuh: the one reduction order of every gate)
+      if (tid < kEcaGroups * kHsC) part[tid] = eca_group_sum(gap, items, kHsC, b, tid % kHsC, tid / kHsC);
       asm volatile("bar.sync 1, %0;" ::"n"(kHsCompute) : "memory");
       if (tid < kHsC) {
         float a = 0.f;
-        for (int grp = 0; grp < 16; ++grp) a += part[grp * kHsC + tid];
+        for (int grp = 0; grp < kEcaGroups; ++grp) a += part[grp * kHsC + tid];
         mean[tid] = a / (float)(H * W);
       }
       asm volatile("bar.sync 1, %0;" ::"n"(kHsCompute) : "memory");
-      if (tid < kHsC) {
-        float z = 0.f;
-        for (int j = 0; j < k; ++j) {
-          const int cc = tid + j - k / 2;
-          if (cc >= 0 && cc < kHsC) z = fmaf(__ldg(eca_w + j), mean[cc], z);
-        }
-        gate[tid] = 1.f / (1.f + expf(-z));
-      }
+      if (tid < kHsC) gate[tid] = eca_gate_of(mean, kHsC, tid, eca_w, k);
       asm volatile("bar.sync 1, %0;" ::"n"(kHsCompute) : "memory");
       cur_b = b;
     }

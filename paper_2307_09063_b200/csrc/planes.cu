@@ -1,5 +1,7 @@
 // Operand-plane helpers: border zeroing and the fused ECA gate + apply kernel.
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 
 #include "planes.cuh"
 #include "ptx.cuh"
@@ -39,20 +41,9 @@ __global__ void __launch_bounds__(kGateThreads) gate_apply_kernel(
   __shared__ float gate[1024];
   const int64_t b = blockIdx.y;
   // gate for this image: fixed-order reduction of the producer's per-item partial sums
-  for (int c = threadIdx.x; c < C; c += blockDim.x) {
-    float s = 0.f;
-    for (int t = 0; t < items; ++t) s += __ldg(gap + (b * items + t) * C + c);
-    mean[c] = s / (float)(H * W);
-  }
+  for (int c = threadIdx.x; c < C; c += blockDim.x) mean[c] = eca_channel_sum(gap, items, C, b, c) / (float)(H * W);
   __syncthreads();
-  for (int c = threadIdx.x; c < C; c += blockDim.x) {
-    float z = 0.f;
-    for (int j = 0; j < k; ++j) {
-      const int cc = c + j - k / 2;
-      if (cc >= 0 && cc < C) z = fmaf(__ldg(eca_w + j), mean[cc], z);
-    }
-    gate[c] = 1.f / (1.f + expf(-z));
-  }
+  for (int c = threadIdx.x; c < C; c += blockDim.x) gate[c] = eca_gate_of(mean, C, c, eca_w, k);
   __syncthreads();
   const int G8 = C / 8;
   const int pix0 = blockIdx.x * kPixPerCta;
@@ -157,20 +148,9 @@ __global__ void __launch_bounds__(kGateThreads) gate_apply_rows_kernel(
     }
   }
   // ECA gate of this image while the copies fly (fixed order: identical in every CTA)
-  for (int c = tid; c < C; c += blockDim.x) {
-    float s = 0.f;
-    for (int t = 0; t < items; ++t) s += __ldg(gap + (b * items + t) * C + c);
-    mean[c] = s / (float)(H * W);
-  }
+  for (int c = tid; c < C; c += blockDim.x) mean[c] = eca_channel_sum(gap, items, C, b, c) / (float)(H * W);
   __syncthreads();
-  for (int c = tid; c < C; c += blockDim.x) {
-    float z = 0.f;
-    for (int j = 0; j < k; ++j) {
-      const int cc = c + j - k / 2;
-      if (cc >= 0 && cc < C) z = fmaf(__ldg(eca_w + j), mean[cc], z);
-    }
-    gate[c] = 1.f / (1.f + expf(-z));
-  }
+  for (int c = tid; c < C; c += blockDim.x) gate[c] = eca_gate_of(mean, C, c, eca_w, k);
   if (blockIdx.x == 0) {  // top / bottom margins of the output planes, once per image
     if (has_pl) pl_zero_margins(out_pl, b, tid, blockDim.x);
     if (has_pp) pl_zero_margins(out_pp, b, tid, blockDim.x);
@@ -284,10 +264,203 @@ void launch_zero_borders(const ZeroList& zl, int64_t B, cudaStream_t st) {
   check_launch("zero_borders_kernel");
 }
 
+namespace {
+
+// ---- persistent strip gate + apply ---------------------------------------------------
+// One CTA per SM walks a contiguous range of strips (R rows of one image).  A producer
+// warp bulk-copies each strip's rows of x (NHWC fp32: one contiguous range) and of the
+// skip plane (one contiguous range per (cg16, pass, cg8) block, pad column included) into
+// a kGsStages-deep ring; 8 compute warps form v = x * gate (+ skip), split hi/lo and store
+// the output plane rows directly (PL, and PP phase planes when requested), pads included.
+// The ECA gate is computed once per image per CTA by a parallel fixed-order reduction of
+// the GAP partials (deterministic, independent of the CTA).
+constexpr int kGsCompute = 512;  // 16 compute warps: the unit chains are latency-bound
+constexpr int kGsThreads = kGsCompute + 32;
+constexpr int kGsStages = 4;
+
+__global__ void __launch_bounds__(kGsThreads, 1) gate_strips_kernel(
+    const float* __restrict__ gap, int items, const float* __restrict__ eca_w, int k,
+    const float* __restrict__ x, PlBuf skip, int has_skip, PlBuf out_pl, PlBuf out_pp, int has_pp, int C,
+    int H, int W, int R, int64_t B, uint32_t x_bytes, uint32_t stage_bytes) {
+  using namespace ptx;
+  extern __shared__ __align__(128) uint8_t gsm[];
+  float* gate = reinterpret_cast<float*>(gsm + (size_t)kGsStages * stage_bytes);  // [C]
+  float* part = gate + C;  // [kEcaGroups][C] group sums, then [C] means
+  uint64_t* full = reinterpret_cast<uint64_t*>(part + (kEcaGroups + 1) * C);
+  uint64_t* empty = full + kGsStages;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int L = W + 1, Lp = W / 2 + 1, G8 = C / 8;
+  const int np = out_pl.np, nblk = (C / 16) * np * 2;
+  const uint32_t sk_blk = (uint32_t)R * L * 16;
+  const int spi = H / R;
+  const int64_t n_strips = B * spi;
+  const int64_t s_begin = blockIdx.x * n_strips / gridDim.x;
+  const int64_t s_end = (blockIdx.x + 1) * n_strips / gridDim.x;
+  if (tid == 0) {
+    for (int s = 0; s < kGsStages; ++s) {
+      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&empty[s]), kGsCompute / 32);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  grid_dep_wait();  // x, gap and skip come from the previous kernels
+
+  if (warp == kGsCompute / 32) {
+    // ===== producer warp: lane 0 posts the byte count, lanes issue one copy each =====
+    const int ncopy = 1 + (has_skip ? nblk : 0);
+    int i = 0;
+    for (int64_t s = s_begin; s < s_end; ++s, ++i) {
+      const int st = i % kGsStages;
+      mbar_wait(smem_u32(&empty[st]), ((i / kGsStages) & 1) ^ 1);
+      const int64_t b = s / spi;
+      const int y0 = (int)(s - b * spi) * R;
+      const uint32_t bar = smem_u32(&full[st]);
+      uint8_t* base = gsm + (size_t)st * stage_bytes;
+      if (lane == 0) mbar_arrive_expect_tx(bar, x_bytes + (has_skip ? nblk * sk_blk : 0u));
+      __syncwarp();
+      for (int c = lane; c < ncopy; c += 32) {
+        if (c == 0)
+          bulk_g2s(smem_u32(base), x + ((size_t)b * H + y0) * W * C, x_bytes, bar);
+        else
+          bulk_g2s(smem_u32(base + x_bytes + (size_t)(c - 1) * sk_blk),
+                   skip.base + b * skip.img_stride + ((size_t)(c - 1) * skip.Q + (size_t)y0 * L + skip.off) * 8,
+                   sk_blk, bar);
+      }
+    }
+    return;
+  }
+
+  // ===== 8 compute warps =====
+  int64_t cur_b = -1;
+  int i = 0;
+  for (int64_t s = s_begin; s < s_end; ++s, ++i) {
+    const int st = i % kGsStages;
+    const int64_t b = s / spi;
+    const int y0 = (int)(s - b * spi) * R;
+    if (b != cur_b) {
+      // ECA gate of image b (model.py:128-135): the kEcaGroups group sums in parallel,
+      // then added in group order (planes.cuh: the one reduction order of every gate)
+      for (int u = tid; u < kEcaGroups * C; u += kGsCompute)
+        part[u] = eca_group_sum(gap, items, C, b, u % C, u / C);
+      asm volatile("bar.sync 1, %0;" ::"n"(kGsCompute) : "memory");
+      float* mean = part + kEcaGroups * C;  // [C]
+      if (tid < C) {
+        float a = 0.f;
+        for (int g = 0; g < kEcaGroups; ++g) a += part[g * C + tid];
+        mean[tid] = a / (float)(H * W);
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(kGsCompute) : "memory");
+      if (tid < C) gate[tid] = eca_gate_of(mean, C, tid, eca_w, k);
+      asm volatile("bar.sync 1, %0;" ::"n"(kGsCompute) : "memory");
+      cur_b = b;
+    }
+    if (y0 == 0) {  // top / bottom margins of the output planes, once per image
+      pl_zero_margins(out_pl, b, tid, kGsCompute);
+      if (has_pp) pl_zero_margins(out_pp, b, tid, kGsCompute);
+    }
+    mbar_wait(smem_u32(&full[st]), (i / kGsStages) & 1);
+    const float* xs = reinterpret_cast<const float*>(gsm + (size_t)st * stage_bytes);
+    const uint8_t* sk = gsm + (size_t)st * stage_bytes + x_bytes;
+    uint16_t* opl = out_pl.base + b * out_pl.img_stride;
+#pragma unroll 2
+    for (int u = tid; u < R * W * G8; u += kGsCompute) {
+      const int c8 = u % G8, pix = u / G8;
+      const int r = pix / W, xx = pix - r * W;
+      const float4 a0 = *reinterpret_cast<const float4*>(xs + (size_t)pix * C + c8 * 8);
+      const float4 a1 = *reinterpret_cast<const float4*>(xs + (size_t)pix * C + c8 * 8 + 4);
+      const float4 g0 = *reinterpret_cast<const float4*>(gate + c8 * 8);
+      const float4 g1 = *reinterpret_cast<const float4*>(gate + c8 * 8 + 4);
+      float v[8] = {a0.x * g0.x, a0.y * g0.y, a0.z * g0.z, a0.w * g0.w,
+                    a1.x * g1.x, a1.y * g1.y, a1.z * g1.z, a1.w * g1.w};  // eca(x) = x * gate
+      const int kh = ((c8 >> 1) * np) * 2 + (c8 & 1);  // hi block of this 8-channel group
+      if (has_skip) {                                  // + skip (model.py:197-198)
+        const size_t so = (size_t)(r * L + xx) * 16;
+        const uint4 h = *reinterpret_cast<const uint4*>(sk + (size_t)kh * sk_blk + so);
+        const uint32_t hw[4] = {h.x, h.y, h.z, h.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          v[2 * j] += __uint_as_float(hw[j] << 16);
+          v[2 * j + 1] += __uint_as_float(hw[j] & 0xFFFF0000u);
+        }
+        if (np == 2) {
+          const uint4 l = *reinterpret_cast<const uint4*>(sk + (size_t)(kh + 2) * sk_blk + so);
+          const uint32_t lw[4] = {l.x, l.y, l.z, l.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            v[2 * j] += __uint_as_float(lw[j] << 16);
+            v[2 * j + 1] += __uint_as_float(lw[j] & 0xFFFF0000u);
+          }
+        }
+      }
+      const int oy = y0 + r;
+      pl_store8(out_pl, b, 0, c8, oy * L + xx, v);
+      if (has_pp) pl_store8(out_pp, b, (oy & 1) * 2 + (xx & 1), c8, (oy >> 1) * Lp + (xx >> 1), v);
+      if (xx >= W - 2 && (c8 & 1) == 0) {  // pad columns (planes.cuh border contract)
+        const int cg16 = c8 >> 1;
+        if (xx == W - 1)
+          for (int kb = 0; kb < np * 2; ++kb)
+            pl_zero16(opl + ((size_t)(cg16 * np * 2 + kb) * out_pl.Q + (size_t)oy * L + W + out_pl.off) * 8);
+        if (has_pp) {
+          const int plane = (oy & 1) * 2 + (xx & 1);
+          uint16_t* pp_img = out_pp.base + b * out_pp.img_stride + (int64_t)plane * out_pp.plane_stride;
+          for (int kb = 0; kb < np * 2; ++kb)
+            pl_zero16(pp_img + ((size_t)(cg16 * np * 2 + kb) * out_pp.Q + (size_t)(oy >> 1) * Lp + W / 2 +
+                                out_pp.off) * 8);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(smem_u32(&empty[st]));  // this warp is done with stage st
+  }
+}
+
+}  // namespace
+
 void launch_gate_apply(const float* gap, int items, const float* eca_w, int k, const float* x,
                        const PlBuf* skip, const PlBuf* out_pl, const PlBuf* out_pp, float* out_f32,
                        int64_t B, int C, int H, int W, cudaStream_t st) {
   STDA_CHECK(C % 8 == 0 && C <= 1024, "gate_apply: channel count");
+  static const bool strips_off = [] {
+    const char* e = std::getenv("STDA_GATE");
+    return e && std::string(e) == "rows";
+  }();
+  if (!strips_off && out_f32 == nullptr && out_pl != nullptr && C % 16 == 0 && C <= 128 && H % 2 == 0 &&
+      W % 2 == 0 && B > 0) {
+    // persistent strips: R rows (even, dividing H) with a stage of about 32 KB
+    const int np = out_pl->np, nblk = (C / 16) * np * 2, L = W + 1;
+    auto stage = [&](int r) {
+      return (size_t)r * W * C * 4 + (skip ? (size_t)nblk * r * L * 16 : 0);
+    };
+    static const size_t stage_cap = [] {  // env STDA_GATE_STAGE_KB (A/B timing), default 32
+      const char* e = std::getenv("STDA_GATE_STAGE_KB");
+      return (size_t)(e ? std::max(8, std::atoi(e)) : 16) * 1024;  // measured best of 16/32/48
+    }();
+    int R = 2;
+    while (R * 2 <= 16 && H % (R * 2) == 0 && stage(R * 2) <= stage_cap) R *= 2;
+    const size_t stage_bytes = (stage(R) + 127) / 128 * 128;
+    const size_t smem = kGsStages * stage_bytes + (size_t)(kEcaGroups + 2) * C * 4 + 2 * kGsStages * 8;
+    int dev = 0, sms = 148;
+    STDA_CUDA(cudaGetDevice(&dev));
+    STDA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    // measured: with fewer than ~4 strips per SM the per-CTA fill (first loads + gate)
+    // dominates and the one-shot row-block kernel is faster
+    if (H % R == 0 && smem <= 227 * 1024 && B * (H / R) >= 4 * (int64_t)sms) {
+      static uint64_t configured = 0;
+      if (!(configured >> (dev & 63) & 1)) {
+        STDA_CUDA(cudaFuncSetAttribute(gate_strips_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       227 * 1024));
+        configured |= 1ull << (dev & 63);
+      }
+      const int64_t n_strips = B * (H / R);
+      const unsigned grid = (unsigned)std::min<int64_t>(n_strips, sms);
+      launch_pdl(gate_strips_kernel, dim3(grid), dim3(kGsThreads), smem, st, "gate_strips_kernel", gap, items,
+                 eca_w, k, x, skip ? *skip : PlBuf{}, (int)(skip != nullptr), *out_pl,
+                 out_pp ? *out_pp : PlBuf{}, (int)(out_pp != nullptr), C, H, W, R, B,
+                 (uint32_t)((size_t)R * W * C * 4), (uint32_t)stage_bytes);
+      return;
+    }
+  }
   STDA_CHECK(B <= 65535, "gate_apply: batch too large for one launch");
   if (out_f32 == nullptr && out_pl != nullptr && C % 16 == 0 && H % 2 == 0 && W % 2 == 0) {
     // bulk-copy row-block path: R rows per CTA, shared memory sized for the buffers used

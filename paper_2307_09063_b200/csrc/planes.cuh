@@ -132,6 +132,36 @@ __device__ __forceinline__ void pl_zero_margins(const PlBuf& p, int64_t b, int t
   }
 }
 
+// ---- ECA channel means (model.py:128-135) from per-item channel sums -------------------
+// ONE reduction order for every kernel that forms a gate, whatever its thread count: the
+// items of a channel are summed in kEcaGroups interleaved groups (t = g, g + kEcaGroups,
+// ...), each in increasing t, and the group sums are added in increasing g.  A thread that
+// loops over the groups itself performs exactly the same float operations as the parallel
+// form below, so the gates — and every output — are bitwise independent of which gate
+// kernel ran (and so of the batch size).
+constexpr int kEcaGroups = 8;
+
+__device__ __forceinline__ float eca_group_sum(const float* gap, int items, int C, int64_t b, int c, int g) {
+  float a = 0.f;
+  for (int t = g; t < items; t += kEcaGroups) a += __ldg(gap + ((size_t)b * items + t) * C + c);
+  return a;
+}
+// sequential form: the channel sum of channel c
+__device__ __forceinline__ float eca_channel_sum(const float* gap, int items, int C, int64_t b, int c) {
+  float s = 0.f;
+  for (int g = 0; g < kEcaGroups; ++g) s += eca_group_sum(gap, items, C, b, c, g);
+  return s;
+}
+// gate[c] = sigmoid(sum_j w[j] * mean[c + j - k/2]), zero-padded 1-D conv over channels
+__device__ __forceinline__ float eca_gate_of(const float* mean, int C, int c, const float* eca_w, int k) {
+  float z = 0.f;
+  for (int j = 0; j < k; ++j) {
+    const int cc = c + j - k / 2;
+    if (cc >= 0 && cc < C) z = fmaf(__ldg(eca_w + j), mean[cc], z);
+  }
+  return 1.f / (1.f + expf(-z));
+}
+
 constexpr int kMaxZeroBufs = 16;
 struct ZeroList {
   PlBuf buf[kMaxZeroBufs];

@@ -40,6 +40,13 @@ std::vector<HostTap> plane_taps(int mode, int pl) {
         if (tpy != py || tpx != px) continue;
         t.push_back({0, dy == -1 ? -1 : 0, dx == -1 ? -1 : 0, ky * 3 + kx});
       }
+  } else if (mode == CONVT4_HALF) {
+    // pl = output row parity py: phases (py, px), shifts relative to the origin moved
+    // down py rows; wk indexes the full 16-entry ConvT phase kernel
+    const int py = pl;
+    for (int px = 0; px < 2; ++px)
+      for (int a = 0; a < 2; ++a)
+        for (int bb = 0; bb < 2; ++bb) t.push_back({px, a - 1, px + bb - 1, (py * 2 + px) * 4 + a * 2 + bb});
   } else {
     for (int ph = 0; ph < 4; ++ph)
       for (int a = 0; a < 2; ++a)
@@ -50,13 +57,22 @@ std::vector<HostTap> plane_taps(int mode, int pl) {
   }
   // the device's constexpr tables must agree with this host table
   for (size_t i = 0; i < t.size(); ++i)
-    STDA_CHECK(t[i].dy == tap_dy(mode, pl, (int)i) && t[i].dx == tap_dx(mode, pl, (int)i) &&
+    STDA_CHECK(t[i].dy == tap_dy(mode, mode == CONVT4_HALF ? 0 : pl, (int)i) &&
+                   t[i].dx == tap_dx(mode, mode == CONVT4_HALF ? 0 : pl, (int)i) &&
                    t[i].acc == tap_acc(mode, (int)i) && (int)t.size() == ntaps(mode, pl),
                "internal: tap table mismatch");
   return t;
 }
 
 }  // namespace
+
+bool half_t_enabled() {  // env STDA_TC_HALF=0 keeps 3-MMA full ConvT items (A/B timing)
+  static const bool on = [] {
+    const char* e = std::getenv("STDA_TC_HALF");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 bool tc_supported(int mode, int cin, int cout) {
   (void)mode;
@@ -68,18 +84,25 @@ void tc_pack_layer(TcLayerDesc& d, int mode, int cin, int cout, const float* w0,
   STDA_CHECK(tc_supported(mode, cin, cout), "layer shape not supported by the tensor-core path");
   STDA_CHECK((mode == CONV3_S1) == (w1 == nullptr), "S1 layers are single-source, S2/T dual");
   std::memset(&d, 0, sizeof(d));
+  // A dual ConvT whose 8 accumulators cannot take the hi/lo N-concat in two TMEM slots
+  // runs as CONVT4_HALF: one output-row parity per work item (4 accumulators), so the
+  // 2-MMA concat applies (fewer operand bytes than 3 MMAs per tap).
+  const bool wide_t = mode == CONVT4_S2 && (w1 ? 2 : 1) * 4 * 2 * cout * 2 > 512;
+  if (wide_t && !bf16 && half_t_enabled()) mode = CONVT4_HALF;
+  const bool tmode = mode == CONVT4_S2 || mode == CONVT4_HALF;
   d.mode = mode;
   d.n_src = w1 ? 2 : 1;
   d.cin = cin;
   d.cout = cout;
   d.n_planes = mode == CONV3_S2 ? 4 : 1;
-  d.n_acc_src = mode == CONVT4_S2 ? 4 : 1;
+  d.n_acc_src = nacc_src(mode);
   d.npass = bf16 ? 1 : 3;
   const int npassB = bf16 ? 1 : 2;
-  const int wk_per = mode == CONVT4_S2 ? 16 : 9;
-  std::vector<std::vector<HostTap>> taps(d.n_planes);
+  const int wk_per = tmode ? 16 : 9;
+  const int n_halves = mode == CONVT4_HALF ? 2 : 1;  // HALF: py = 0 taps, then py = 1 taps
+  std::vector<std::vector<HostTap>> taps(d.n_planes * n_halves);
+  for (int pl = 0; pl < d.n_planes * n_halves; ++pl) taps[pl] = plane_taps(mode, pl);
   for (int pl = 0; pl < d.n_planes; ++pl) {
-    taps[pl] = plane_taps(mode, pl);
     PlaneTaps& pt = d.planes[pl];
     pt.n = (int8_t)taps[pl].size();
     for (size_t t = 0; t < taps[pl].size(); ++t) {
@@ -107,8 +130,9 @@ void tc_pack_layer(TcLayerDesc& d, int mode, int cin, int cout, const float* w0,
   };
   for (int c = 0; c < n_chunks; ++c) {
     const int pl = c / cgroups, cgi = c % cgroups;
+    for (int hv = 0; hv < n_halves; ++hv)
     for (int s = 0; s < d.n_src; ++s)
-      for (const HostTap& t : taps[pl]) {
+      for (const HostTap& t : taps[pl + hv]) {
         if (d.concat) {
           for (int kg = 0; kg < 2; ++kg)
             for (int pass = 0; pass < 2; ++pass)
@@ -125,6 +149,16 @@ void tc_pack_layer(TcLayerDesc& d, int mode, int cin, int cout, const float* w0,
   }
 }
 
+namespace {
+int slots_cap() {  // env STDA_TC_SLOTS (A/B timing), default kMaxSlots
+  static const int v = [] {
+    const char* e = std::getenv("STDA_TC_SLOTS");
+    return e ? std::max(1, std::min(kMaxSlots, std::atoi(e))) : kMaxSlots;
+  }();
+  return v;
+}
+}  // namespace
+
 TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W) {
   TcGeometry g{};
   g.B = B;
@@ -135,7 +169,7 @@ TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W) {
     g.Wp = W / 2;
     g.Ho = H / 2;
     g.Wo = W / 2;
-  } else if (d.mode == CONVT4_S2) {
+  } else if (d.mode == CONVT4_S2 || d.mode == CONVT4_HALF) {
     g.Hp = H;
     g.Wp = W;
     g.Ho = 2 * H;
@@ -173,8 +207,13 @@ TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W) {
   // overlaps the MMAs of item i+1), (3) the largest G, (4) resident weights (loaded once
   // per CTA instead of once per work item); fall back step by step.
   bool ok = false;
-  for (int pass = 0; pass < 3 && !ok; ++pass) {
-    const int want_stages = pass == 2 ? 1 : 2, want_slots = pass == 0 ? 2 : 1;
+  static const int pref_stages = [] {  // env STDA_TC_MINSTAGES: stage depth preferred over G
+    const char* e = std::getenv("STDA_TC_MINSTAGES");
+    return e ? std::max(2, std::min(kMaxStages, std::atoi(e))) : 2;
+  }();
+  const int pref = d.mode == CONV3_S2 ? pref_stages : 2;
+  for (int pass = 0; pass < 4 && !ok; ++pass) {
+    const int want_stages = pass == 0 ? pref : pass == 3 ? 1 : 2, want_slots = pass <= 1 ? 2 : 1;
     for (int G : {4, 2, 1}) {
       const int P8 = (G * 128 + span + 7) / 8 * 8;
       const uint32_t a_stage = (uint32_t)d.n_src * npassA * 2 * P8 * 16;
@@ -182,7 +221,8 @@ TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W) {
       if (acc_cols * want_slots > 512 || G * n_acc > 32) continue;
       for (bool resident : {true, false}) {
         int stages = 0;
-        for (int st : {3, 2, 1}) {
+        // measured: S1/T layers are slower beyond 3 stages; S2 layers (L2-fed) may go deeper
+        for (int st = d.mode == CONV3_S2 ? kMaxStages : 3; st >= 1; --st) {
           const size_t need = resident ? (size_t)st * a_stage + w_res : (size_t)st * (a_stage + b_stage);
           if (need + fixed <= (size_t)kMaxSmem) {
             stages = st;
@@ -193,7 +233,9 @@ TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W) {
         g.G = G;
         g.P_max = P8;
         g.stages = stages;
-        g.slots = want_slots;
+        // extra TMEM slots (free columns) absorb epilogue jitter: the MMA warp then rarely
+        // waits for a slot
+        g.slots = want_slots == 2 ? std::min(slots_cap(), 512 / acc_cols) : want_slots;
         g.a_stage_bytes = a_stage;
         g.b_stage_bytes = resident ? 0 : b_stage;
         g.resident = resident;
@@ -211,7 +253,7 @@ TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W) {
   }
   STDA_CHECK(ok, "tensor-core conv: no tiling fits shared memory");
   const int positions = g.Hp * g.L;
-  g.items_per_image = cdiv(positions, g.G * 128);
+  g.items_per_image = cdiv(positions, g.G * 128) * (d.mode == CONVT4_HALF ? 2 : 1);
   return g;
 }
 
@@ -284,6 +326,9 @@ void tc_launch(const TcLayerDesc& d, const TcGeometry& g, const PlBuf& src0, con
   switch (d.mode) {
     case CONV3_S1: return dispatch_s1(d.cout, npm, g.G, p, grid, g.smem_bytes, st);
     case CONV3_S2: return dispatch_s2(d.cout, npm, g.G, p, grid, g.smem_bytes, st);
+    case CONVT4_HALF:
+      STDA_CHECK(out.mode == 0, "half-phase ConvT writes NHWC fp32");
+      return dispatch_th(d.cout, npm, g.G, p, grid, g.smem_bytes, st);
     default: return dispatch_t(d.cout, npm, g.G, p, grid, g.smem_bytes, st);
   }
 }

@@ -23,6 +23,8 @@ constexpr int kEpiWarp0 = 2;   // warps 2..9: epilogue (warp % 4 = TMEM lane qua
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = (kEpiWarp0 + kEpiWarps) * 32;
 constexpr int kMaxSmem = 227 * 1024;
+constexpr int kMaxStages = 6;  // smem ring depth cap
+constexpr int kMaxSlots = 4;   // TMEM accumulator slots cap
 
 // precision schemes
 constexpr int kNpmBf16 = 0;    // one pass: A_hi x B_hi
@@ -67,27 +69,40 @@ __device__ __forceinline__ void trace_at(unsigned long long* tr, int region, int
 // S2:  plane (py,px) = (dy != 0, dx != 0); shift (dy == -1 ? -1 : 0, dx == -1 ? -1 : 0),
 //      taps of a plane in (ky, kx) order
 // T:   t = ph*4 + a*2 + b, accumulator ph, shift (py + a - 1, px + b - 1)
+// HALF (ConvT, one output-row parity py per work item): t = px*4 + a*2 + b, accumulator px,
+//      shift (a - 1, px + b - 1) relative to the item's origin shifted down by py rows
 __host__ __device__ constexpr int ntaps(int mode, int pl) {
-  return mode == CONV3_S1 ? 9 : mode == CONVT4_S2 ? 16 : (pl == 0 ? 1 : pl == 3 ? 4 : 2);
+  return mode == CONV3_S1      ? 9
+         : mode == CONVT4_S2   ? 16
+         : mode == CONVT4_HALF ? 8
+                               : (pl == 0 ? 1 : pl == 3 ? 4 : 2);
 }
 __host__ __device__ constexpr int tap_dy(int mode, int pl, int t) {
-  return mode == CONV3_S1    ? t / 3 - 1
-         : mode == CONVT4_S2 ? (t / 4 >> 1) + ((t >> 1) & 1) - 1
-         : pl == 2           ? (t == 0 ? -1 : 0)
-         : pl == 3           ? (t < 2 ? -1 : 0)
-                             : 0;
+  return mode == CONV3_S1      ? t / 3 - 1
+         : mode == CONVT4_S2   ? (t / 4 >> 1) + ((t >> 1) & 1) - 1
+         : mode == CONVT4_HALF ? ((t >> 1) & 1) - 1
+         : pl == 2             ? (t == 0 ? -1 : 0)
+         : pl == 3             ? (t < 2 ? -1 : 0)
+                               : 0;
 }
 __host__ __device__ constexpr int tap_dx(int mode, int pl, int t) {
-  return mode == CONV3_S1    ? t % 3 - 1
-         : mode == CONVT4_S2 ? ((t / 4) & 1) + (t & 1) - 1
-         : pl == 1           ? (t == 0 ? -1 : 0)
-         : pl == 3           ? ((t & 1) == 0 ? -1 : 0)
-                             : 0;
+  return mode == CONV3_S1      ? t % 3 - 1
+         : mode == CONVT4_S2   ? ((t / 4) & 1) + (t & 1) - 1
+         : mode == CONVT4_HALF ? (t >> 2) + (t & 1) - 1
+         : pl == 1             ? (t == 0 ? -1 : 0)
+         : pl == 3             ? ((t & 1) == 0 ? -1 : 0)
+                               : 0;
 }
-__host__ __device__ constexpr int tap_acc(int mode, int t) { return mode == CONVT4_S2 ? t / 4 : 0; }
+__host__ __device__ constexpr int tap_acc(int mode, int t) {
+  return mode == CONVT4_S2 || mode == CONVT4_HALF ? t / 4 : 0;
+}
 // first tap touching its accumulator (in chunk 0 = plane 0, channel group 0)
 __host__ __device__ constexpr bool tap_first(int mode, int t) {
-  return mode == CONVT4_S2 ? (t & 3) == 0 : t == 0;
+  return mode == CONVT4_S2 || mode == CONVT4_HALF ? (t & 3) == 0 : t == 0;
+}
+// accumulators per source
+__host__ __device__ constexpr int nacc_src(int mode) {
+  return mode == CONVT4_S2 ? 4 : mode == CONVT4_HALF ? 2 : 1;
 }
 // minimum shift over a plane's taps, as a*L + b
 __host__ __device__ constexpr int plane_lo_a(int mode, int pl) {
@@ -204,7 +219,7 @@ __device__ __forceinline__ void issue_chunk(bool leader, uint64_t a0, uint64_t b
                                             int L, bool first_chunk, uint32_t src_units,
                                             uint32_t lo_units) {
   constexpr int NT = ntaps(MODE, PL);
-  constexpr int NACC_SRC = MODE == CONVT4_S2 ? 4 : 1;
+  constexpr int NACC_SRC = nacc_src(MODE);
   constexpr int NACC = (DUAL ? 2 : 1) * NACC_SRC;
   constexpr int AW = NPM == kNpmConcat ? 2 * N : N;
   constexpr uint32_t TAP_UNITS = (NPM == kNpmBf16 ? 32u * N : 64u * N) / 16u;
@@ -245,7 +260,7 @@ template <int N, int MODE, bool DUAL, int NPM, int G>
 __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int NSRC = DUAL ? 2 : 1;
-  constexpr int NACC_SRC = MODE == CONVT4_S2 ? 4 : 1;
+  constexpr int NACC_SRC = nacc_src(MODE);
   constexpr int NACC = NSRC * NACC_SRC;
   constexpr int NPLANES = MODE == CONV3_S2 ? 4 : 1;
   constexpr int NPASS_A = NPM == kNpmBf16 ? 1 : 2;
@@ -298,52 +313,52 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
 
   if (warp == kProdWarp) {
     // ===================== producer: cp.async.bulk of A ranges + packed weights =========
-    if (lane == 0) {
-      if (p.resident) {
-        mbar_arrive_expect_tx(smem_u32(wbar), p.w_total);
-        bulk_g2s(smem_u32(b_base), d.w, p.w_total, smem_u32(wbar));
-      }
-      grid_dep_wait();  // weights are static; activations come from the previous kernel
-      uint32_t k = 0;
-      for (int item = blockIdx.x; item < p.total_items; item += gridDim.x) {
-        const int b = item / p.items_per_image;
-        const int q0 = (item - b * p.items_per_image) * p.G * 128;
-        for (int c = 0; c < n_chunks; ++c, ++k) {
-          const int stage = k % p.stages;
-          const uint32_t phase = (k / p.stages) & 1;
-          mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
-          trace_at(p.trace, 0, 2 * k);
-          const int pl = c / cgroups, cgi = c - pl * cgroups;
-          const PlaneTaps& pt = d.planes[pl];
-          const int P = p.G * 128 + pt.hi - pt.lo;
-          const uint32_t a_bytes = (uint32_t)P * 16;
-          const uint32_t w_bytes = p.resident ? 0u : (uint32_t)(d.chunk_off[c + 1] - d.chunk_off[c]);
-          const uint32_t fb = smem_u32(&full[stage]);
-          if ((p.dbg & 4) && k >= (uint32_t)p.stages) {
-            mbar_arrive(fb);
-            continue;
-          }
-          mbar_arrive_expect_tx(fb, w_bytes + (uint32_t)NSRC * NPASS_A * 2 * a_bytes);
-          if (!p.resident)
-            bulk_g2s(smem_u32(b_base + (size_t)stage * p.b_stage_bytes),
-                     reinterpret_cast<const uint8_t*>(d.w) + d.chunk_off[c], w_bytes, fb);
-          uint8_t* sa = a_base + (size_t)stage * p.a_stage_bytes;
-#pragma unroll
-          for (int s = 0; s < NSRC; ++s) {
-            const PlBuf& S = p.src[s];
-            const uint16_t* img =
-                S.base + (int64_t)b * S.img_stride + (int64_t)(NPLANES == 4 ? pl : 0) * S.plane_stride;
-#pragma unroll
-            for (int pass = 0; pass < NPASS_A; ++pass)
-#pragma unroll
-              for (int cg8 = 0; cg8 < 2; ++cg8) {
-                const uint16_t* src = img + (S.block_index(cgi, pass, cg8) + q0 + pt.lo + S.off) * 8;
-                bulk_g2s(smem_u32(sa + (size_t)s * src_bytes + (size_t)(pass * 2 + cg8) * p.P_max * 16), src,
-                         a_bytes, fb);
-              }
-          }
-          trace_at(p.trace, 0, 2 * k + 1);
+    // The whole warp runs the loop; lane 0 posts the stage's byte count, then lane l
+    // issues copy l (source, pass, 8-channel group) — the per-copy address arithmetic runs
+    // in parallel instead of ~130 serial cycles per copy on one thread.
+    constexpr int NCOPY = NSRC * NPASS_A * 2;
+    const int cs = lane / (NPASS_A * 2), cpass = (lane >> 1) % NPASS_A, ccg8 = lane & 1;
+    if (lane == 0 && p.resident) {
+      mbar_arrive_expect_tx(smem_u32(wbar), p.w_total);
+      bulk_g2s(smem_u32(b_base), d.w, p.w_total, smem_u32(wbar));
+    }
+    grid_dep_wait();  // weights are static; activations come from the previous kernel
+    const PlBuf& S = p.src[lane < NCOPY ? cs : 0];
+    uint32_t k = 0;
+    for (int item = blockIdx.x; item < p.total_items; item += gridDim.x) {
+      const int b = item / p.items_per_image;
+      const int it = item - b * p.items_per_image;
+      // HALF: items (tile, py) interleaved; the tile origin moves down py rows
+      const int q0 = MODE == CONVT4_HALF ? (it >> 1) * p.G * 128 + (it & 1) * p.L : it * p.G * 128;
+      const uint16_t* img = S.base + (int64_t)b * S.img_stride;
+      for (int c = 0; c < n_chunks; ++c, ++k) {
+        const int stage = k % p.stages;
+        const uint32_t phase = (k / p.stages) & 1;
+        mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+        if (lane == 0) trace_at(p.trace, 0, 2 * k);
+        const int pl = c / cgroups, cgi = c - pl * cgroups;
+        const PlaneTaps& pt = d.planes[pl];
+        const int P = p.G * 128 + pt.hi - pt.lo;
+        const uint32_t a_bytes = (uint32_t)P * 16;
+        const uint32_t w_bytes = p.resident ? 0u : (uint32_t)(d.chunk_off[c + 1] - d.chunk_off[c]);
+        const uint32_t fb = smem_u32(&full[stage]);
+        if ((p.dbg & 4) && k >= (uint32_t)p.stages) {
+          if (lane == 0) mbar_arrive(fb);
+          continue;
         }
+        if (lane == 0) mbar_arrive_expect_tx(fb, w_bytes + (uint32_t)NCOPY * a_bytes);
+        __syncwarp();  // byte count posted before any copy can complete
+        if (lane == NCOPY && !p.resident)
+          bulk_g2s(smem_u32(b_base + (size_t)stage * p.b_stage_bytes),
+                   reinterpret_cast<const uint8_t*>(d.w) + d.chunk_off[c], w_bytes, fb);
+        if (lane < NCOPY) {
+          const uint16_t* src = img + (int64_t)(NPLANES == 4 ? pl : 0) * S.plane_stride +
+                                (S.block_index(cgi, cpass, ccg8) + q0 + pt.lo + S.off) * 8;
+          bulk_g2s(smem_u32(a_base + (size_t)stage * p.a_stage_bytes + (size_t)cs * src_bytes +
+                            (size_t)(cpass * 2 + ccg8) * p.P_max * 16),
+                   src, a_bytes, fb);
+        }
+        if (lane == 0) trace_at(p.trace, 0, 2 * k + 1);
       }
     }
     __syncwarp();
@@ -375,9 +390,14 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
         tc_fence_after();
         if (leader) trace_at(p.trace, 1, 2 * k);
         const uint64_t a0 = smem_desc(smem_u32(a_base + (size_t)stage * p.a_stage_bytes), lboA, 128);
+        // HALF: each weight chunk holds the py = 0 taps, then the py = 1 taps
+        const size_t half_off =
+            MODE == CONVT4_HALF ? (size_t)((item - (item / p.items_per_image) * p.items_per_image) & 1) * NSRC *
+                                      ntaps(MODE, 0) * (NPM == kNpmBf16 ? 32 : 64) * N
+                                : 0;
         const uint64_t b0 = smem_desc(
-            smem_u32(b_base + (p.resident ? (size_t)d.chunk_off[c] : (size_t)stage * p.b_stage_bytes)), lboB,
-            128);
+            smem_u32(b_base + (p.resident ? (size_t)d.chunk_off[c] : (size_t)stage * p.b_stage_bytes) + half_off),
+            lboB, 128);
         if constexpr (MODE == CONV3_S2) {
           switch (c / cgroups) {
             case 0: issue_chunk<N, MODE, 0, DUAL, NPM, G>(leader, a0, b0, dslot, p.L, c == 0, src_units, lo_units); break;
@@ -412,7 +432,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
       const uint32_t sphase = (ic / p.slots) & 1;
       const int b = item / p.items_per_image;
       const int it = item - b * p.items_per_image;
-      const int q0 = it * p.G * 128;
+      const int q0 = (MODE == CONVT4_HALF ? it >> 1 : it) * p.G * 128;
+      const int py = MODE == CONVT4_HALF ? (it & 1) : 0;  // output row parity of a HALF item
       mbar_wait(smem_u32(&tfull[slot]), sphase);
       __syncwarp();
       tc_fence_after();
@@ -447,6 +468,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
           if (MODE == CONVT4_S2) {
             oy = 2 * y + (ph >> 1);
             ox = 2 * x + (ph & 1);
+          } else if (MODE == CONVT4_HALF) {
+            oy = 2 * y + py;
+            ox = 2 * x + ph;
           }
 #pragma unroll
           for (int j = 0; j < N; j += 16) {
@@ -588,6 +612,7 @@ void dispatch_mode(int n, int npm, int G, const Params& p, int grid, size_t smem
 void dispatch_s1(int n, int npm, int G, const Params& p, int grid, size_t smem, cudaStream_t st);
 void dispatch_s2(int n, int npm, int G, const Params& p, int grid, size_t smem, cudaStream_t st);
 void dispatch_t(int n, int npm, int G, const Params& p, int grid, size_t smem, cudaStream_t st);
+void dispatch_th(int n, int npm, int G, const Params& p, int grid, size_t smem, cudaStream_t st);
 
 }  // namespace detail
 }  // namespace tc

@@ -70,6 +70,16 @@ def test_batch_invariance_bitwise():
     assert torch.equal(full, torch.cat([net(x[:2]), net(x[2:5]), net(x[5:])]))
 
 
+def test_batch_invariance_across_gate_kernels():
+    """Kernel choices that depend on the batch (persistent strip gate vs row-block gate)
+    must not change a single bit: every gate uses one reduction order (planes.cuh)."""
+    net = StdaNet(StdaConfig(map_height=128, map_width=128)).eval().cuda()
+    x = synth_triplets(48, 128, 128, seed=11)
+    full = net(x)                                   # enough strips for the persistent gates
+    halves = torch.cat([net(x[:24]), net(x[24:])])  # row-block gates
+    assert torch.equal(full, halves)
+
+
 def test_stream_window_equals_per_triplet_forward():            # BASELINE config 4 semantics
     net = StdaNet(StdaConfig(map_height=64, map_width=64)).eval().cuda()
     frames = synth_frames(12, 64, 64, seed=3)
