@@ -432,7 +432,7 @@ void launch_gate_apply(const float* gap, int items, const float* eca_w, int k, c
     auto stage = [&](int r) {
       return (size_t)r * W * C * 4 + (skip ? (size_t)nblk * r * L * 16 : 0);
     };
-    static const size_t stage_cap = [] {  // env STDA_GATE_STAGE_KB (A/B timing), default 32
+    static const size_t stage_cap = [] {  // env STDA_GATE_STAGE_KB (A/B timing), default 16
       const char* e = std::getenv("STDA_GATE_STAGE_KB");
       return (size_t)(e ? std::max(8, std::atoi(e)) : 16) * 1024;  // measured best of 16/32/48
     }();
