@@ -128,6 +128,15 @@ int stda_synth_frames(uint64_t seed, int32_t scene, int64_t seq, int64_t first_f
 int stda_synth_triplets(uint64_t seed, int32_t scene, int64_t first_seq, int64_t batch,
                         int32_t frames, int32_t h, int32_t w, float* x, void* stream);
 
+/* ---- batched-inference epilogue (replaces the per-sample numpy tail of reference
+ * denoise.py:40-42 and NormStats.denormalize, data.py:34-36) ----
+ * out[b][x][h] = (clip(y[b][0][h][x], 0, 1) * scale + z_min) * std + mean, float32 with every
+ * product and sum rounded separately; scale = float32(z_max - z_min) computed in double.
+ * y [batch][1][h][w] (network orientation h = Doppler, w = range) -> out [batch][w][h]
+ * (the dataset's range x Doppler orientation).  Device pointers, stream-ordered. */
+int stda_denoise_epilogue(const float* y, float* out, int64_t batch, int32_t h, int32_t w, float scale,
+                          float z_min, float std_, float mean, void* stream);
+
 /* ---- debug (no reference counterpart) ----
  * Arm a one-shot clock64 timeline of CTA 0 for the launch_index-th following tensor-core
  * conv launch; dev_buf holds 5 x 8192 uint64 (layout in csrc/tc_kernel.cuh, trace_at). */

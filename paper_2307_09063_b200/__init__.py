@@ -19,3 +19,8 @@ from .model import (  # noqa: F401
     parameter_count,
 )
 from .fold import fold_state_dict  # noqa: F401
+# batched inference driver and its data formats (reference
+# denoise.py, data.py, rdc1.py)
+from .data import ManifestInfo, NormStats, TripletDataset, load_manifest  # noqa: F401
+from .denoise import denoise_dataset  # noqa: F401
+from .rdc1 import read_cube, write_magnitude_cube  # noqa: F401

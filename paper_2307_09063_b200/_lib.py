@@ -47,6 +47,8 @@ SIGNATURES = {
     "stda_synth_frames": (C.c_int, [_u64, _i32, _i64, _i64, _i64, _i32, _i32, _vp, _vp]),
     "stda_synth_triplets": (C.c_int, [_u64, _i32, _i64, _i64, _i32, _i32, _i32, _vp, _vp]),
     "stda_debug_trace": (C.c_int, [_vp, _i32]),
+    "stda_denoise_epilogue": (C.c_int, [_vp, _vp, _i64, _i32, _i32, C.c_float, C.c_float, C.c_float, C.c_float,
+                                        _vp]),
 }
 
 ABI_VERSION = 1
@@ -177,6 +179,11 @@ def synth_frames(seed, scene, seq, first_frame, n, hh, ww, out, stream) -> None:
 def synth_triplets(seed, scene, first_seq, batch, frames, hh, ww, x, stream) -> None:
     _check(lib().stda_synth_triplets(seed, scene, first_seq, batch, frames, hh, ww, x, stream),
            "stda_synth_triplets")
+
+
+def denoise_epilogue(y, out, batch, hh, ww, scale, z_min, std, mean, stream) -> None:
+    _check(lib().stda_denoise_epilogue(y, out, batch, hh, ww, scale, z_min, std, mean, stream),
+           "stda_denoise_epilogue")
 
 
 def loaded_path() -> str:

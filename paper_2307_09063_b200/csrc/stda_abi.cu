@@ -29,6 +29,8 @@ namespace stda {
 void launch_synth(uint64_t seed, int scene, int64_t seq0, int64_t seq_step, int64_t frame0,
                   int frames_per_seq, int frame_order, int64_t n_out, int H, int W, float* out,
                   cudaStream_t st);
+void launch_denoise_epilogue(const float* y, float* out, int64_t B, int H, int W, float scale, float z_min,
+                             float stdv, float mean, cudaStream_t st);
 
 static thread_local std::string g_last_error;
 void set_error(const std::string& msg) { g_last_error = msg; }
@@ -784,6 +786,16 @@ int stda_synth_frames(uint64_t seed, int32_t scene, int64_t seq, int64_t first_f
     STDA_CHECK(n_frames < (1ll << 31), "too many frames");
     launch_synth(seed, scene, seq, 0, first_frame, (int)n_frames, 0, n_frames, h, w, out,
                  static_cast<cudaStream_t>(stream));
+  });
+}
+
+int stda_denoise_epilogue(const float* y, float* out, int64_t batch, int32_t h, int32_t w, float scale,
+                          float z_min, float std_, float mean, void* stream) {
+  return guarded([&] {
+    STDA_CHECK(batch >= 0 && h > 0 && w > 0, "bad epilogue shape");
+    if (batch == 0) return;
+    STDA_CHECK(y && out, "null buffer");
+    launch_denoise_epilogue(y, out, batch, h, w, scale, z_min, std_, mean, static_cast<cudaStream_t>(stream));
   });
 }
 
