@@ -63,11 +63,12 @@ def denoise_dataset(checkpoint_path, dataset_dir, out_dir, split: Optional[str] 
     maps = torch.empty((B, w, h), dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
-    def flush(job):
+    def flush(job):  # measured: a thread pool for these 32 KB writes is slower
         k, idx, done = job
         done.synchronize()
+        maps_k = m_host[k].numpy()
         for j, i in enumerate(idx):
-            write_magnitude_cube(m_host[k][j].numpy(), out / f"{dataset.sample_id(i)}.rdc")
+            write_magnitude_cube(maps_k[j], out / f"{dataset.sample_id(i)}.rdc")
 
     pending = None
     with torch.no_grad():
