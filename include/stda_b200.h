@@ -137,6 +137,18 @@ int stda_synth_triplets(uint64_t seed, int32_t scene, int64_t first_seq, int64_t
 int stda_denoise_epilogue(const float* y, float* out, int64_t batch, int32_t h, int32_t w, float scale,
                           float z_min, float std_, float mean, void* stream);
 
+/* ---- range-Doppler front end (the step before the denoiser; reference
+ * rdlab/rd_pipeline.py:82-159 range_doppler_map -> to_db -> normalize and
+ * rdlab/dataset.py:184-211 clutter_filter), float64 inside ----
+ * beat: n frames of N x M complex64 (fast time x slow time, re/im interleaved), N <= P,
+ * M <= Q (zero padded); P, Q powers of two with P*Q*24 bytes <= 227 KB (64 x 128 default).
+ * stats: device pointer to 5 doubles {mean, std, z_min, z_max, degenerate} (the dataset's
+ * normalisation record) or NULL for single-frame statistics.  clutter: apply the median
+ * clutter filter.  layout 0: out [n][P][Q] range x Doppler; 1: out [n][Q][P] Doppler x range
+ * (the network's h x w: a frame stream for stda_forward_window). */
+int stda_rd_frontend(const void* beat, int64_t n, int32_t N, int32_t M, int32_t P, int32_t Q,
+                     const double* stats, int32_t clutter, int32_t layout, float* out, void* stream);
+
 /* ---- debug (no reference counterpart) ----
  * Arm a one-shot clock64 timeline of CTA 0 for the launch_index-th following tensor-core
  * conv launch; dev_buf holds 5 x 8192 uint64 (layout in csrc/tc_kernel.cuh, trace_at). */

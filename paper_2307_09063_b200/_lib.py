@@ -49,6 +49,7 @@ SIGNATURES = {
     "stda_debug_trace": (C.c_int, [_vp, _i32]),
     "stda_denoise_epilogue": (C.c_int, [_vp, _vp, _i64, _i32, _i32, C.c_float, C.c_float, C.c_float, C.c_float,
                                         _vp]),
+    "stda_rd_frontend": (C.c_int, [_vp, _i64, _i32, _i32, _i32, _i32, _vp, _i32, _i32, _vp, _vp]),
 }
 
 ABI_VERSION = 1
@@ -184,6 +185,10 @@ def synth_triplets(seed, scene, first_seq, batch, frames, hh, ww, x, stream) -> 
 def denoise_epilogue(y, out, batch, hh, ww, scale, z_min, std, mean, stream) -> None:
     _check(lib().stda_denoise_epilogue(y, out, batch, hh, ww, scale, z_min, std, mean, stream),
            "stda_denoise_epilogue")
+
+
+def rd_frontend(beat, n, N, M, P, Q, stats, clutter, layout, out, stream) -> None:
+    _check(lib().stda_rd_frontend(beat, n, N, M, P, Q, stats, clutter, layout, out, stream), "stda_rd_frontend")
 
 
 def loaded_path() -> str:

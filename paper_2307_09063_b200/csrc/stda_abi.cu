@@ -31,6 +31,8 @@ void launch_synth(uint64_t seed, int scene, int64_t seq0, int64_t seq_step, int6
                   cudaStream_t st);
 void launch_denoise_epilogue(const float* y, float* out, int64_t B, int H, int W, float scale, float z_min,
                              float stdv, float mean, cudaStream_t st);
+void launch_rd_frontend(const float2* beat, int64_t n, int N, int M, int P, int Q, const double* stats,
+                        bool clutter, int layout, float* out, cudaStream_t st);
 
 static thread_local std::string g_last_error;
 void set_error(const std::string& msg) { g_last_error = msg; }
@@ -786,6 +788,17 @@ int stda_synth_frames(uint64_t seed, int32_t scene, int64_t seq, int64_t first_f
     STDA_CHECK(n_frames < (1ll << 31), "too many frames");
     launch_synth(seed, scene, seq, 0, first_frame, (int)n_frames, 0, n_frames, h, w, out,
                  static_cast<cudaStream_t>(stream));
+  });
+}
+
+int stda_rd_frontend(const void* beat, int64_t n, int32_t N, int32_t M, int32_t P, int32_t Q,
+                     const double* stats, int32_t clutter, int32_t layout, float* out, void* stream) {
+  return guarded([&] {
+    STDA_CHECK(n >= 0, "bad frame count");
+    if (n == 0) return;
+    STDA_CHECK(beat && out, "null buffer");
+    launch_rd_frontend(static_cast<const float2*>(beat), n, N, M, P, Q, stats, clutter != 0, layout, out,
+                       static_cast<cudaStream_t>(stream));
   });
 }
 

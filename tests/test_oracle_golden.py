@@ -4,8 +4,12 @@ import numpy as np
 import pytest
 import torch
 
+from pathlib import Path
+
 from tests._helpers import folded_forward, golden_index, golden_names, load_golden, nmax_err
 from oracle import np64, port
+
+GOLDEN = Path(__file__).resolve().parent / "golden"
 
 
 @pytest.mark.parametrize("name", golden_names())
@@ -50,3 +54,14 @@ def test_port_eca_and_shape_errors():
     w = torch.zeros(1, 1, 3)
     t = torch.rand(2, 8, 4, 4)
     assert torch.allclose(port.eca(w, t), 0.5 * t)
+
+
+def test_frontend_port_matches_rdlab_golden():
+    """oracle/frontend.py (the front end's checker and CPU baseline) against the reference
+    rdlab chain's own outputs (tests/golden/make_frontend_golden.py)."""
+    from oracle import frontend as fe
+
+    g = np.load(GOLDEN / "frontend.npz")
+    assert np.abs(fe.frontend(g["beat"]) - g["single"]).max() <= 1e-12
+    assert np.abs(fe.frontend(g["beat"], stats=g["stats"]) - g["given"]).max() <= 1e-12
+    assert np.abs(fe.frontend(g["beat"], use_clutter=False) - g["noclutter"]).max() <= 1e-12
