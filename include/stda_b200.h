@@ -149,6 +149,20 @@ int stda_denoise_epilogue(const float* y, float* out, int64_t batch, int32_t h, 
 int stda_rd_frontend(const void* beat, int64_t n, int32_t N, int32_t M, int32_t P, int32_t Q,
                      const double* stats, int32_t clutter, int32_t layout, float* out, void* stream);
 
+/* ---- scoring of denoised maps (the step after the denoiser; reference
+ * rdlab/evaluation.py:160-201 method "denoised", rdlab/detection_metrics.py:119-259) ----
+ * clean: n maps P x Q, complex64 (clean_kind 0: the clean RD map) or float32 magnitudes
+ * (kind 1); test_db: n float32 dB maps P x Q (the denoiser's output, range x Doppler).
+ * CA-CFAR cross window guard (g0, g1) / training (t0, t1) cells per axis (even), threshold
+ * factors alpha_obj (object extraction on |clean|) and alpha_det (detections on the
+ * linearised test map), object dilation `margin`.  out: n x {sinr_db, evm, n_object,
+ * n_noise, status} doubles (status 0 ok, 1 no object cells, 2 clean map zero at an object
+ * cell, 3 empty noise set; sinr/evm NaN unless 0); det_hits: n x P x Q bytes (test-map
+ * CFAR hits, for host-side clustering).  Device pointers, float64 inside. */
+int stda_score(const void* clean, int32_t clean_kind, const float* test_db, int64_t n, int32_t P, int32_t Q,
+               int32_t guard0, int32_t guard1, int32_t train0, int32_t train1, double alpha_obj, double alpha_det,
+               int32_t margin, double* out, unsigned char* det_hits, void* stream);
+
 /* ---- debug (no reference counterpart) ----
  * Arm a one-shot clock64 timeline of CTA 0 for the launch_index-th following tensor-core
  * conv launch; dev_buf holds 5 x 8192 uint64 (layout in csrc/tc_kernel.cuh, trace_at). */

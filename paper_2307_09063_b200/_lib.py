@@ -50,6 +50,8 @@ SIGNATURES = {
     "stda_denoise_epilogue": (C.c_int, [_vp, _vp, _i64, _i32, _i32, C.c_float, C.c_float, C.c_float, C.c_float,
                                         _vp]),
     "stda_rd_frontend": (C.c_int, [_vp, _i64, _i32, _i32, _i32, _i32, _vp, _i32, _i32, _vp, _vp]),
+    "stda_score": (C.c_int, [_vp, _i32, _vp, _i64, _i32, _i32, _i32, _i32, _i32, _i32, C.c_double, C.c_double,
+                             _i32, _vp, _vp, _vp]),
 }
 
 ABI_VERSION = 1
@@ -189,6 +191,12 @@ def denoise_epilogue(y, out, batch, hh, ww, scale, z_min, std, mean, stream) -> 
 
 def rd_frontend(beat, n, N, M, P, Q, stats, clutter, layout, out, stream) -> None:
     _check(lib().stda_rd_frontend(beat, n, N, M, P, Q, stats, clutter, layout, out, stream), "stda_rd_frontend")
+
+
+def score(clean, clean_kind, test_db, n, P, Q, g0, g1, t0, t1, alpha_obj, alpha_det, margin, out, hits,
+          stream) -> None:
+    _check(lib().stda_score(clean, clean_kind, test_db, n, P, Q, g0, g1, t0, t1, alpha_obj, alpha_det, margin, out,
+                            hits, stream), "stda_score")
 
 
 def loaded_path() -> str:

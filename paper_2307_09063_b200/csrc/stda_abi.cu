@@ -33,6 +33,9 @@ void launch_denoise_epilogue(const float* y, float* out, int64_t B, int H, int W
                              float stdv, float mean, cudaStream_t st);
 void launch_rd_frontend(const float2* beat, int64_t n, int N, int M, int P, int Q, const double* stats,
                         bool clutter, int layout, float* out, cudaStream_t st);
+void launch_score(const void* clean, int clean_kind, const float* test_db, int64_t n, int P, int Q, int guard0,
+                  int guard1, int train0, int train1, double alpha_obj, double alpha_det, int margin, double* out,
+                  unsigned char* det_hits, cudaStream_t st);
 
 static thread_local std::string g_last_error;
 void set_error(const std::string& msg) { g_last_error = msg; }
@@ -788,6 +791,18 @@ int stda_synth_frames(uint64_t seed, int32_t scene, int64_t seq, int64_t first_f
     STDA_CHECK(n_frames < (1ll << 31), "too many frames");
     launch_synth(seed, scene, seq, 0, first_frame, (int)n_frames, 0, n_frames, h, w, out,
                  static_cast<cudaStream_t>(stream));
+  });
+}
+
+int stda_score(const void* clean, int32_t clean_kind, const float* test_db, int64_t n, int32_t P, int32_t Q,
+               int32_t guard0, int32_t guard1, int32_t train0, int32_t train1, double alpha_obj, double alpha_det,
+               int32_t margin, double* out, unsigned char* det_hits, void* stream) {
+  return guarded([&] {
+    STDA_CHECK(n >= 0 && P > 0 && Q > 0, "bad map count/shape");
+    if (n == 0) return;
+    STDA_CHECK(clean && test_db && out && det_hits, "null buffer");
+    launch_score(clean, clean_kind, test_db, n, P, Q, guard0, guard1, train0, train1, alpha_obj, alpha_det, margin,
+                 out, det_hits, static_cast<cudaStream_t>(stream));
   });
 }
 

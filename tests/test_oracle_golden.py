@@ -65,3 +65,17 @@ def test_frontend_port_matches_rdlab_golden():
     assert np.abs(fe.frontend(g["beat"]) - g["single"]).max() <= 1e-12
     assert np.abs(fe.frontend(g["beat"], stats=g["stats"]) - g["given"]).max() <= 1e-12
     assert np.abs(fe.frontend(g["beat"], use_clutter=False) - g["noclutter"]).max() <= 1e-12
+
+
+def test_scoring_port_matches_rdlab_golden():
+    """oracle/scoring.py (the scoring path's checker and CPU baseline) against the reference
+    rdlab evaluator's per-sample metrics (tests/golden/make_scoring_golden.py)."""
+    from oracle import scoring as sc
+
+    g = np.load(GOLDEN / "scoring.npz")
+    for i, row in enumerate(g["rows"]):
+        s, e, no, nn, status, det = sc.score(g["clean"][i], g["test_db"][i])
+        assert status == row[4] and np.array_equal(det, g["hits"][i])
+        if status == 0:
+            assert (no, nn) == (row[2], row[3])
+            assert abs(s - row[0]) <= 1e-12 * abs(row[0]) and abs(e - row[1]) <= 1e-12 * abs(row[1])
