@@ -316,7 +316,7 @@ def run_engine(args, world, rank, local):
     cfg = StdaConfig(map_height=H, map_width=W)
     net = seeded_net(cfg, args.precision).to(dev)
     x = synth_triplets(batch, H, W, seed=1234, scene=scene, first_seq=rank * batch, device=dev)
-    cap = CapturedForward(net, x)
+    cap = CapturedForward(net, x, split=args.split)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
@@ -402,7 +402,8 @@ def run_engine(args, world, rank, local):
                    "global_batch": batch * world, "map": [H, W], "precision": args.precision,
                    "parallelism": f"dp{world} (independent batches, no collective)",
                    "l2": "flushed between timed steps (256 MiB write)",
-                   "timing": "CUDA-graph replay of the whole forward, CUDA events per step"},
+                   "timing": "CUDA-graph replay of the whole forward, CUDA events per step",
+                   "concurrent_slices": len(cap.slices)},
         "gpu_launches": cap.launches * args.steps,
         "roofline": {
             **roof, "launch_ms": share[dom],
@@ -436,6 +437,8 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
     ap.add_argument("--batch", type=int, default=0, help="override the config's per-GPU batch")
     ap.add_argument("--precision", choices=["fp32", "bf16"], default="fp32")
+    ap.add_argument("--split", type=int, default=1,
+                    help="run the batch as this many concurrent slices (streams) inside the graph")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

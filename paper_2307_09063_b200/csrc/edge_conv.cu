@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(kThreads) head_fused_kernel(
                              dv[u][1].x, dv[u][1].y, dv[u][1].z, dv[u][1].w};
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          v[i] = dd[i] * gate[c8 * 8 + i] + sv[u][i];  // eca(d) + skip (model.py:197-198)
+          v[i] = gate_fma(dd[i], gate[c8 * 8 + i], sv[u][i]);  // eca(d) + skip (model.py:197-198)
           if (bf16) v[i] = bf16_round(v[i]);
         }
       }
@@ -530,10 +530,10 @@ __global__ void __launch_bounds__(kHsThreads, 1) head_strips_kernel(
           s4[3] += __uint_as_float(lv.y & 0xFFFF0000u);
         }
         const float4 g4 = *reinterpret_cast<const float4*>(gate + q * 4);
-        u.x = fmaf(dv.x, g4.x, s4[0]);  // eca(d) + skip (model.py:197-198)
-        u.y = fmaf(dv.y, g4.y, s4[1]);
-        u.z = fmaf(dv.z, g4.z, s4[2]);
-        u.w = fmaf(dv.w, g4.w, s4[3]);
+        u.x = gate_fma(dv.x, g4.x, s4[0]);  // eca(d) + skip (model.py:197-198)
+        u.y = gate_fma(dv.y, g4.y, s4[1]);
+        u.z = gate_fma(dv.z, g4.z, s4[2]);
+        u.w = gate_fma(dv.w, g4.w, s4[3]);
         if (bf16) {
           u.x = bf16_round(u.x);
           u.y = bf16_round(u.y);

@@ -81,10 +81,8 @@ __global__ void __launch_bounds__(kGateThreads) gate_apply_kernel(
       float v[8] = {xa[j][0].x, xa[j][0].y, xa[j][0].z, xa[j][0].w,
                     xa[j][1].x, xa[j][1].y, xa[j][1].z, xa[j][1].w};
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        v[i] = v[i] * gate[c8 * 8 + i];                 // eca(x) = x * gate
-        if (has_skip) v[i] = v[i] + sk[j][i];           // + skip (model.py:197-198)
-      }
+      for (int i = 0; i < 8; ++i)  // eca(x) = x * gate (+ skip, model.py:197-198)
+        v[i] = has_skip ? gate_fma(v[i], gate[c8 * 8 + i], sk[j][i]) : gate_mul(v[i], gate[c8 * 8 + i]);
       if (has_pl) pl_store8(out_pl, b, 0, c8, y * out_pl.L + xx, v);
       if (has_pp) pl_store8(out_pp, b, (y & 1) * 2 + (xx & 1), c8, (y >> 1) * out_pp.L + (xx >> 1), v);
       if (c8 == 0 && xx >= W - 2) {  // pad columns of the rows ending here
@@ -166,9 +164,10 @@ __global__ void __launch_bounds__(kGateThreads) gate_apply_rows_kernel(
     const float4 a0 = *reinterpret_cast<const float4*>(xs + (size_t)pix * C + c8 * 8);
     const float4 a1 = *reinterpret_cast<const float4*>(xs + (size_t)pix * C + c8 * 8 + 4);
     float v[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+    if (!has_skip) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = v[i] * gate[c8 * 8 + i];  // eca(x) = x * gate
-    if (has_skip) {                                              // + skip (model.py:197-198)
+      for (int i = 0; i < 8; ++i) v[i] = gate_mul(v[i], gate[c8 * 8 + i]);  // eca(x) = x * gate
+    } else {                                                               // + skip (model.py:197-198)
       const int kh = ((c8 >> 1) * np) * 2 + (c8 & 1);
       const uint4 h = *reinterpret_cast<const uint4*>(sk + kh * sk_blk + (size_t)(r * L + xx) * 16);
       const __nv_bfloat162* hb = reinterpret_cast<const __nv_bfloat162*>(&h);
@@ -190,7 +189,7 @@ __global__ void __launch_bounds__(kGateThreads) gate_apply_rows_kernel(
         }
       }
 #pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] = v[i] + s[i];
+      for (int i = 0; i < 8; ++i) v[i] = gate_fma(v[i], gate[c8 * 8 + i], s[i]);
     }
     float hi[8], lo[8];
 #pragma unroll
@@ -371,8 +370,10 @@ __global__ void __launch_bounds__(kGsThreads, 1) gate_strips_kernel(
       const float4 a1 = *reinterpret_cast<const float4*>(xs + (size_t)pix * C + c8 * 8 + 4);
       const float4 g0 = *reinterpret_cast<const float4*>(gate + c8 * 8);
       const float4 g1 = *reinterpret_cast<const float4*>(gate + c8 * 8 + 4);
-      float v[8] = {a0.x * g0.x, a0.y * g0.y, a0.z * g0.z, a0.w * g0.w,
-                    a1.x * g1.x, a1.y * g1.y, a1.z * g1.z, a1.w * g1.w};  // eca(x) = x * gate
+      const float xv[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const float gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+      float v[8];
+      float sk8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       const int kh = ((c8 >> 1) * np) * 2 + (c8 & 1);  // hi block of this 8-channel group
       if (has_skip) {                                  // + skip (model.py:197-198)
         const size_t so = (size_t)(r * L + xx) * 16;
@@ -380,19 +381,22 @@ __global__ void __launch_bounds__(kGsThreads, 1) gate_strips_kernel(
         const uint32_t hw[4] = {h.x, h.y, h.z, h.w};
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          v[2 * j] += __uint_as_float(hw[j] << 16);
-          v[2 * j + 1] += __uint_as_float(hw[j] & 0xFFFF0000u);
+          sk8[2 * j] = __uint_as_float(hw[j] << 16);
+          sk8[2 * j + 1] = __uint_as_float(hw[j] & 0xFFFF0000u);
         }
         if (np == 2) {
           const uint4 l = *reinterpret_cast<const uint4*>(sk + (size_t)(kh + 2) * sk_blk + so);
           const uint32_t lw[4] = {l.x, l.y, l.z, l.w};
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            v[2 * j] += __uint_as_float(lw[j] << 16);
-            v[2 * j + 1] += __uint_as_float(lw[j] & 0xFFFF0000u);
+            sk8[2 * j] += __uint_as_float(lw[j] << 16);
+            sk8[2 * j + 1] += __uint_as_float(lw[j] & 0xFFFF0000u);
           }
         }
       }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)  // eca(x) = x * gate (+ skip): planes.cuh rounding order
+        v[i] = has_skip ? gate_fma(xv[i], gv[i], sk8[i]) : gate_mul(xv[i], gv[i]);
       const int oy = y0 + r;
       pl_store8(out_pl, b, 0, c8, oy * L + xx, v);
       if (has_pp) pl_store8(out_pp, b, (oy & 1) * 2 + (xx & 1), c8, (oy >> 1) * Lp + (xx >> 1), v);

@@ -152,6 +152,13 @@ __device__ __forceinline__ float eca_channel_sum(const float* gap, int items, in
   for (int g = 0; g < kEcaGroups; ++g) s += eca_group_sum(gap, items, C, b, c, g);
   return s;
 }
+// eca(x) (+ skip) (model.py:95-98, 197-198) in ONE rounding order for every kernel that
+// applies a gate: skip = hi + lo of its operand plane (exact in fp32), then one fused
+// multiply-add; without a skip one multiply.  Explicit intrinsics: no kernel may differ
+// by compiler contraction (batch invariance across gate-kernel choices).
+__device__ __forceinline__ float gate_mul(float x, float g) { return __fmul_rn(x, g); }
+__device__ __forceinline__ float gate_fma(float x, float g, float skip) { return __fmaf_rn(x, g, skip); }
+
 // gate[c] = sigmoid(sum_j w[j] * mean[c + j - k/2]), zero-padded 1-D conv over channels
 __device__ __forceinline__ float eca_gate_of(const float* mean, int C, int c, const float* eca_w, int k) {
   float z = 0.f;

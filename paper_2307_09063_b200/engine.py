@@ -238,7 +238,11 @@ class CapturedForward:
     The input buffer `self.x` may be refilled in place between replays.
     """
 
-    def __init__(self, net, x: torch.Tensor):
+    def __init__(self, net, x: torch.Tensor, split: int = 1):
+        """split > 1: the batch runs as `split` contiguous slices, each a full forward on
+        its own stream and workspace, forked from and joined back into the capture stream,
+        so one slice's latency-bound kernels overlap another's (results are bitwise those
+        of the whole batch: the forward is batch-invariant)."""
         device = _device_of(x)
         if net.training:
             raise RuntimeError("capture an eval-mode network")
@@ -248,20 +252,36 @@ class CapturedForward:
         self.plan = _net_plan(net, device)
         self.device = device
         L = self.plan.L
+        split = max(1, min(int(split), self.batch))
+        bounds = [self.batch * i // split for i in range(split + 1)]
+        self.slices = [(b0, b1 - b0) for b0, b1 in zip(bounds[:-1], bounds[1:]) if b1 > b0]
         with torch.cuda.device(device):
             self.y = torch.empty((self.batch, 1, cfg.map_height, cfg.map_width), device=device)
-            self.ws = torch.empty(L.workspace_bytes(self.plan.handle, self.batch), device=device,
-                                  dtype=torch.uint8)
+            self.ws = [torch.empty(L.workspace_bytes(self.plan.handle, n), device=device, dtype=torch.uint8)
+                       for _, n in self.slices]
+            self.streams = [torch.cuda.Stream(device) for _ in self.slices] if len(self.slices) > 1 else []
             self._launch()                      # eager run configures kernels before capture
             torch.cuda.synchronize(device)
             self.graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(self.graph):
                 self._launch()
-        self.launches = L.launches_per_forward(self.plan.handle)
+        self.launches = L.launches_per_forward(self.plan.handle) * len(self.slices)
 
     def _launch(self) -> None:
-        self.plan.L.forward(self.plan.handle, self.x.data_ptr(), self.y.data_ptr(), self.batch,
-                            self.ws.data_ptr(), self.ws.numel(), _stream_ptr(self.device))
+        L, h = self.plan.L, self.plan.handle
+        xs, ys = self.x[0].numel() * 4, self.y[0].numel() * 4
+        if not self.streams:
+            L.forward(h, self.x.data_ptr(), self.y.data_ptr(), self.batch, self.ws[0].data_ptr(),
+                      self.ws[0].numel(), _stream_ptr(self.device))
+            return
+        main = torch.cuda.current_stream(self.device)
+        for s in self.streams:
+            s.wait_stream(main)
+        for (b0, n), ws, s in zip(self.slices, self.ws, self.streams):
+            L.forward(h, self.x.data_ptr() + b0 * xs, self.y.data_ptr() + b0 * ys, n, ws.data_ptr(), ws.numel(),
+                      s.cuda_stream)
+        for s in self.streams:
+            main.wait_stream(s)
 
     def replay(self) -> torch.Tensor:
         self.graph.replay()
@@ -271,7 +291,8 @@ class CapturedForward:
         """Per-launch device times (ms) of one eager forward + the launch names."""
         L = self.plan.L
         with torch.cuda.device(self.device):
+            ws = self.ws[0] if len(self.slices) == 1 else torch.empty(
+                L.workspace_bytes(self.plan.handle, self.batch), device=self.device, dtype=torch.uint8)
             ms = L.forward_profiled(self.plan.handle, self.x.data_ptr(), self.y.data_ptr(),
-                                    self.batch, self.ws.data_ptr(), self.ws.numel(),
-                                    _stream_ptr(self.device))
+                                    self.batch, ws.data_ptr(), ws.numel(), _stream_ptr(self.device))
         return L.launch_names(self.plan.handle), ms
