@@ -203,6 +203,16 @@ def seeded_net(cfg, precision):
     return StdaNet(cfg, precision=precision).eval()
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo", encoding="utf-8"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
 def cpu_cores() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -298,6 +308,7 @@ def run_reference(args, world, rank):
         "config": {"workload": f"BASELINE config {idx + 1}: [{batch},3,{H},{W}] fp32",
                    "sample_per_step": sample, "parallelism": "cpu threads"},
         "cpu_baseline": {"value": rate, "unit": "triplets/s", "cores": cpu_cores(), "kind": "port",
+                         "cpu_model": cpu_model(),
                          "sample": f"{sample} triplets of the workload per step, {args.steps} steps"},
         "e2e": {"value": rate, "unit": "triplets/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -341,6 +352,10 @@ def run_engine(args, world, rank, local):
     total_ms = max_over_ranks(sum(step_ms), world)
     ms_per_step = total_ms / args.steps
     value = batch * world * args.steps / (total_ms / 1000.0)
+    ordered = sorted(step_ms)
+    step_stats = {"median_ms": max_over_ranks(ordered[len(ordered) // 2], world),
+                  "best_ms": max_over_ranks(ordered[0], world),
+                  "worst_ms": max_over_ranks(ordered[-1], world)}
 
     # dominant kernel, timed live between launches (eager profiled forwards)
     names, acc = None, None
@@ -395,7 +410,7 @@ def run_engine(args, world, rank, local):
 
     line = {
         "metric": METRIC, "value": value, "unit": "triplets/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "step_ms": step_stats,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": args.precision, "data": "synthetic (GPU RD-map generator, seeded; seeded random-init weights)",
         "config": {"workload": f"BASELINE config {idx + 1}: [{batch},3,{H},{W}] per GPU",
@@ -422,7 +437,7 @@ def run_engine(args, world, rank, local):
     if rank == 0 and world == 1 and not args.no_cpu:
         rate, done, el = cpu_forward_rate(net, x.cpu(), args.cpu_seconds)
         line["cpu_baseline"] = {"value": rate, "unit": "triplets/s", "cores": cpu_cores(),
-                                "kind": "port",
+                                "kind": "port", "cpu_model": cpu_model(),
                                 "sample": f"{done} triplets of the workload in chunks of 16, {el:.1f} s"}
     if rank == 0:
         print(json.dumps(line), flush=True)

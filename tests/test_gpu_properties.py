@@ -80,6 +80,30 @@ def test_batch_invariance_across_gate_kernels():
     assert torch.equal(full, slices)
 
 
+def test_c4_stream_at_128():
+    """BASELINE config 4 semantics at its map size: a coherent stream's
+    sliding windows equal independent per-triplet forwards bitwise, a G=3 time split with
+    the 2-frame halo reproduces the stream bitwise, and a subset matches the oracle."""
+    from oracle import port
+    from tests._helpers import CONFIG_FIELDS, nmax_err
+
+    net = StdaNet(StdaConfig(map_height=128, map_width=128)).eval().cuda()
+    T = 98
+    frames = synth_frames(T, 128, 128, seed=44)
+    y = net.forward_window(frames)
+    assert y.shape == (T - 2, 1, 128, 128)
+    trip = torch.stack([frames[t - 2:t + 1].flip(0) for t in range(2, T)])
+    assert torch.equal(y, net(trip))
+    cuts = [2, 34, 66, T]  # outputs t in [cuts[g], cuts[g+1]) on "GPU" g, frames from t0 - 2
+    parts = [net.forward_window(frames[a - 2:b]) for a, b in zip(cuts[:-1], cuts[1:])]
+    assert torch.equal(torch.cat(parts), y)
+    sd = {k: v.detach().cpu() for k, v in net.state_dict().items()}
+    cfg = {f: getattr(net.config, f) for f in CONFIG_FIELDS}
+    idx = [0, 31, 64, T - 3]
+    ref = port.forward(sd, cfg, trip[idx].cpu()).numpy()
+    assert nmax_err(y[idx].cpu().numpy(), ref) <= 1e-4
+
+
 def test_stream_window_equals_per_triplet_forward():            # BASELINE config 4 semantics
     net = StdaNet(StdaConfig(map_height=64, map_width=64)).eval().cuda()
     frames = synth_frames(12, 64, 64, seed=3)
