@@ -159,6 +159,20 @@ int stda_rd_frontend(const void* beat, int64_t n, int32_t N, int32_t M, int32_t 
  * n_noise, status} doubles (status 0 ok, 1 no object cells, 2 clean map zero at an object
  * cell, 3 empty noise set; sinr/evm NaN unless 0); det_hits: n x P x Q bytes (test-map
  * CFAR hits, for host-side clustering).  Device pointers, float64 inside. */
+/* ---- the paper's baselines behind the same forward boundary (reference
+ * stda/model.py:202-258), fp32 ----
+ * kind 0 = BaselineMlp (blob: torch Linear layout W1 [hidden][h*w], b1 [hidden],
+ *          W2 [hidden][hidden], b2, W3 [h*w][hidden], b3 [h*w]);
+ * kind 1 = BaselineCae (blob: conv1 w [32][1][3][3] b [32], conv2 w [64][32][3][3] b [64],
+ *          convT1 4-phase canonical [32][64][2][2][2][2] b [32] (as the network's ConvT),
+ *          convT2 [1][32][2][2][2][2] b [1]); h, w divisible by 4.
+ * forward: x [batch][x_channels][h][w] (channel 0 = frame t is used) -> y [batch][1][h][w]. */
+int stda_baseline_plan_create(int32_t kind, int32_t h, int32_t w, int32_t hidden, const float* blob,
+                              size_t n_floats, int device, stda_plan** out);
+size_t stda_baseline_workspace_bytes(const stda_plan* plan, int64_t batch);
+int stda_baseline_forward(const stda_plan* plan, const float* x, int32_t x_channels, float* y, int64_t batch,
+                          void* workspace, size_t ws_bytes, void* stream);
+
 int stda_score(const void* clean, int32_t clean_kind, const float* test_db, int64_t n, int32_t P, int32_t Q,
                int32_t guard0, int32_t guard1, int32_t train0, int32_t train1, double alpha_obj, double alpha_det,
                int32_t margin, double* out, unsigned char* det_hits, void* stream);

@@ -24,3 +24,5 @@ from .fold import fold_state_dict  # noqa: F401
 from .data import ManifestInfo, NormStats, TripletDataset, load_manifest  # noqa: F401
 from .denoise import denoise_dataset  # noqa: F401
 from .rdc1 import read_cube, write_magnitude_cube  # noqa: F401
+# the paper's baselines behind the same forward boundary
+from .baselines import BASELINE_KINDS, BaselineCae, BaselineMlp, baseline_forward, build_baseline  # noqa: F401

@@ -52,6 +52,9 @@ SIGNATURES = {
     "stda_rd_frontend": (C.c_int, [_vp, _i64, _i32, _i32, _i32, _i32, _vp, _i32, _i32, _vp, _vp]),
     "stda_score": (C.c_int, [_vp, _i32, _vp, _i64, _i32, _i32, _i32, _i32, _i32, _i32, C.c_double, C.c_double,
                              _i32, _vp, _vp, _vp]),
+    "stda_baseline_plan_create": (C.c_int, [_i32, _i32, _i32, _i32, _fp, _sz, C.c_int, C.POINTER(_vp)]),
+    "stda_baseline_workspace_bytes": (_sz, [_vp, _i64]),
+    "stda_baseline_forward": (C.c_int, [_vp, _vp, _i32, _vp, _i64, _vp, _sz, _vp]),
 }
 
 ABI_VERSION = 1

@@ -33,6 +33,10 @@ void launch_denoise_epilogue(const float* y, float* out, int64_t B, int H, int W
                              float stdv, float mean, cudaStream_t st);
 void launch_rd_frontend(const float2* beat, int64_t n, int N, int M, int P, int Q, const double* stats,
                         bool clutter, int layout, float* out, cudaStream_t st);
+void launch_linear(const float* X, int64_t xs, const float* Wt, const float* b, float* Y, int M, int N, int K,
+                   bool relu, float* partial, cudaStream_t st);
+int linear_splits(int K);
+void launch_maxpool2(const float* x, float* y, int64_t planes, int H, int W, cudaStream_t st);
 void launch_score(const void* clean, int clean_kind, const float* test_db, int64_t n, int P, int Q, int guard0,
                   int guard1, int train0, int train1, double alpha_obj, double alpha_det, int margin, double* out,
                   unsigned char* det_hits, cudaStream_t st);
@@ -157,6 +161,11 @@ struct stda_plan {
 
   bool use_tc = false;  // every encoder/decoder conv runs on the tcgen05 kernel
   float* head_wt = nullptr;  // head weights [9][c0] for the NHWC head kernel
+  // baselines (kind 3 = MLP, kind 4 = CAE; stda_baseline_plan_create)
+  int bh = 0, bw = 0, hidden = 0;
+  float* lin_w[3] = {};
+  float* lin_b[3] = {};
+  ConvLayer cae[6];  // conv1, conv2, convT1, its all-zero twin, convT2, its all-zero twin
 };
 
 namespace {
@@ -791,6 +800,117 @@ int stda_synth_frames(uint64_t seed, int32_t scene, int64_t seq, int64_t first_f
     STDA_CHECK(n_frames < (1ll << 31), "too many frames");
     launch_synth(seed, scene, seq, 0, first_frame, (int)n_frames, 0, n_frames, h, w, out,
                  static_cast<cudaStream_t>(stream));
+  });
+}
+
+namespace {
+size_t baseline_blob_floats(int kind, int h, int w, int hidden) {
+  const size_t hw = (size_t)h * w, hd = hidden;
+  if (kind == 0) return hd * hw + hd + hd * hd + hd + hw * hd + hw;
+  return 32 * 9 + 32 + 64 * 32 * 9 + 64 + 32 * 64 * 16 + 32 + 1 * 32 * 16 + 1;
+}
+}  // namespace
+
+int stda_baseline_plan_create(int32_t kind, int32_t h, int32_t w, int32_t hidden, const float* blob,
+                              size_t n_floats, int device, stda_plan** out) {
+  return guarded([&] {
+    STDA_CHECK(blob && out, "null argument");
+    STDA_CHECK(kind == 0 || kind == 1, "kind must be 0 (MLP) or 1 (CAE)");
+    STDA_CHECK(h > 0 && w > 0 && (kind == 1 || hidden > 0), "bad baseline shape");
+    STDA_CHECK(kind == 0 || (h % 4 == 0 && w % 4 == 0), "CAE needs h, w divisible by 4");
+    STDA_CHECK(n_floats == baseline_blob_floats(kind, h, w, hidden), "baseline blob size mismatch");
+    DeviceGuard g(device);
+    auto p = std::make_unique<stda_plan>();
+    p->kind = 3 + kind;
+    p->device = device;
+    p->bh = h;
+    p->bw = w;
+    p->hidden = hidden;
+    const float* src = blob;
+    if (kind == 0) {
+      const size_t hw = (size_t)h * w;
+      const size_t dims[3][2] = {{(size_t)hidden, hw}, {(size_t)hidden, (size_t)hidden}, {hw, (size_t)hidden}};
+      for (int l = 0; l < 3; ++l) {
+        const size_t nw = dims[l][0] * dims[l][1];
+        p->lin_w[l] = p->upload(std::vector<float>(src, src + nw));
+        src += nw;
+        p->lin_b[l] = p->upload(std::vector<float>(src, src + dims[l][0]));
+        src += dims[l][0];
+      }
+    } else {
+      p->cae[0] = p->make_layer(CONV3_S1, 1, 32, src);
+      p->cae[1] = p->make_layer(CONV3_S1, 32, 64, src);
+      const std::vector<float> z1(32 * 64 * 16 + 32, 0.f), z2(32 * 16 + 1, 0.f);
+      p->cae[2] = p->make_layer(CONVT4_S2, 64, 32, src);
+      const float* zs = z1.data();
+      p->cae[3] = p->make_layer(CONVT4_S2, 64, 32, zs);
+      p->cae[4] = p->make_layer(CONVT4_S2, 32, 1, src);
+      zs = z2.data();
+      p->cae[5] = p->make_layer(CONVT4_S2, 32, 1, zs);
+    }
+    *out = p.release();
+  });
+}
+
+size_t stda_baseline_workspace_bytes(const stda_plan* p, int64_t batch) {
+  if (!p || batch < 0 || p->kind < 3) return 0;
+  const size_t B = batch, hw = (size_t)p->bh * p->bw;
+  if (p->kind == 3) {
+    const int S = linear_splits((int)hw);
+    return 2 * align_up(B * p->hidden * sizeof(float)) +
+           (S > 1 ? align_up((size_t)S * B * p->hidden * sizeof(float)) : 0);
+  }
+  return align_up(B * 32 * hw * 4) + align_up(B * 32 * hw) + align_up(B * 64 * hw) + align_up(B * 64 * hw / 4) +
+         align_up(B * 32 * hw);
+}
+
+int stda_baseline_forward(const stda_plan* p, const float* x, int32_t x_channels, float* y, int64_t batch,
+                          void* ws, size_t ws_bytes, void* stream) {
+  return guarded([&] {
+    STDA_CHECK(p && p->kind >= 3, "not a baseline plan");
+    STDA_CHECK(batch >= 0 && x_channels >= 1, "bad batch/channels");
+    if (batch == 0) return;
+    STDA_CHECK(x && y && ws, "null buffer");
+    STDA_CHECK(ws_bytes >= stda_baseline_workspace_bytes(p, batch), "workspace too small");
+    DeviceGuard g(p->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int H = p->bh, W = p->bw;
+    const int64_t hw = (int64_t)H * W;
+    char* base = static_cast<char*>(ws);
+    size_t off = 0;
+    auto take = [&](size_t nf) {
+      float* r = reinterpret_cast<float*>(base + off);
+      off += align_up(nf * sizeof(float));
+      return r;
+    };
+    if (p->kind == 3) {  // frame t (channel 0) of each triplet, flattened
+      float* h1 = take((size_t)batch * p->hidden);
+      float* h2 = take((size_t)batch * p->hidden);
+      const int S = linear_splits((int)hw);
+      float* part = S > 1 ? take((size_t)S * batch * p->hidden) : nullptr;
+      launch_linear(x, (int64_t)x_channels * hw, p->lin_w[0], p->lin_b[0], h1, (int)batch, p->hidden, (int)hw, true,
+                    part, st);
+      launch_linear(h1, p->hidden, p->lin_w[1], p->lin_b[1], h2, (int)batch, p->hidden, p->hidden, true, nullptr,
+                    st);
+      launch_linear(h2, p->hidden, p->lin_w[2], p->lin_b[2], y, (int)batch, (int)hw, p->hidden, false, nullptr, st);
+      return;
+    }
+    float* a1 = take((size_t)batch * 32 * hw);
+    float* p1 = take((size_t)batch * 32 * hw / 4);
+    float* a2 = take((size_t)batch * 64 * hw / 4);
+    float* p2 = take((size_t)batch * 64 * hw / 16);
+    float* t1 = take((size_t)batch * 32 * hw / 4);
+    Src in = plain_src(x, 1, H, W);
+    in.xb = (int64_t)x_channels * hw;  // channel 0 of each triplet
+    launch_conv(p->cae[0], nullptr, in, nullptr, a1, nullptr, batch, H, W, true, false, st);
+    launch_maxpool2(a1, p1, batch * 32, H, W, st);
+    const Src s1 = plain_src(p1, 32, H / 2, W / 2);
+    launch_conv(p->cae[1], nullptr, s1, nullptr, a2, nullptr, batch, H / 2, W / 2, true, false, st);
+    launch_maxpool2(a2, p2, batch * 64, H / 2, W / 2, st);
+    const Src s2 = plain_src(p2, 64, H / 4, W / 4);
+    launch_conv(p->cae[2], &p->cae[3], s2, &s2, t1, nullptr, batch, H / 4, W / 4, true, false, st);
+    const Src s3 = plain_src(t1, 32, H / 2, W / 2);
+    launch_conv(p->cae[4], &p->cae[5], s3, &s3, y, nullptr, batch, H / 2, W / 2, false, false, st);
   });
 }
 
