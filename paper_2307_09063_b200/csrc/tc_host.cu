@@ -88,7 +88,11 @@ void tc_pack_layer(TcLayerDesc& d, int mode, int cin, int cout, const float* w0,
   // runs as CONVT4_HALF: one output-row parity per work item (4 accumulators), so the
   // 2-MMA concat applies (fewer operand bytes than 3 MMAs per tap).
   const bool wide_t = mode == CONVT4_S2 && (w1 ? 2 : 1) * 4 * 2 * cout * 2 > 512;
-  if (wide_t && !bf16 && half_t_enabled()) mode = CONVT4_HALF;
+  static const bool half_all = [] {  // env STDA_TC_HALF=2: every fp32 ConvT in half-phase items
+    const char* e = std::getenv("STDA_TC_HALF");
+    return e && e[0] == '2';
+  }();
+  if (mode == CONVT4_S2 && !bf16 && half_t_enabled() && (wide_t || half_all)) mode = CONVT4_HALF;
   const bool tmode = mode == CONVT4_S2 || mode == CONVT4_HALF;
   d.mode = mode;
   d.n_src = w1 ? 2 : 1;
@@ -222,7 +226,12 @@ TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W) {
       for (bool resident : {true, false}) {
         int stages = 0;
         // measured: S1/T layers are slower beyond 3 stages; S2 layers (L2-fed) may go deeper
-        for (int st = d.mode == CONV3_S2 ? kMaxStages : 3; st >= 1; --st) {
+        static const int t_stages = [] {  // env STDA_TC_TSTAGES: ring depth cap of ConvT layers
+          const char* e = std::getenv("STDA_TC_TSTAGES");
+          return e ? std::max(1, std::min(kMaxStages, std::atoi(e))) : 3;
+        }();
+        const bool tmode = d.mode == CONVT4_S2 || d.mode == CONVT4_HALF;
+        for (int st = d.mode == CONV3_S2 ? kMaxStages : tmode ? t_stages : 3; st >= 1; --st) {
           const size_t need = resident ? (size_t)st * a_stage + w_res : (size_t)st * (a_stage + b_stage);
           if (need + fixed <= (size_t)kMaxSmem) {
             stages = st;
