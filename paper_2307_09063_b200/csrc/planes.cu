@@ -1,4 +1,4 @@
-// Operand-plane helpers: border zeroing and the fused ECA gate + apply kernel.
+// Operand-plane writers: the fused ECA gate + apply kernels (generic, row-block, persistent strips).
 #include <algorithm>
 #include <cstdlib>
 #include <string>
@@ -8,26 +8,6 @@
 
 namespace stda {
 namespace {
-
-// One CTA per (buffer, image, plane, cg16/pass/cg8 block); its threads zero the border
-// positions of that block: the top margin (rows -2/-1), the bottom margin (row Hp) and
-// the pad column of every row.  blocks_before[i] = first CTA index of buffer i.
-__global__ void zero_borders_kernel(ZeroList zl, ZeroOffsets zo) {
-  int i = 0;
-  while (i + 1 < zl.n && (int64_t)blockIdx.x >= zo.blocks_before[i + 1]) ++i;
-  const PlBuf& p = zl.buf[i];
-  const int64_t blk = blockIdx.x - zo.blocks_before[i];  // b * blocks_per_img + inner
-  uint16_t* base = p.base + blk * (int64_t)p.Q * 8;      // blocks are contiguous per image
-  const int margin = p.L + 8;
-  const int per_block = 2 * margin + p.Hp;
-  for (int r = threadIdx.x; r < per_block; r += blockDim.x) {
-    int q;
-    if (r < margin) q = -margin + r;                       // rows -2/-1 region
-    else if (r < 2 * margin) q = p.Hp * p.L + (r - margin);  // row Hp (+ margin)
-    else q = (r - 2 * margin) * p.L + p.Wp;                // pad column of row y
-    *reinterpret_cast<uint4*>(base + (size_t)(q + p.off) * 8) = make_uint4(0, 0, 0, 0);
-  }
-}
 
 constexpr int kGateThreads = 256;
 constexpr int kPixPerCta = 128;
@@ -246,22 +226,6 @@ __global__ void __launch_bounds__(kGateThreads) gate_apply_rows_kernel(
 }
 
 }  // namespace
-
-void launch_zero_borders(const ZeroList& zl, int64_t B, cudaStream_t st) {
-  if (zl.n == 0 || B == 0) return;
-  // (b, plane, cg16, pass, cg8) blocks of an image buffer are contiguous Q*8-element
-  // blocks: img_stride = planes * blocks_per_plane * Q * 8
-  ZeroOffsets zo;
-  int64_t total = 0;
-  for (int i = 0; i < zl.n; ++i) {
-    const PlBuf& p = zl.buf[i];
-    zo.blocks_before[i] = total;
-    total += B * (int64_t)p.planes * (p.C / 16) * p.np * 2;
-  }
-  STDA_CHECK(total < (1ll << 31), "zero_borders: too many blocks");
-  zero_borders_kernel<<<(unsigned)total, 128, 0, st>>>(zl, zo);
-  check_launch("zero_borders_kernel");
-}
 
 namespace {
 

@@ -15,8 +15,8 @@
 //   planes = 4 ("PP"): phase planes (py, px) of a 2Hp x 2Wp tensor, plane = py*2 + px,
 //                      (y, x) <-> source pixel (2y+py, 2x+px) (stride-2 conv inputs).
 // Borders that taps can reach — rows -1 and Hp (with margins) and the pad column — are
-// zeroed once per forward (launch_zero_borders); positions past row Hp are only ever read
-// into discarded (junk) output rows.
+// kept zero by the kernels that write the plane (pads of the rows they write, margins once
+// per image); positions past row Hp are only ever read into discarded (junk) output rows.
 #pragma once
 
 #include "common.cuh"
@@ -168,17 +168,6 @@ __device__ __forceinline__ float eca_gate_of(const float* mean, int C, int c, co
   }
   return 1.f / (1.f + expf(-z));
 }
-
-constexpr int kMaxZeroBufs = 16;
-struct ZeroList {
-  PlBuf buf[kMaxZeroBufs];
-  int n = 0;
-};
-struct ZeroOffsets {
-  int64_t blocks_before[kMaxZeroBufs];
-};
-// zero every tap-reachable border position of each listed buffer (all images)
-void launch_zero_borders(const ZeroList& zl, int64_t B, cudaStream_t st);
 
 // ECA gate for image b computed from GAP partials, then applied:
 //   v = x * g (+ skip)   x: NHWC fp32 [B][H][W][C]; skip: PL over H x W (or null)
