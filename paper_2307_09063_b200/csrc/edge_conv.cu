@@ -383,6 +383,104 @@ __global__ void __launch_bounds__(kRowThreads, 4) stem_rows_kernel(const float* 
   }
 }
 
+// ---- stem with weights in the kernel-parameter (constant) bank (C0 = 16, F <= 4) --------
+// Same row blocks and direct plane stores as stem_rows_kernel, but the 16 x F x 9 weights
+// and the bias are a __grid_constant__ parameter: every FMA takes its weight straight
+// from the constant bank (uniform across the warp), so the only shared-memory traffic is
+// the frame rows.  ncu on stem_rows_kernel: LSU wavefronts ~80 % busy, mostly weights.
+constexpr int kStemC = 16, kStemMaxF = 4;
+struct StemConst {
+  float w[kStemMaxF * 9 * kStemC];  // [ci][ky][kx][co]
+  float b[kStemC];
+};
+
+template <int F, int PX>
+__global__ void __launch_bounds__(kRowThreads, 4) stem_const_kernel(const __grid_constant__ StemConst cw, Src x,
+                                                                   PlBuf pl, PlBuf pp, int H, int W, int R,
+                                                                   int bf16, int64_t b_base) {
+  grid_dep_wait();  // PDL: previous kernel complete (common.cuh)
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t bar;
+  const int tid = threadIdx.x;
+  const int64_t b = b_base + blockIdx.y;
+  const int y0 = blockIdx.x * R;
+  const int L = W + 1, Lp = W / 2 + 1;
+  float* xs = reinterpret_cast<float*>(smem_raw);  // [F][R+2][W]
+  const int r_lo = max(y0 - 1, 0), r_hi = min(y0 + R + 1, H);
+  if (tid == 0) {
+    ptx::mbar_init(ptx::smem_u32(&bar), 1);
+    ptx::fence_barrier_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const uint32_t rb = (uint32_t)(r_hi - r_lo) * W * 4;
+    ptx::mbar_arrive_expect_tx(ptx::smem_u32(&bar), rb * F);
+#pragma unroll
+    for (int ci = 0; ci < F; ++ci)
+      ptx::bulk_g2s(ptx::smem_u32(xs + ((size_t)ci * (R + 2) + (r_lo - (y0 - 1))) * W),
+                    x.x + b * x.xb + (int64_t)ci * x.xc + (int64_t)r_lo * W, rb, ptx::smem_u32(&bar));
+  }
+#pragma unroll
+  for (int ci = 0; ci < F; ++ci)  // rows outside the image are zero
+    for (int e = tid; e < W; e += kRowThreads) {
+      if (y0 - 1 < 0) xs[((size_t)ci * (R + 2)) * W + e] = 0.f;
+      if (y0 + R >= H) xs[((size_t)ci * (R + 2) + R + 1) * W + e] = 0.f;
+    }
+  if (blockIdx.x == 0) {  // top / bottom margins of the output planes, once per image
+    pl_zero_margins(pl, b, tid, kRowThreads);
+    pl_zero_margins(pp, b, tid, kRowThreads);
+  }
+  ptx::mbar_wait(ptx::smem_u32(&bar), 0);
+  __syncthreads();
+  for (int it = tid; it < (R / PX) * W; it += kRowThreads) {  // PX vertically adjacent pixels
+    const int r0 = (it / W) * PX, xx = it - (it / W) * W;
+    float acc[PX][kStemC];
+#pragma unroll
+    for (int o = 0; o < PX; ++o)
+#pragma unroll
+      for (int co = 0; co < kStemC; ++co) acc[o][co] = cw.b[co];
+#pragma unroll
+    for (int ci = 0; ci < F; ++ci) {
+      const float* xc = xs + (size_t)ci * (R + 2) * W;
+#pragma unroll
+      for (int kx = 0; kx < 3; ++kx) {
+        const int ix = xx + kx - 1;
+        float v[PX + 2];
+#pragma unroll
+        for (int k = 0; k < PX + 2; ++k) {
+          const float t = (ix >= 0 && ix < W) ? xc[(r0 + k) * W + ix] : 0.f;
+          v[k] = bf16 ? bf16_round(t) : t;
+        }
+#pragma unroll
+        for (int ky = 0; ky < 3; ++ky)
+#pragma unroll
+          for (int co = 0; co < kStemC; ++co) {
+            const float wv = cw.w[((ci * 3 + ky) * 3 + kx) * kStemC + co];
+#pragma unroll
+            for (int o = 0; o < PX; ++o) acc[o][co] = fmaf(v[ky + o], wv, acc[o][co]);
+          }
+      }
+    }
+#pragma unroll
+    for (int o = 0; o < PX; ++o) {
+      const int oy = y0 + r0 + o;
+      const int plane = (oy & 1) * 2 + (xx & 1);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float v8[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v8[i] = fmaxf(acc[o][8 * h + i], 0.f);
+        pl_store8(pl, b, 0, h, oy * L + xx, v8);
+        pl_store8(pp, b, plane, h, (oy >> 1) * Lp + (xx >> 1), v8);
+      }
+      if (xx >= W - 2) {  // pad columns (planes.cuh border contract)
+        if (xx == W - 1) pl_zero_pos(pl, b, 0, oy * L + W);
+        pl_zero_pos(pp, b, plane, (oy >> 1) * Lp + W / 2);
+      }
+    }
+  }
+}
+
 // ---- persistent strip head (C0 = 16, W in {32, 64, 128}) ------------------------------
 // One CTA per SM walks a contiguous range of strips (R = 512 / W rows x W columns; an
 // image's ECA gate is computed once per CTA-image, halo rows of neighbouring strips hit
@@ -604,8 +702,53 @@ void set_smem(K kern) {
 
 void launch_stem_planes(const float* w, const float* bias, const Src& x, int F, int C0,
                         const PlBuf& pl, const PlBuf& pp, int64_t B, int H, int W, bool bf16,
-                        cudaStream_t st) {
+                        cudaStream_t st, const float* canon_host) {
   STDA_CHECK(C0 % 16 == 0, "stem kernel needs stem_channels % 16 == 0");
+  static const bool const_off = [] {
+    const char* e = std::getenv("STDA_STEM");
+    return e && std::string(e) == "rows";
+  }();
+  if (!const_off && canon_host && C0 == kStemC && F >= 1 && F <= kStemMaxF && x.xp == 1 && H % 2 == 0 &&
+      W % 2 == 0 && W <= 1024) {
+    StemConst cw{};
+    for (int co = 0; co < kStemC; ++co) {
+      for (int ci = 0; ci < F; ++ci)
+        for (int t = 0; t < 9; ++t) cw.w[(ci * 9 + t) * kStemC + co] = canon_host[((size_t)co * F + ci) * 9 + t];
+      cw.b[co] = canon_host[(size_t)kStemC * F * 9 + co];
+    }
+    static const int px = [] {  // env STDA_STEM_PX: pixels per thread (2, or 4: spills at 4 CTAs/SM)
+      const char* e = std::getenv("STDA_STEM_PX");
+      return e && std::atoi(e) == 4 ? 4 : 2;
+    }();
+    const int PXr = (H % (2 * px) == 0) ? px : 2;
+    int R = PXr;
+    while (R * 2 * W <= 256 * PXr && H % (R * 2) == 0) R *= 2;
+    const size_t smem = (size_t)F * (R + 2) * W * 4;
+    STDA_CHECK(smem <= 200 * 1024, "stem: rows do not fit shared memory");
+    auto go = [&](auto fc) {
+      constexpr int FF = decltype(fc)::value;
+      const auto kern = PXr == 4 ? stem_const_kernel<FF, 4> : stem_const_kernel<FF, 2>;
+      static uint64_t configured = 0;  // per F
+      int dev = 0;
+      STDA_CUDA(cudaGetDevice(&dev));
+      if (!(configured >> (dev & 63) & 1)) {
+        STDA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        configured |= 1ull << (dev & 63);
+      }
+      for (int64_t b0 = 0; b0 < B; b0 += 65535) {
+        dim3 grid(H / R, (unsigned)std::min<int64_t>(65535, B - b0));
+        launch_pdl(kern, grid, dim3(kRowThreads), smem, st, "stem_const_kernel", cw, x, pl, pp, H, W, R, (int)bf16,
+                   b0);
+      }
+    };
+    switch (F) {
+      case 1: go(std::integral_constant<int, 1>{}); break;
+      case 2: go(std::integral_constant<int, 2>{}); break;
+      case 3: go(std::integral_constant<int, 3>{}); break;
+      default: go(std::integral_constant<int, 4>{}); break;
+    }
+    return;
+  }
   if (x.xp == 1 && H % 2 == 0 && W % 2 == 0 && W <= 1024) {
     // bulk-copy row-block path: R rows (even, dividing H) with R*W ~ 512 pixels
     // (256 threads x 2 vertically adjacent pixels)

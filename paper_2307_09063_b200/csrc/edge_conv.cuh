@@ -10,9 +10,11 @@ namespace stda {
 // x: F input frames (Src strides; NCHW or sliding window) -> relu(conv3x3) written as
 // operand planes pl (PL over H x W) and pp (PP over H/2 x W/2).
 // w: SIMT layout with cob = 16 ([C0/16][F][9][16]), bias [C0].
+// canon_host (optional): host copy of the canonical weights [C0][F][3][3] + bias [C0];
+// with C0 = 16 and F <= 4 it selects the constant-bank stem kernel.
 void launch_stem_planes(const float* w, const float* bias, const Src& x, int F, int C0,
                         const PlBuf& pl, const PlBuf& pp, int64_t B, int H, int W, bool bf16,
-                        cudaStream_t st);
+                        cudaStream_t st, const float* canon_host = nullptr);
 
 // y[b][h][w] = bias + conv3x3(d * gate + skip) over C0 channels, gate = ECA of d computed
 // from its per-item channel sums gap [B][items][C0]; d NHWC fp32, skip a PL plane.

@@ -161,6 +161,7 @@ struct stda_plan {
 
   bool use_tc = false;  // every encoder/decoder conv runs on the tcgen05 kernel
   float* head_wt = nullptr;  // head weights [9][c0] for the NHWC head kernel
+  std::vector<float> stem_canon;  // host copy of the stem's canonical weights + bias (constant-bank stem)
   // baselines (kind 3 = MLP, kind 4 = CAE; stda_baseline_plan_create)
   int bh = 0, bw = 0, hidden = 0;
   float* lin_w[3] = {};
@@ -305,7 +306,8 @@ void run_net_tc(const stda_plan& p, const Src& x, float* y, int64_t B, const Net
   // stage-1 outputs: PP for encoder stride-2 consumers, PL for decoder ConvT consumers
   const std::vector<PlBuf>& mviews = w.pl_m;
   (void)np;
-  launch_stem_planes(p.stem.w, p.stem.b, x, c.input_frames, c0, w.pl_s, w.pp_s, B, h, wd, bf, st);
+  launch_stem_planes(p.stem.w, p.stem.b, x, c.input_frames, c0, w.pl_s, w.pp_s, B, h, wd, bf, st,
+                     p.stem_canon.empty() ? nullptr : p.stem_canon.data());
   mk.mark(st);
   PlBuf cur_pl = w.pl_s, cur_pp = w.pp_s;
   std::vector<PlBuf> skips{w.pl_s};
@@ -491,6 +493,12 @@ int stda_plan_create(const stda_config* cfg, const float* blob, size_t n_floats,
     }
     const char* force = std::getenv("STDA_ENGINE_PATH");  // "simt" forces the generic path
     p->use_tc = tc_ok && !(force && std::strcmp(force, "simt") == 0);
+    {
+      const size_t n_stem = (size_t)c0 * cfg->input_frames * 9 + c0;
+      p->stem_canon.assign(src, src + n_stem);
+      if (p->bf16)
+        for (float& v : p->stem_canon) v = __bfloat162float(__float2bfloat16_rn(v));
+    }
     p->stem = p->make_layer(CONV3_S1, cfg->input_frames, c0, src);
     for (int i = 0; i < S; ++i) {
       const int ch = c0 << i;
