@@ -514,9 +514,13 @@ __host__ __device__ constexpr HeadStrips head_strips_geom(int W) {
 
 __device__ __forceinline__ int hs_swz(int p) { return (p >> 1) & 3; }
 
+struct HeadConst {
+  float w[9 * kHsC];  // [tap][channel]: read by the conv from the kernel-parameter bank
+};
+
 template <int W>
 __global__ void __launch_bounds__(kHsThreads, 1) head_strips_kernel(
-    const float* __restrict__ w, const float* __restrict__ bias, const float* __restrict__ gap, int items,
+    const __grid_constant__ HeadConst cw, const float* __restrict__ bias, const float* __restrict__ gap, int items,
     const float* __restrict__ eca_w, int k, const float* __restrict__ d, PlBuf skip, float* __restrict__ y,
     int64_t B, int H, int bf16) {
   using namespace ptx;
@@ -543,7 +547,6 @@ __global__ void __launch_bounds__(kHsThreads, 1) head_strips_kernel(
     }
     fence_barrier_init();
   }
-  for (int e = tid; e < 9 * kHsC; e += kHsThreads) ws[e] = __ldg(w + e);
   __syncthreads();
   grid_dep_wait();  // d, gap and skip come from the previous kernels
 
@@ -661,7 +664,9 @@ __global__ void __launch_bounds__(kHsThreads, 1) head_strips_kernel(
         }
 #pragma unroll
         for (int ky = 0; ky < 3; ++ky) {
-          const float4 w4 = *reinterpret_cast<const float4*>(ws + (ky * 3 + kx) * kHsC + j * 4);
+          const float4 w4 = make_float4(cw.w[(ky * 3 + kx) * kHsC + j * 4], cw.w[(ky * 3 + kx) * kHsC + j * 4 + 1],
+                                        cw.w[(ky * 3 + kx) * kHsC + j * 4 + 2],
+                                        cw.w[(ky * 3 + kx) * kHsC + j * 4 + 3]);
           acc0 = fmaf(u[ky].x, w4.x, acc0);
           acc0 = fmaf(u[ky].y, w4.y, acc0);
           acc0 = fmaf(u[ky].z, w4.z, acc0);
@@ -782,13 +787,15 @@ void launch_stem_planes(const float* w, const float* bias, const Src& x, int F, 
 
 void launch_head_fused(const float* w, const float* bias, const float* gap, int items,
                        const float* eca_w, int k, const float* d, const PlBuf& skip, int C0, float* y,
-                       int64_t B, int H, int W, bool bf16, cudaStream_t st) {
+                       int64_t B, int H, int W, bool bf16, cudaStream_t st, const float* w_host) {
   STDA_CHECK(C0 % 8 == 0, "head kernel needs stem_channels % 8 == 0");
   static const bool strips_off = [] {
     const char* e = std::getenv("STDA_HEAD");
     return e && std::string(e) == "tiles";
   }();
-  if (!strips_off && head_strips_ok(C0, B, H, W)) {
+  if (!strips_off && w_host != nullptr && head_strips_ok(C0, B, H, W)) {
+    HeadConst hc{};
+    for (int e = 0; e < 9 * kHsC; ++e) hc.w[e] = w_host[e];
     int dev = 0, sms = 148;
     STDA_CUDA(cudaGetDevice(&dev));
     STDA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -802,7 +809,7 @@ void launch_head_fused(const float* w, const float* bias, const float* gap, int 
         STDA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         configured |= 1ull << (dev & 63);
       }
-      launch_pdl(kern, dim3(grid), dim3(kHsThreads), g.smem, st, "head_strips_kernel", w, bias, gap, items, eca_w,
+      launch_pdl(kern, dim3(grid), dim3(kHsThreads), g.smem, st, "head_strips_kernel", hc, bias, gap, items, eca_w,
                  k, d, skip, y, B, H, (int)bf16);
     };
     if (W == 32) go(std::integral_constant<int, 32>{});

@@ -19,8 +19,10 @@ void launch_stem_planes(const float* w, const float* bias, const Src& x, int F, 
 // y[b][h][w] = bias + conv3x3(d * gate + skip) over C0 channels, gate = ECA of d computed
 // from its per-item channel sums gap [B][items][C0]; d NHWC fp32, skip a PL plane.
 // w [9][C0].
+// w_host (optional): host copy of w ([9][C0]); the strip head then takes the weights from
+// the kernel-parameter bank instead of shared memory.
 void launch_head_fused(const float* w, const float* bias, const float* gap, int items,
                        const float* eca_w, int k, const float* d, const PlBuf& skip, int C0, float* y,
-                       int64_t B, int H, int W, bool bf16, cudaStream_t st);
+                       int64_t B, int H, int W, bool bf16, cudaStream_t st, const float* w_host = nullptr);
 
 }  // namespace stda

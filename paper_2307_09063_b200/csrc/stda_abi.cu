@@ -162,6 +162,7 @@ struct stda_plan {
   bool use_tc = false;  // every encoder/decoder conv runs on the tcgen05 kernel
   float* head_wt = nullptr;  // head weights [9][c0] for the NHWC head kernel
   std::vector<float> stem_canon;  // host copy of the stem's canonical weights + bias (constant-bank stem)
+  std::vector<float> head_host;   // host copy of head_wt (constant-bank strip head)
   // baselines (kind 3 = MLP, kind 4 = CAE; stda_baseline_plan_create)
   int bh = 0, bw = 0, hidden = 0;
   float* lin_w[3] = {};
@@ -362,7 +363,7 @@ void run_net_tc(const stda_plan& p, const Src& x, float* y, int64_t B, const Net
       cur_pl = w.pl_b[j];
     } else {
       launch_head_fused(p.head_wt, p.head.b, w.pd[j], g2.items_per_image, D.eca, k, w.d[j], sk, c0, y, B, h,
-                        wd, bf, st);
+                        wd, bf, st, p.head_host.empty() ? nullptr : p.head_host.data());
       mk.mark(st);
     }
   }
@@ -542,6 +543,7 @@ int stda_plan_create(const stda_config* cfg, const float* blob, size_t n_floats,
           wt[(size_t)t * c0 + ci] = p->bf16 ? __bfloat162float(__float2bfloat16_rn(v)) : v;
         }
       p->head_wt = p->upload(wt);
+      p->head_host = wt;  // [9][c0] for the constant-bank strip head
     }
     p->head = p->make_layer(CONV3_S1, c0, 1, src);
     STDA_CHECK((size_t)(src - blob) == n_floats, "internal: blob parse mismatch");
