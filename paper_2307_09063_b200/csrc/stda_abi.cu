@@ -156,6 +156,10 @@ struct stda_plan {
     d.w = static_cast<const uint16_t*>(upload_bytes(packed.data(), packed.size() * 2));
     d.bias0 = upload(std::vector<float>(b0, b0 + cout));
     d.bias1 = w1 ? upload(std::vector<float>(b1, b1 + cout)) : nullptr;
+    for (int c = 0; c < cout && c < 64; ++c) {
+      d.bias0_c[c] = b0[c];
+      d.bias1_c[c] = w1 ? b1[c] : 0.f;
+    }
     return d;
   }
 

@@ -63,6 +63,9 @@ struct TcLayerDesc {
   int64_t chunk_off[kMaxChunks + 1];
   const float* bias0 = nullptr;
   const float* bias1 = nullptr;
+  // the same biases by value: the kernel reads them from its parameter (constant) bank
+  float bias0_c[64] = {};
+  float bias1_c[64] = {};
 };
 
 // Host: canonical fp32 weights (see include/stda_b200.h) -> descriptor + packed bf16.

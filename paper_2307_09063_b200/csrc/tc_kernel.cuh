@@ -504,9 +504,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
             float v[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
-              float t = a0[i] + __ldg(d.bias0 + j + i);
+              float t = a0[i] + d.bias0_c[j + i];
               if (p.relu0) t = fmaxf(t, 0.f);
-              if (DUAL) t = t + (a1[i] + __ldg(d.bias1 + j + i));
+              if (DUAL) t = t + (a1[i] + d.bias1_c[j + i]);
               v[i] = t;
             }
             if (!valid || (p.dbg & 1)) continue;
