@@ -124,7 +124,11 @@ void tc_pack_layer(TcLayerDesc& d, int mode, int cin, int cout, const float* w0,
   // hi/lo N-concatenation (one A_hi read for hi*hi and hi*lo) when the doubled
   // accumulators still leave two TMEM slots at one M-tile per item
   const int n_acc = d.n_src * d.n_acc_src;
-  d.concat = !bf16 && n_acc * 2 * cout * 2 <= 512;
+  static const bool s2_noconcat = [] {  // env STDA_TC_S2_NOCONCAT=1: 3-MMA stride-2 layers
+    const char* e = std::getenv("STDA_TC_S2_NOCONCAT");
+    return e && e[0] == '1';
+  }();
+  d.concat = !bf16 && n_acc * 2 * cout * 2 <= 512 && !(mode == CONV3_S2 && s2_noconcat);
   // per (src, tap): concat -> [kgrp 2][pass 2][n][8] (kgrp row block = [B_hi; B_lo], 2N rows)
   //                 else   -> [pass][kgrp 2][n][8]
   auto put = [&](const float* w, int n, int ci, int wk, int pass) {
