@@ -76,8 +76,11 @@ size_t stda_blob_floats(const stda_config* cfg);
 int stda_plan_create(const stda_config* cfg, const float* folded_host_blob, size_t n_floats,
                      int device, stda_plan** out);
 void stda_plan_destroy(stda_plan* plan);
-/* kernels launched by one stda_forward call */
+/* profiled launch slots of one stda_forward call (stda_forward_profiled / stda_launch_names) */
 int stda_launches_per_forward(const stda_plan* plan);
+/* kernels launched by one stda_forward call (slots + the separate ECA gate kernels of
+   large maps, which are timed inside the slot of the gate they feed) */
+int stda_kernels_per_forward(const stda_plan* plan);
 
 /* ---- StdaNet.forward (model.py:185-199) on device buffers ---- */
 size_t stda_workspace_bytes(const stda_plan* plan, int64_t batch);

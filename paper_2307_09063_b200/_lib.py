@@ -32,6 +32,7 @@ SIGNATURES = {
     "stda_plan_create": (C.c_int, [C.POINTER(StdaConfigC), _fp, _sz, C.c_int, C.POINTER(_vp)]),
     "stda_plan_destroy": (None, [_vp]),
     "stda_launches_per_forward": (C.c_int, [_vp]),
+    "stda_kernels_per_forward": (C.c_int, [_vp]),
     "stda_workspace_bytes": (_sz, [_vp, _i64]),
     "stda_forward": (C.c_int, [_vp, _vp, _vp, _i64, _vp, _sz, _vp]),
     "stda_forward_profiled": (C.c_int, [_vp, _vp, _vp, _i64, _vp, _sz, _vp, _vp, _i32]),
@@ -116,6 +117,10 @@ def blob_floats(cfg) -> int:
 
 def launches_per_forward(h) -> int:
     return lib().stda_launches_per_forward(h)
+
+
+def kernels_per_forward(h) -> int:
+    return lib().stda_kernels_per_forward(h)
 
 
 def workspace_bytes(h, batch: int) -> int:

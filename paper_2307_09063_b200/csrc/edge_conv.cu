@@ -144,9 +144,13 @@ __global__ void __launch_bounds__(kThreads) head_fused_kernel(
   const int64_t b = b_base + blockIdx.z;
   for (int e = tid; e < 9 * C0; e += kThreads) ws[e] = __ldg(w + e);
   // ECA gate of this image (fixed-order reduction: identical in every CTA)
-  for (int ch = tid; ch < C0; ch += kThreads) mean[ch] = eca_channel_sum(gap, items, C0, b, ch) / (float)(H * W);
-  __syncthreads();
-  for (int ch = tid; ch < C0; ch += kThreads) gate[ch] = eca_gate_of(mean, C0, ch, eca_w, k);
+  if (items == kGatesReady) {
+    for (int ch = tid; ch < C0; ch += kThreads) gate[ch] = __ldg(gap + b * C0 + ch);
+  } else {
+    for (int ch = tid; ch < C0; ch += kThreads) mean[ch] = eca_channel_sum(gap, items, C0, b, ch) / (float)(H * W);
+    __syncthreads();
+    for (int ch = tid; ch < C0; ch += kThreads) gate[ch] = eca_gate_of(mean, C0, ch, eca_w, k);
+  }
   __syncthreads();
   const int n = kIH * kIW * G8;
   for (int e0 = tid; e0 < n; e0 += 4 * kThreads) {
@@ -587,7 +591,12 @@ __global__ void __launch_bounds__(kHsThreads, 1) head_strips_kernel(
     const int st = i & 1;
     const int64_t b = s / spi;
     const int y0 = (int)(s - b * spi) * R;
-    if (b != cur_b) {
+    if (b != cur_b && items == kGatesReady) {
+      asm volatile("bar.sync 1, %0;" ::"n"(kHsCompute) : "memory");  // previous image's gate readers
+      if (tid < kHsC) gate[tid] = __ldg(gap + b * kHsC + tid);
+      asm volatile("bar.sync 1, %0;" ::"n"(kHsCompute) : "memory");
+      cur_b = b;
+    } else if (b != cur_b) {
       // ECA gate of image b (model.py:128-135): kEcaGroups group sums in parallel, added
       // in group order (planes.cuh: the one reduction order of every gate)
       if (tid < kEcaGroups * kHsC) part[tid] = eca_group_sum(gap, items, kHsC, b, tid % kHsC, tid / kHsC);

@@ -21,9 +21,13 @@ __global__ void __launch_bounds__(kGateThreads) gate_apply_kernel(
   __shared__ float gate[1024];
   const int64_t b = blockIdx.y;
   // gate for this image: fixed-order reduction of the producer's per-item partial sums
-  for (int c = threadIdx.x; c < C; c += blockDim.x) mean[c] = eca_channel_sum(gap, items, C, b, c) / (float)(H * W);
-  __syncthreads();
-  for (int c = threadIdx.x; c < C; c += blockDim.x) gate[c] = eca_gate_of(mean, C, c, eca_w, k);
+  if (items == kGatesReady) {
+    for (int c = threadIdx.x; c < C; c += blockDim.x) gate[c] = __ldg(gap + b * C + c);
+  } else {
+    for (int c = threadIdx.x; c < C; c += blockDim.x) mean[c] = eca_channel_sum(gap, items, C, b, c) / (float)(H * W);
+    __syncthreads();
+    for (int c = threadIdx.x; c < C; c += blockDim.x) gate[c] = eca_gate_of(mean, C, c, eca_w, k);
+  }
   __syncthreads();
   const int G8 = C / 8;
   const int pix0 = blockIdx.x * kPixPerCta;
@@ -126,9 +130,13 @@ __global__ void __launch_bounds__(kGateThreads) gate_apply_rows_kernel(
     }
   }
   // ECA gate of this image while the copies fly (fixed order: identical in every CTA)
-  for (int c = tid; c < C; c += blockDim.x) mean[c] = eca_channel_sum(gap, items, C, b, c) / (float)(H * W);
-  __syncthreads();
-  for (int c = tid; c < C; c += blockDim.x) gate[c] = eca_gate_of(mean, C, c, eca_w, k);
+  if (items == kGatesReady) {
+    for (int c = tid; c < C; c += blockDim.x) gate[c] = __ldg(gap + b * C + c);
+  } else {
+    for (int c = tid; c < C; c += blockDim.x) mean[c] = eca_channel_sum(gap, items, C, b, c) / (float)(H * W);
+    __syncthreads();
+    for (int c = tid; c < C; c += blockDim.x) gate[c] = eca_gate_of(mean, C, c, eca_w, k);
+  }
   if (blockIdx.x == 0) {  // top / bottom margins of the output planes, once per image
     if (has_pl) pl_zero_margins(out_pl, b, tid, blockDim.x);
     if (has_pp) pl_zero_margins(out_pp, b, tid, blockDim.x);
@@ -301,7 +309,12 @@ __global__ void __launch_bounds__(kGsThreads, 1) gate_strips_kernel(
     const int st = i % kGsStages;
     const int64_t b = s / spi;
     const int y0 = (int)(s - b * spi) * R;
-    if (b != cur_b) {
+    if (b != cur_b && items == kGatesReady) {
+      asm volatile("bar.sync 1, %0;" ::"n"(kGsCompute) : "memory");  // previous image's gate readers
+      if (tid < C) gate[tid] = __ldg(gap + b * C + tid);
+      asm volatile("bar.sync 1, %0;" ::"n"(kGsCompute) : "memory");
+      cur_b = b;
+    } else if (b != cur_b) {
       // ECA gate of image b (model.py:128-135): the kEcaGroups group sums in parallel,
       // then added in group order (planes.cuh: the one reduction order of every gate)
       for (int u = tid; u < kEcaGroups * C; u += kGsCompute)
@@ -384,6 +397,38 @@ __global__ void __launch_bounds__(kGsThreads, 1) gate_strips_kernel(
 }
 
 }  // namespace
+
+namespace {
+// gates[b][c] from per-item channel sums, one CTA per image: the kEcaGroups group sums in
+// parallel, added in group order — the arithmetic of every in-kernel gate (planes.cuh)
+__global__ void __launch_bounds__(256) eca_gates_kernel(const float* __restrict__ gap, int items,
+                                                        const float* __restrict__ eca_w, int k,
+                                                        float* __restrict__ gates, int C, int64_t hw) {
+  grid_dep_wait();
+  extern __shared__ float esm[];  // part [kEcaGroups][C], mean [C]
+  float* part = esm;
+  float* mean = esm + kEcaGroups * C;
+  const int64_t b = blockIdx.x;
+  for (int u = threadIdx.x; u < kEcaGroups * C; u += blockDim.x)
+    part[u] = eca_group_sum(gap, items, C, b, u % C, u / C);
+  __syncthreads();
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    float a = 0.f;
+    for (int g = 0; g < kEcaGroups; ++g) a += part[g * C + c];
+    mean[c] = a / (float)hw;
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < C; c += blockDim.x) gates[b * C + c] = eca_gate_of(mean, C, c, eca_w, k);
+}
+}  // namespace
+
+void launch_eca_gates(const float* gap, int items, const float* eca_w, int k, float* gates, int64_t B, int C,
+                      int64_t hw, cudaStream_t st) {
+  STDA_CHECK(B <= 0x7fffffff && C <= 4096, "eca gates: shape");
+  if (B == 0) return;
+  launch_pdl(eca_gates_kernel, dim3((unsigned)B), dim3(256), (size_t)(kEcaGroups + 1) * C * 4, st,
+             "eca_gates_kernel", gap, items, eca_w, k, gates, C, hw);
+}
 
 void launch_gate_apply(const float* gap, int items, const float* eca_w, int k, const float* x,
                        const PlBuf* skip, const PlBuf* out_pl, const PlBuf* out_pp, float* out_f32,

@@ -141,6 +141,15 @@ __device__ __forceinline__ void pl_zero_margins(const PlBuf& p, int64_t b, int t
 // kernel ran (and so of the batch size).
 constexpr int kEcaGroups = 8;
 
+// Gate source of the gate / head kernels: `gap` holds per-item channel sums (items > 0)
+// from which the kernel forms the gate itself, or, with items == kGatesReady, the finished
+// gates [B][C] (launch_eca_gates, same arithmetic: used when an image has so many items
+// that every CTA re-reducing them would dominate, i.e. large maps).
+constexpr int kGatesReady = -1;
+inline bool precompute_gates(int items, int C) { return (int64_t)items * C >= 4096; }
+void launch_eca_gates(const float* gap, int items, const float* eca_w, int k, float* gates, int64_t B, int C,
+                      int64_t hw, cudaStream_t st);
+
 __device__ __forceinline__ float eca_group_sum(const float* gap, int items, int C, int64_t b, int c, int g) {
   float a = 0.f;
   for (int t = g; t < items; t += kEcaGroups) a += __ldg(gap + ((size_t)b * items + t) * C + c);

@@ -334,7 +334,15 @@ void run_net_tc(const stda_plan& p, const Src& x, float* y, int64_t B, const Net
     h /= 2;
     wd /= 2;
     // a_i = e_i * gate_i -> PL (next stage-1 / decoder input / skip) and PP (next stride-2)
-    launch_gate_apply(w.pe[i], g2.items_per_image, E.eca, k, w.e[i], nullptr, &w.pl_a[i],
+    // large maps: the gate once per image (planes.cuh kGatesReady), not once per CTA
+    const float* gsrc = w.pe[i];
+    int gitems = g2.items_per_image;
+    if (precompute_gates(gitems, d2.cout)) {
+      launch_eca_gates(gsrc, gitems, E.eca, k, w.ge[i], B, d2.cout, (int64_t)h * wd, st);
+      gsrc = w.ge[i];
+      gitems = kGatesReady;
+    }
+    launch_gate_apply(gsrc, gitems, E.eca, k, w.e[i], nullptr, &w.pl_a[i],
                       i + 1 < S ? &w.pp_a[i] : nullptr, nullptr, B, d2.cout, h, wd, st);
     mk.mark(st);
     cur_pl = w.pl_a[i];
@@ -360,13 +368,20 @@ void run_net_tc(const stda_plan& p, const Src& x, float* y, int64_t B, const Net
     wd *= 2;
     // b_j = d_j * gate + skip  (model.py:197-198); the last one is fused into the head
     const PlBuf& sk = skips[S - 1 - j];
+    const float* gsrc = w.pd[j];
+    int gitems = g2.items_per_image;
+    if (precompute_gates(gitems, d2.cout)) {
+      launch_eca_gates(gsrc, gitems, D.eca, k, w.gd[j], B, d2.cout, (int64_t)h * wd, st);
+      gsrc = w.gd[j];
+      gitems = kGatesReady;
+    }
     if (j + 1 < S) {
-      launch_gate_apply(w.pd[j], g2.items_per_image, D.eca, k, w.d[j], &sk, &w.pl_b[j], nullptr, nullptr, B,
-                        d2.cout, h, wd, st);
+      launch_gate_apply(gsrc, gitems, D.eca, k, w.d[j], &sk, &w.pl_b[j], nullptr, nullptr, B, d2.cout, h, wd,
+                        st);
       mk.mark(st);
       cur_pl = w.pl_b[j];
     } else {
-      launch_head_fused(p.head_wt, p.head.b, w.pd[j], g2.items_per_image, D.eca, k, w.d[j], sk, c0, y, B, h,
+      launch_head_fused(p.head_wt, p.head.b, gsrc, gitems, D.eca, k, w.d[j], sk, c0, y, B, h,
                         wd, bf, st, p.head_host.empty() ? nullptr : p.head_host.data());
       mk.mark(st);
     }
@@ -568,6 +583,28 @@ int stda_launches_per_forward(const stda_plan* plan) {
   if (!plan) return -1;
   if (plan->kind != 0) return 2;
   return (plan->use_tc ? 1 : 2) + 6 * plan->cfg.stages;  // tensor-core path: last gate fused in head
+}
+
+int stda_kernels_per_forward(const stda_plan* plan) {
+  if (!plan) return -1;
+  int n = stda_launches_per_forward(plan);
+  if (plan->kind != 0 || !plan->use_tc) return n;
+  // + the separate gate kernels of large maps (run_net_tc: precompute_gates)
+  const stda_config& c = plan->cfg;
+  int h = c.map_height, wd = c.map_width;
+  for (int i = 0; i < c.stages; ++i) {
+    tc::TcLayerDesc d2 = plan->enc[i].s2_tc;
+    n += precompute_gates(tc::tc_plan(d2, 1, h, wd).items_per_image, d2.cout);
+    h /= 2;
+    wd /= 2;
+  }
+  for (int j = 0; j < c.stages; ++j) {
+    tc::TcLayerDesc d2 = plan->dec[j].s2_tc;
+    n += precompute_gates(tc::tc_plan(d2, 1, h, wd).items_per_image, d2.cout);
+    h *= 2;
+    wd *= 2;
+  }
+  return n;
 }
 
 size_t stda_workspace_bytes(const stda_plan* plan, int64_t batch) {

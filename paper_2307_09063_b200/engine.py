@@ -265,7 +265,7 @@ class CapturedForward:
             self.graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(self.graph):
                 self._launch()
-        self.launches = L.launches_per_forward(self.plan.handle) * len(self.slices)
+        self.launches = L.kernels_per_forward(self.plan.handle) * len(self.slices)
 
     def _launch(self) -> None:
         L, h = self.plan.L, self.plan.handle
