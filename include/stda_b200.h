@@ -181,8 +181,9 @@ int stda_score(const void* clean, int32_t clean_kind, const float* test_db, int6
                int32_t margin, double* out, unsigned char* det_hits, void* stream);
 
 /* ---- debug (no reference counterpart) ----
- * Arm a one-shot clock64 timeline of CTA 0 for the launch_index-th following tensor-core
- * conv launch; dev_buf holds 5 x 8192 uint64 (layout in csrc/tc_kernel.cuh, trace_at). */
+ * Arm a one-shot clock64 timeline of CTA 0 (+ %globaltimer start/end of every CTA) for the
+ * launch_index-th following tensor-core conv launch; dev_buf holds 6 x 8192 uint64 (layout
+ * in csrc/tc_kernel.cuh, trace_at / trace_cta). */
 int stda_debug_trace(void* dev_buf, int32_t launch_index);
 
 #ifdef __cplusplus

@@ -61,6 +61,10 @@ struct TcLayerDesc {
   // weight pass (hi[, lo]): [kgrp 2][n cout][8] bf16.  chunk_off = byte offsets.
   const uint16_t* w = nullptr;
   int64_t chunk_off[kMaxChunks + 1];
+  // CONVT4_HALF: the weights are two blocks, py = 0 then py = 1, each chunk-ordered
+  // (chunk_off are offsets inside one block); a CTA of an even grid only ever sees items
+  // of one py (items alternate py), so it loads / keeps one block
+  int64_t half_bytes = 0;
   const float* bias0 = nullptr;
   const float* bias1 = nullptr;
   // the same biases by value: the kernel reads them from its parameter (constant) bank

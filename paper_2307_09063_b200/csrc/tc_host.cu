@@ -136,9 +136,47 @@ void tc_pack_layer(TcLayerDesc& d, int mode, int cin, int cout, const float* w0,
     const float hi = bf16_val(v);
     packed.push_back(bf16_bits(pass == 0 ? v : v - hi));
   };
+  if (tmode && d.concat) {
+    // shift groups (tc_kernel.cuh grouped_t): per (half, src, group) the stacked tiles
+    // [kgrp 2][phase slot n][pass 2][cout][8]; zero tile for a phase not using the shift
+    const int NG = ngroups(mode);
+    // every (phase, tap) product exactly once
+    std::vector<int> seen(16, 0);
+    for (int g = 0; g < NG; ++g)
+      for (int j = 0; j < grp_n(mode, g); ++j) {
+        const int ph = grp_p0(mode, g) + j;
+        const int py = mode == CONVT4_S2 ? ph >> 1 : 0, px = mode == CONVT4_S2 ? ph & 1 : ph;
+        const int a = grp_dy(mode, g) - py + 1, b = grp_dx(mode, g) - px + 1;
+        if (a >= 0 && a <= 1 && b >= 0 && b <= 1) seen[ph * 4 + a * 2 + b]++;
+      }
+    for (int i = 0; i < (mode == CONVT4_S2 ? 16 : 8); ++i) STDA_CHECK(seen[i] == 1, "internal: shift groups");
+    for (int hv = 0; hv < n_halves; ++hv)
+    for (int c = 0; c < n_chunks; ++c) {
+      const int cgi = c % cgroups;
+        for (int s = 0; s < d.n_src; ++s)
+          for (int g = 0; g < NG; ++g)
+            for (int kg = 0; kg < 2; ++kg)
+              for (int j = 0; j < grp_n(mode, g); ++j) {
+                const int ph = grp_p0(mode, g) + j;
+                const int py = mode == CONVT4_S2 ? ph >> 1 : hv, px = mode == CONVT4_S2 ? ph & 1 : ph;
+                const int a = grp_dy(mode, g) - (mode == CONVT4_S2 ? py : 0) + 1, b = grp_dx(mode, g) - px + 1;
+                const bool used = a >= 0 && a <= 1 && b >= 0 && b <= 1;
+                const int wk = (py * 2 + px) * 4 + a * 2 + b;
+                for (int pass = 0; pass < 2; ++pass)
+                  for (int n = 0; n < cout; ++n)
+                    for (int e = 0; e < 8; ++e) {
+                      if (used) put(ws[s], n, cgi * 16 + kg * 8 + e, wk, pass);
+                      else packed.push_back(0);
+                    }
+              }
+      if (hv == 0) d.chunk_off[c + 1] = (int64_t)packed.size() * 2;
+    }
+    if (n_halves == 2) d.half_bytes = d.chunk_off[n_chunks];
+    return;
+  }
+  for (int hv = 0; hv < n_halves; ++hv)
   for (int c = 0; c < n_chunks; ++c) {
     const int pl = c / cgroups, cgi = c % cgroups;
-    for (int hv = 0; hv < n_halves; ++hv)
     for (int s = 0; s < d.n_src; ++s)
       for (const HostTap& t : taps[pl + hv]) {
         if (d.concat) {
@@ -153,8 +191,9 @@ void tc_pack_layer(TcLayerDesc& d, int mode, int cin, int cout, const float* w0,
                 for (int e = 0; e < 8; ++e) put(ws[s], n, cgi * 16 + kg * 8 + e, t.wk, pass);
         }
       }
-    d.chunk_off[c + 1] = (int64_t)packed.size() * 2;
+    if (hv == 0) d.chunk_off[c + 1] = (int64_t)packed.size() * 2;
   }
+  if (n_halves == 2) d.half_bytes = d.chunk_off[n_chunks];
 }
 
 namespace {
@@ -234,8 +273,12 @@ TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W) {
           const char* e = std::getenv("STDA_TC_TSTAGES");
           return e ? std::max(1, std::min(kMaxStages, std::atoi(e))) : 3;
         }();
+        static const int s1_stages = [] {  // env STDA_TC_S1STAGES: ring depth cap of stride-1 layers
+          const char* e = std::getenv("STDA_TC_S1STAGES");
+          return e ? std::max(1, std::min(kMaxStages, std::atoi(e))) : 3;
+        }();
         const bool tmode = d.mode == CONVT4_S2 || d.mode == CONVT4_HALF;
-        for (int st = d.mode == CONV3_S2 ? kMaxStages : tmode ? t_stages : 3; st >= 1; --st) {
+        for (int st = d.mode == CONV3_S2 ? kMaxStages : tmode ? t_stages : s1_stages; st >= 1; --st) {
           const size_t need = resident ? (size_t)st * a_stage + w_res : (size_t)st * (a_stage + b_stage);
           if (need + fixed <= (size_t)kMaxSmem) {
             stages = st;
@@ -332,7 +375,10 @@ void tc_launch(const TcLayerDesc& d, const TcGeometry& g, const PlBuf& src0, con
   int dev = 0, sms = 148;
   STDA_CUDA(cudaGetDevice(&dev));
   STDA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const int grid = std::min(p.total_items, sms);
+  int grid = std::min(p.total_items, sms);
+  // HALF: an even grid keeps every CTA on items of one py (items alternate py), so each
+  // CTA loads one weight block (TcLayerDesc::half_bytes)
+  if (d.mode == CONVT4_HALF) grid &= ~1;
   const int npm = d.npass == 1 ? kNpmBf16 : (d.concat ? kNpmConcat : kNpm3);
   STDA_CHECK(d.cout == 16 || d.cout == 32 || d.cout == 64, "unsupported cout for the tensor-core path");
   STDA_CHECK(g.G == 1 || g.G == 2 || g.G == 4, "unsupported tile count per item");

@@ -63,6 +63,13 @@ __device__ __forceinline__ void trace_at(unsigned long long* tr, int region, int
   if (tr != nullptr && blockIdx.x == 0 && idx < kTraceRegion)
     tr[region * kTraceRegion + idx] = clock64();
 }
+// region 5: every CTA, [2*cta + {0 start, 1 end}] in %globaltimer ns (comparable across SMs)
+__device__ __forceinline__ void trace_cta(unsigned long long* tr, int which) {
+  if (tr == nullptr || 2 * (int)blockIdx.x + 1 >= kTraceRegion) return;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  tr[5 * kTraceRegion + 2 * blockIdx.x + which] = t;
+}
 
 // ---- compile-time tap tables (must match plane_taps() on the host) ----------------
 // S1:  t = ky*3+kx, shift (ky-1, kx-1)
@@ -111,6 +118,43 @@ __host__ __device__ constexpr int plane_lo_a(int mode, int pl) {
 __host__ __device__ constexpr int plane_lo_b(int mode, int pl) {
   return mode == CONV3_S2 ? ((pl & 1) ? -1 : 0) : -1;
 }
+
+// ---- shift groups of the transposed conv (fp32 concat scheme) ------------------------
+// The 16 (phase, tap) products of a ConvT item read only 9 distinct A shifts: shift
+// (dy, dx) is used by every phase (py, px) with dy - py, dx - px in {-1, 0} (tap
+// a = dy - py + 1, b = dx - px + 1).  One MMA per shift covers a contiguous run of
+// accumulators [p0, p0 + n) — their TMEM blocks are adjacent — with the B tiles of those
+// phases stacked along N (a zero tile for a phase in the run that does not use the shift):
+// 9 A reads per source and chunk instead of 16 (HALF: 6 instead of 8).  Group 0 touches
+// every accumulator (it initialises them in chunk 0).
+//   T    (acc = py*2+px): (0,0)x4 (-1,0)x2@0 (1,0)x2@2 (0,-1)x3@0 (0,1)x3@1 and the 4 corners
+//   HALF (acc = px, shifts relative to the item origin): (0,0)x2 (-1,0)x2 (0,-1) (0,1)
+//        (-1,-1) (-1,1)
+__host__ __device__ constexpr bool grouped_t(int mode, int npm) {
+  return (mode == CONVT4_S2 || mode == CONVT4_HALF) && npm == kNpmConcat;
+}
+__host__ __device__ constexpr int ngroups(int mode) { return mode == CONVT4_S2 ? 9 : 6; }
+__host__ __device__ constexpr int grp_dy(int mode, int g) {
+  return mode == CONVT4_S2 ? (g == 1 || g == 5 || g == 6 ? -1 : g == 2 || g == 7 || g == 8 ? 1 : 0)
+                           : (g == 1 || g == 4 || g == 5 ? -1 : 0);
+}
+__host__ __device__ constexpr int grp_dx(int mode, int g) {
+  return mode == CONVT4_S2 ? (g == 3 || g == 5 || g == 7 ? -1 : g == 4 || g == 6 || g == 8 ? 1 : 0)
+                           : (g == 2 || g == 4 ? -1 : g == 3 || g == 5 ? 1 : 0);
+}
+__host__ __device__ constexpr int grp_p0(int mode, int g) {
+  return mode == CONVT4_S2 ? (g == 2 ? 2 : g == 4 ? 1 : g >= 5 ? g - 5 : 0) : (g == 3 || g == 5 ? 1 : 0);
+}
+__host__ __device__ constexpr int grp_n(int mode, int g) {
+  return mode == CONVT4_S2 ? (g == 0 ? 4 : g <= 2 ? 2 : g <= 4 ? 3 : 1) : (g <= 1 ? 2 : 1);
+}
+__host__ __device__ constexpr int grp_slot0(int mode, int g) {  // first B tile of group g
+  int s = 0;
+  for (int i = 0; i < g; ++i) s += grp_n(mode, i);
+  return s;
+}
+// B tiles per source and chunk: T 18 (16 + 2 zero tiles), HALF 8
+__host__ __device__ constexpr int grp_slots(int mode) { return grp_slot0(mode, ngroups(mode)); }
 
 // ---- PTX helpers -----------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -227,6 +271,32 @@ __device__ __forceinline__ void issue_chunk(bool leader, uint64_t a0, uint64_t b
   constexpr uint32_t IDESC_N = idesc_bf16(N);
   constexpr uint32_t IDESC_W = idesc_bf16(AW);
   const int lo = plane_lo_a(MODE, PL) * L + plane_lo_b(MODE, PL);
+  if constexpr (grouped_t(MODE, NPM)) {
+    // one MMA pair per shift group: A_hi x [tiles] + A_lo x [tiles], each tile [B_hi | B_lo]
+    // (the A_lo x B_lo product is kept: it costs nothing extra at this width)
+    constexpr int NG = ngroups(MODE), NS = grp_slots(MODE);
+#pragma unroll
+    for (int s = 0; s < (DUAL ? 2 : 1); ++s) {
+#pragma unroll
+      for (int gi = 0; gi < NG; ++gi) {
+        const int n = grp_n(MODE, gi);
+        const uint32_t idesc = idesc_bf16(n * AW);
+        const uint64_t ad0 = a0 + (uint32_t)s * src_units + (uint32_t)(grp_dy(MODE, gi) * L + grp_dx(MODE, gi) - lo);
+        // B descriptor of the stacked tiles: K-half stride (LBO) = n * AW rows of 16 B
+        const uint64_t bd = b0 + (uint32_t)(s * NS + grp_slot0(MODE, gi)) * TAP_UNITS +
+                            ((uint64_t)((n - 1) * AW) << 16);
+        const uint32_t accum0 = (first_chunk && gi == 0) ? 0u : 1u;
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const uint64_t ad = ad0 + (uint32_t)(g * 128);
+          const uint32_t dcol = dslot + (uint32_t)((g * NACC + s * NACC_SRC + grp_p0(MODE, gi)) * AW);
+          tc_mma(leader, dcol, ad, bd, idesc, accum0);      // A_hi x [B_hi | B_lo] (n tiles)
+          tc_mma(leader, dcol, ad + lo_units, bd, idesc, 1u);  // A_lo x [B_hi | B_lo]
+        }
+      }
+    }
+    return;
+  }
 #pragma unroll
   for (int s = 0; s < (DUAL ? 2 : 1); ++s) {
 #pragma unroll
@@ -285,6 +355,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
 
   if (threadIdx.x == 0) {
     trace_at(p.trace, 4, 0);
+    trace_cta(p.trace, 0);
     for (int s = 0; s < p.stages; ++s) {
       mbar_init(smem_u32(&full[s]), 1);
       mbar_init(smem_u32(&empty[s]), 1);
@@ -320,7 +391,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
     const int cs = lane / (NPASS_A * 2), cpass = (lane >> 1) % NPASS_A, ccg8 = lane & 1;
     if (lane == 0 && p.resident) {
       mbar_arrive_expect_tx(smem_u32(wbar), p.w_total);
-      bulk_g2s(smem_u32(b_base), d.w, p.w_total, smem_u32(wbar));
+      // HALF: this CTA's py block only (even grid: item parity == blockIdx.x parity)
+      bulk_g2s(smem_u32(b_base),
+               reinterpret_cast<const uint8_t*>(d.w) + (MODE == CONVT4_HALF ? (blockIdx.x & 1) * d.half_bytes : 0),
+               p.w_total, smem_u32(wbar));
     }
     grid_dep_wait();  // weights are static; activations come from the previous kernel
     const PlBuf& S = p.src[lane < NCOPY ? cs : 0];
@@ -350,7 +424,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
         __syncwarp();  // byte count posted before any copy can complete
         if (lane == NCOPY && !p.resident)
           bulk_g2s(smem_u32(b_base + (size_t)stage * p.b_stage_bytes),
-                   reinterpret_cast<const uint8_t*>(d.w) + d.chunk_off[c], w_bytes, fb);
+                   reinterpret_cast<const uint8_t*>(d.w) + (MODE == CONVT4_HALF ? (it & 1) * d.half_bytes : 0) +
+                       d.chunk_off[c],
+                   w_bytes, fb);
         if (lane < NCOPY) {
           const uint16_t* src = img + (int64_t)(NPLANES == 4 ? pl : 0) * S.plane_stride +
                                 (S.block_index(cgi, cpass, ccg8) + q0 + pt.lo + S.off) * 8;
@@ -390,14 +466,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
         tc_fence_after();
         if (leader) trace_at(p.trace, 1, 2 * k);
         const uint64_t a0 = smem_desc(smem_u32(a_base + (size_t)stage * p.a_stage_bytes), lboA, 128);
-        // HALF: each weight chunk holds the py = 0 taps, then the py = 1 taps
-        const size_t half_off =
-            MODE == CONVT4_HALF ? (size_t)((item - (item / p.items_per_image) * p.items_per_image) & 1) * NSRC *
-                                      ntaps(MODE, 0) * (NPM == kNpmBf16 ? 32 : 64) * N
-                                : 0;
+        // (HALF: the resident block / the staged chunk is already the item's py block)
         const uint64_t b0 = smem_desc(
-            smem_u32(b_base + (p.resident ? (size_t)d.chunk_off[c] : (size_t)stage * p.b_stage_bytes) + half_off),
-            lboB, 128);
+            smem_u32(b_base + (p.resident ? (size_t)d.chunk_off[c] : (size_t)stage * p.b_stage_bytes)), lboB, 128);
         if constexpr (MODE == CONV3_S2) {
           switch (c / cgroups) {
             case 0: issue_chunk<N, MODE, 0, DUAL, NPM, G>(leader, a0, b0, dslot, p.L, c == 0, src_units, lo_units); break;
@@ -564,7 +635,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
 
   tc_fence_before();
   __syncthreads();
-  if (threadIdx.x == 0) trace_at(p.trace, 4, 1);
+  if (threadIdx.x == 0) {
+    trace_at(p.trace, 4, 1);
+    trace_cta(p.trace, 1);
+  }
   if (warp == kMmaWarp) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(p.tmem_cols)

@@ -41,17 +41,26 @@ def stats(a):
 
 
 for li in range(n_tc):
-    buf = torch.zeros(5 * R, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(6 * R, dtype=torch.int64, device="cuda")
     _lib._check(_lib.lib().stda_debug_trace(buf.data_ptr(), li), "stda_debug_trace")
     with torch.no_grad():
         net(x)
     torch.cuda.synchronize()
-    t = buf.cpu().numpy().astype(np.int64).reshape(5, R)
+    t = buf.cpu().numpy().astype(np.int64).reshape(6, R)
     t0, t1 = t[4, 0], t[4, 1]
     prod, mma, slot, epi = t[0], t[1], t[2], t[3]
     nk = int(np.count_nonzero(mma[1::2]))
     ni = int(np.count_nonzero(slot))
     print(f"== {names[li]}: {t1 - t0} cycles, {ni} items, {nk} chunks")
+    g = t[5][: 2 * 148].reshape(-1, 2)
+    g = g[g[:, 1] > 0]
+    if len(g):
+        st, en = g[:, 0] - g[:, 0].min(), g[:, 1] - g[:, 0].min()
+        dur = en - st
+        slow = np.argsort(-en)[:4]
+        print(f"  CTAs (globaltimer ns): start spread {st.max()}, end min {en.min()} median {int(np.median(en))} "
+              f"max {en.max()}; duration min {dur.min()} median {int(np.median(dur))} max {dur.max()}; "
+              f"last to end: {list(slow)}")
     pe = prod[0 : 2 * nk : 2] - np.concatenate([[t0], prod[1 : 2 * nk - 1 : 2]])
     pi = prod[1 : 2 * nk : 2] - prod[0 : 2 * nk : 2]
     print(f"  producer  wait-empty {stats(pe)} | issue {stats(pi)}")
