@@ -249,19 +249,42 @@ constexpr int kGsCompute = 512;  // 16 compute warps: the unit chains are latenc
 constexpr int kGsThreads = kGsCompute + 32;
 constexpr int kGsStages = 4;
 
+// 8 channels -> bf16 hi (+ lo) at hi[0..7] and hi[lo_delta ..] (planes.cuh split)
+template <int NP>
+__device__ __forceinline__ void store8_split(uint16_t* hi, size_t lo_delta, const float (&v)[8]) {
+  uint32_t h[4], l[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const __nv_bfloat162 hb = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+    h[j] = *reinterpret_cast<const uint32_t*>(&hb);
+    if (NP == 2) {
+      const float2 hf = __bfloat1622float2(hb);
+      l[j] = pack_bf16x2(v[2 * j] - hf.x, v[2 * j + 1] - hf.y);
+    }
+  }
+  *reinterpret_cast<uint4*>(hi) = make_uint4(h[0], h[1], h[2], h[3]);
+  if (NP == 2) *reinterpret_cast<uint4*>(hi + lo_delta) = make_uint4(l[0], l[1], l[2], l[3]);
+}
+
+// Compile-time channel count / passes / skip / phase-plane output: the unit loop has no
+// runtime division and each thread keeps one 8-channel group (kGsCompute % (C / 8) == 0),
+// so its plane block offsets are loop-invariant.
+template <int C, int NP, bool SKIP, bool PP>
 __global__ void __launch_bounds__(kGsThreads, 1) gate_strips_kernel(
     const float* __restrict__ gap, int items, const float* __restrict__ eca_w, int k,
-    const float* __restrict__ x, PlBuf skip, int has_skip, PlBuf out_pl, PlBuf out_pp, int has_pp, int C,
-    int H, int W, int R, int64_t B, uint32_t x_bytes, uint32_t stage_bytes) {
+    const float* __restrict__ x, PlBuf skip, PlBuf out_pl, PlBuf out_pp, int H, int W, uint32_t W_mul, int R,
+    int64_t B, uint32_t x_bytes, uint32_t stage_bytes) {
   using namespace ptx;
+  constexpr int G8 = C / 8;
+  constexpr int nblk = (C / 16) * NP * 2;
+  static_assert(kGsCompute % G8 == 0, "one channel group per thread");
   extern __shared__ __align__(128) uint8_t gsm[];
   float* gate = reinterpret_cast<float*>(gsm + (size_t)kGsStages * stage_bytes);  // [C]
   float* part = gate + C;  // [kEcaGroups][C] group sums, then [C] means
   uint64_t* full = reinterpret_cast<uint64_t*>(part + (kEcaGroups + 1) * C);
   uint64_t* empty = full + kGsStages;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int L = W + 1, Lp = W / 2 + 1, G8 = C / 8;
-  const int np = out_pl.np, nblk = (C / 16) * np * 2;
+  const int L = W + 1, Lp = W / 2 + 1;
   const uint32_t sk_blk = (uint32_t)R * L * 16;
   const int spi = H / R;
   const int64_t n_strips = B * spi;
@@ -279,7 +302,7 @@ __global__ void __launch_bounds__(kGsThreads, 1) gate_strips_kernel(
 
   if (warp == kGsCompute / 32) {
     // ===== producer warp: lane 0 posts the byte count, lanes issue one copy each =====
-    const int ncopy = 1 + (has_skip ? nblk : 0);
+    constexpr int ncopy = 1 + (SKIP ? nblk : 0);
     int i = 0;
     for (int64_t s = s_begin; s < s_end; ++s, ++i) {
       const int st = i % kGsStages;
@@ -288,7 +311,7 @@ __global__ void __launch_bounds__(kGsThreads, 1) gate_strips_kernel(
       const int y0 = (int)(s - b * spi) * R;
       const uint32_t bar = smem_u32(&full[st]);
       uint8_t* base = gsm + (size_t)st * stage_bytes;
-      if (lane == 0) mbar_arrive_expect_tx(bar, x_bytes + (has_skip ? nblk * sk_blk : 0u));
+      if (lane == 0) mbar_arrive_expect_tx(bar, x_bytes + (SKIP ? nblk * sk_blk : 0u));
       __syncwarp();
       for (int c = lane; c < ncopy; c += 32) {
         if (c == 0)
@@ -302,66 +325,70 @@ __global__ void __launch_bounds__(kGsThreads, 1) gate_strips_kernel(
     return;
   }
 
-  // ===== 8 compute warps =====
+  // ===== 16 compute warps =====
+  const int c8 = tid % G8, cg16 = c8 >> 1, cg8 = c8 & 1;
+  const int kh = (cg16 * NP) * 2 + cg8;  // hi block of this 8-channel group (lo: kh + 2)
+  const size_t pl_blk = ((size_t)kh * out_pl.Q + out_pl.off) * 8;
+  const size_t pp_blk = PP ? ((size_t)kh * out_pp.Q + out_pp.off) * 8 : 0;
+  const size_t pl_lo = (size_t)2 * out_pl.Q * 8, pp_lo = PP ? (size_t)2 * out_pp.Q * 8 : 0;
   int64_t cur_b = -1;
   int i = 0;
+  float g8[8];
   for (int64_t s = s_begin; s < s_end; ++s, ++i) {
     const int st = i % kGsStages;
     const int64_t b = s / spi;
     const int y0 = (int)(s - b * spi) * R;
-    if (b != cur_b && items == kGatesReady) {
-      asm volatile("bar.sync 1, %0;" ::"n"(kGsCompute) : "memory");  // previous image's gate readers
-      if (tid < C) gate[tid] = __ldg(gap + b * C + tid);
-      asm volatile("bar.sync 1, %0;" ::"n"(kGsCompute) : "memory");
-      cur_b = b;
-    } else if (b != cur_b) {
-      // ECA gate of image b (model.py:128-135): the kEcaGroups group sums in parallel,
-      // then added in group order (planes.cuh: the one reduction order of every gate)
-      for (int u = tid; u < kEcaGroups * C; u += kGsCompute)
-        part[u] = eca_group_sum(gap, items, C, b, u % C, u / C);
-      asm volatile("bar.sync 1, %0;" ::"n"(kGsCompute) : "memory");
-      float* mean = part + kEcaGroups * C;  // [C]
-      if (tid < C) {
-        float a = 0.f;
-        for (int g = 0; g < kEcaGroups; ++g) a += part[g * C + tid];
-        mean[tid] = a / (float)(H * W);
+    if (b != cur_b) {
+      if (items == kGatesReady) {
+        asm volatile("bar.sync 1, %0;" ::"n"(kGsCompute) : "memory");  // previous image's gate readers
+        if (tid < C) gate[tid] = __ldg(gap + b * C + tid);
+      } else {
+        // ECA gate of image b (model.py:128-135): the kEcaGroups group sums in parallel,
+        // then added in group order (planes.cuh: the one reduction order of every gate)
+        for (int u = tid; u < kEcaGroups * C; u += kGsCompute)
+          part[u] = eca_group_sum(gap, items, C, b, u % C, u / C);
+        asm volatile("bar.sync 1, %0;" ::"n"(kGsCompute) : "memory");
+        float* mean = part + kEcaGroups * C;  // [C]
+        if (tid < C) {
+          float a = 0.f;
+          for (int g = 0; g < kEcaGroups; ++g) a += part[g * C + tid];
+          mean[tid] = a / (float)(H * W);
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kGsCompute) : "memory");
+        if (tid < C) gate[tid] = eca_gate_of(mean, C, tid, eca_w, k);
       }
       asm volatile("bar.sync 1, %0;" ::"n"(kGsCompute) : "memory");
-      if (tid < C) gate[tid] = eca_gate_of(mean, C, tid, eca_w, k);
-      asm volatile("bar.sync 1, %0;" ::"n"(kGsCompute) : "memory");
+#pragma unroll
+      for (int j = 0; j < 8; ++j) g8[j] = gate[c8 * 8 + j];
       cur_b = b;
     }
     if (y0 == 0) {  // top / bottom margins of the output planes, once per image
       pl_zero_margins(out_pl, b, tid, kGsCompute);
-      if (has_pp) pl_zero_margins(out_pp, b, tid, kGsCompute);
+      if (PP) pl_zero_margins(out_pp, b, tid, kGsCompute);
     }
     mbar_wait(smem_u32(&full[st]), (i / kGsStages) & 1);
     const float* xs = reinterpret_cast<const float*>(gsm + (size_t)st * stage_bytes);
     const uint8_t* sk = gsm + (size_t)st * stage_bytes + x_bytes;
-    uint16_t* opl = out_pl.base + b * out_pl.img_stride;
+    uint16_t* opl = out_pl.base + b * out_pl.img_stride + pl_blk;
+    uint16_t* opp = PP ? out_pp.base + b * out_pp.img_stride + pp_blk : nullptr;
 #pragma unroll 2
-    for (int u = tid; u < R * W * G8; u += kGsCompute) {
-      const int c8 = u % G8, pix = u / G8;
-      const int r = pix / W, xx = pix - r * W;
+    for (int pix = tid / G8; pix < R * W; pix += kGsCompute / G8) {
+      const int r = (int)__umulhi((uint32_t)pix, W_mul), xx = pix - r * W;
       const float4 a0 = *reinterpret_cast<const float4*>(xs + (size_t)pix * C + c8 * 8);
       const float4 a1 = *reinterpret_cast<const float4*>(xs + (size_t)pix * C + c8 * 8 + 4);
-      const float4 g0 = *reinterpret_cast<const float4*>(gate + c8 * 8);
-      const float4 g1 = *reinterpret_cast<const float4*>(gate + c8 * 8 + 4);
       const float xv[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-      const float gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
       float v[8];
-      float sk8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-      const int kh = ((c8 >> 1) * np) * 2 + (c8 & 1);  // hi block of this 8-channel group
-      if (has_skip) {                                  // + skip (model.py:197-198)
+      if (SKIP) {  // + skip (model.py:197-198), exact hi + lo of its plane
         const size_t so = (size_t)(r * L + xx) * 16;
         const uint4 h = *reinterpret_cast<const uint4*>(sk + (size_t)kh * sk_blk + so);
         const uint32_t hw[4] = {h.x, h.y, h.z, h.w};
+        float sk8[8];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           sk8[2 * j] = __uint_as_float(hw[j] << 16);
           sk8[2 * j + 1] = __uint_as_float(hw[j] & 0xFFFF0000u);
         }
-        if (np == 2) {
+        if (NP == 2) {
           const uint4 l = *reinterpret_cast<const uint4*>(sk + (size_t)(kh + 2) * sk_blk + so);
           const uint32_t lw[4] = {l.x, l.y, l.z, l.w};
 #pragma unroll
@@ -370,24 +397,28 @@ __global__ void __launch_bounds__(kGsThreads, 1) gate_strips_kernel(
             sk8[2 * j + 1] += __uint_as_float(lw[j] & 0xFFFF0000u);
           }
         }
-      }
 #pragma unroll
-      for (int i = 0; i < 8; ++i)  // eca(x) = x * gate (+ skip): planes.cuh rounding order
-        v[i] = has_skip ? gate_fma(xv[i], gv[i], sk8[i]) : gate_mul(xv[i], gv[i]);
+        for (int j = 0; j < 8; ++j) v[j] = gate_fma(xv[j], g8[j], sk8[j]);  // planes.cuh rounding order
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = gate_mul(xv[j], g8[j]);
+      }
       const int oy = y0 + r;
-      pl_store8(out_pl, b, 0, c8, oy * L + xx, v);
-      if (has_pp) pl_store8(out_pp, b, (oy & 1) * 2 + (xx & 1), c8, (oy >> 1) * Lp + (xx >> 1), v);
-      if (xx >= W - 2 && (c8 & 1) == 0) {  // pad columns (planes.cuh border contract)
-        const int cg16 = c8 >> 1;
-        if (xx == W - 1)
-          for (int kb = 0; kb < np * 2; ++kb)
-            pl_zero16(opl + ((size_t)(cg16 * np * 2 + kb) * out_pl.Q + (size_t)oy * L + W + out_pl.off) * 8);
-        if (has_pp) {
-          const int plane = (oy & 1) * 2 + (xx & 1);
-          uint16_t* pp_img = out_pp.base + b * out_pp.img_stride + (int64_t)plane * out_pp.plane_stride;
-          for (int kb = 0; kb < np * 2; ++kb)
-            pl_zero16(pp_img + ((size_t)(cg16 * np * 2 + kb) * out_pp.Q + (size_t)(oy >> 1) * Lp + W / 2 +
-                                out_pp.off) * 8);
+      store8_split<NP>(opl + (size_t)(oy * L + xx) * 8, pl_lo, v);
+      if (PP) {
+        const int64_t pofs = (int64_t)((oy & 1) * 2 + (xx & 1)) * out_pp.plane_stride;
+        store8_split<NP>(opp + pofs + (size_t)((oy >> 1) * Lp + (xx >> 1)) * 8, pp_lo, v);
+      }
+      if (xx >= W - 2) {  // pad columns of this thread's blocks (planes.cuh border contract)
+        if (xx == W - 1) {
+          pl_zero16(opl + (size_t)(oy * L + W) * 8);
+          if (NP == 2) pl_zero16(opl + pl_lo + (size_t)(oy * L + W) * 8);
+        }
+        if (PP) {
+          uint16_t* pz = opp + (int64_t)((oy & 1) * 2 + (xx & 1)) * out_pp.plane_stride +
+                         (size_t)((oy >> 1) * Lp + W / 2) * 8;
+          pl_zero16(pz);
+          if (NP == 2) pl_zero16(pz + pp_lo);
         }
       }
     }
@@ -459,18 +490,39 @@ void launch_gate_apply(const float* gap, int items, const float* eca_w, int k, c
     // measured: with fewer than ~4 strips per SM the per-CTA fill (first loads + gate)
     // dominates and the one-shot row-block kernel is faster
     if (H % R == 0 && smem <= 227 * 1024 && B * (H / R) >= 4 * (int64_t)sms) {
-      static uint64_t configured = 0;
-      if (!(configured >> (dev & 63) & 1)) {
-        STDA_CUDA(cudaFuncSetAttribute(gate_strips_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       227 * 1024));
-        configured |= 1ull << (dev & 63);
-      }
       const int64_t n_strips = B * (H / R);
       const unsigned grid = (unsigned)std::min<int64_t>(n_strips, sms);
-      launch_pdl(gate_strips_kernel, dim3(grid), dim3(kGsThreads), smem, st, "gate_strips_kernel", gap, items,
-                 eca_w, k, x, skip ? *skip : PlBuf{}, (int)(skip != nullptr), *out_pl,
-                 out_pp ? *out_pp : PlBuf{}, (int)(out_pp != nullptr), C, H, W, R, B,
-                 (uint32_t)((size_t)R * W * C * 4), (uint32_t)stage_bytes);
+      const uint32_t W_mul = (uint32_t)((((uint64_t)1 << 32) + (uint64_t)W - 1) / (uint64_t)W);
+      STDA_CHECK((uint64_t)R * W * W < ((uint64_t)1 << 32), "gate strips: row index");
+      auto go = [&](auto cc, auto npc, auto skc, auto ppc) {
+        const auto kern = gate_strips_kernel<decltype(cc)::value, decltype(npc)::value, decltype(skc)::value,
+                                             decltype(ppc)::value>;
+        static uint64_t configured = 0;  // per instantiation (integral_constant-keyed lambda)
+        if (!(configured >> (dev & 63) & 1)) {
+          STDA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+          configured |= 1ull << (dev & 63);
+        }
+        launch_pdl(kern, dim3(grid), dim3(kGsThreads), smem, st, "gate_strips_kernel", gap, items, eca_w, k, x,
+                   skip ? *skip : PlBuf{}, *out_pl, out_pp ? *out_pp : PlBuf{}, H, W, W_mul, R, B,
+                   (uint32_t)((size_t)R * W * C * 4), (uint32_t)stage_bytes);
+      };
+      using std::integral_constant;
+      auto g3 = [&](auto cc, auto npc) {
+        if (skip && out_pp) go(cc, npc, integral_constant<bool, true>{}, integral_constant<bool, true>{});
+        else if (skip) go(cc, npc, integral_constant<bool, true>{}, integral_constant<bool, false>{});
+        else if (out_pp) go(cc, npc, integral_constant<bool, false>{}, integral_constant<bool, true>{});
+        else go(cc, npc, integral_constant<bool, false>{}, integral_constant<bool, false>{});
+      };
+      auto g2 = [&](auto cc) {
+        if (np == 2) g3(cc, integral_constant<int, 2>{});
+        else g3(cc, integral_constant<int, 1>{});
+      };
+      switch (C) {
+        case 16: g2(integral_constant<int, 16>{}); break;
+        case 32: g2(integral_constant<int, 32>{}); break;
+        case 64: g2(integral_constant<int, 64>{}); break;
+        default: g2(integral_constant<int, 128>{}); break;
+      }
       return;
     }
   }
