@@ -614,84 +614,102 @@ __global__ void __launch_bounds__(kHsThreads, 1) head_strips_kernel(
     mbar_wait(smem_u32(&full[st]), (i >> 1) & 1);
     float* ubase = reinterpret_cast<float*>(hsm + (size_t)st * g.stage);
     const uint8_t* sbase = hsm + (size_t)st * g.stage + g.dbytes;
-    // transform: one (stage pixel, channel quad) per thread step
+    // transform: one (stage pixel, channel quad) per thread step, NB steps per batch: all
+    // loads of a batch, one __syncwarp (the 4 quads of a pixel are lanes of one warp and
+    // are rewritten in place; steps touch disjoint pixels), then all stores
+    constexpr int NIT = SR * W * 4 / kHsCompute;
+    static_assert(NIT * kHsCompute == SR * W * 4, "transform steps");
+    constexpr int NB = NIT % 4 == 0 ? 4 : NIT % 3 == 0 ? 3 : 2;
+    static_assert(NIT % NB == 0, "transform batches");
+    const int q = tid & 3;
+    const float4 g4 = *reinterpret_cast<const float4*>(gate + q * 4);
 #pragma unroll
-    for (int e0 = 0; e0 < SR * W * 4; e0 += kHsCompute) {
-      const int e = e0 + tid;
-      const int q = e & 3, p = e >> 2;
-      const int r = p / W, x = p - r * W;
-      const int iy = y0 - 1 + r;
-      float4 u = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (iy >= 0 && iy < H) {
-        const float4 dv = *reinterpret_cast<const float4*>(ubase + p * kHsC + q * 4);
+    for (int it0 = 0; it0 < NIT; it0 += NB) {
+      float4 dv[NB];
+      uint2 hv[NB], lv[NB];
+      bool in[NB];
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        const int p = ((it0 + j) * kHsCompute + tid) >> 2;
+        const int r = p / W, x = p - r * W;
+        const int iy = y0 - 1 + r;
+        in[j] = iy >= 0 && iy < H;
+        dv[j] = *reinterpret_cast<const float4*>(ubase + p * kHsC + q * 4);
         // channels 4q..4q+3: cg8 block (q >> 1), bytes (q & 1) * 8 of position r*L + x
         const size_t so = (size_t)(r * L + x) * 16 + (q & 1) * 8;
-        const uint2 hv = *reinterpret_cast<const uint2*>(sbase + (size_t)(q >> 1) * g.sblk + so);
-        float s4[4];
-        s4[0] = __uint_as_float(hv.x << 16);
-        s4[1] = __uint_as_float(hv.x & 0xFFFF0000u);
-        s4[2] = __uint_as_float(hv.y << 16);
-        s4[3] = __uint_as_float(hv.y & 0xFFFF0000u);
-        if (np == 2) {
-          const uint2 lv = *reinterpret_cast<const uint2*>(sbase + (size_t)(2 + (q >> 1)) * g.sblk + so);
-          s4[0] += __uint_as_float(lv.x << 16);
-          s4[1] += __uint_as_float(lv.x & 0xFFFF0000u);
-          s4[2] += __uint_as_float(lv.y << 16);
-          s4[3] += __uint_as_float(lv.y & 0xFFFF0000u);
-        }
-        const float4 g4 = *reinterpret_cast<const float4*>(gate + q * 4);
-        u.x = gate_fma(dv.x, g4.x, s4[0]);  // eca(d) + skip (model.py:197-198)
-        u.y = gate_fma(dv.y, g4.y, s4[1]);
-        u.z = gate_fma(dv.z, g4.z, s4[2]);
-        u.w = gate_fma(dv.w, g4.w, s4[3]);
-        if (bf16) {
-          u.x = bf16_round(u.x);
-          u.y = bf16_round(u.y);
-          u.z = bf16_round(u.z);
-          u.w = bf16_round(u.w);
-        }
+        hv[j] = *reinterpret_cast<const uint2*>(sbase + (size_t)(q >> 1) * g.sblk + so);
+        lv[j] = np == 2 ? *reinterpret_cast<const uint2*>(sbase + (size_t)(2 + (q >> 1)) * g.sblk + so)
+                        : make_uint2(0u, 0u);
       }
-      __syncwarp();  // the 4 quads of a pixel are lanes of one warp: all read before any write
-      *reinterpret_cast<float4*>(ubase + p * kHsC + (q ^ hs_swz(p)) * 4) = u;
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        const int p = ((it0 + j) * kHsCompute + tid) >> 2;
+        float4 u = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (in[j]) {
+          float s4[4];
+          s4[0] = __uint_as_float(hv[j].x << 16);
+          s4[1] = __uint_as_float(hv[j].x & 0xFFFF0000u);
+          s4[2] = __uint_as_float(hv[j].y << 16);
+          s4[3] = __uint_as_float(hv[j].y & 0xFFFF0000u);
+          if (np == 2) {
+            s4[0] += __uint_as_float(lv[j].x << 16);
+            s4[1] += __uint_as_float(lv[j].x & 0xFFFF0000u);
+            s4[2] += __uint_as_float(lv[j].y << 16);
+            s4[3] += __uint_as_float(lv[j].y & 0xFFFF0000u);
+          }
+          u.x = gate_fma(dv[j].x, g4.x, s4[0]);  // eca(d) + skip (model.py:197-198)
+          u.y = gate_fma(dv[j].y, g4.y, s4[1]);
+          u.z = gate_fma(dv[j].z, g4.z, s4[2]);
+          u.w = gate_fma(dv[j].w, g4.w, s4[3]);
+          if (bf16) {
+            u.x = bf16_round(u.x);
+            u.y = bf16_round(u.y);
+            u.z = bf16_round(u.z);
+            u.w = bf16_round(u.w);
+          }
+        }
+        *reinterpret_cast<float4*>(ubase + p * kHsC + (q ^ hs_swz(p)) * 4) = u;
+      }
     }
     fence_proxy_async();  // generic writes of this stage before its next async refill
     asm volatile("bar.sync 1, %0;" ::"n"(kHsCompute) : "memory");
     // conv3x3 (model.py:158,199): rows 2rp, 2rp+1 of the strip at column cx
-    float acc0 = 0.f, acc1 = 0.f;
+    // 4 independent chains per output (channel quads j), summed at the end
+    float acc0[4] = {0.f, 0.f, 0.f, 0.f}, acc1[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
     for (int kx = 0; kx < 3; ++kx) {
       const int xx = cx + kx - 1;
       const bool in = xx >= 0 && xx < W;
+      float4 u[4][4];  // [channel quad][row]: all loads of this column first
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        float4 u[4];
+      for (int j = 0; j < 4; ++j)
 #pragma unroll
         for (int rr = 0; rr < 4; ++rr) {
           const int p = (2 * rp + rr) * W + (in ? xx : 0);
-          u[rr] = *reinterpret_cast<const float4*>(ubase + p * kHsC + (j ^ hs_swz(p)) * 4);
-          if (!in) u[rr] = make_float4(0.f, 0.f, 0.f, 0.f);
+          u[j][rr] = *reinterpret_cast<const float4*>(ubase + p * kHsC + (j ^ hs_swz(p)) * 4);
+          if (!in) u[j][rr] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
         for (int ky = 0; ky < 3; ++ky) {
-          const float4 w4 = make_float4(cw.w[(ky * 3 + kx) * kHsC + j * 4], cw.w[(ky * 3 + kx) * kHsC + j * 4 + 1],
-                                        cw.w[(ky * 3 + kx) * kHsC + j * 4 + 2],
-                                        cw.w[(ky * 3 + kx) * kHsC + j * 4 + 3]);
-          acc0 = fmaf(u[ky].x, w4.x, acc0);
-          acc0 = fmaf(u[ky].y, w4.y, acc0);
-          acc0 = fmaf(u[ky].z, w4.z, acc0);
-          acc0 = fmaf(u[ky].w, w4.w, acc0);
-          acc1 = fmaf(u[ky + 1].x, w4.x, acc1);
-          acc1 = fmaf(u[ky + 1].y, w4.y, acc1);
-          acc1 = fmaf(u[ky + 1].z, w4.z, acc1);
-          acc1 = fmaf(u[ky + 1].w, w4.w, acc1);
+          const float* wt = &cw.w[(ky * 3 + kx) * kHsC + j * 4];
+          acc0[j] = fmaf(u[j][ky].x, wt[0], acc0[j]);
+          acc0[j] = fmaf(u[j][ky].y, wt[1], acc0[j]);
+          acc0[j] = fmaf(u[j][ky].z, wt[2], acc0[j]);
+          acc0[j] = fmaf(u[j][ky].w, wt[3], acc0[j]);
+          acc1[j] = fmaf(u[j][ky + 1].x, wt[0], acc1[j]);
+          acc1[j] = fmaf(u[j][ky + 1].y, wt[1], acc1[j]);
+          acc1[j] = fmaf(u[j][ky + 1].z, wt[2], acc1[j]);
+          acc1[j] = fmaf(u[j][ky + 1].w, wt[3], acc1[j]);
         }
-      }
     }
     __syncwarp();
     if ((tid & 31) == 0) mbar_arrive(smem_u32(&empty[st]));  // this warp is done with stage st
     float* yo = y + ((size_t)b * H + y0 + 2 * rp) * W + cx;
-    yo[0] = acc0 + bv;
-    yo[W] = acc1 + bv;
+    yo[0] = ((acc0[0] + acc0[1]) + (acc0[2] + acc0[3])) + bv;
+    yo[W] = ((acc1[0] + acc1[1]) + (acc1[2] + acc1[3])) + bv;
   }
 }
 
