@@ -5,7 +5,9 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 
+#include <mutex>
 #include <string>
+#include <vector>
 #include <utility>
 
 namespace stda {
@@ -28,6 +30,24 @@ struct Error {
   do {                                                                               \
     if (!(cond)) throw ::stda::Error{std::string(msg)};                              \
   } while (0)
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize, bytes) once per (kernel, device);
+// thread-safe (plans may be used from several host threads)
+inline void ensure_dyn_smem(const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<const void*, int>, int>> done;  // ((fn, device), bytes)
+  int dev = 0;
+  STDA_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  for (const auto& e : done)
+    if (e.first.first == fn && e.first.second == dev && e.second >= bytes) return;
+  STDA_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done.push_back({{fn, dev}, bytes});
+}
+template <typename... A>
+inline void ensure_dyn_smem(void (*kern)(A...), int bytes) {
+  ensure_dyn_smem(reinterpret_cast<const void*>(kern), bytes);
+}
 
 // After kernel launches: surface configuration errors immediately.
 inline void check_launch(const char* what) {

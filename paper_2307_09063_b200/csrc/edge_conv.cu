@@ -393,15 +393,16 @@ __global__ void __launch_bounds__(kRowThreads, 4) stem_rows_kernel(const float* 
 // from the constant bank (uniform across the warp), so the only shared-memory traffic is
 // the frame rows.  ncu on stem_rows_kernel: LSU wavefronts ~80 % busy, mostly weights.
 constexpr int kStemC = 16, kStemMaxF = 4;
-struct StemConst {
-  float w[kStemMaxF * 9 * kStemC];  // [ci][ky][kx][co]
+struct alignas(16) StemConst {
+  float w[kStemMaxF * 9 * kStemC];  // [ci][ky][kx][co]: channel pairs (co, co+1) are 8-byte units
   float b[kStemC];
 };
 
-template <int F, int PX>
+template <int F, int PX, int NP>  // NP = 1: bf16 operands (inputs rounded, hi plane only)
 __global__ void __launch_bounds__(kRowThreads, 4) stem_const_kernel(const __grid_constant__ StemConst cw, Src x,
                                                                    PlBuf pl, PlBuf pp, int H, int W, int R,
-                                                                   int bf16, int64_t b_base) {
+                                                                   int64_t b_base) {
+  constexpr bool bf16 = NP == 1;
   grid_dep_wait();  // PDL: previous kernel complete (common.cuh)
   extern __shared__ __align__(128) uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t bar;
@@ -436,46 +437,61 @@ __global__ void __launch_bounds__(kRowThreads, 4) stem_const_kernel(const __grid
   }
   ptx::mbar_wait(ptx::smem_u32(&bar), 0);
   __syncthreads();
+  // C0 = 16: one cg16, blocks (pass, cg8) at (pass * 2 + cg8) * Q (planes.cuh)
+  const size_t QB = (size_t)pl.Q * 8, QBp = (size_t)pp.Q * 8;
+  uint16_t* plb = pl.base + b * pl.img_stride + (size_t)pl.off * 8;
+  uint16_t* ppb = pp.base + b * pp.img_stride + (size_t)pp.off * 8;
   for (int it = tid; it < (R / PX) * W; it += kRowThreads) {  // PX vertically adjacent pixels
     const int r0 = (it / W) * PX, xx = it - (it / W) * W;
-    float acc[PX][kStemC];
+    // channel-pair accumulators: one FFMA2 = (x broadcast) x (uniform weight pair) + pair,
+    // bit-identical to two fmaf() in the same order, half the issue slots
+    unsigned long long acc2[PX][kStemC / 2];
 #pragma unroll
     for (int o = 0; o < PX; ++o)
 #pragma unroll
-      for (int co = 0; co < kStemC; ++co) acc[o][co] = cw.b[co];
+      for (int j = 0; j < kStemC / 2; ++j) acc2[o][j] = *reinterpret_cast<const unsigned long long*>(&cw.b[2 * j]);
 #pragma unroll
     for (int ci = 0; ci < F; ++ci) {
       const float* xc = xs + (size_t)ci * (R + 2) * W;
 #pragma unroll
       for (int kx = 0; kx < 3; ++kx) {
         const int ix = xx + kx - 1;
-        float v[PX + 2];
+        unsigned long long v2[PX + 2];
 #pragma unroll
         for (int k = 0; k < PX + 2; ++k) {
-          const float t = (ix >= 0 && ix < W) ? xc[(r0 + k) * W + ix] : 0.f;
-          v[k] = bf16 ? bf16_round(t) : t;
+          float t = (ix >= 0 && ix < W) ? xc[(r0 + k) * W + ix] : 0.f;
+          if (bf16) t = bf16_round(t);
+          v2[k] = f2_pack(t, t);
         }
 #pragma unroll
         for (int ky = 0; ky < 3; ++ky)
 #pragma unroll
-          for (int co = 0; co < kStemC; ++co) {
-            const float wv = cw.w[((ci * 3 + ky) * 3 + kx) * kStemC + co];
+          for (int j = 0; j < kStemC / 2; ++j) {
+            const unsigned long long w2 =
+                *reinterpret_cast<const unsigned long long*>(&cw.w[((ci * 3 + ky) * 3 + kx) * kStemC + 2 * j]);
 #pragma unroll
-            for (int o = 0; o < PX; ++o) acc[o][co] = fmaf(v[ky + o], wv, acc[o][co]);
+            for (int o = 0; o < PX; ++o) f2_fma(acc2[o][j], v2[ky + o], w2);
           }
       }
     }
+    float acc[PX][kStemC];
+#pragma unroll
+    for (int o = 0; o < PX; ++o)
+#pragma unroll
+      for (int j = 0; j < kStemC / 2; ++j) f2_unpack(acc2[o][j], acc[o][2 * j], acc[o][2 * j + 1]);
 #pragma unroll
     for (int o = 0; o < PX; ++o) {
       const int oy = y0 + r0 + o;
       const int plane = (oy & 1) * 2 + (xx & 1);
+      uint16_t* po = plb + (size_t)(oy * L + xx) * 8;
+      uint16_t* pq = ppb + (int64_t)plane * pp.plane_stride + (size_t)((oy >> 1) * Lp + (xx >> 1)) * 8;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         float v8[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) v8[i] = fmaxf(acc[o][8 * h + i], 0.f);
-        pl_store8(pl, b, 0, h, oy * L + xx, v8);
-        pl_store8(pp, b, plane, h, (oy >> 1) * Lp + (xx >> 1), v8);
+        store8_split<NP>(po + h * QB, 2 * QB, v8);
+        store8_split<NP>(pq + h * QBp, 2 * QBp, v8);
       }
       if (xx >= W - 2) {  // pad columns (planes.cuh border contract)
         if (xx == W - 1) pl_zero_pos(pl, b, 0, oy * L + W);
@@ -721,13 +737,7 @@ bool head_strips_ok(int C0, int64_t B, int H, int W) {
 
 template <typename K>
 void set_smem(K kern) {
-  static uint64_t configured = 0;
-  int dev = 0;
-  STDA_CUDA(cudaGetDevice(&dev));
-  if (!(configured >> (dev & 63) & 1)) {
-    STDA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    configured |= 1ull << (dev & 63);
-  }
+  ensure_dyn_smem(kern, 200 * 1024);
 }
 
 }  // namespace
@@ -759,18 +769,12 @@ void launch_stem_planes(const float* w, const float* bias, const Src& x, int F, 
     STDA_CHECK(smem <= 200 * 1024, "stem: rows do not fit shared memory");
     auto go = [&](auto fc) {
       constexpr int FF = decltype(fc)::value;
-      const auto kern = PXr == 4 ? stem_const_kernel<FF, 4> : stem_const_kernel<FF, 2>;
-      static uint64_t configured = 0;  // per F
-      int dev = 0;
-      STDA_CUDA(cudaGetDevice(&dev));
-      if (!(configured >> (dev & 63) & 1)) {
-        STDA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        configured |= 1ull << (dev & 63);
-      }
+      const auto kern = bf16 ? (PXr == 4 ? stem_const_kernel<FF, 4, 1> : stem_const_kernel<FF, 2, 1>)
+                             : (PXr == 4 ? stem_const_kernel<FF, 4, 2> : stem_const_kernel<FF, 2, 2>);
+      ensure_dyn_smem(kern, 200 * 1024);
       for (int64_t b0 = 0; b0 < B; b0 += 65535) {
         dim3 grid(H / R, (unsigned)std::min<int64_t>(65535, B - b0));
-        launch_pdl(kern, grid, dim3(kRowThreads), smem, st, "stem_const_kernel", cw, x, pl, pp, H, W, R, (int)bf16,
-                   b0);
+        launch_pdl(kern, grid, dim3(kRowThreads), smem, st, "stem_const_kernel", cw, x, pl, pp, H, W, R, b0);
       }
     };
     switch (F) {
@@ -831,11 +835,7 @@ void launch_head_fused(const float* w, const float* bias, const float* gap, int 
     const unsigned grid = (unsigned)std::min<int64_t>(n_strips, sms);
     auto go = [&](auto wc) {
       const auto kern = head_strips_kernel<decltype(wc)::value>;
-      static uint64_t configured = 0;  // per instantiation of this generic lambda (per W)
-      if (!(configured >> (dev & 63) & 1)) {
-        STDA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        configured |= 1ull << (dev & 63);
-      }
+      ensure_dyn_smem(kern, 227 * 1024);
       launch_pdl(kern, dim3(grid), dim3(kHsThreads), g.smem, st, "head_strips_kernel", hc, bias, gap, items, eca_w,
                  k, d, skip, y, B, H, (int)bf16);
     };

@@ -269,13 +269,7 @@ void launch_rd_frontend(const float2* beat, int64_t n, int N, int M, int P, int 
   constexpr int kMaxDyn = 220 * 1024;  // + the kernel's static reduction scratch
   STDA_CHECK(rd_frontend_smem(P, Q) <= (size_t)kMaxDyn, "rd front end: P x Q too large for one CTA");
   STDA_CHECK(layout == 0 || layout == 1, "rd front end: layout");
-  static uint64_t configured = 0;
-  int dev = 0;
-  STDA_CUDA(cudaGetDevice(&dev));
-  if (!(configured >> (dev & 63) & 1)) {
-    STDA_CUDA(cudaFuncSetAttribute(rd_frontend_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDyn));
-    configured |= 1ull << (dev & 63);
-  }
+  ensure_dyn_smem(rd_frontend_kernel, kMaxDyn);
   for (int64_t f0 = 0; f0 < n; f0 += 65535) {
     const unsigned nf = (unsigned)std::min<int64_t>(65535, n - f0);
     rd_frontend_kernel<<<nf, kFeThreads, rd_frontend_smem(P, Q), st>>>(

@@ -249,23 +249,6 @@ constexpr int kGsCompute = 512;  // 16 compute warps: the unit chains are latenc
 constexpr int kGsThreads = kGsCompute + 32;
 constexpr int kGsStages = 4;
 
-// 8 channels -> bf16 hi (+ lo) at hi[0..7] and hi[lo_delta ..] (planes.cuh split)
-template <int NP>
-__device__ __forceinline__ void store8_split(uint16_t* hi, size_t lo_delta, const float (&v)[8]) {
-  uint32_t h[4], l[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const __nv_bfloat162 hb = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
-    h[j] = *reinterpret_cast<const uint32_t*>(&hb);
-    if (NP == 2) {
-      const float2 hf = __bfloat1622float2(hb);
-      l[j] = pack_bf16x2(v[2 * j] - hf.x, v[2 * j + 1] - hf.y);
-    }
-  }
-  *reinterpret_cast<uint4*>(hi) = make_uint4(h[0], h[1], h[2], h[3]);
-  if (NP == 2) *reinterpret_cast<uint4*>(hi + lo_delta) = make_uint4(l[0], l[1], l[2], l[3]);
-}
-
 // Compile-time channel count / passes / skip / phase-plane output: the unit loop has no
 // runtime division and each thread keeps one 8-channel group (kGsCompute % (C / 8) == 0),
 // so its plane block offsets are loop-invariant.
@@ -497,11 +480,7 @@ void launch_gate_apply(const float* gap, int items, const float* eca_w, int k, c
       auto go = [&](auto cc, auto npc, auto skc, auto ppc) {
         const auto kern = gate_strips_kernel<decltype(cc)::value, decltype(npc)::value, decltype(skc)::value,
                                              decltype(ppc)::value>;
-        static uint64_t configured = 0;  // per instantiation (integral_constant-keyed lambda)
-        if (!(configured >> (dev & 63) & 1)) {
-          STDA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-          configured |= 1ull << (dev & 63);
-        }
+        ensure_dyn_smem(kern, 227 * 1024);
         launch_pdl(kern, dim3(grid), dim3(kGsThreads), smem, st, "gate_strips_kernel", gap, items, eca_w, k, x,
                    skip ? *skip : PlBuf{}, *out_pl, out_pp ? *out_pp : PlBuf{}, H, W, W_mul, R, B,
                    (uint32_t)((size_t)R * W * C * 4), (uint32_t)stage_bytes);
@@ -539,14 +518,7 @@ void launch_gate_apply(const float* gap, int items, const float* eca_w, int k, c
     while (R * 2 <= 8 && H % (R * 2) == 0 && (size_t)R * 2 * W <= 512 && bytes(R * 2) <= 96 * 1024) R *= 2;
     const size_t smem = bytes(R);
     STDA_CHECK(smem <= 200 * 1024, "gate_apply: rows do not fit shared memory");
-    static uint64_t configured = 0;
-    int dev = 0;
-    STDA_CUDA(cudaGetDevice(&dev));
-    if (!(configured >> (dev & 63) & 1)) {
-      STDA_CUDA(cudaFuncSetAttribute(gate_apply_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     200 * 1024));
-      configured |= 1ull << (dev & 63);
-    }
+    ensure_dyn_smem(gate_apply_rows_kernel, 200 * 1024);
     dim3 grid(H / R, (unsigned)B);
     launch_pdl(gate_apply_rows_kernel, grid, dim3(kGateThreads), smem, st, "gate_apply_rows_kernel", gap, items,
                eca_w, k, x, skip ? *skip : PlBuf{}, (int)(skip != nullptr), *out_pl, 1,

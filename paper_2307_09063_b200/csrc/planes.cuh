@@ -82,6 +82,24 @@ __device__ __forceinline__ void pl_store8(const PlBuf& p, int64_t b, int plane, 
   }
 }
 
+// pl_store8 with the pass count known at compile time and the block address precomputed:
+// 8 channels -> bf16 hi at hi[0..7] (+ lo = v - hi at hi[lo_delta ..]), same bits as pl_store8
+template <int NP>
+__device__ __forceinline__ void store8_split(uint16_t* hi, size_t lo_delta, const float (&v)[8]) {
+  uint32_t h[4], l[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const __nv_bfloat162 hb = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+    h[j] = *reinterpret_cast<const uint32_t*>(&hb);
+    if (NP == 2) {
+      const float2 hf = __bfloat1622float2(hb);
+      l[j] = pack_bf16x2(v[2 * j] - hf.x, v[2 * j + 1] - hf.y);
+    }
+  }
+  *reinterpret_cast<uint4*>(hi) = make_uint4(h[0], h[1], h[2], h[3]);
+  if (NP == 2) *reinterpret_cast<uint4*>(hi + lo_delta) = make_uint4(l[0], l[1], l[2], l[3]);
+}
+
 // Read back 8 channels as fp32 (hi + lo).
 __device__ __forceinline__ void pl_load8(const PlBuf& p, int64_t b, int plane, int c8, int q,
                                          float (&v)[8]) {

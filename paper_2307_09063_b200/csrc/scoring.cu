@@ -165,13 +165,7 @@ void launch_score(const void* clean, int clean_kind, const float* test_db, int64
   STDA_CHECK(margin >= 0 && clean_kind >= 0 && clean_kind <= 1, "scoring: bad arguments");
   const size_t smem = (size_t)P * Q * (16 + 3);
   STDA_CHECK(smem <= 200 * 1024, "scoring: map too large for one CTA");
-  static uint64_t configured = 0;
-  int dev = 0;
-  STDA_CUDA(cudaGetDevice(&dev));
-  if (!(configured >> (dev & 63) & 1)) {
-    STDA_CUDA(cudaFuncSetAttribute(score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    configured |= 1ull << (dev & 63);
-  }
+  ensure_dyn_smem(score_kernel, 200 * 1024);
   const CfarOffsets off = make_offsets(guard0, guard1, train0, train1);
   for (int64_t s0 = 0; s0 < n; s0 += 65535) {
     const unsigned ns = (unsigned)std::min<int64_t>(65535, n - s0);

@@ -299,13 +299,7 @@ void launch_impl(Args a, int64_t B, int nblk, cudaStream_t st) {
   const size_t smem = sizeof(float) * ((DUAL ? 2 : 1) * (CICH * TAPSZ + CICH * G::IH * G::IWP) +
                                        (kThreads / 32) * COB);
   auto kern = conv_simt_kernel<MODE, DUAL, COB, CICH>;
-  static uint64_t configured = 0;  // per instantiation, bit per device
-  int dev = 0;
-  STDA_CUDA(cudaGetDevice(&dev));
-  if (!(configured >> (dev & 63) & 1)) {
-    STDA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured |= 1ull << (dev & 63);
-  }
+  ensure_dyn_smem(kern, (int)smem);
   for (int64_t b0 = 0; b0 < B; b0 += 65535) {
     a.b_base = b0;
     dim3 grid(a.ntiles, nblk, (unsigned)std::min<int64_t>(65535, B - b0));

@@ -649,13 +649,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
 template <int N, int MODE, bool DUAL, int NPM, int G>
 void launch_k(const Params& p, int grid, size_t smem, cudaStream_t st) {
   auto kern = tc_conv_kernel<N, MODE, DUAL, NPM, G>;
-  static uint64_t configured = 0;
-  int dev = 0;
-  STDA_CUDA(cudaGetDevice(&dev));
-  if (!(configured >> (dev & 63) & 1)) {
-    STDA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
-    configured |= 1ull << (dev & 63);
-  }
+  ensure_dyn_smem(kern, kMaxSmem);
   launch_pdl(kern, dim3(grid), dim3(kThreads), smem, st, "tc_conv_kernel", p);
 }
 
