@@ -13,7 +13,8 @@ from pathlib import Path
 
 import numpy as np
 
-LIB_PATH = Path(__file__).resolve().parent / "libstda_b200.so"
+# STDA_LIB_PATH: load another build of the same ABI (A/B timing of kernel variants)
+LIB_PATH = Path(os.environ.get("STDA_LIB_PATH") or Path(__file__).resolve().parent / "libstda_b200.so")
 
 # every symbol include/stda_b200.h declares, with (restype, argtypes)
 _vp, _i32, _i64, _sz, _u64, _fp = C.c_void_p, C.c_int32, C.c_int64, C.c_size_t, C.c_uint64, C.c_void_p
