@@ -450,6 +450,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
       mbar_wait(smem_u32(wbar), 0);
       __syncwarp();
     }
+    int mstage = 0;
+    uint32_t mphase = 0;
     for (int item = blockIdx.x; item < p.total_items; item += gridDim.x, ++ic) {
       const int slot = ic % p.slots;
       const uint32_t sphase = (ic / p.slots) & 1;
@@ -459,11 +461,16 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
       if (leader) trace_at(p.trace, 2, ic);
       const uint32_t dslot = tmem_base + (uint32_t)slot * p.slot_cols;
       for (int c = 0; c < n_chunks; ++c, ++k) {
-        const int stage = k % p.stages;
-        const uint32_t phase = (k / p.stages) & 1;
-        mbar_wait(smem_u32(&full[stage]), phase);
+        // ring position by counters (no integer division between the MMA bursts: the
+        // issue runs in lockstep with the tensor pipe, so this code is pipe idle time)
+        const int stage = mstage;
+        const uint32_t phase = mphase;
+        if (++mstage == p.stages) {
+          mstage = 0;
+          mphase ^= 1u;
+        }
+        mbar_wait(smem_u32(&full[stage]), phase);  // TMA -> MMA: both async proxy, no fence
         __syncwarp();
-        tc_fence_after();
         if (leader) trace_at(p.trace, 1, 2 * k);
         const uint64_t a0 = smem_desc(smem_u32(a_base + (size_t)stage * p.a_stage_bytes), lboA, 128);
         // (HALF: the resident block / the staged chunk is already the item's py block)
