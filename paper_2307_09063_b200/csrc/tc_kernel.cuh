@@ -399,6 +399,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
     grid_dep_wait();  // weights are static; activations come from the previous kernel
     const PlBuf& S = p.src[lane < NCOPY ? cs : 0];
     uint32_t k = 0;
+    int pstage = 0;
+    uint32_t pphase = 0;
     for (int item = blockIdx.x; item < p.total_items; item += gridDim.x) {
       const int b = item / p.items_per_image;
       const int it = item - b * p.items_per_image;
@@ -406,8 +408,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
       const int q0 = MODE == CONVT4_HALF ? (it >> 1) * p.G * 128 + (it & 1) * p.L : it * p.G * 128;
       const uint16_t* img = S.base + (int64_t)b * S.img_stride;
       for (int c = 0; c < n_chunks; ++c, ++k) {
-        const int stage = k % p.stages;
-        const uint32_t phase = (k / p.stages) & 1;
+        const int stage = pstage;
+        const uint32_t phase = pphase;
+        if (++pstage == p.stages) {
+          pstage = 0;
+          pphase ^= 1u;
+        }
         mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
         if (lane == 0) trace_at(p.trace, 0, 2 * k);
         const int pl = c / cgroups, cgi = c - pl * cgroups;
@@ -450,11 +456,13 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
       mbar_wait(smem_u32(wbar), 0);
       __syncwarp();
     }
-    int mstage = 0;
-    uint32_t mphase = 0;
+    int mstage = 0, slot = 0;
+    uint32_t mphase = 0, sphase = 0;
     for (int item = blockIdx.x; item < p.total_items; item += gridDim.x, ++ic) {
-      const int slot = ic % p.slots;
-      const uint32_t sphase = (ic / p.slots) & 1;
+      if (ic > 0 && ++slot == p.slots) {
+        slot = 0;
+        sphase ^= 1u;
+      }
       mbar_wait(smem_u32(&tempty[slot]), sphase ^ 1);
       __syncwarp();
       tc_fence_after();
