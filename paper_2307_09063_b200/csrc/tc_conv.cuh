@@ -86,6 +86,8 @@ struct TcGeometry {
   int tmem_cols;
   int P_max;              // staged positions per plane
   uint32_t a_stage_bytes, b_stage_bytes;
+  int cps;                // K chunks per ring stage (one barrier round trip per cps chunks)
+  uint32_t chunk_a_bytes, chunk_b_bytes;
   bool resident;          // packed weights stay in smem for the whole launch
   uint32_t w_total;       // packed weight bytes
   size_t smem_bytes;

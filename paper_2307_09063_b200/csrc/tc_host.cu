@@ -308,6 +308,33 @@ TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W) {
     }
   }
   STDA_CHECK(ok, "tensor-core conv: no tiling fits shared memory");
+  // Two K chunks per ring stage when they fit >= 2 stages: the MMA warp's per-stage
+  // barrier wait / commit / descriptor setup (tensor-pipe idle time, the issue runs in
+  // lockstep with execution) is paid once per two chunks
+  g.cps = 1;
+  g.chunk_a_bytes = g.a_stage_bytes;
+  g.chunk_b_bytes = g.b_stage_bytes;
+  {
+    static const int cps_cap = [] {  // env STDA_TC_CPS=1: one chunk per stage (A/B timing)
+      const char* e = std::getenv("STDA_TC_CPS");
+      return e && e[0] == '1' ? 1 : 2;
+    }();
+    const int n_chunks = d.n_planes * (d.cin / 16);
+    // measured: helps the transposed convs (dec0.s2 -4 %, dec1.s2 -1.5 %), not S1/S2
+    const bool tmode = d.mode == CONVT4_S2 || d.mode == CONVT4_HALF;
+    if (cps_cap >= 2 && tmode && n_chunks % 2 == 0) {
+      const size_t per = 2 * (size_t)g.a_stage_bytes + (g.resident ? 0 : 2 * (size_t)g.b_stage_bytes);
+      const size_t base = (g.resident ? (size_t)((g.w_total + 127) / 128 * 128) : 0) + fixed;
+      const int st2 = (int)std::min<size_t>((size_t)std::max(2, (g.stages + 1) / 2), ((size_t)kMaxSmem - base) / per);
+      if (st2 >= 2) {
+        g.cps = 2;
+        g.stages = st2;
+        g.a_stage_bytes = 2 * g.chunk_a_bytes;
+        g.b_stage_bytes = g.resident ? 0 : 2 * g.chunk_b_bytes;
+        g.smem_bytes = base + (size_t)st2 * per;
+      }
+    }
+  }
   const int positions = g.Hp * g.L;
   g.items_per_image = cdiv(positions, g.G * 128) * (d.mode == CONVT4_HALF ? 2 : 1);
   return g;
@@ -354,6 +381,9 @@ void tc_launch(const TcLayerDesc& d, const TcGeometry& g, const PlBuf& src0, con
   p.P_max = g.P_max;
   p.a_stage_bytes = g.a_stage_bytes;
   p.b_stage_bytes = g.b_stage_bytes;
+  p.cps = g.cps;
+  p.chunk_a_bytes = g.chunk_a_bytes;
+  p.chunk_b_bytes = g.chunk_b_bytes;
   p.resident = g.resident ? 1 : 0;
   p.w_total = g.w_total;
   p.slot_cols = (uint32_t)(g.G * d.n_src * d.n_acc_src * d.cout * (d.concat ? 2 : 1));

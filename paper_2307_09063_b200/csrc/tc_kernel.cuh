@@ -41,6 +41,8 @@ struct Params {
   int G, stages, slots, items_per_image, total_items;
   int P_max;
   uint32_t a_stage_bytes, b_stage_bytes, slot_cols;
+  int cps;                          // K chunks per ring stage (1 or 2)
+  uint32_t chunk_a_bytes, chunk_b_bytes;  // one chunk's A (all sources) / staged weights
   int resident;       // all packed weights loaded once into smem (else one chunk per stage)
   uint32_t w_total;   // packed weight bytes of the layer
   uint32_t tmem_cols;
@@ -326,7 +328,7 @@ __device__ __forceinline__ void issue_chunk(bool leader, uint64_t a0, uint64_t b
 }
 
 // ---- the kernel ----------------------------------------------------------------------
-template <int N, int MODE, bool DUAL, int NPM, int G>
+template <int N, int MODE, bool DUAL, int NPM, int G, int CPS>
 __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int NSRC = DUAL ? 2 : 1;
@@ -407,7 +409,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
       // HALF: items (tile, py) interleaved; the tile origin moves down py rows
       const int q0 = MODE == CONVT4_HALF ? (it >> 1) * p.G * 128 + (it & 1) * p.L : it * p.G * 128;
       const uint16_t* img = S.base + (int64_t)b * S.img_stride;
-      for (int c = 0; c < n_chunks; ++c, ++k) {
+      for (int c0 = 0; c0 < n_chunks; c0 += CPS, ++k) {  // one ring stage = cps chunks
         const int stage = pstage;
         const uint32_t phase = pphase;
         if (++pstage == p.stages) {
@@ -416,29 +418,39 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
         }
         mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
         if (lane == 0) trace_at(p.trace, 0, 2 * k);
-        const int pl = c / cgroups, cgi = c - pl * cgroups;
-        const PlaneTaps& pt = d.planes[pl];
-        const int P = p.G * 128 + pt.hi - pt.lo;
-        const uint32_t a_bytes = (uint32_t)P * 16;
-        const uint32_t w_bytes = p.resident ? 0u : (uint32_t)(d.chunk_off[c + 1] - d.chunk_off[c]);
         const uint32_t fb = smem_u32(&full[stage]);
         if ((p.dbg & 4) && k >= (uint32_t)p.stages) {
           if (lane == 0) mbar_arrive(fb);
           continue;
         }
-        if (lane == 0) mbar_arrive_expect_tx(fb, w_bytes + (uint32_t)NCOPY * a_bytes);
+        uint32_t tx = 0;
+#pragma unroll
+        for (int cc = 0; cc < CPS; ++cc) {
+          const int c = c0 + cc;
+          const PlaneTaps& pt = d.planes[c / cgroups];
+          tx += (uint32_t)NCOPY * (uint32_t)(p.G * 128 + pt.hi - pt.lo) * 16 +
+                (p.resident ? 0u : (uint32_t)(d.chunk_off[c + 1] - d.chunk_off[c]));
+        }
+        if (lane == 0) mbar_arrive_expect_tx(fb, tx);
         __syncwarp();  // byte count posted before any copy can complete
-        if (lane == NCOPY && !p.resident)
-          bulk_g2s(smem_u32(b_base + (size_t)stage * p.b_stage_bytes),
-                   reinterpret_cast<const uint8_t*>(d.w) + (MODE == CONVT4_HALF ? (it & 1) * d.half_bytes : 0) +
-                       d.chunk_off[c],
-                   w_bytes, fb);
-        if (lane < NCOPY) {
-          const uint16_t* src = img + (int64_t)(NPLANES == 4 ? pl : 0) * S.plane_stride +
-                                (S.block_index(cgi, cpass, ccg8) + q0 + pt.lo + S.off) * 8;
-          bulk_g2s(smem_u32(a_base + (size_t)stage * p.a_stage_bytes + (size_t)cs * src_bytes +
-                            (size_t)(cpass * 2 + ccg8) * p.P_max * 16),
-                   src, a_bytes, fb);
+#pragma unroll
+        for (int cc = 0; cc < CPS; ++cc) {
+          const int c = c0 + cc;
+          const int pl = c / cgroups, cgi = c - pl * cgroups;
+          const PlaneTaps& pt = d.planes[pl];
+          const uint32_t a_bytes = (uint32_t)(p.G * 128 + pt.hi - pt.lo) * 16;
+          if (lane == NCOPY && !p.resident)
+            bulk_g2s(smem_u32(b_base + (size_t)stage * p.b_stage_bytes + (size_t)cc * p.chunk_b_bytes),
+                     reinterpret_cast<const uint8_t*>(d.w) + (MODE == CONVT4_HALF ? (it & 1) * d.half_bytes : 0) +
+                         d.chunk_off[c],
+                     (uint32_t)(d.chunk_off[c + 1] - d.chunk_off[c]), fb);
+          if (lane < NCOPY) {
+            const uint16_t* src = img + (int64_t)(NPLANES == 4 ? pl : 0) * S.plane_stride +
+                                  (S.block_index(cgi, cpass, ccg8) + q0 + pt.lo + S.off) * 8;
+            bulk_g2s(smem_u32(a_base + (size_t)stage * p.a_stage_bytes + (size_t)cc * p.chunk_a_bytes +
+                              (size_t)cs * src_bytes + (size_t)(cpass * 2 + ccg8) * p.P_max * 16),
+                     src, a_bytes, fb);
+          }
         }
         if (lane == 0) trace_at(p.trace, 0, 2 * k + 1);
       }
@@ -468,7 +480,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
       tc_fence_after();
       if (leader) trace_at(p.trace, 2, ic);
       const uint32_t dslot = tmem_base + (uint32_t)slot * p.slot_cols;
-      for (int c = 0; c < n_chunks; ++c, ++k) {
+      for (int c0 = 0; c0 < n_chunks; c0 += CPS, ++k) {
         // ring position by counters (no integer division between the MMA bursts: the
         // issue runs in lockstep with the tensor pipe, so this code is pipe idle time)
         const int stage = mstage;
@@ -480,19 +492,26 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
         mbar_wait(smem_u32(&full[stage]), phase);  // TMA -> MMA: both async proxy, no fence
         __syncwarp();
         if (leader) trace_at(p.trace, 1, 2 * k);
-        const uint64_t a0 = smem_desc(smem_u32(a_base + (size_t)stage * p.a_stage_bytes), lboA, 128);
-        // (HALF: the resident block / the staged chunk is already the item's py block)
-        const uint64_t b0 = smem_desc(
-            smem_u32(b_base + (p.resident ? (size_t)d.chunk_off[c] : (size_t)stage * p.b_stage_bytes)), lboB, 128);
-        if constexpr (MODE == CONV3_S2) {
-          switch (c / cgroups) {
-            case 0: issue_chunk<N, MODE, 0, DUAL, NPM, G>(leader, a0, b0, dslot, p.L, c == 0, src_units, lo_units); break;
-            case 1: issue_chunk<N, MODE, 1, DUAL, NPM, G>(leader, a0, b0, dslot, p.L, c == 0, src_units, lo_units); break;
-            case 2: issue_chunk<N, MODE, 2, DUAL, NPM, G>(leader, a0, b0, dslot, p.L, c == 0, src_units, lo_units); break;
-            default: issue_chunk<N, MODE, 3, DUAL, NPM, G>(leader, a0, b0, dslot, p.L, c == 0, src_units, lo_units); break;
+#pragma unroll
+        for (int cc = 0; cc < CPS; ++cc) {  // CPS chunks per barrier round trip
+          const int c = c0 + cc;
+          const uint64_t a0 = smem_desc(
+              smem_u32(a_base + (size_t)stage * p.a_stage_bytes + (size_t)cc * p.chunk_a_bytes), lboA, 128);
+          // (HALF: the resident block / the staged chunk is already the item's py block)
+          const uint64_t b0 = smem_desc(
+              smem_u32(b_base + (p.resident ? (size_t)d.chunk_off[c]
+                                            : (size_t)stage * p.b_stage_bytes + (size_t)cc * p.chunk_b_bytes)),
+              lboB, 128);
+          if constexpr (MODE == CONV3_S2) {
+            switch (c / cgroups) {
+              case 0: issue_chunk<N, MODE, 0, DUAL, NPM, G>(leader, a0, b0, dslot, p.L, c == 0, src_units, lo_units); break;
+              case 1: issue_chunk<N, MODE, 1, DUAL, NPM, G>(leader, a0, b0, dslot, p.L, c == 0, src_units, lo_units); break;
+              case 2: issue_chunk<N, MODE, 2, DUAL, NPM, G>(leader, a0, b0, dslot, p.L, c == 0, src_units, lo_units); break;
+              default: issue_chunk<N, MODE, 3, DUAL, NPM, G>(leader, a0, b0, dslot, p.L, c == 0, src_units, lo_units); break;
+            }
+          } else {
+            issue_chunk<N, MODE, 0, DUAL, NPM, G>(leader, a0, b0, dslot, p.L, c == 0, src_units, lo_units);
           }
-        } else {
-          issue_chunk<N, MODE, 0, DUAL, NPM, G>(leader, a0, b0, dslot, p.L, c == 0, src_units, lo_units);
         }
         __syncwarp();
         tc_commit(leader, smem_u32(&empty[stage]));
@@ -663,7 +682,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
 
 template <int N, int MODE, bool DUAL, int NPM, int G>
 void launch_k(const Params& p, int grid, size_t smem, cudaStream_t st) {
-  auto kern = tc_conv_kernel<N, MODE, DUAL, NPM, G>;
+  auto kern = p.cps == 2 ? tc_conv_kernel<N, MODE, DUAL, NPM, G, 2> : tc_conv_kernel<N, MODE, DUAL, NPM, G, 1>;
   ensure_dyn_smem(kern, kMaxSmem);
   launch_pdl(kern, dim3(grid), dim3(kThreads), smem, st, "tc_conv_kernel", p);
 }
