@@ -255,26 +255,31 @@ constexpr int kGsStages = 4;
 template <int C, int NP, bool SKIP, bool PP>
 __global__ void __launch_bounds__(kGsThreads, 1) gate_strips_kernel(
     const float* __restrict__ gap, int items, const float* __restrict__ eca_w, int k,
-    const float* __restrict__ x, PlBuf skip, PlBuf out_pl, PlBuf out_pp, int H, int W, uint32_t W_mul, int R,
-    int64_t B, uint32_t x_bytes, uint32_t stage_bytes) {
+    const float* __restrict__ x, PlBuf skip, PlBuf out_pl, PlBuf out_pp, int H, int W, int TW, uint32_t TW_mul,
+    int R, int64_t B, uint32_t x_bytes, uint32_t stage_bytes, int stages) {
   using namespace ptx;
   constexpr int G8 = C / 8;
   constexpr int nblk = (C / 16) * NP * 2;
   static_assert(kGsCompute % G8 == 0, "one channel group per thread");
   extern __shared__ __align__(128) uint8_t gsm[];
-  float* gate = reinterpret_cast<float*>(gsm + (size_t)kGsStages * stage_bytes);  // [C]
+  float* gate = reinterpret_cast<float*>(gsm + (size_t)stages * stage_bytes);  // [C]
   float* part = gate + C;  // [kEcaGroups][C] group sums, then [C] means
   uint64_t* full = reinterpret_cast<uint64_t*>(part + (kEcaGroups + 1) * C);
-  uint64_t* empty = full + kGsStages;
+  uint64_t* empty = full + stages;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int L = W + 1, Lp = W / 2 + 1;
-  const uint32_t sk_blk = (uint32_t)R * L * 16;
-  const int spi = H / R;
+  // a strip is R rows x TW columns; whole-width strips stage the skip rows with their pad
+  // column (one contiguous range per block), column tiles stage TW positions per row
+  const bool whole = TW == W;
+  const int Ls = whole ? L : TW;
+  const uint32_t sk_blk = (uint32_t)R * Ls * 16;
+  const int tpr = W / TW;  // column tiles per row band
+  const int spi = (H / R) * tpr;
   const int64_t n_strips = B * spi;
   const int64_t s_begin = blockIdx.x * n_strips / gridDim.x;
   const int64_t s_end = (blockIdx.x + 1) * n_strips / gridDim.x;
   if (tid == 0) {
-    for (int s = 0; s < kGsStages; ++s) {
+    for (int s = 0; s < stages; ++s) {
       mbar_init(smem_u32(&full[s]), 1);
       mbar_init(smem_u32(&empty[s]), kGsCompute / 32);
     }
@@ -285,24 +290,35 @@ __global__ void __launch_bounds__(kGsThreads, 1) gate_strips_kernel(
 
   if (warp == kGsCompute / 32) {
     // ===== producer warp: lane 0 posts the byte count, lanes issue one copy each =====
-    constexpr int ncopy = 1 + (SKIP ? nblk : 0);
-    int i = 0;
+    // (whole-width strips: one range per tensor / block; column tiles: one per row)
+    constexpr int nk = 1 + (SKIP ? nblk : 0);
+    const int ncopy = whole ? nk : R * nk;
+    int i = 0, st = 0;
+    uint32_t ph = 0;
     for (int64_t s = s_begin; s < s_end; ++s, ++i) {
-      const int st = i % kGsStages;
-      mbar_wait(smem_u32(&empty[st]), ((i / kGsStages) & 1) ^ 1);
+      mbar_wait(smem_u32(&empty[st]), ph ^ 1);
       const int64_t b = s / spi;
-      const int y0 = (int)(s - b * spi) * R;
+      const int rem = (int)(s - b * spi);
+      const int y0 = (rem / tpr) * R, x0 = (rem - (rem / tpr) * tpr) * TW;
       const uint32_t bar = smem_u32(&full[st]);
       uint8_t* base = gsm + (size_t)st * stage_bytes;
       if (lane == 0) mbar_arrive_expect_tx(bar, x_bytes + (SKIP ? nblk * sk_blk : 0u));
       __syncwarp();
       for (int c = lane; c < ncopy; c += 32) {
-        if (c == 0)
-          bulk_g2s(smem_u32(base), x + ((size_t)b * H + y0) * W * C, x_bytes, bar);
+        const int r = whole ? 0 : c / nk, kk = whole ? c : c - r * nk;
+        const int nr = whole ? R : 1;
+        if (kk == 0)
+          bulk_g2s(smem_u32(base + (size_t)r * TW * C * 4), x + (((size_t)b * H + y0 + r) * W + x0) * C,
+                   (uint32_t)nr * TW * C * 4, bar);
         else
-          bulk_g2s(smem_u32(base + x_bytes + (size_t)(c - 1) * sk_blk),
-                   skip.base + b * skip.img_stride + ((size_t)(c - 1) * skip.Q + (size_t)y0 * L + skip.off) * 8,
-                   sk_blk, bar);
+          bulk_g2s(smem_u32(base + x_bytes + (size_t)(kk - 1) * sk_blk + (size_t)r * Ls * 16),
+                   skip.base + b * skip.img_stride +
+                       ((size_t)(kk - 1) * skip.Q + (size_t)(y0 + r) * L + x0 + skip.off) * 8,
+                   (uint32_t)nr * Ls * 16, bar);
+      }
+      if (++st == stages) {
+        st = 0;
+        ph ^= 1u;
       }
     }
     return;
@@ -315,12 +331,13 @@ __global__ void __launch_bounds__(kGsThreads, 1) gate_strips_kernel(
   const size_t pp_blk = PP ? ((size_t)kh * out_pp.Q + out_pp.off) * 8 : 0;
   const size_t pl_lo = (size_t)2 * out_pl.Q * 8, pp_lo = PP ? (size_t)2 * out_pp.Q * 8 : 0;
   int64_t cur_b = -1;
-  int i = 0;
+  int st = 0;
+  uint32_t ph = 0;
   float g8[8];
-  for (int64_t s = s_begin; s < s_end; ++s, ++i) {
-    const int st = i % kGsStages;
+  for (int64_t s = s_begin; s < s_end; ++s) {
     const int64_t b = s / spi;
-    const int y0 = (int)(s - b * spi) * R;
+    const int rem = (int)(s - b * spi);
+    const int y0 = (rem / tpr) * R, x0 = (rem - (rem / tpr) * tpr) * TW;
     if (b != cur_b) {
       if (items == kGatesReady) {
         asm volatile("bar.sync 1, %0;" ::"n"(kGsCompute) : "memory");  // previous image's gate readers
@@ -345,24 +362,24 @@ __global__ void __launch_bounds__(kGsThreads, 1) gate_strips_kernel(
       for (int j = 0; j < 8; ++j) g8[j] = gate[c8 * 8 + j];
       cur_b = b;
     }
-    if (y0 == 0) {  // top / bottom margins of the output planes, once per image
+    if (y0 == 0 && x0 == 0) {  // top / bottom margins of the output planes, once per image
       pl_zero_margins(out_pl, b, tid, kGsCompute);
       if (PP) pl_zero_margins(out_pp, b, tid, kGsCompute);
     }
-    mbar_wait(smem_u32(&full[st]), (i / kGsStages) & 1);
+    mbar_wait(smem_u32(&full[st]), ph);
     const float* xs = reinterpret_cast<const float*>(gsm + (size_t)st * stage_bytes);
     const uint8_t* sk = gsm + (size_t)st * stage_bytes + x_bytes;
     uint16_t* opl = out_pl.base + b * out_pl.img_stride + pl_blk;
     uint16_t* opp = PP ? out_pp.base + b * out_pp.img_stride + pp_blk : nullptr;
 #pragma unroll 2
-    for (int pix = tid / G8; pix < R * W; pix += kGsCompute / G8) {
-      const int r = (int)__umulhi((uint32_t)pix, W_mul), xx = pix - r * W;
+    for (int pix = tid / G8; pix < R * TW; pix += kGsCompute / G8) {
+      const int r = (int)__umulhi((uint32_t)pix, TW_mul), xl = pix - r * TW, xx = x0 + xl;
       const float4 a0 = *reinterpret_cast<const float4*>(xs + (size_t)pix * C + c8 * 8);
       const float4 a1 = *reinterpret_cast<const float4*>(xs + (size_t)pix * C + c8 * 8 + 4);
       const float xv[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
       float v[8];
       if (SKIP) {  // + skip (model.py:197-198), exact hi + lo of its plane
-        const size_t so = (size_t)(r * L + xx) * 16;
+        const size_t so = (size_t)(r * Ls + xl) * 16;
         const uint4 h = *reinterpret_cast<const uint4*>(sk + (size_t)kh * sk_blk + so);
         const uint32_t hw[4] = {h.x, h.y, h.z, h.w};
         float sk8[8];
@@ -407,6 +424,10 @@ __global__ void __launch_bounds__(kGsThreads, 1) gate_strips_kernel(
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(smem_u32(&empty[st]));  // this warp is done with stage st
+    if (++st == stages) {
+      st = 0;
+      ph ^= 1u;
+    }
   }
 }
 
@@ -454,36 +475,41 @@ void launch_gate_apply(const float* gap, int items, const float* eca_w, int k, c
   }();
   if (!strips_off && out_f32 == nullptr && out_pl != nullptr && C % 16 == 0 && C <= 128 && H % 2 == 0 &&
       W % 2 == 0 && B > 0) {
-    // persistent strips: R rows (even, dividing H) with a stage of about 32 KB
+    // persistent strips: R rows (even, dividing H) x TW columns; whole-width strips unless
+    // kGsStages of them do not fit shared memory (large maps: column tiles, per-row copies)
     const int np = out_pl->np, nblk = (C / 16) * np * 2, L = W + 1;
-    auto stage = [&](int r) {
-      return (size_t)r * W * C * 4 + (skip ? (size_t)nblk * r * L * 16 : 0);
+    auto stage = [&](int r, int tw) {
+      return (size_t)r * tw * C * 4 + (skip ? (size_t)nblk * r * (tw == W ? L : tw) * 16 : 0);
     };
     static const size_t stage_cap = [] {  // env STDA_GATE_STAGE_KB (A/B timing), default 16
       const char* e = std::getenv("STDA_GATE_STAGE_KB");
       return (size_t)(e ? std::max(8, std::atoi(e)) : 16) * 1024;  // measured best of 16/32/48
     }();
+    const size_t fixed = (size_t)(kEcaGroups + 2) * C * 4 + 2 * kGsStages * 8;
+    auto smem_of = [&](size_t sb) { return kGsStages * ((sb + 127) / 128 * 128) + fixed; };
+    int TW = W;
+    while (smem_of(stage(2, TW)) > 227 * 1024 && TW % 2 == 0 && TW / 2 >= 16) TW /= 2;
     int R = 2;
-    while (R * 2 <= 16 && H % (R * 2) == 0 && stage(R * 2) <= stage_cap) R *= 2;
-    const size_t stage_bytes = (stage(R) + 127) / 128 * 128;
-    const size_t smem = kGsStages * stage_bytes + (size_t)(kEcaGroups + 2) * C * 4 + 2 * kGsStages * 8;
+    while (R * 2 <= 16 && H % (R * 2) == 0 && stage(R * 2, TW) <= stage_cap) R *= 2;
+    const size_t stage_bytes = (stage(R, TW) + 127) / 128 * 128;
+    const size_t smem = smem_of(stage(R, TW));
     int dev = 0, sms = 148;
     STDA_CUDA(cudaGetDevice(&dev));
     STDA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int64_t n_strips = B * (H / R) * (W / TW);
     // measured: with fewer than ~4 strips per SM the per-CTA fill (first loads + gate)
     // dominates and the one-shot row-block kernel is faster
-    if (H % R == 0 && smem <= 227 * 1024 && B * (H / R) >= 4 * (int64_t)sms) {
-      const int64_t n_strips = B * (H / R);
+    if (H % R == 0 && smem <= 227 * 1024 && n_strips >= 4 * (int64_t)sms) {
       const unsigned grid = (unsigned)std::min<int64_t>(n_strips, sms);
-      const uint32_t W_mul = (uint32_t)((((uint64_t)1 << 32) + (uint64_t)W - 1) / (uint64_t)W);
-      STDA_CHECK((uint64_t)R * W * W < ((uint64_t)1 << 32), "gate strips: row index");
+      const uint32_t TW_mul = (uint32_t)((((uint64_t)1 << 32) + (uint64_t)TW - 1) / (uint64_t)TW);
+      STDA_CHECK((uint64_t)R * TW * TW < ((uint64_t)1 << 32), "gate strips: row index");
       auto go = [&](auto cc, auto npc, auto skc, auto ppc) {
         const auto kern = gate_strips_kernel<decltype(cc)::value, decltype(npc)::value, decltype(skc)::value,
                                              decltype(ppc)::value>;
         ensure_dyn_smem(kern, 227 * 1024);
         launch_pdl(kern, dim3(grid), dim3(kGsThreads), smem, st, "gate_strips_kernel", gap, items, eca_w, k, x,
-                   skip ? *skip : PlBuf{}, *out_pl, out_pp ? *out_pp : PlBuf{}, H, W, W_mul, R, B,
-                   (uint32_t)((size_t)R * W * C * 4), (uint32_t)stage_bytes);
+                   skip ? *skip : PlBuf{}, *out_pl, out_pp ? *out_pp : PlBuf{}, H, W, TW, TW_mul, R, B,
+                   (uint32_t)((size_t)R * TW * C * 4), (uint32_t)stage_bytes, kGsStages);
       };
       using std::integral_constant;
       auto g3 = [&](auto cc, auto npc) {

@@ -80,6 +80,24 @@ def test_batch_invariance_across_gate_kernels():
     assert torch.equal(full, slices)
 
 
+@pytest.mark.parametrize("hw,batch,step", [(256, 12, 3), (512, 3, 1)])
+def test_wide_map_strip_tiles(hw, batch, step):
+    """Wide maps cut the persistent gate / head strips into column tiles (per-row copies,
+    halo columns): bitwise equal to small-batch slices that run the one-shot row-block gates,
+    and within tolerance of the oracle."""
+    from oracle import port
+    from tests._helpers import CONFIG_FIELDS, nmax_err
+    net = StdaNet(StdaConfig(map_height=hw, map_width=hw)).eval().cuda()
+    x = synth_triplets(batch, hw, hw, seed=13, scene="dense" if hw == 512 else "default")
+    full = net(x)
+    slices = torch.cat([net(x[i:i + step]) for i in range(0, batch, step)])
+    assert torch.equal(full, slices)
+    sd = {k: v.detach().cpu() for k, v in net.state_dict().items()}
+    cfg = {f: getattr(net.config, f) for f in CONFIG_FIELDS}
+    ref = port.forward_batched(sd, cfg, x[:1].cpu()).numpy()
+    assert nmax_err(full[:1].cpu().numpy(), ref) <= 1e-4
+
+
 def test_c4_stream_at_128():
     """BASELINE config 4 semantics at its map size: a coherent stream's
     sliding windows equal independent per-triplet forwards bitwise, a G=3 time split with
