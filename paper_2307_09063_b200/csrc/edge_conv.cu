@@ -501,34 +501,32 @@ __global__ void __launch_bounds__(kRowThreads, 4) stem_const_kernel(const __grid
   }
 }
 
-// ---- persistent strip head (C0 = 16) ---------------------------------------------------
-// One CTA per SM walks a contiguous range of strips (R = 512 / TW rows x TW columns, TW =
-// min(W, 128): wide maps are cut into column tiles; an image's ECA gate is computed once
-// per CTA-image, halo rows/columns of neighbouring strips hit L2).  A producer warp
-// bulk-copies, per staged row y0-1 .. y0+R, the row segment x0-1 .. x0+TW of d (NHWC fp32,
-// in-image columns only) and of each skip-plane block (the plane's pad column / top margin
-// supply the zero borders) into a 2-stage ring — lanes issue the copies in parallel — so
-// strip i+1 is in flight while the 8 compute warps transform and convolve strip i.
-// u = d * gate + skip is formed in place over d (zero outside the image), channel quad j of
-// stage pixel p stored at quad slot j ^ ((p >> 1) & 3): the conv's float4 reads of 8
-// consecutive pixels then hit 8 distinct 16-byte bank groups.  Each compute thread
-// produces 2 output rows of one column.
+// ---- persistent strip head (C0 = 16, W in {32, 64, 128}) ------------------------------
+// One CTA per SM walks a contiguous range of strips (R = 512 / W rows x W columns; an
+// image's ECA gate is computed once per CTA-image, halo rows of neighbouring strips hit
+// L2).  A producer warp bulk-copies rows y0-1 .. y0+R of d (NHWC fp32: one contiguous
+// range) and of the skip plane (per (pass, cg8) block one contiguous range of rows with
+// their zero pad column) into a 2-stage ring, so strip i+1 is in flight while the 8
+// compute warps transform and convolve strip i.  u = d * gate + skip is formed in place
+// over d, channel quad j of stage pixel p stored at quad slot j ^ ((p >> 1) & 3): the
+// conv's float4 reads of 8 consecutive pixels then hit 8 distinct 16-byte bank groups.
+// Each compute thread produces 2 output rows of one column.
 constexpr int kHsCompute = 256;              // 8 compute warps
 constexpr int kHsThreads = kHsCompute + 32;  // + producer warp
 constexpr int kHsC = 16;
 
 struct HeadStrips {
-  int R, SR, SW, dbytes, sblk, stage;  // rows, staged rows / columns, d / skip-block / stage bytes
+  int R, SR, L, dbytes, sblk, stage;  // rows, staged rows, plane row stride, d / skip-block / stage bytes
   size_t smem;
 };
 
-__host__ __device__ constexpr HeadStrips head_strips_geom(int TW) {
+__host__ __device__ constexpr HeadStrips head_strips_geom(int W) {
   HeadStrips g{};
-  g.R = 2 * kHsCompute / TW;
+  g.R = 2 * kHsCompute / W;
   g.SR = g.R + 2;
-  g.SW = TW + 2;
-  g.dbytes = g.SR * g.SW * kHsC * 4;
-  g.sblk = g.SR * g.SW * 16;
+  g.L = W + 1;
+  g.dbytes = g.SR * W * kHsC * 4;
+  g.sblk = g.SR * g.L * 16;
   g.stage = g.dbytes + 4 * g.sblk;
   g.smem = 2 * (size_t)g.stage + (9 * kHsC + kHsC + 16 * kHsC + kHsC) * 4 + 4 * 8;
   return g;
@@ -540,14 +538,234 @@ struct HeadConst {
   float w[9 * kHsC];  // [tap][channel]: read by the conv from the kernel-parameter bank
 };
 
-template <int TW>
+template <int W>
 __global__ void __launch_bounds__(kHsThreads, 1) head_strips_kernel(
+    const __grid_constant__ HeadConst cw, const float* __restrict__ bias, const float* __restrict__ gap, int items,
+    const float* __restrict__ eca_w, int k, const float* __restrict__ d, PlBuf skip, float* __restrict__ y,
+    int64_t B, int H, int bf16) {
+  using namespace ptx;
+  extern __shared__ __align__(128) uint8_t hsm[];
+  constexpr HeadStrips g = head_strips_geom(W);
+  constexpr int R = g.R, SR = g.SR, L = g.L;
+  float* ws = reinterpret_cast<float*>(hsm + 2 * (size_t)g.stage);  // [9][16]
+  float* gate = ws + 9 * kHsC;                                       // [16]
+  float* part = gate + kHsC;                                         // [16 groups][16]
+  float* mean = part + 16 * kHsC;                                    // [16]
+  uint64_t* full = reinterpret_cast<uint64_t*>(mean + kHsC);         // [2]
+  uint64_t* empty = full + 2;                                        // [2]
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int spi = H / R;  // strips per image
+  const int64_t n_strips = B * spi;
+  const int64_t s_begin = blockIdx.x * n_strips / gridDim.x;
+  const int64_t s_end = (blockIdx.x + 1) * n_strips / gridDim.x;
+  const int np = skip.np;
+
+  if (tid == 0) {
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&empty[s]), kHsCompute / 32);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  grid_dep_wait();  // d, gap and skip come from the previous kernels
+
+  if (warp == kHsCompute / 32) {
+    // ===== producer warp: one bulk copy per tensor (and skip block) per strip =====
+    if ((tid & 31) == 0) {
+      int i = 0;
+      for (int64_t s = s_begin; s < s_end; ++s, ++i) {
+        const int st = i & 1;
+        mbar_wait(smem_u32(&empty[st]), ((i >> 1) & 1) ^ 1);
+        const int64_t b = s / spi;
+        const int y0 = (int)(s - b * spi) * R;
+        const int r0 = y0 == 0 ? 1 : 0;                // first staged row inside the image
+        const int r1 = y0 + R == H ? SR - 1 : SR;      // one past the last
+        const int nr = r1 - r0, iy0 = y0 - 1 + r0;
+        const uint32_t bar = smem_u32(&full[st]);
+        uint8_t* base = hsm + (size_t)st * g.stage;
+        mbar_arrive_expect_tx(bar, (uint32_t)(nr * W * kHsC * 4 + np * 2 * nr * L * 16));
+        bulk_g2s(smem_u32(base + (size_t)r0 * W * kHsC * 4), d + ((size_t)b * H + iy0) * W * kHsC,
+                 (uint32_t)(nr * W * kHsC * 4), bar);
+        const uint16_t* simg = skip.base + b * skip.img_stride;
+        for (int pass = 0; pass < np; ++pass)
+          for (int cg8 = 0; cg8 < 2; ++cg8)
+            bulk_g2s(smem_u32(base + g.dbytes + (size_t)(pass * 2 + cg8) * g.sblk + (size_t)r0 * L * 16),
+                     simg + (skip.block_index(0, pass, cg8) + skip.off + (size_t)iy0 * L) * 8,
+                     (uint32_t)(nr * L * 16), bar);
+      }
+    }
+    return;
+  }
+
+  // ===== 8 compute warps =====
+  const float bv = __ldg(bias);
+  const int cx = tid % W, rp = tid / W;  // conv: column, row pair
+  int64_t cur_b = -1;
+  int i = 0;
+  for (int64_t s = s_begin; s < s_end; ++s, ++i) {
+    const int st = i & 1;
+    const int64_t b = s / spi;
+    const int y0 = (int)(s - b * spi) * R;
+    if (b != cur_b && items == kGatesReady) {
+      asm volatile("bar.sync 1, %0;" ::"n"(kHsCompute) : "memory");  // previous image's gate readers
+      if (tid < kHsC) gate[tid] = __ldg(gap + b * kHsC + tid);
+      asm volatile("bar.sync 1, %0;" ::"n"(kHsCompute) : "memory");
+      cur_b = b;
+    } else if (b != cur_b) {
+      // ECA gate of image b (model.py:128-135): kEcaGroups group sums in parallel, added
+      // in group order (planes.cuh: the one reduction order of every gate)
+      if (tid < kEcaGroups * kHsC) part[tid] = eca_group_sum(gap, items, kHsC, b, tid % kHsC, tid / kHsC);
+      asm volatile("bar.sync 1, %0;" ::"n"(kHsCompute) : "memory");
+      if (tid < kHsC) {
+        float a = 0.f;
+        for (int grp = 0; grp < kEcaGroups; ++grp) a += part[grp * kHsC + tid];
+        mean[tid] = a / (float)(H * W);
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(kHsCompute) : "memory");
+      if (tid < kHsC) gate[tid] = eca_gate_of(mean, kHsC, tid, eca_w, k);
+      asm volatile("bar.sync 1, %0;" ::"n"(kHsCompute) : "memory");
+      cur_b = b;
+    }
+    mbar_wait(smem_u32(&full[st]), (i >> 1) & 1);
+    float* ubase = reinterpret_cast<float*>(hsm + (size_t)st * g.stage);
+    const uint8_t* sbase = hsm + (size_t)st * g.stage + g.dbytes;
+    // transform: one (stage pixel, channel quad) per thread step, NB steps per batch: all
+    // loads of a batch, one __syncwarp (the 4 quads of a pixel are lanes of one warp and
+    // are rewritten in place; steps touch disjoint pixels), then all stores
+    constexpr int NIT = SR * W * 4 / kHsCompute;
+    static_assert(NIT * kHsCompute == SR * W * 4, "transform steps");
+    constexpr int NB = NIT % 4 == 0 ? 4 : NIT % 3 == 0 ? 3 : 2;
+    static_assert(NIT % NB == 0, "transform batches");
+    const int q = tid & 3;
+    const float4 g4 = *reinterpret_cast<const float4*>(gate + q * 4);
+#pragma unroll
+    for (int it0 = 0; it0 < NIT; it0 += NB) {
+      float4 dv[NB];
+      uint2 hv[NB], lv[NB];
+      bool in[NB];
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        const int p = ((it0 + j) * kHsCompute + tid) >> 2;
+        const int r = p / W, x = p - r * W;
+        const int iy = y0 - 1 + r;
+        in[j] = iy >= 0 && iy < H;
+        dv[j] = *reinterpret_cast<const float4*>(ubase + p * kHsC + q * 4);
+        // channels 4q..4q+3: cg8 block (q >> 1), bytes (q & 1) * 8 of position r*L + x
+        const size_t so = (size_t)(r * L + x) * 16 + (q & 1) * 8;
+        hv[j] = *reinterpret_cast<const uint2*>(sbase + (size_t)(q >> 1) * g.sblk + so);
+        lv[j] = np == 2 ? *reinterpret_cast<const uint2*>(sbase + (size_t)(2 + (q >> 1)) * g.sblk + so)
+                        : make_uint2(0u, 0u);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        const int p = ((it0 + j) * kHsCompute + tid) >> 2;
+        float4 u = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (in[j]) {
+          float s4[4];
+          s4[0] = __uint_as_float(hv[j].x << 16);
+          s4[1] = __uint_as_float(hv[j].x & 0xFFFF0000u);
+          s4[2] = __uint_as_float(hv[j].y << 16);
+          s4[3] = __uint_as_float(hv[j].y & 0xFFFF0000u);
+          if (np == 2) {
+            s4[0] += __uint_as_float(lv[j].x << 16);
+            s4[1] += __uint_as_float(lv[j].x & 0xFFFF0000u);
+            s4[2] += __uint_as_float(lv[j].y << 16);
+            s4[3] += __uint_as_float(lv[j].y & 0xFFFF0000u);
+          }
+          u.x = gate_fma(dv[j].x, g4.x, s4[0]);  // eca(d) + skip (model.py:197-198)
+          u.y = gate_fma(dv[j].y, g4.y, s4[1]);
+          u.z = gate_fma(dv[j].z, g4.z, s4[2]);
+          u.w = gate_fma(dv[j].w, g4.w, s4[3]);
+          if (bf16) {
+            u.x = bf16_round(u.x);
+            u.y = bf16_round(u.y);
+            u.z = bf16_round(u.z);
+            u.w = bf16_round(u.w);
+          }
+        }
+        *reinterpret_cast<float4*>(ubase + p * kHsC + (q ^ hs_swz(p)) * 4) = u;
+      }
+    }
+    fence_proxy_async();  // generic writes of this stage before its next async refill
+    asm volatile("bar.sync 1, %0;" ::"n"(kHsCompute) : "memory");
+    // conv3x3 (model.py:158,199): rows 2rp, 2rp+1 of the strip at column cx
+    // 4 independent chains per output (channel quads j), summed at the end
+    float acc0[4] = {0.f, 0.f, 0.f, 0.f}, acc1[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int kx = 0; kx < 3; ++kx) {
+      const int xx = cx + kx - 1;
+      const bool in = xx >= 0 && xx < W;
+      float4 u[4][4];  // [channel quad][row]: all loads of this column first
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int rr = 0; rr < 4; ++rr) {
+          const int p = (2 * rp + rr) * W + (in ? xx : 0);
+          u[j][rr] = *reinterpret_cast<const float4*>(ubase + p * kHsC + (j ^ hs_swz(p)) * 4);
+          if (!in) u[j][rr] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int ky = 0; ky < 3; ++ky) {
+          const float* wt = &cw.w[(ky * 3 + kx) * kHsC + j * 4];
+          acc0[j] = fmaf(u[j][ky].x, wt[0], acc0[j]);
+          acc0[j] = fmaf(u[j][ky].y, wt[1], acc0[j]);
+          acc0[j] = fmaf(u[j][ky].z, wt[2], acc0[j]);
+          acc0[j] = fmaf(u[j][ky].w, wt[3], acc0[j]);
+          acc1[j] = fmaf(u[j][ky + 1].x, wt[0], acc1[j]);
+          acc1[j] = fmaf(u[j][ky + 1].y, wt[1], acc1[j]);
+          acc1[j] = fmaf(u[j][ky + 1].z, wt[2], acc1[j]);
+          acc1[j] = fmaf(u[j][ky + 1].w, wt[3], acc1[j]);
+        }
+    }
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive(smem_u32(&empty[st]));  // this warp is done with stage st
+    float* yo = y + ((size_t)b * H + y0 + 2 * rp) * W + cx;
+    yo[0] = ((acc0[0] + acc0[1]) + (acc0[2] + acc0[3])) + bv;
+    yo[W] = ((acc1[0] + acc1[1]) + (acc1[2] + acc1[3])) + bv;
+  }
+}
+
+// ---- column-tiled strip head (C0 = 16, W a multiple of 128 above 128) -----------------
+// One CTA per SM walks a contiguous range of strips (R = 512 / TW rows x TW columns, TW =
+// min(W, 128): wide maps are cut into column tiles; an image's ECA gate is computed once
+// per CTA-image, halo rows/columns of neighbouring strips hit L2).  A producer warp
+// bulk-copies, per staged row y0-1 .. y0+R, the row segment x0-1 .. x0+TW of d (NHWC fp32,
+// in-image columns only) and of each skip-plane block (the plane's pad column / top margin
+// supply the zero borders) into a 2-stage ring — lanes issue the copies in parallel — so
+// strip i+1 is in flight while the 8 compute warps transform and convolve strip i.
+// u = d * gate + skip is formed in place over d (zero outside the image), channel quad j of
+// stage pixel p stored at quad slot j ^ ((p >> 1) & 3): the conv's float4 reads of 8
+// consecutive pixels then hit 8 distinct 16-byte bank groups.  Each compute thread
+// produces 2 output rows of one column.
+struct HeadTiles {
+  int R, SR, SW, dbytes, sblk, stage;  // rows, staged rows / columns, d / skip-block / stage bytes
+  size_t smem;
+};
+
+__host__ __device__ constexpr HeadTiles head_tiles_geom(int TW) {
+  HeadTiles g{};
+  g.R = 2 * kHsCompute / TW;
+  g.SR = g.R + 2;
+  g.SW = TW + 2;
+  g.dbytes = g.SR * g.SW * kHsC * 4;
+  g.sblk = g.SR * g.SW * 16;
+  g.stage = g.dbytes + 4 * g.sblk;
+  g.smem = 2 * (size_t)g.stage + (9 * kHsC + kHsC + 16 * kHsC + kHsC) * 4 + 4 * 8;
+  return g;
+}
+
+template <int TW>
+__global__ void __launch_bounds__(kHsThreads, 1) head_tiles_kernel(
     const __grid_constant__ HeadConst cw, const float* __restrict__ bias, const float* __restrict__ gap, int items,
     const float* __restrict__ eca_w, int k, const float* __restrict__ d, PlBuf skip, float* __restrict__ y,
     int64_t B, int H, int W, int bf16) {
   using namespace ptx;
   extern __shared__ __align__(128) uint8_t hsm[];
-  constexpr HeadStrips g = head_strips_geom(TW);
+  constexpr HeadTiles g = head_tiles_geom(TW);
   constexpr int R = g.R, SR = g.SR, SW = g.SW;
   float* ws = reinterpret_cast<float*>(hsm + 2 * (size_t)g.stage);  // [9][16]
   float* gate = ws + 9 * kHsC;                                       // [16]
@@ -743,13 +961,14 @@ __global__ void __launch_bounds__(kHsThreads, 1) head_strips_kernel(
   }
 }
 
-int head_tile_w(int W) { return W >= 128 ? 128 : W; }
-
 bool head_strips_ok(int C0, int64_t B, int H, int W) {
-  const int TW = head_tile_w(W);
-  if (C0 != kHsC || (TW != 32 && TW != 64 && TW != 128) || W % TW != 0 || B <= 0) return false;
-  const HeadStrips g = head_strips_geom(TW);
-  return H % g.R == 0 && g.smem <= 227 * 1024;
+  if (C0 != kHsC || B <= 0) return false;
+  if (W == 32 || W == 64 || W == 128) {
+    const HeadStrips g = head_strips_geom(W);
+    return H % g.R == 0 && g.smem <= 227 * 1024;
+  }
+  const HeadTiles g = head_tiles_geom(128);  // wide maps: 128-column tiles
+  return W % 128 == 0 && H % g.R == 0 && g.smem <= 227 * 1024;
 }
 
 template <typename K>
@@ -847,18 +1066,27 @@ void launch_head_fused(const float* w, const float* bias, const float* gap, int 
     int dev = 0, sms = 148;
     STDA_CUDA(cudaGetDevice(&dev));
     STDA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const int TW = head_tile_w(W);
-    const HeadStrips g = head_strips_geom(TW);
-    const int64_t n_strips = B * (H / g.R) * (W / TW);
+    if (W > 128) {  // column tiles
+      const HeadTiles g = head_tiles_geom(128);
+      const int64_t n_strips = B * (H / g.R) * (W / 128);
+      const unsigned grid = (unsigned)std::min<int64_t>(n_strips, sms);
+      const auto kern = head_tiles_kernel<128>;
+      ensure_dyn_smem(kern, 227 * 1024);
+      launch_pdl(kern, dim3(grid), dim3(kHsThreads), g.smem, st, "head_tiles_kernel", hc, bias, gap, items, eca_w, k,
+                 d, skip, y, B, H, W, (int)bf16);
+      return;
+    }
+    const HeadStrips g = head_strips_geom(W);
+    const int64_t n_strips = B * (H / g.R);
     const unsigned grid = (unsigned)std::min<int64_t>(n_strips, sms);
     auto go = [&](auto wc) {
       const auto kern = head_strips_kernel<decltype(wc)::value>;
       ensure_dyn_smem(kern, 227 * 1024);
       launch_pdl(kern, dim3(grid), dim3(kHsThreads), g.smem, st, "head_strips_kernel", hc, bias, gap, items, eca_w,
-                 k, d, skip, y, B, H, W, (int)bf16);
+                 k, d, skip, y, B, H, (int)bf16);
     };
-    if (TW == 32) go(std::integral_constant<int, 32>{});
-    else if (TW == 64) go(std::integral_constant<int, 64>{});
+    if (W == 32) go(std::integral_constant<int, 32>{});
+    else if (W == 64) go(std::integral_constant<int, 64>{});
     else go(std::integral_constant<int, 128>{});
     return;
   }

@@ -252,11 +252,12 @@ constexpr int kGsStages = 4;
 // Compile-time channel count / passes / skip / phase-plane output: the unit loop has no
 // runtime division and each thread keeps one 8-channel group (kGsCompute % (C / 8) == 0),
 // so its plane block offsets are loop-invariant.
-template <int C, int NP, bool SKIP, bool PP>
+template <int C, int NP, bool SKIP, bool PP, bool WHOLE>
 __global__ void __launch_bounds__(kGsThreads, 1) gate_strips_kernel(
     const float* __restrict__ gap, int items, const float* __restrict__ eca_w, int k,
     const float* __restrict__ x, PlBuf skip, PlBuf out_pl, PlBuf out_pp, int H, int W, int TW, uint32_t TW_mul,
-    int R, int64_t B, uint32_t x_bytes, uint32_t stage_bytes, int stages) {
+    int R, int64_t B, uint32_t x_bytes, uint32_t stage_bytes) {
+  constexpr int stages = kGsStages;
   using namespace ptx;
   constexpr int G8 = C / 8;
   constexpr int nblk = (C / 16) * NP * 2;
@@ -270,10 +271,10 @@ __global__ void __launch_bounds__(kGsThreads, 1) gate_strips_kernel(
   const int L = W + 1, Lp = W / 2 + 1;
   // a strip is R rows x TW columns; whole-width strips stage the skip rows with their pad
   // column (one contiguous range per block), column tiles stage TW positions per row
-  const bool whole = TW == W;
+  constexpr bool whole = WHOLE;  // TW == W
   const int Ls = whole ? L : TW;
   const uint32_t sk_blk = (uint32_t)R * Ls * 16;
-  const int tpr = W / TW;  // column tiles per row band
+  const int tpr = WHOLE ? 1 : W / TW;  // column tiles per row band
   const int spi = (H / R) * tpr;
   const int64_t n_strips = B * spi;
   const int64_t s_begin = blockIdx.x * n_strips / gridDim.x;
@@ -299,7 +300,7 @@ __global__ void __launch_bounds__(kGsThreads, 1) gate_strips_kernel(
       mbar_wait(smem_u32(&empty[st]), ph ^ 1);
       const int64_t b = s / spi;
       const int rem = (int)(s - b * spi);
-      const int y0 = (rem / tpr) * R, x0 = (rem - (rem / tpr) * tpr) * TW;
+      const int y0 = (rem / tpr) * R, x0 = WHOLE ? 0 : (rem - (rem / tpr) * tpr) * TW;
       const uint32_t bar = smem_u32(&full[st]);
       uint8_t* base = gsm + (size_t)st * stage_bytes;
       if (lane == 0) mbar_arrive_expect_tx(bar, x_bytes + (SKIP ? nblk * sk_blk : 0u));
@@ -337,7 +338,7 @@ __global__ void __launch_bounds__(kGsThreads, 1) gate_strips_kernel(
   for (int64_t s = s_begin; s < s_end; ++s) {
     const int64_t b = s / spi;
     const int rem = (int)(s - b * spi);
-    const int y0 = (rem / tpr) * R, x0 = (rem - (rem / tpr) * tpr) * TW;
+    const int y0 = (rem / tpr) * R, x0 = WHOLE ? 0 : (rem - (rem / tpr) * tpr) * TW;
     if (b != cur_b) {
       if (items == kGatesReady) {
         asm volatile("bar.sync 1, %0;" ::"n"(kGsCompute) : "memory");  // previous image's gate readers
@@ -504,12 +505,14 @@ void launch_gate_apply(const float* gap, int items, const float* eca_w, int k, c
       const uint32_t TW_mul = (uint32_t)((((uint64_t)1 << 32) + (uint64_t)TW - 1) / (uint64_t)TW);
       STDA_CHECK((uint64_t)R * TW * TW < ((uint64_t)1 << 32), "gate strips: row index");
       auto go = [&](auto cc, auto npc, auto skc, auto ppc) {
-        const auto kern = gate_strips_kernel<decltype(cc)::value, decltype(npc)::value, decltype(skc)::value,
-                                             decltype(ppc)::value>;
+        const auto kern = TW == W ? gate_strips_kernel<decltype(cc)::value, decltype(npc)::value,
+                                                       decltype(skc)::value, decltype(ppc)::value, true>
+                                  : gate_strips_kernel<decltype(cc)::value, decltype(npc)::value,
+                                                       decltype(skc)::value, decltype(ppc)::value, false>;
         ensure_dyn_smem(kern, 227 * 1024);
         launch_pdl(kern, dim3(grid), dim3(kGsThreads), smem, st, "gate_strips_kernel", gap, items, eca_w, k, x,
                    skip ? *skip : PlBuf{}, *out_pl, out_pp ? *out_pp : PlBuf{}, H, W, TW, TW_mul, R, B,
-                   (uint32_t)((size_t)R * TW * C * 4), (uint32_t)stage_bytes, kGsStages);
+                   (uint32_t)((size_t)R * TW * C * 4), (uint32_t)stage_bytes);
       };
       using std::integral_constant;
       auto g3 = [&](auto cc, auto npc) {
