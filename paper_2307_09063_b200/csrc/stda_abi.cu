@@ -149,10 +149,10 @@ struct stda_plan {
 
   // tensor-core layer from canonical weights w0/b0 (+ w1/b1 for a dual stage)
   tc::TcLayerDesc make_tc(int mode, int cin, int cout, const float* w0, const float* b0,
-                          const float* w1, const float* b1) {
+                          const float* w1, const float* b1, int plane_w) {
     tc::TcLayerDesc d;
     std::vector<uint16_t> packed;
-    tc::tc_pack_layer(d, mode, cin, cout, w0, w1, bf16, packed);
+    tc::tc_pack_layer(d, mode, cin, cout, w0, w1, bf16, packed, plane_w);
     d.w = static_cast<const uint16_t*>(upload_bytes(packed.data(), packed.size() * 2));
     d.bias0 = upload(std::vector<float>(b0, b0 + cout));
     d.bias1 = w1 ? upload(std::vector<float>(b1, b1 + cout)) : nullptr;
@@ -531,8 +531,8 @@ int stda_plan_create(const stda_config* cfg, const float* blob, size_t n_floats,
       E.rs = p->make_layer(CONV3_S2, ch, 2 * ch, src);
       if (p->use_tc) {
         const size_t n1 = (size_t)ch * ch * 9, n2 = (size_t)2 * ch * ch * 9;
-        E.s1_tc = p->make_tc(CONV3_S1, ch, ch, w_s1, w_s1 + n1, nullptr, nullptr);
-        E.s2_tc = p->make_tc(CONV3_S2, ch, 2 * ch, w_dn, w_dn + n2, w_rs, w_rs + n2);
+        E.s1_tc = p->make_tc(CONV3_S1, ch, ch, w_s1, w_s1 + n1, nullptr, nullptr, cfg->map_width >> i);
+        E.s2_tc = p->make_tc(CONV3_S2, ch, 2 * ch, w_dn, w_dn + n2, w_rs, w_rs + n2, 0);
       }
       E.eca = p->make_vec(k, src);
       p->enc.push_back(E);
@@ -548,8 +548,8 @@ int stda_plan_create(const stda_config* cfg, const float* blob, size_t n_floats,
       D.rs = p->make_layer(CONVT4_S2, c2, ch, src);
       if (p->use_tc) {
         const size_t n1 = (size_t)c2 * c2 * 9, n2 = (size_t)ch * c2 * 16;
-        D.s1_tc = p->make_tc(CONV3_S1, c2, c2, w_s1, w_s1 + n1, nullptr, nullptr);
-        D.s2_tc = p->make_tc(CONVT4_S2, c2, ch, w_up, w_up + n2, w_rs, w_rs + n2);
+        D.s1_tc = p->make_tc(CONV3_S1, c2, c2, w_s1, w_s1 + n1, nullptr, nullptr, cfg->map_width >> (S - j));
+        D.s2_tc = p->make_tc(CONVT4_S2, c2, ch, w_up, w_up + n2, w_rs, w_rs + n2, 0);
       }
       D.eca = p->make_vec(k, src);
       p->dec.push_back(D);

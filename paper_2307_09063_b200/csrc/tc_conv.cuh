@@ -10,6 +10,8 @@
 //                         (py,px) + shift (oy,ox) in {-1,0}^2
 //   T   ConvT 4x4 s2 p1   A = input plane (PL), 4 output phases = 4 TMEM accumulators,
 //                         each a 2x2 sub-pixel kernel (shifts in {-1,0,1})
+//   ROWS 3x3 stride 1 over planes of width 128k: row bands, one A read per (input row, dx)
+//                         for three dy taps (tc_kernel.cuh kRowsSL)
 // Stage-2 blocks are dual: the block input (second source, own weights) feeds separate
 // accumulators; the epilogue forms relu(acc0 + b0) + (acc1 + b1).
 //
@@ -73,8 +75,10 @@ struct TcLayerDesc {
 };
 
 // Host: canonical fp32 weights (see include/stda_b200.h) -> descriptor + packed bf16.
+// plane_w = width of the input plane (stride-1 layers over widths that are multiples of 128
+// are packed for the row-band kernel, CONV3_ROWS); 0 = unknown.
 void tc_pack_layer(TcLayerDesc& d, int mode, int cin, int cout, const float* w0, const float* w1,
-                   bool bf16, std::vector<uint16_t>& packed);
+                   bool bf16, std::vector<uint16_t>& packed, int plane_w = 0);
 
 struct TcGeometry {
   int B, H, W;            // input grid

@@ -28,7 +28,7 @@ struct HostTap {
 
 std::vector<HostTap> plane_taps(int mode, int pl) {
   std::vector<HostTap> t;
-  if (mode == CONV3_S1) {
+  if (mode == CONV3_S1 || mode == CONV3_ROWS) {
     for (int ky = 0; ky < 3; ++ky)
       for (int kx = 0; kx < 3; ++kx) t.push_back({0, ky - 1, kx - 1, ky * 3 + kx});
   } else if (mode == CONV3_S2) {
@@ -79,10 +79,26 @@ bool tc_supported(int mode, int cin, int cout) {
   return cin % 16 == 0 && cin >= 16 && cin <= 64 && (cout == 16 || cout == 32 || cout == 64);
 }
 
+// env STDA_TC_ROWS=1: stride-1 layers over 128k-wide planes as row bands (CONV3_ROWS).
+// Measured off by default: it cuts the MMA stream per output 1.65x, but these layers are
+// bound by their operand fills and epilogue stores, not the MMA (enc0.s1 43.4 -> 45.4 us
+// at C2, 2.01 -> 2.21 ms at C3; profiles/r1_rows_ab.txt).
+bool rows_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("STDA_TC_ROWS");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 void tc_pack_layer(TcLayerDesc& d, int mode, int cin, int cout, const float* w0, const float* w1,
-                   bool bf16, std::vector<uint16_t>& packed) {
+                   bool bf16, std::vector<uint16_t>& packed, int plane_w) {
   STDA_CHECK(tc_supported(mode, cin, cout), "layer shape not supported by the tensor-core path");
   STDA_CHECK((mode == CONV3_S1) == (w1 == nullptr), "S1 layers are single-source, S2/T dual");
+  // stride-1 layers over planes whose width is a multiple of 128 run as row bands (one A
+  // read per input row serves three dy taps) when three stacked tap blocks fit one MMA
+  if (mode == CONV3_S1 && rows_enabled() && plane_w > 0 && plane_w % 128 == 0 && 3 * (bf16 ? 1 : 2) * cout <= 256)
+    mode = CONV3_ROWS;
   std::memset(&d, 0, sizeof(d));
   // A dual ConvT whose 8 accumulators cannot take the hi/lo N-concat in two TMEM slots
   // runs as CONVT4_HALF: one output-row parity per work item (4 accumulators), so the
@@ -136,6 +152,19 @@ void tc_pack_layer(TcLayerDesc& d, int mode, int cin, int cout, const float* w0,
     const float hi = bf16_val(v);
     packed.push_back(bf16_bits(pass == 0 ? v : v - hi));
   };
+  if (mode == CONV3_ROWS) {
+    // per chunk, per dx group: [kgrp 2][block dy = -1, 0, +1][pass hi(, lo)][cout][8]
+    for (int c = 0; c < n_chunks; ++c) {
+      for (int dx = -1; dx <= 1; ++dx)
+        for (int kg = 0; kg < 2; ++kg)
+          for (int dy = -1; dy <= 1; ++dy)
+            for (int pass = 0; pass < npassB; ++pass)
+              for (int n = 0; n < cout; ++n)
+                for (int e = 0; e < 8; ++e) put(ws[0], n, c * 16 + kg * 8 + e, (dy + 1) * 3 + (dx + 1), pass);
+      d.chunk_off[c + 1] = (int64_t)packed.size() * 2;
+    }
+    return;
+  }
   if (tmode && d.concat) {
     // shift groups (tc_kernel.cuh grouped_t): per (half, src, group) the stacked tiles
     // [kgrp 2][phase slot n][pass 2][cout][8]; zero tile for a phase not using the shift
@@ -244,6 +273,45 @@ TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W) {
   }
   const int n_acc = d.n_src * d.n_acc_src;
   const int npassA = d.npass == 3 ? 2 : 1;
+  if (d.mode == CONV3_ROWS) {
+    // row bands of T output rows x 128 columns: the largest T with two TMEM slots and a
+    // >= 2-deep ring, weights resident
+    STDA_CHECK(g.Wp % 128 == 0, "row-band conv: plane width must be a multiple of 128");
+    const int AW = d.cout * (d.concat ? 2 : 1);
+    const uint32_t w_total = (uint32_t)d.chunk_off[d.cin / 16];
+    const size_t fixed = 1024 + 80 + kEpiWarps * 64 * sizeof(float);
+    bool found = false;
+    static const int t_cap = [] {  // env STDA_TC_ROWS_T: largest rows per item (A/B timing)
+      const char* e = std::getenv("STDA_TC_ROWS_T");
+      return e ? std::atoi(e) : 8;
+    }();
+    for (int T : {8, 4, 2}) {
+      if (T > t_cap || g.Hp % T != 0 || T * AW * 2 > 512) continue;
+      const int P8 = ((T + 2) * kRowsSL + 7) / 8 * 8;
+      const uint32_t a_stage = (uint32_t)npassA * 2 * P8 * 16;
+      const size_t w_res = (w_total + 127) / 128 * 128;
+      int st = std::min(3, (int)(((size_t)kMaxSmem - fixed - w_res) / a_stage));
+      if (st < 2) continue;
+      g.G = T;
+      g.P_max = P8;
+      g.stages = st;
+      g.slots = std::min(slots_cap(), 512 / (T * AW));
+      g.a_stage_bytes = g.chunk_a_bytes = a_stage;
+      g.b_stage_bytes = g.chunk_b_bytes = 0;
+      g.resident = true;
+      g.w_total = w_total;
+      g.cps = 1;
+      g.smem_bytes = (size_t)st * a_stage + w_res + fixed;
+      int cols = 32;
+      while (cols < g.slots * T * AW) cols *= 2;
+      g.tmem_cols = cols;
+      found = true;
+      break;
+    }
+    STDA_CHECK(found, "row-band conv: no tiling fits");
+    g.items_per_image = (g.Hp / g.G) * (g.Wp / 128);
+    return g;
+  }
   uint32_t b_stage = 0;
   for (int c = 0; c < d.n_planes * (d.cin / 16); ++c)
     b_stage = std::max<uint32_t>(b_stage, (uint32_t)(d.chunk_off[c + 1] - d.chunk_off[c]));
@@ -411,9 +479,10 @@ void tc_launch(const TcLayerDesc& d, const TcGeometry& g, const PlBuf& src0, con
   if (d.mode == CONVT4_HALF) grid &= ~1;
   const int npm = d.npass == 1 ? kNpmBf16 : (d.concat ? kNpmConcat : kNpm3);
   STDA_CHECK(d.cout == 16 || d.cout == 32 || d.cout == 64, "unsupported cout for the tensor-core path");
-  STDA_CHECK(g.G == 1 || g.G == 2 || g.G == 4, "unsupported tile count per item");
+  STDA_CHECK(g.G == 1 || g.G == 2 || g.G == 4 || (d.mode == CONV3_ROWS && g.G == 8), "unsupported tile count per item");
   switch (d.mode) {
     case CONV3_S1: return dispatch_s1(d.cout, npm, g.G, p, grid, g.smem_bytes, st);
+    case CONV3_ROWS: return dispatch_rows(d.cout, npm, g.G, p, grid, g.smem_bytes, st);
     case CONV3_S2: return dispatch_s2(d.cout, npm, g.G, p, grid, g.smem_bytes, st);
     case CONVT4_HALF:
       STDA_CHECK(out.mode == 0, "half-phase ConvT writes NHWC fp32");

@@ -81,13 +81,13 @@ __device__ __forceinline__ void trace_cta(unsigned long long* tr, int which) {
 // HALF (ConvT, one output-row parity py per work item): t = px*4 + a*2 + b, accumulator px,
 //      shift (a - 1, px + b - 1) relative to the item's origin shifted down by py rows
 __host__ __device__ constexpr int ntaps(int mode, int pl) {
-  return mode == CONV3_S1      ? 9
+  return mode == CONV3_S1 || mode == CONV3_ROWS ? 9
          : mode == CONVT4_S2   ? 16
          : mode == CONVT4_HALF ? 8
                                : (pl == 0 ? 1 : pl == 3 ? 4 : 2);
 }
 __host__ __device__ constexpr int tap_dy(int mode, int pl, int t) {
-  return mode == CONV3_S1      ? t / 3 - 1
+  return mode == CONV3_S1 || mode == CONV3_ROWS ? t / 3 - 1
          : mode == CONVT4_S2   ? (t / 4 >> 1) + ((t >> 1) & 1) - 1
          : mode == CONVT4_HALF ? ((t >> 1) & 1) - 1
          : pl == 2             ? (t == 0 ? -1 : 0)
@@ -95,7 +95,7 @@ __host__ __device__ constexpr int tap_dy(int mode, int pl, int t) {
                                : 0;
 }
 __host__ __device__ constexpr int tap_dx(int mode, int pl, int t) {
-  return mode == CONV3_S1      ? t % 3 - 1
+  return mode == CONV3_S1 || mode == CONV3_ROWS ? t % 3 - 1
          : mode == CONVT4_S2   ? ((t / 4) & 1) + (t & 1) - 1
          : mode == CONVT4_HALF ? (t >> 2) + (t & 1) - 1
          : pl == 1             ? (t == 0 ? -1 : 0)
@@ -157,6 +157,18 @@ __host__ __device__ constexpr int grp_slot0(int mode, int g) {  // first B tile 
 }
 // B tiles per source and chunk: T 18 (16 + 2 zero tiles), HALF 8
 __host__ __device__ constexpr int grp_slots(int mode) { return grp_slot0(mode, ngroups(mode)); }
+
+// ---- row-band 3x3 conv (CONV3_ROWS: stride 1, plane width a multiple of 128) -----------
+// An item is T = G output rows x 128 columns; M-tile = one row segment.  The item's input
+// rows y0-1 .. y0+T are staged one per kRowsSL positions (columns x0-1 .. x0+128, the
+// plane's pad column / margins supplying the zero borders), so the A tile of input row i
+// and column shift dx is the staged range starting at i*kRowsSL + dx + 1.  One A read
+// serves the three dy taps of the output rows i+1, i, i-1: B = the dx group's three tap
+// blocks [W(dy=-1) | W(0) | W(+1)] stacked along N, and the accumulator of output row j
+// sits at TMEM column (T-1-j)*AW, so block b of the MMA for input row i (output row
+// i-b) lands on its row's accumulator (a window sliding one block per input row).
+// 3 A reads per input row and K chunk instead of 9 per output row.
+constexpr int kRowsSL = 130;
 
 // ---- PTX helpers -----------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -272,6 +284,30 @@ __device__ __forceinline__ void issue_chunk(bool leader, uint64_t a0, uint64_t b
   constexpr uint32_t BLO_UNITS = 32u * N / 16u;
   constexpr uint32_t IDESC_N = idesc_bf16(N);
   constexpr uint32_t IDESC_W = idesc_bf16(AW);
+  if constexpr (MODE == CONV3_ROWS) {
+    // b0 carries LBO = 3 blocks of AW rows (one dx group = [kgrp 2][block 3][AW rows][16 B])
+    constexpr int T = G;
+    constexpr uint32_t GRP_UNITS = 6u * AW;
+#pragma unroll
+    for (int i = 0; i < T + 2; ++i) {
+      const int b_lo = i - T + 1 > 0 ? i - T + 1 : 0, b_hi = i < 2 ? i : 2;
+      const int nb = b_hi - b_lo + 1;
+#pragma unroll
+      for (int dx = 0; dx < 3; ++dx) {
+        const uint64_t ad = a0 + (uint32_t)(i * L + dx);
+        const uint64_t bd = b0 + (uint32_t)dx * GRP_UNITS + (uint32_t)(b_lo * AW);
+        const uint32_t dcol = dslot + (uint32_t)((T - 1 - i + b_lo) * AW);
+        if (first_chunk && dx == 0 && b_lo == 0) {
+          // block 0 starts output row i's accumulator; the others continue theirs
+          tc_mma(leader, dcol, ad, bd, idesc_bf16(AW), 0u);
+          if (nb > 1) tc_mma(leader, dcol + AW, ad, bd + AW, idesc_bf16((nb - 1) * AW), 1u);
+        } else {
+          tc_mma(leader, dcol, ad, bd, idesc_bf16(nb * AW), 1u);
+        }
+        if (NPM == kNpmConcat) tc_mma(leader, dcol, ad + lo_units, bd, idesc_bf16(nb * AW), 1u);  // A_lo
+      }
+    }
+  } else {
   const int lo = plane_lo_a(MODE, PL) * L + plane_lo_b(MODE, PL);
   if constexpr (grouped_t(MODE, NPM)) {
     // one MMA pair per shift group: A_hi x [tiles] + A_lo x [tiles], each tile [B_hi | B_lo]
@@ -324,6 +360,7 @@ __device__ __forceinline__ void issue_chunk(bool leader, uint64_t a0, uint64_t b
         }
       }
     }
+  }
   }
 }
 
@@ -409,6 +446,36 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
       // HALF: items (tile, py) interleaved; the tile origin moves down py rows
       const int q0 = MODE == CONVT4_HALF ? (it >> 1) * p.G * 128 + (it & 1) * p.L : it * p.G * 128;
       const uint16_t* img = S.base + (int64_t)b * S.img_stride;
+      if constexpr (MODE == CONV3_ROWS) {
+        // per staged row and (pass, cg8) block one copy of kRowsSL positions (weights resident)
+        const int tpr = p.Wp / 128, band = it / tpr;
+        const int y0 = band * p.G, x0 = (it - band * tpr) * 128;
+        constexpr int NCP = NPASS_A * 2;
+        for (int c0 = 0; c0 < n_chunks; c0 += CPS, ++k) {
+          const int stage = pstage;
+          const uint32_t phase = pphase;
+          if (++pstage == p.stages) {
+            pstage = 0;
+            pphase ^= 1u;
+          }
+          mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+          const uint32_t fb = smem_u32(&full[stage]);
+          if (lane == 0) mbar_arrive_expect_tx(fb, (uint32_t)(CPS * (p.G + 2) * NCP * kRowsSL * 16));
+          __syncwarp();
+#pragma unroll
+          for (int cc = 0; cc < CPS; ++cc) {
+            const int cgi = c0 + cc;
+            for (int u = lane; u < (p.G + 2) * NCP; u += 32) {
+              const int i = u / NCP, blk = u - i * NCP;
+              const uint16_t* src =
+                  img + (S.block_index(cgi, blk >> 1, blk & 1) + (int64_t)(y0 - 1 + i) * p.L + x0 - 1 + S.off) * 8;
+              bulk_g2s(smem_u32(a_base + (size_t)stage * p.a_stage_bytes + (size_t)cc * p.chunk_a_bytes +
+                                (size_t)blk * p.P_max * 16 + (size_t)i * kRowsSL * 16),
+                       src, (uint32_t)(kRowsSL * 16), fb);
+            }
+          }
+        }
+      } else {
       for (int c0 = 0; c0 < n_chunks; c0 += CPS, ++k) {  // one ring stage = cps chunks
         const int stage = pstage;
         const uint32_t phase = pphase;
@@ -454,13 +521,15 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
         }
         if (lane == 0) trace_at(p.trace, 0, 2 * k + 1);
       }
+      }
     }
     __syncwarp();
   } else if (warp == kMmaWarp) {
     // ===================== MMA issuer: whole warp runs the loop, one lane issues ========
     const bool leader = elect_one();
     const uint32_t lboA = (uint32_t)p.P_max * 16;
-    const uint32_t lboB = (uint32_t)AW * 16;
+    const uint32_t lboB = (uint32_t)AW * 16 * (MODE == CONV3_ROWS ? 3 : 1);
+    const int a_rs = MODE == CONV3_ROWS ? kRowsSL : p.L;  // ROWS: staged row stride
     const uint32_t src_units = src_bytes >> 4;
     const uint32_t lo_units = (2 * lboA) >> 4;  // A_lo planes follow the A_hi planes
     uint32_t k = 0, ic = 0;
@@ -510,7 +579,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
               default: issue_chunk<N, MODE, 3, DUAL, NPM, G>(leader, a0, b0, dslot, p.L, c == 0, src_units, lo_units); break;
             }
           } else {
-            issue_chunk<N, MODE, 0, DUAL, NPM, G>(leader, a0, b0, dslot, p.L, c == 0, src_units, lo_units);
+            issue_chunk<N, MODE, 0, DUAL, NPM, G>(leader, a0, b0, dslot, a_rs, c == 0, src_units, lo_units);
           }
         }
         __syncwarp();
@@ -539,6 +608,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
       const int it = item - b * p.items_per_image;
       const int q0 = (MODE == CONVT4_HALF ? it >> 1 : it) * p.G * 128;
       const int py = MODE == CONVT4_HALF ? (it & 1) : 0;  // output row parity of a HALF item
+      int ry0 = 0, rx0 = 0;  // ROWS: the item's first output row / column
+      if (MODE == CONV3_ROWS) {
+        const int tpr = p.Wp / 128, band = it / tpr;
+        ry0 = band * G;
+        rx0 = (it - band * tpr) * 128;
+      }
       mbar_wait(smem_u32(&tfull[slot]), sphase);
       __syncwarp();
       tc_fence_after();
@@ -553,11 +628,21 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
       for (int c = 0; c < N; ++c) gsum[c] = 0.f;
       const uint32_t trow = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)slot * p.slot_cols;
       for (int g = 0; g < G; ++g) {
-        const int q = q0 + g * 128 + ew * 32 + lane;
-        const int y = (int)__umulhi((uint32_t)q, p.L_mul);  // q / L (host-checked exact)
-        const int x = q - y * p.L;
+        int y, x;
+        if (MODE == CONV3_ROWS) {
+          y = ry0 + g;
+          x = rx0 + ew * 32 + lane;
+        } else {
+          const int q = q0 + g * 128 + ew * 32 + lane;
+          y = (int)__umulhi((uint32_t)q, p.L_mul);  // q / L (host-checked exact)
+          x = q - y * p.L;
+        }
         const bool valid = y < p.Hp && x < p.Wp;
-        if (p.out.mode != 0 && ((g * NACC_SRC * NJ) & 1) == half && y < p.Hp && x == p.Wp) {
+        // the output row's pad position: ROWS tiles never cover it, the last lane of the
+        // row's last tile clears it
+        const bool padpos = MODE == CONV3_ROWS ? (rx0 + 128 == p.Wp && ew == 3 && lane == 31)
+                                               : (y < p.Hp && x == p.Wp);
+        if (p.out.mode != 0 && ((g * NACC_SRC * NJ) & 1) == half && padpos) {
           // this position is a pad of the output grid: keep the operand plane's pad
           // column zero (planes.cuh border contract)
           if (p.out.mode == 1) {
@@ -581,8 +666,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
           for (int j = 0; j < N; j += 16) {
             if ((((g * NACC_SRC + ph) * NJ + j / 16) & 1) != half) continue;  // warp-uniform
             float a0[16], a1[16];
-            const uint32_t c0 = (uint32_t)((g * NACC + ph) * AW + j);
-            const uint32_t c1 = (uint32_t)((g * NACC + NACC_SRC + ph) * AW + j);
+            const int gt = MODE == CONV3_ROWS ? G - 1 - g : g;  // ROWS: row j at column (T-1-j)*AW
+            const uint32_t c0 = (uint32_t)((gt * NACC + ph) * AW + j);
+            const uint32_t c1 = (uint32_t)((gt * NACC + NACC_SRC + ph) * AW + j);
             auto ld = [&](uint32_t a, float(&v)[16]) {
               if (p.dbg & 2) {
 #pragma unroll
@@ -715,6 +801,7 @@ void dispatch_s1(int n, int npm, int G, const Params& p, int grid, size_t smem, 
 void dispatch_s2(int n, int npm, int G, const Params& p, int grid, size_t smem, cudaStream_t st);
 void dispatch_t(int n, int npm, int G, const Params& p, int grid, size_t smem, cudaStream_t st);
 void dispatch_th(int n, int npm, int G, const Params& p, int grid, size_t smem, cudaStream_t st);
+void dispatch_rows(int n, int npm, int G, const Params& p, int grid, size_t smem, cudaStream_t st);
 
 }  // namespace detail
 }  // namespace tc
