@@ -180,3 +180,30 @@ def test_synth_properties():
     # noise floor bulk in 0.4..0.9, targets are the brightest bins
     med = x.flatten(-2).median(dim=-1).values
     assert bool(((med > 0.3) & (med < 0.95)).all())
+
+
+def test_row_band_conv_path():
+    """STDA_TC_ROWS=1 (row-band stride-1 conv, off by default) stays within tolerance of the
+    default path at 128^2 and 256^2 (checked in a subprocess: the switch is read once)."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import torch, numpy as np\n"
+        "from paper_2307_09063_b200 import StdaConfig, StdaNet\n"
+        "from paper_2307_09063_b200.synth import synth_triplets\n"
+        "for hw, b in ((128, 4), (256, 2)):\n"
+        "    torch.manual_seed(hw)\n"
+        "    net = StdaNet(StdaConfig(map_height=hw, map_width=hw)).eval().cuda()\n"
+        "    x = synth_triplets(b, hw, hw, seed=5)\n"
+        "    y = net(x).cpu().numpy()\n"
+        "    np.save(f'/tmp/rows_{hw}_' + __import__('os').environ['STDA_TC_ROWS'] + '.npy', y)\n"
+    )
+    for flag in ("0", "1"):
+        env = dict(os.environ, STDA_TC_ROWS=flag)
+        subprocess.run([sys.executable, "-c", code], check=True, env=env,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import numpy as np
+    for hw in (128, 256):
+        a, b = np.load(f"/tmp/rows_{hw}_0.npy"), np.load(f"/tmp/rows_{hw}_1.npy")
+        assert np.abs(a - b).max() / np.abs(a).max() <= 2e-5
