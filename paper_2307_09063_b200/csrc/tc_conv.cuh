@@ -87,6 +87,7 @@ struct TcGeometry {
   int G;                  // M-tiles of 128 positions per work item
   int stages, slots;      // smem pipeline depth, TMEM accumulator slots
   int items_per_image;
+  int tail = 0;           // partial items per image, scheduled last (tc_kernel.cuh item_coords)
   int tmem_cols;
   int P_max;              // staged positions per plane
   uint32_t a_stage_bytes, b_stage_bytes;

@@ -405,6 +405,11 @@ TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W) {
   }
   const int positions = g.Hp * g.L;
   g.items_per_image = cdiv(positions, g.G * 128) * (d.mode == CONVT4_HALF ? 2 : 1);
+  static const bool tail_last = [] {  // env STDA_TC_TAIL=0: image-major item order (A/B timing)
+    const char* e = std::getenv("STDA_TC_TAIL");
+    return !(e && e[0] == '0');
+  }();
+  g.tail = tail_last && positions % (g.G * 128) != 0 ? (d.mode == CONVT4_HALF ? 2 : 1) : 0;
   return g;
 }
 
@@ -446,6 +451,7 @@ void tc_launch(const TcLayerDesc& d, const TcGeometry& g, const PlBuf& src0, con
   p.slots = g.slots;
   p.items_per_image = g.items_per_image;
   p.total_items = g.B * g.items_per_image;
+  p.tail = g.tail;
   p.P_max = g.P_max;
   p.a_stage_bytes = g.a_stage_bytes;
   p.b_stage_bytes = g.b_stage_bytes;

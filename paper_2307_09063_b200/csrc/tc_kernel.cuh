@@ -39,6 +39,7 @@ struct Params {
   int Hp, Wp, L, Ho, Wo;
   uint32_t L_mul;          // ceil(2^32 / L): q / L == umulhi(q, L_mul) for q * L < 2^32
   int G, stages, slots, items_per_image, total_items;
+  int tail;  // partial items per image (the last 1, HALF 2) scheduled after all full ones
   int P_max;
   uint32_t a_stage_bytes, b_stage_bytes, slot_cols;
   int cps;                          // K chunks per ring stage (1 or 2)
@@ -71,6 +72,32 @@ __device__ __forceinline__ void trace_cta(unsigned long long* tr, int which) {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   tr[5 * kTraceRegion + 2 * blockIdx.x + which] = t;
+}
+// region 5 from 512: every CTA, [512 + 32*cta + ic] = %globaltimer when the epilogue
+// released item ic's accumulators (ic < 31); [512 + 32*cta + 31] = first MMA stage acquired
+__device__ __forceinline__ void trace_cta_item(unsigned long long* tr, int idx) {
+  if (tr == nullptr || idx > 31 || 512 + 32 * (int)blockIdx.x + 31 >= kTraceRegion) return;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  tr[5 * kTraceRegion + 512 + 32 * blockIdx.x + idx] = t;
+}
+
+// Work item n -> (image, item of the image).  The last `tail` items of an image cover a
+// partial tile group; they are numbered after every full item, so the final round of the
+// strided persistent schedule is made of the cheap partial items instead of full ones (the
+// image-major numbering left e.g. 40 full enc0.s1 items for a 15th round on 40 CTAs).
+// Parity of `it` equals parity of n when tail is even (HALF: items alternate py).
+__device__ __forceinline__ void item_coords(int n, const Params& p, int& b, int& it) {
+  const int full = p.items_per_image - p.tail;
+  const int nf = (p.total_items / p.items_per_image) * full;
+  if (n < nf) {
+    b = n / full;
+    it = n - b * full;
+  } else {
+    const int r = n - nf;
+    b = r / p.tail;
+    it = full + (r - b * p.tail);
+  }
 }
 
 // ---- compile-time tap tables (must match plane_taps() on the host) ----------------
@@ -441,8 +468,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
     int pstage = 0;
     uint32_t pphase = 0;
     for (int item = blockIdx.x; item < p.total_items; item += gridDim.x) {
-      const int b = item / p.items_per_image;
-      const int it = item - b * p.items_per_image;
+      int b, it;
+      item_coords(item, p, b, it);
       // HALF: items (tile, py) interleaved; the tile origin moves down py rows
       const int q0 = MODE == CONVT4_HALF ? (it >> 1) * p.G * 128 + (it & 1) * p.L : it * p.G * 128;
       const uint16_t* img = S.base + (int64_t)b * S.img_stride;
@@ -561,6 +588,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
         mbar_wait(smem_u32(&full[stage]), phase);  // TMA -> MMA: both async proxy, no fence
         __syncwarp();
         if (leader) trace_at(p.trace, 1, 2 * k);
+        if (leader && k == 0) trace_cta_item(p.trace, 31);
 #pragma unroll
         for (int cc = 0; cc < CPS; ++cc) {  // CPS chunks per barrier round trip
           const int c = c0 + cc;
@@ -604,8 +632,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
     for (int item = blockIdx.x; item < p.total_items; item += gridDim.x, ++ic) {
       const int slot = ic % p.slots;
       const uint32_t sphase = (ic / p.slots) & 1;
-      const int b = item / p.items_per_image;
-      const int it = item - b * p.items_per_image;
+      int b, it;
+      item_coords(item, p, b, it);
       const int q0 = (MODE == CONVT4_HALF ? it >> 1 : it) * p.G * 128;
       const int py = MODE == CONVT4_HALF ? (it & 1) : 0;  // output row parity of a HALF item
       int ry0 = 0, rx0 = 0;  // ROWS: the item's first output row / column
@@ -731,6 +759,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
       tc_fence_before();
       mbar_arrive(smem_u32(&tempty[slot]));
       if (et == 0) trace_at(p.trace, 3, 2 * ic + 1);
+      if (et == 0) trace_cta_item(p.trace, (int)ic);
       if (p.out.mode != 0 && it == 0) pl_zero_margins(p.out.pl, b, et, kEpiWarps * 32);
       if (p.out.mode == 0 && p.out.gap) {
         // deterministic: fixed-order sum of the 8 warp partials

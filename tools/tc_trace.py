@@ -61,6 +61,16 @@ for li in range(n_tc):
         print(f"  CTAs (globaltimer ns): start spread {st.max()}, end min {en.min()} median {int(np.median(en))} "
               f"max {en.max()}; duration min {dur.min()} median {int(np.median(dur))} max {dur.max()}; "
               f"last to end: {list(slow)}")
+    if "--ctas" in sys.argv:
+        it = t[5][512 : 512 + 32 * 148].reshape(148, 32)
+        base = t[5][: 2 * 148].reshape(-1, 2)[:, 0].min()
+        for c in range(148):
+            row = it[c]
+            n = int(np.count_nonzero(row[:31]))
+            if n == 0:
+                continue
+            items = row[:n] - base
+            print(f"   cta {c:3d}: first-mma {row[31] - base:6d} items " + " ".join(f"{v:6d}" for v in items))
     pe = prod[0 : 2 * nk : 2] - np.concatenate([[t0], prod[1 : 2 * nk - 1 : 2]])
     pi = prod[1 : 2 * nk : 2] - prod[0 : 2 * nk : 2]
     print(f"  producer  wait-empty {stats(pe)} | issue {stats(pi)}")
