@@ -323,7 +323,7 @@ void run_net_tc(const stda_plan& p, const Src& x, float* y, int64_t B, const Net
     tc::TcOut o1;
     o1.mode = 2;  // phase planes for the stride-2 consumer
     o1.pl = mviews[i];
-    tc::tc_launch(d1, g1, cur_pl, nullptr, o1, true, st);
+    tc::tc_launch(d1, g1, cur_pl, nullptr, o1, true, st, /*rev=*/true);
     mk.mark(st);
     const tc::TcGeometry g2 = tc::tc_plan(d2, (int)B, h, wd);
     tc::TcOut o2;
@@ -356,7 +356,7 @@ void run_net_tc(const stda_plan& p, const Src& x, float* y, int64_t B, const Net
     tc::TcOut o1;
     o1.mode = 1;  // plane for the ConvT consumer
     o1.pl = mviews[S + j];
-    tc::tc_launch(d1, g1, cur_pl, nullptr, o1, true, st);
+    tc::tc_launch(d1, g1, cur_pl, nullptr, o1, true, st, /*rev=*/true);
     mk.mark(st);
     const tc::TcGeometry g2 = tc::tc_plan(d2, (int)B, h, wd);
     tc::TcOut o2;

@@ -110,8 +110,11 @@ struct TcOut {
   PlBuf pl;
 };
 
+// rev: process the images last to first.  A stage-2 conv reads the stage-1 output written
+// just before it; running stage 1 in reverse image order makes the stage-1 output it wrote
+// last (still in L2) the first thing stage 2 reads.
 void tc_launch(const TcLayerDesc& d, const TcGeometry& g, const PlBuf& src0, const PlBuf* src1,
-               const TcOut& out, bool relu0, cudaStream_t st);
+               const TcOut& out, bool relu0, cudaStream_t st, bool rev = false);
 
 // Debug: record a clock64 timeline of CTA 0 (see tc_kernel.cuh trace_at) into dev_buf
 // during the launch_index-th following tc_launch.

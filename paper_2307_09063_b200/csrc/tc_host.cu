@@ -424,7 +424,7 @@ void tc_debug_trace(void* dev_buf, int launch_index) {
 }
 
 void tc_launch(const TcLayerDesc& d, const TcGeometry& g, const PlBuf& src0, const PlBuf* src1,
-               const TcOut& out, bool relu0, cudaStream_t st) {
+               const TcOut& out, bool relu0, cudaStream_t st, bool rev) {
   Params p;
   std::memset(&p, 0, sizeof(p));
   p.d = d;
@@ -452,6 +452,11 @@ void tc_launch(const TcLayerDesc& d, const TcGeometry& g, const PlBuf& src0, con
   p.items_per_image = g.items_per_image;
   p.total_items = g.B * g.items_per_image;
   p.tail = g.tail;
+  static const bool rev_on = [] {  // env STDA_TC_REV=0: every launch walks images first to last
+    const char* e = std::getenv("STDA_TC_REV");
+    return !(e && e[0] == '0');
+  }();
+  p.rev = rev && rev_on ? 1 : 0;
   p.P_max = g.P_max;
   p.a_stage_bytes = g.a_stage_bytes;
   p.b_stage_bytes = g.b_stage_bytes;

@@ -40,6 +40,7 @@ struct Params {
   uint32_t L_mul;          // ceil(2^32 / L): q / L == umulhi(q, L_mul) for q * L < 2^32
   int G, stages, slots, items_per_image, total_items;
   int tail;  // partial items per image (the last 1, HALF 2) scheduled after all full ones
+  int rev;   // walk the images last to first (L2 reuse of the previous launch's output)
   int P_max;
   uint32_t a_stage_bytes, b_stage_bytes, slot_cols;
   int cps;                          // K chunks per ring stage (1 or 2)
@@ -98,6 +99,7 @@ __device__ __forceinline__ void item_coords(int n, const Params& p, int& b, int&
     b = r / p.tail;
     it = full + (r - b * p.tail);
   }
+  if (p.rev) b = p.total_items / p.items_per_image - 1 - b;
 }
 
 // ---- compile-time tap tables (must match plane_taps() on the host) ----------------
