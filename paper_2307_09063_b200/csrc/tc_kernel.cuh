@@ -731,6 +731,48 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
               if (DUAL) t = t + (a1[i] + d.bias1_c[j + i]);
               v[i] = t;
             }
+            if (p.out.mode == 0 && MODE == CONV3_S2) {  // measured: slower for the ConvT phases
+              // NHWC fp32: the 64-byte pixel rows of a lane quad are transposed in registers
+              // (4x4 exchange of 16-byte chunks by shfl_xor 2, then 1), so each store
+              // instruction writes 8 whole 64-byte pixel segments instead of 32 scattered
+              // 16-byte pieces (half the L2 sector writes, a third of the L1 wavefronts)
+              if (valid) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) gsum[j + i] += v[i];
+              }
+              float4 c4[4];
+#pragma unroll
+              for (int c = 0; c < 4; ++c) c4[c] = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+              const int r = lane & 3;
+              auto xchg = [&](float4& keep_or_recv_a, float4& keep_or_recv_b, bool hi, int m) {
+                // hi lanes send a and receive into a; lo lanes send b and receive into b
+                const float4 x = hi ? keep_or_recv_a : keep_or_recv_b;
+                float4 y;
+                y.x = __shfl_xor_sync(0xffffffffu, x.x, m);
+                y.y = __shfl_xor_sync(0xffffffffu, x.y, m);
+                y.z = __shfl_xor_sync(0xffffffffu, x.z, m);
+                y.w = __shfl_xor_sync(0xffffffffu, x.w, m);
+                if (hi) keep_or_recv_a = y;
+                else keep_or_recv_b = y;
+              };
+              xchg(c4[0], c4[2], (r & 2) != 0, 2);
+              xchg(c4[1], c4[3], (r & 2) != 0, 2);
+              xchg(c4[0], c4[1], (r & 1) != 0, 1);
+              xchg(c4[2], c4[3], (r & 1) != 0, 1);
+              // c4[c] = channels j + 4r .. j + 4r + 3 of the pixel of lane (lane & ~3) + c
+              if (!(p.dbg & 1)) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                  const int qc = q0 + g * 128 + ew * 32 + (lane & ~3) + c;
+                  const int yc = (int)__umulhi((uint32_t)qc, p.L_mul);
+                  const int xc = qc - yc * p.L;
+                  if (yc >= p.Hp || xc >= p.Wp) continue;
+                  *reinterpret_cast<float4*>(p.out.f32 + (((size_t)b * p.Ho + yc) * p.Wo + xc) * N + j + 4 * r) =
+                      c4[c];
+                }
+              }
+              continue;
+            }
             if (!valid || (p.dbg & 1)) continue;
             if (p.out.mode == 0) {
               float* op = p.out.f32 + (((size_t)b * p.Ho + oy) * p.Wo + ox) * N;
