@@ -326,10 +326,17 @@ def run_engine(args, world, rank, local):
     batch, H, W, scene, idx = CONFIGS[args.config]
     if args.batch:
         batch = args.batch
+    # BASELINE configs 3 and 5 fix the whole job's batch and shard it over the GPUs (strong
+    # scaling); configs 1 and 2 give every GPU the config's batch (weak scaling)
+    strong = args.config in ("c3", "c5") and not args.batch
+    total = batch if strong else batch * world
+    first = total * rank // world if strong else rank * batch
+    if strong:
+        batch = total * (rank + 1) // world - first
     dev = torch.device("cuda", local)
     cfg = StdaConfig(map_height=H, map_width=W)
     net = seeded_net(cfg, args.precision).to(dev)
-    x = synth_triplets(batch, H, W, seed=1234, scene=scene, first_seq=rank * batch, device=dev)
+    x = synth_triplets(batch, H, W, seed=1234, scene=scene, first_seq=first, device=dev)
     cap = CapturedForward(net, x, split=args.split)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
@@ -354,7 +361,7 @@ def run_engine(args, world, rank, local):
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     total_ms = max_over_ranks(sum(step_ms), world)
     ms_per_step = total_ms / args.steps
-    value = batch * world * args.steps / (total_ms / 1000.0)
+    value = total * args.steps / (total_ms / 1000.0)
     ordered = sorted(step_ms)
     step_stats = {"median_ms": max_over_ranks(ordered[len(ordered) // 2], world),
                   "best_ms": max_over_ranks(ordered[0], world),
@@ -408,16 +415,17 @@ def run_engine(args, world, rank, local):
     t0 = time.perf_counter()
     net.denoise_host(x_host, y_host)
     e2e_s = max_over_ranks(time.perf_counter() - t0, world)
-    e2e_rate = batch * world * e2e_steps / e2e_s
+    e2e_rate = total * e2e_steps / e2e_s
     assert torch.equal(y_host[:batch], cap.replay().cpu()), "host path differs from device path"
 
     line = {
         "metric": METRIC, "value": value, "unit": "triplets/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "step_ms": step_stats,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
         "dtype": args.precision, "data": "synthetic (GPU RD-map generator, seeded; seeded random-init weights)",
-        "config": {"workload": f"BASELINE config {idx + 1}: [{batch},3,{H},{W}] per GPU",
-                   "global_batch": batch * world, "map": [H, W], "precision": args.precision,
+        "config": {"workload": (f"BASELINE config {idx + 1}: [{total},3,{H},{W}] sharded over {world} GPU(s)"
+                                if strong else f"BASELINE config {idx + 1}: [{batch},3,{H},{W}] per GPU"),
+                   "global_batch": total, "map": [H, W], "precision": args.precision,
                    "parallelism": f"dp{world} (independent batches, no collective)",
                    "l2": "flushed between timed steps (256 MiB write)",
                    "timing": "CUDA-graph replay of the whole forward, CUDA events per step",
