@@ -169,8 +169,20 @@ void launch_eca_gates(const float* gap, int items, const float* eca_w, int k, fl
                       int64_t hw, cudaStream_t st);
 
 __device__ __forceinline__ float eca_group_sum(const float* gap, int items, int C, int64_t b, int c, int g) {
+  // loads batched 8 at a time ahead of the adds (one L2 round trip per 8 items instead of
+  // one per item); the adds keep the order t = g, g + 8, ...
+  const float* src = gap + ((size_t)b * items + g) * C + c;
+  const size_t step = (size_t)kEcaGroups * C;
+  const int n = items > g ? (items - g + kEcaGroups - 1) / kEcaGroups : 0;
   float a = 0.f;
-  for (int t = g; t < items; t += kEcaGroups) a += __ldg(gap + ((size_t)b * items + t) * C + c);
+  for (int t0 = 0; t0 < n; t0 += 8) {
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = t0 + u < n ? __ldg(src + (size_t)(t0 + u) * step) : 0.f;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (t0 + u < n) a += v[u];
+  }
   return a;
 }
 // sequential form: the channel sum of channel c
