@@ -323,16 +323,8 @@ def run_engine(args, world, rank, local):
     from paper_2307_09063_b200.engine import CapturedForward
     from paper_2307_09063_b200.synth import synth_triplets
 
-    batch, H, W, scene, idx = CONFIGS[args.config]
-    if args.batch:
-        batch = args.batch
-    # BASELINE configs 3 and 5 fix the whole job's batch and shard it over the GPUs (strong
-    # scaling); configs 1 and 2 give every GPU the config's batch (weak scaling)
-    strong = args.config in ("c3", "c5") and not args.batch
-    total = batch if strong else batch * world
-    first = total * rank // world if strong else rank * batch
-    if strong:
-        batch = total * (rank + 1) // world - first
+    _, H, W, scene, idx = CONFIGS[args.config]
+    first, batch, total, strong = shard(args.config, world, rank, args.batch)
     dev = torch.device("cuda", local)
     cfg = StdaConfig(map_height=H, map_width=W)
     net = seeded_net(cfg, args.precision).to(dev)
@@ -454,6 +446,21 @@ def run_engine(args, world, rank, local):
         print(json.dumps(line), flush=True)
 
 
+def shard(config: str, world: int, rank: int, batch_override: int = 0):
+    """This rank's slice of the workload: (first global index, count, job total, strong).
+
+    Configs 3 and 5 fix the job's batch and split it over the ranks (strong scaling, as
+    BASELINE states); config 4 splits the stream's 4094 windows into contiguous time chunks
+    (each rank also reads the 2 frames before its first window); configs 1 and 2 give every
+    rank the config's batch (weak scaling).  Slices are contiguous and disjoint."""
+    batch = batch_override or CONFIGS[config][0]
+    strong = config == "c4" or (config in ("c3", "c5") and not batch_override)
+    if not strong:
+        return rank * batch, batch, batch * world, False
+    first, end = batch * rank // world, batch * (rank + 1) // world
+    return first, end - first, batch, True
+
+
 def run_stream(args, world, rank, local):
     """BASELINE config 4: stride-1 sliding-window denoise of one coherent frame stream
     (StdaNet.forward_window).  Outputs t = 2..4095 are split into `world` contiguous chunks;
@@ -463,12 +470,11 @@ def run_stream(args, world, rank, local):
     from paper_2307_09063_b200.engine import CapturedForward
     from paper_2307_09063_b200.synth import synth_frames
 
-    n_total, H, W, scene, idx = CONFIGS["c4"]
+    _, H, W, scene, idx = CONFIGS["c4"]
     dev = torch.device("cuda", local)
     cfg = StdaConfig(map_height=H, map_width=W)
     net = seeded_net(cfg, args.precision).to(dev)
-    o0, o1 = n_total * rank // world, n_total * (rank + 1) // world
-    n_out = o1 - o0
+    o0, n_out, n_total, _ = shard("c4", world, rank)
     frames = synth_frames(n_out + 2, H, W, seed=1234, scene=scene, first_frame=o0, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)

@@ -52,6 +52,25 @@ def test_max_over_ranks_and_disjoint_shards_gloo():
         assert sorted(shards) == [(0, 64), (64, 128)]
 
 
+@pytest.mark.parametrize("config", ["c1", "c2", "c3", "c4", "c5"])
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_bench_shards_tile_the_job(config, world):
+    """bench.shard: every rank's slice is contiguous, slices are disjoint and cover the job
+    (weak configs: world x the config batch; strong configs: the config's fixed total)."""
+    sys.path.insert(0, str(ROOT))
+    import bench
+    got = [bench.shard(config, world, r) for r in range(world)]
+    total = got[0][2]
+    strong = config in ("c3", "c4", "c5")
+    assert all(g[3] == strong and g[2] == total for g in got)
+    assert total == bench.CONFIGS[config][0] * (1 if strong else world)
+    pos = 0
+    for first, count, _, _ in got:
+        assert first == pos and count >= 0
+        pos += count
+    assert pos == total
+
+
 def test_reference_arm_under_torchrun_prints_once():
     """`bench.py --impl reference` launched like the driver's N>1 run: rank 0 alone times
     the CPU reference and prints one JSON line, the other rank exits 0 without work."""
