@@ -207,3 +207,28 @@ def test_row_band_conv_path():
     for hw in (128, 256):
         a, b = np.load(f"/tmp/rows_{hw}_0.npy"), np.load(f"/tmp/rows_{hw}_1.npy")
         assert np.abs(a - b).max() / np.abs(a).max() <= 2e-5
+
+
+def test_schedule_orders_do_not_change_results():
+    """Item scheduling (partial items last, stage-1 convs in reverse image order, the S1
+    tile-count rule) only reorders work: outputs are bitwise those of the plain image-major
+    order (checked in subprocesses: the switches are read once)."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import torch, numpy as np, os\n"
+        "from paper_2307_09063_b200 import StdaConfig, StdaNet\n"
+        "from paper_2307_09063_b200.synth import synth_triplets\n"
+        "torch.manual_seed(7)\n"
+        "net = StdaNet(StdaConfig(map_height=128, map_width=128)).eval().cuda()\n"
+        "x = synth_triplets(20, 128, 128, seed=3)\n"
+        "np.save('/tmp/sched_' + os.environ['TAG'] + '.npy', net(x).cpu().numpy())\n"
+    )
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    runs = {"default": {}, "plain": {"STDA_TC_TAIL": "0", "STDA_TC_REV": "0", "STDA_TC_GMAX": "4444"}}
+    for tag, extra in runs.items():
+        env = dict(os.environ, TAG=tag, **extra)
+        subprocess.run([sys.executable, "-c", code], check=True, env=env, cwd=root)
+    import numpy as np
+    assert np.array_equal(np.load("/tmp/sched_default.npy"), np.load("/tmp/sched_plain.npy"))
