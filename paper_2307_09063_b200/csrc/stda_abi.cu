@@ -686,9 +686,17 @@ int64_t stda_host_chunk(const stda_plan* plan, int64_t batch) {
   if (!plan || plan->kind != 0 || batch <= 0) return 0;
   const stda_config& c = plan->cfg;
   const int64_t per = (int64_t)c.input_frames * c.map_height * c.map_width * 4;
-  // ~16 MB of input per chunk (64 triplets at 128x128): big enough for full-efficiency
-  // forwards, small enough that H2D / forward / D2H of neighbouring chunks overlap
-  const int64_t chunk = std::max<int64_t>(1, (16ll << 20) / per);
+  // input bytes per pipelined chunk: 1/16 of the call's input, clamped to [16, 128] MB —
+  // large chunks keep the per-forward efficiency of big batches (256^2 / 512^2 maps: 21 / 5
+  // triplets per 16 MB chunk cost 10-15 % of e2e throughput), and 16 chunks keep the
+  // exposed first copy-in / last copy-out small.  env STDA_HOST_CHUNK_MB fixes it (A/B).
+  static const int64_t mb_env = [] {
+    const char* e = std::getenv("STDA_HOST_CHUNK_MB");
+    return e ? std::max<int64_t>(1, std::atoll(e)) : 0;
+  }();
+  const int64_t bytes = mb_env ? (mb_env << 20)
+                               : std::min<int64_t>(128ll << 20, std::max<int64_t>(16ll << 20, batch * per / 16));
+  const int64_t chunk = std::max<int64_t>(1, bytes / per);
   return std::min(batch, chunk);
 }
 
