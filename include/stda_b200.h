@@ -104,7 +104,8 @@ int stda_forward_window(const stda_plan* plan, const float* frames, int64_t n_fr
 
 /* ---- host-buffer entry (the end-to-end path): pinned host x in, host y out.
  * Chunks of `chunk` triplets are pipelined H2D / forward / D2H on internal streams
- * ordered after `stream`; returns after y_host is complete. ---- */
+ * ordered after `stream`; returns after y_host is complete.  stda_host_chunk suggests a
+ * chunk for a batch: 1/16 of its input bytes, clamped to [16, 128] MB. ---- */
 int64_t stda_host_chunk(const stda_plan* plan, int64_t batch);
 size_t stda_host_workspace_bytes(const stda_plan* plan, int64_t chunk);
 int stda_forward_host(const stda_plan* plan, const float* x_host, float* y_host, int64_t batch,
