@@ -88,7 +88,6 @@ struct TcGeometry {
   int stages, slots;      // smem pipeline depth, TMEM accumulator slots
   int items_per_image;
   int tail = 0;           // partial items per image, scheduled last (tc_kernel.cuh item_coords)
-  int cta_per_sm = 1;     // 2: smem / TMEM sized for two co-resident CTAs per SM
   int tmem_cols;
   int P_max;              // staged positions per plane
   uint32_t a_stage_bytes, b_stage_bytes;

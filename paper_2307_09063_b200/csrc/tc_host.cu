@@ -322,47 +322,6 @@ TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W) {
   // overlaps the MMAs of item i+1), (3) the largest G, (4) resident weights (loaded once
   // per CTA instead of once per work item); fall back step by step.
   bool ok = false;
-  // env STDA_TC_CTA2=<mode mask>: plans for two co-resident CTAs per SM (2 stages, 2 TMEM
-  // slots of <= 128 columns each, <= 113 KB of shared memory) for the modes in the mask
-  // (bit = 1 << mode); the launch keeps one per SM when registers do not allow two
-  static const int cta2_mask = [] {
-    const char* e = std::getenv("STDA_TC_CTA2");
-    return e ? std::atoi(e) : 0;
-  }();
-  if ((cta2_mask >> d.mode) & 1) {
-    const size_t w_res = (w_total + 127) / 128 * 128;
-    for (int G : {4, 2, 1}) {
-      const int P8 = (G * 128 + span + 7) / 8 * 8;
-      const uint32_t a_stage = (uint32_t)d.n_src * npassA * 2 * P8 * 16;
-      const int acc_cols = G * n_acc * d.cout * (d.concat ? 2 : 1);
-      if (acc_cols * 2 > 256 || G * n_acc > 32) continue;
-      for (bool resident : {true, false}) {
-        const size_t need = resident ? 2 * (size_t)a_stage + w_res : 2 * ((size_t)a_stage + b_stage);
-        if (need + fixed > 113 * 1024) continue;
-        g.G = G;
-        g.P_max = P8;
-        g.stages = 2;
-        g.slots = 2;
-        g.a_stage_bytes = g.chunk_a_bytes = a_stage;
-        g.b_stage_bytes = g.chunk_b_bytes = resident ? 0 : b_stage;
-        g.resident = resident;
-        g.w_total = w_total;
-        g.cps = 1;
-        g.smem_bytes = need + fixed;
-        g.tmem_cols = acc_cols * 2 <= 32 ? 32 : acc_cols * 2 <= 64 ? 64 : acc_cols * 2 <= 128 ? 128 : 256;
-        g.cta_per_sm = 2;
-        ok = true;
-        break;
-      }
-      if (ok) break;
-    }
-    if (ok) {
-      const int positions = g.Hp * g.L;
-      g.items_per_image = cdiv(positions, g.G * 128) * (d.mode == CONVT4_HALF ? 2 : 1);
-      g.tail = positions % (g.G * 128) != 0 ? (d.mode == CONVT4_HALF ? 2 : 1) : 0;
-      return g;
-    }
-  }
   static const int pref_stages = [] {  // env STDA_TC_MINSTAGES: stage depth preferred over G
     const char* e = std::getenv("STDA_TC_MINSTAGES");
     return e ? std::max(2, std::min(kMaxStages, std::atoi(e))) : 2;
@@ -547,8 +506,7 @@ void tc_launch(const TcLayerDesc& d, const TcGeometry& g, const PlBuf& src0, con
   int dev = 0, sms = 148;
   STDA_CUDA(cudaGetDevice(&dev));
   STDA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  p.cta_per_sm = g.cta_per_sm;
-  int grid = std::min(p.total_items, sms * g.cta_per_sm);
+  int grid = std::min(p.total_items, sms);
   // HALF: an even grid keeps every CTA on items of one py (items alternate py), so each
   // CTA loads one weight block (TcLayerDesc::half_bytes)
   if (d.mode == CONVT4_HALF) grid &= ~1;

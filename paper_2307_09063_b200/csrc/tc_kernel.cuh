@@ -41,7 +41,6 @@ struct Params {
   int G, stages, slots, items_per_image, total_items;
   int tail;  // partial items per image (the last 1, HALF 2) scheduled after all full ones
   int rev;   // walk the images last to first (L2 reuse of the previous launch's output)
-  int cta_per_sm;  // host: 2 = plan sized for two co-resident CTAs per SM
   int P_max;
   uint32_t a_stage_bytes, b_stage_bytes, slot_cols;
   int cps;                          // K chunks per ring stage (1 or 2)
@@ -844,15 +843,6 @@ template <int N, int MODE, bool DUAL, int NPM, int G>
 void launch_k(const Params& p, int grid, size_t smem, cudaStream_t st) {
   auto kern = p.cps == 2 ? tc_conv_kernel<N, MODE, DUAL, NPM, G, 2> : tc_conv_kernel<N, MODE, DUAL, NPM, G, 1>;
   ensure_dyn_smem(kern, kMaxSmem);
-  if (p.cta_per_sm > 1) {
-    // two-CTA plans: as many CTAs as actually fit per SM (registers may allow only one)
-    int occ = 1, dev = 0, sms = 148;
-    STDA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem));
-    STDA_CUDA(cudaGetDevice(&dev));
-    STDA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    grid = std::min(grid, std::max(1, std::min(occ, p.cta_per_sm)) * sms);
-    if (MODE == CONVT4_HALF) grid &= ~1;
-  }
   launch_pdl(kern, dim3(grid), dim3(kThreads), smem, st, "tc_conv_kernel", p);
 }
 
