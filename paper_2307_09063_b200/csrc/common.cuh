@@ -87,7 +87,7 @@ __device__ __forceinline__ void grid_dep_launch() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-bool pdl_enabled();  // env STDA_PDL=0 disables the programmatic edges (A/B timing)
+bool pdl_enabled();  // env STDA_PDL=1 enables the programmatic edges (off by default; stda_abi.cu)
 
 template <typename... KArgs, typename... Args>
 void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
