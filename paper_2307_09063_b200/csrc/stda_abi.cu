@@ -44,17 +44,21 @@ void launch_score(const void* clean, int clean_kind, const float* test_db, int64
 static thread_local std::string g_last_error;
 void set_error(const std::string& msg) { g_last_error = msg; }
 
-// Programmatic dependent launch edges between the forward's kernels.  Off by default:
-// re-measured at the end of round 1 (C2 graph replay, 4 runs each) plain stream order is
-// 0.3 % faster (165.95K vs 165.45K) — no CTA of the next kernel fits beside a running one
-// (shared memory), so the early launch buys nothing and griddepcontrol.wait costs a little.
-// env STDA_PDL=1 turns them on.
-bool pdl_enabled() {
-  static const bool on = [] {
+// Programmatic dependent launch edges between the forward's kernels.  Measured at the end
+// of round 1: inside a CUDA graph plain stream order is 0.3 % faster (165.95K vs 165.45K
+// triplets/s at C2: no CTA of the next kernel fits beside a running one, so the early
+// launch buys nothing), while eager launches (the host-buffer path) are 7 % faster with
+// the edges (they hide the kernel-to-kernel launch gap).  So: on unless the stream is
+// being captured.  env STDA_PDL=1 / 0 forces them on / off.
+bool pdl_enabled(cudaStream_t st) {
+  static const int mode = [] {
     const char* e = std::getenv("STDA_PDL");
-    return e && e[0] == '1';
+    return e ? (e[0] == '1' ? 1 : 0) : -1;
   }();
-  return on;
+  if (mode >= 0) return mode == 1;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) return true;
+  return cs == cudaStreamCaptureStatusNone;
 }
 
 namespace {
