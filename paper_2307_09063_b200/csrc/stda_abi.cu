@@ -558,7 +558,7 @@ int stda_plan_create(const stda_config* cfg, const float* blob, size_t n_floats,
       if (p->use_tc) {
         const size_t n1 = (size_t)c2 * c2 * 9, n2 = (size_t)ch * c2 * 16;
         D.s1_tc = p->make_tc(CONV3_S1, c2, c2, w_s1, w_s1 + n1, nullptr, nullptr, cfg->map_width >> (S - j));
-        D.s2_tc = p->make_tc(CONVT4_S2, c2, ch, w_up, w_up + n2, w_rs, w_rs + n2, 0);
+        D.s2_tc = p->make_tc(CONVT4_S2, c2, ch, w_up, w_up + n2, w_rs, w_rs + n2, cfg->map_width >> (S - j));
       }
       D.eca = p->make_vec(k, src);
       p->dec.push_back(D);

@@ -76,7 +76,8 @@ struct TcLayerDesc {
 
 // Host: canonical fp32 weights (see include/stda_b200.h) -> descriptor + packed bf16.
 // plane_w = width of the input plane (stride-1 layers over widths that are multiples of 128
-// are packed for the row-band kernel, CONV3_ROWS); 0 = unknown.
+// may be packed for the row-band kernel, CONV3_ROWS; transposed convs over planes >= 256
+// wide run as half-phase items); 0 = unknown.
 void tc_pack_layer(TcLayerDesc& d, int mode, int cin, int cout, const float* w0, const float* w1,
                    bool bf16, std::vector<uint16_t>& packed, int plane_w = 0);
 

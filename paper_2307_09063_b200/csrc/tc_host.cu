@@ -108,7 +108,10 @@ void tc_pack_layer(TcLayerDesc& d, int mode, int cin, int cout, const float* w0,
     const char* e = std::getenv("STDA_TC_HALF");
     return e && e[0] == '2';
   }();
-  if (mode == CONVT4_S2 && !bf16 && half_t_enabled() && (wide_t || half_all)) mode = CONVT4_HALF;
+  // ... and over planes >= 256 wide: a full-ConvT item stages 128 + 2L + 2 positions per
+  // chunk (three input rows), so at 256-wide planes the ring drops to one stage; half-phase
+  // items stage 128 + L + 2 (measured C5 dec1.s2: 4.10 -> 3.04 ms)
+  if (mode == CONVT4_S2 && !bf16 && half_t_enabled() && (wide_t || half_all || plane_w >= 256)) mode = CONVT4_HALF;
   const bool tmode = mode == CONVT4_S2 || mode == CONVT4_HALF;
   d.mode = mode;
   d.n_src = w1 ? 2 : 1;
