@@ -1,5 +1,6 @@
 // tcgen05 implicit-GEMM convolution: host side (weight packing, tiling plan, launch).
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -430,6 +431,11 @@ TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W) {
   }
   const int positions = g.Hp * g.L;
   g.items_per_image = cdiv(positions, g.G * 128) * (d.mode == CONVT4_HALF ? 2 : 1);
+  static const bool planlog = std::getenv("STDA_TC_PLANLOG") != nullptr;  // debug: print plans
+  if (planlog)
+    std::fprintf(stderr, "tc_plan mode %d cin %d cout %d grid %dx%d B %d: G %d stages %d cps %d slots %d resident %d "
+                 "a_stage %u smem %zu items/img %d\n", d.mode, d.cin, d.cout, g.Hp, g.Wp, B, g.G, g.stages, g.cps,
+                 g.slots, (int)g.resident, g.a_stage_bytes, g.smem_bytes, g.items_per_image);
   static const bool tail_last = [] {  // env STDA_TC_TAIL=0: image-major item order (A/B timing)
     const char* e = std::getenv("STDA_TC_TAIL");
     return !(e && e[0] == '0');
