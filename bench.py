@@ -143,61 +143,83 @@ def ncu_traffic(kernel: str, batch: int, H: int, W: int, precision: str):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and clock-event (throttle) reasons sampled DURING the timed region.
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    In-process NVML polling every ~1 ms on a side thread (a timed region of a few ms still
+    gets samples); `nvidia-smi -lms 50` is the fallback when NVML is unavailable."""
 
-    def __init__(self, index: int):
+    # nvmlClocksEventReason* bits
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, index: int, period_s: float = 0.001):
         self.index = index
-        self.proc = None
-        self.lines = []
+        self.period = period_s
+        self.sm, self.smax, self.reasons, self.source = [], None, set(), None
+        self._stop = threading.Event()
+        self._thread = None
+
+    def _handle(self):
+        import pynvml
+        pynvml.nvmlInit()
+        try:
+            p = torch.cuda.get_device_properties(self.index)
+            bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
+
+    def _poll(self, nv, h):
+        get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while True:
+            try:
+                self.sm.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+                r = int(get_reasons(h))
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            if self._stop.wait(self.period):
+                break
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
+            nv, h = self._handle()
+            self.smax = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            self.source = "nvml, 1 ms polling"
+            self._thread = threading.Thread(target=self._poll, args=(nv, h), daemon=True)
+            self._thread.start()
         except Exception:
-            self.proc = None
+            self._thread = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        if self._thread is not None:
+            self._thread.join(timeout=5)
+        if not self.sm:
+            self._smi_once()
+
+    def _smi_once(self):
+        try:
+            out = subprocess.run(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm",
+                 "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=10).stdout
+            a, b = [float(v) for v in out.strip().split(",")[:2]]
+            self.sm.append(a)
+            self.smax = b
+            self.source = "nvidia-smi after the timed region (NVML unavailable)"
+        except Exception:
+            pass
 
     def summary(self):
-        sm, smax, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 8:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                smax = float(parts[1])
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[4:8]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": smax, "reasons": [], "samples": 0}
-        sm.sort()
-        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": smax, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        if not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": self.smax, "reasons": [], "samples": 0}
+        sm = sorted(self.sm)
+        return {"sm_mhz": sm[len(sm) // 2], "sm_min_mhz": sm[0], "sm_max_mhz": self.smax,
+                "reasons": sorted(self.reasons), "samples": len(sm), "source": self.source}
 
 
 def seeded_net(cfg, precision):
@@ -223,20 +245,66 @@ def cpu_cores() -> int:
         return os.cpu_count() or 1
 
 
-def cpu_forward_rate(net, x_cpu: torch.Tensor, budget_s: float, chunk: int = 16):
-    """Oracle port (reference op sequence on torch CPU) triplets/s over a bounded sample."""
-    from oracle import port  # test infrastructure: the CPU baseline leg only
-    from tests._helpers import CONFIG_FIELDS
-    sd = {k: v.detach().cpu() for k, v in net.state_dict().items()}
-    cfg = {f: getattr(net.config, f) for f in CONFIG_FIELDS}
+# triplets (c4: windows) the CPU reference processes per timed step: the whole per-GPU batch
+# for configs 1 and 2, a bounded sample of the larger ones (a C3 batch is ~22 s of CPU work)
+REF_SAMPLE = {"c1": 1, "c2": 64, "c3": 16, "c4": 64, "c5": 4}
+SCENE_ID = {"default": 0, "dense": 1}
+
+
+def workload_config(args, world: int) -> dict:
+    """The `config` object of the JSON line — identical for the engine and reference arms."""
+    batch, H, W, scene, idx = CONFIGS[args.config]
+    first, per_rank, total, strong = shard(args.config, world, 0, args.batch)
+    if args.config == "c4":
+        return {"workload": f"BASELINE config {idx + 1}: 4096 frames of {H}x{W}, stride-1 windows "
+                            f"(4094 outputs) split over {world} GPU(s) with a 2-frame halo",
+                "windows_per_gpu": per_rank, "map": [H, W], "precision": args.precision,
+                "parallelism": f"time chunks x{world} (no collective)",
+                "l2": "flushed between timed steps (256 MiB write)",
+                "timing": "StdaNet.forward_window per step, CUDA events"}
+    return {"workload": (f"BASELINE config {idx + 1}: [{total},3,{H},{W}] sharded over {world} GPU(s)"
+                         if strong else f"BASELINE config {idx + 1}: [{per_rank},3,{H},{W}] per GPU"),
+            "global_batch": total, "map": [H, W], "precision": args.precision,
+            "parallelism": f"dp{world} (independent batches, no collective)",
+            "l2": "flushed between timed steps (256 MiB write)",
+            "timing": "CUDA-graph replay of the whole forward, CUDA events per step",
+            "concurrent_slices": max(1, min(args.split, per_rank))}
+
+
+def reference_inputs(config: str, n: int, first: int):
+    """CPU-built inputs for the reference arm: `oracle/synth.py`, the numpy restatement of
+    the GPU generator (same seed, scene, sequence / frame indices as the engine arm)."""
+    from oracle import synth as osynth  # test infrastructure: the reference arm only
+    _, H, W, scene, _ = CONFIGS[config]
+    if config == "c4":
+        f = torch.from_numpy(osynth.stream(n + 2, H, W, seed=1234, scene=SCENE_ID[scene],
+                                           first_frame=first))
+        return torch.stack([f[2:], f[1:-1], f[:-2]], dim=1).contiguous()
+    return torch.from_numpy(osynth.triplets(n, H, W, seed=1234, scene=SCENE_ID[scene],
+                                            first_seq=first))
+
+
+def reference_forward(sd, cfg: dict, x: torch.Tensor, chunk: int = 16) -> None:
+    """The reference eval forward (oracle port, op for op) over x in chunks of 16 triplets
+    (CPU throughput peaks there)."""
+    from oracle import port  # test infrastructure: CPU baseline / reference arm only
+    for i in range(0, x.shape[0], chunk):
+        port.forward(sd, cfg, x[i:i + chunk])
+
+
+def cpu_reference_rate(H: int, W: int, x_cpu: torch.Tensor, budget_s: float):
+    """CPU reference forward triplets/s on all host cores over a bounded sample: one warm-up
+    chunk, then chunks of 16 until `budget_s` has elapsed."""
+    from oracle import init as oinit
+    sd = oinit.seeded_state_dict(0, map_height=H, map_width=W)
+    cfg = oinit.config(map_height=H, map_width=W)
     torch.set_num_threads(cpu_cores())
     with torch.inference_mode():
-        port.forward(sd, cfg, x_cpu[:chunk])                      # warm-up
-        done, t0 = 0, time.perf_counter()
-        i = 0
+        reference_forward(sd, cfg, x_cpu[:16])                    # warm-up
+        done, i, t0 = 0, 0, time.perf_counter()
         while True:
-            xb = x_cpu[(i * chunk) % x_cpu.shape[0]:][:chunk]
-            port.forward(sd, cfg, xb)
+            xb = x_cpu[(i * 16) % x_cpu.shape[0]:][:16]
+            reference_forward(sd, cfg, xb)
             done += xb.shape[0]
             i += 1
             el = time.perf_counter() - t0
@@ -249,14 +317,25 @@ def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if world > 1:
         import torch.distributed as dist
         backend = "nccl" if args.impl == "engine" else "gloo"
         if backend == "nccl":
+            # NCCL's INIT log (nranks / cudaDev / busId per rank) on stderr, stdout stays JSON
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
             torch.cuda.set_device(local)
         dist.init_process_group(backend)
-    elif torch.cuda.is_available():
+    elif args.impl == "engine" and torch.cuda.is_available():
         torch.cuda.set_device(local)
+    if args.impl == "engine":
+        p = torch.cuda.get_device_properties(local)
+        print(f"bench rank {rank}/{world}: cuda:{local} {p.name} pci "
+              f"{p.pci_domain_id:04x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x} sms {p.multi_processor_count}",
+              file=sys.stderr, flush=True)
     return world, rank, local
 
 
@@ -276,44 +355,49 @@ def barrier(world):
 
 
 def run_reference(args, world, rank):
-    """--impl reference: the reference's CPU forward (oracle port) on the host cores."""
-    from paper_2307_09063_b200 import StdaConfig
-    batch, H, W, scene, idx = CONFIGS[args.config]
+    """--impl reference: the reference's CPU forward on the host cores (rank 0 only).
+
+    Imports nothing from the product package and maps no repo shared library: the weights
+    are the reference module tree's seeded init (`oracle/init.py`, torch.manual_seed(0)),
+    the inputs come from the numpy restatement of the generator (`oracle/synth.py`), and
+    the forward is the op-for-op CPU port (`oracle/port.py`).  Each step is rank 0's slice
+    of the engine arm's workload (all 64 triplets of config 2), bounded for the large
+    configs (REF_SAMPLE), in chunks of 16 triplets on all host threads."""
     if rank != 0:
         return
-    cfg = StdaConfig(map_height=H, map_width=W)
-    net = seeded_net(cfg, "fp32")
-    sample = min(batch, 16)
-    if torch.cuda.is_available():
-        from paper_2307_09063_b200.synth import synth_triplets
-        x = synth_triplets(sample, H, W, seed=1234, scene=scene).cpu()
-    else:  # the reference arm needs no GPU
-        g = torch.Generator().manual_seed(1234)
-        x = torch.rand(sample, 3, H, W, generator=g)
-    from oracle import port
-    from tests._helpers import CONFIG_FIELDS
-    sd = {k: v.detach().cpu() for k, v in net.state_dict().items()}
-    c = {f: getattr(cfg, f) for f in CONFIG_FIELDS}
+    from oracle import init as oinit
+    batch, H, W, scene, idx = CONFIGS[args.config]
+    first, per_rank, total, strong = shard(args.config, world, 0, args.batch)
+    sample = max(1, min(per_rank, REF_SAMPLE[args.config]))
+    sd = oinit.seeded_state_dict(0, map_height=H, map_width=W)
+    cfg = oinit.config(map_height=H, map_width=W)
+    x = reference_inputs(args.config, sample, first)
     torch.set_num_threads(cpu_cores())
     with torch.inference_mode():
         for _ in range(args.warmup):
-            port.forward(sd, c, x)
-        t0 = time.perf_counter()
+            reference_forward(sd, cfg, x)
+        times = []
         for _ in range(args.steps):
-            port.forward(sd, c, x)
-        el = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            reference_forward(sd, cfg, x)
+            times.append(time.perf_counter() - t0)
+    el = sum(times)
     rate = sample * args.steps / el
+    unit = "triplets/s"
     line = {
-        "impl": "reference", "metric": METRIC, "value": rate, "unit": "triplets/s",
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": unit,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1000 * el / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "fp32", "data": "synthetic (GPU RD-map generator, seeded)",
-        "config": {"workload": f"BASELINE config {idx + 1}: [{batch},3,{H},{W}] fp32",
-                   "sample_per_step": sample, "parallelism": "cpu threads"},
-        "cpu_baseline": {"value": rate, "unit": "triplets/s", "cores": cpu_cores(), "kind": "port",
-                         "cpu_model": cpu_model(),
-                         "sample": f"{sample} triplets of the workload per step, {args.steps} steps"},
-        "e2e": {"value": rate, "unit": "triplets/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "ms_per_step": 1000 * el / args.steps, "higher_is_better": True,
+        "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "fp32",
+        "data": "synthetic (RD-map generator restated on the host, oracle/synth.py, seeded; "
+                "seeded random-init weights)",
+        "config": workload_config(args, world),
+        "cpu_baseline": {"value": rate, "unit": unit, "cores": cpu_cores(), "kind": "port",
+                         "cpu_model": cpu_model(), "threads": torch.get_num_threads(),
+                         "sample": f"{sample} of rank 0's {per_rank} "
+                                   f"{'windows' if args.config == 'c4' else 'triplets'} per step, "
+                                   f"chunks of 16, {args.steps} steps"},
+        "e2e": {"value": rate, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
@@ -393,35 +477,35 @@ def run_engine(args, world, rank, local):
                 "bytes_per_launch": byt[dom] * batch}
     roof["traffic"] = ncu_traffic(dom, batch, H, W, args.precision)
 
-    # end-to-end through the public host-buffer API: a stream of e2e_steps batches in
-    # pinned host memory goes through ONE StdaNet.denoise_host call, which pipelines
-    # H2D / forward / D2H per batch-sized chunk on separate streams.  Every step's H2D of
-    # its inputs and D2H of its result are inside the timed region.
-    e2e_steps = max(3, min(32, args.steps // 4))
+    # end-to-end through the public host-buffer API: a fixed stream of batches in pinned host
+    # memory (32 batches at 128^2, ~2 GB of input for the large configs, independent of
+    # --steps) goes through ONE StdaNet.denoise_host call, which pipelines H2D / forward / D2H
+    # per chunk on separate streams.  Every batch's H2D of its inputs and D2H of its result are
+    # inside the timed region.  Median of 3 calls.
+    per_batch = batch * 3 * H * W * 4
+    e2e_steps = max(2, min(32, (2 << 30) // per_batch))
     x_host = torch.empty((e2e_steps * batch, 3, H, W), dtype=torch.float32).pin_memory()
     for s in range(e2e_steps):
         x_host[s * batch:(s + 1) * batch].copy_(x)
     y_host = torch.empty((e2e_steps * batch, 1, H, W), dtype=torch.float32).pin_memory()
     net.denoise_host(x_host, y_host)                            # warm-up (plans, streams)
-    barrier(world)
-    t0 = time.perf_counter()
-    net.denoise_host(x_host, y_host)
-    e2e_s = max_over_ranks(time.perf_counter() - t0, world)
+    e2e_times = []
+    for _ in range(3):
+        barrier(world)
+        t0 = time.perf_counter()
+        net.denoise_host(x_host, y_host)
+        e2e_times.append(max_over_ranks(time.perf_counter() - t0, world))
+    e2e_s = sorted(e2e_times)[1]
     e2e_rate = total * e2e_steps / e2e_s
     assert torch.equal(y_host[:batch], cap.replay().cpu()), "host path differs from device path"
+    del x_host, y_host
 
     line = {
         "metric": METRIC, "value": value, "unit": "triplets/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "step_ms": step_stats,
         "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
         "dtype": args.precision, "data": "synthetic (GPU RD-map generator, seeded; seeded random-init weights)",
-        "config": {"workload": (f"BASELINE config {idx + 1}: [{total},3,{H},{W}] sharded over {world} GPU(s)"
-                                if strong else f"BASELINE config {idx + 1}: [{batch},3,{H},{W}] per GPU"),
-                   "global_batch": total, "map": [H, W], "precision": args.precision,
-                   "parallelism": f"dp{world} (independent batches, no collective)",
-                   "l2": "flushed between timed steps (256 MiB write)",
-                   "timing": "CUDA-graph replay of the whole forward, CUDA events per step",
-                   "concurrent_slices": len(cap.slices)},
+        "config": workload_config(args, world),
         "gpu_launches": cap.launches * args.steps,
         "roofline": {
             **roof, "launch_ms": share[dom],
@@ -434,16 +518,49 @@ def run_engine(args, world, rank, local):
         },
         "e2e": {"value": e2e_rate, "unit": "triplets/s",
                 "h2d_bytes_per_step": batch * 3 * H * W * 4, "d2h_bytes_per_step": batch * H * W * 4,
-                "steps": e2e_steps, "api": "StdaNet.denoise_host (pinned host in/out, pipelined chunks)"},
+                "steps": e2e_steps, "calls": [total * e2e_steps / t for t in e2e_times],
+                "api": "StdaNet.denoise_host (pinned host in/out, pipelined chunks), median of 3 calls"},
         "clocks": clocks.summary(),
     }
-    if rank == 0 and world == 1 and not args.no_cpu:
-        rate, done, el = cpu_forward_rate(net, x.cpu(), args.cpu_seconds)
+    if args.config == "c1" or args.latency:
+        line["latency"] = latency_stats(net, cap, x)
+    if rank == 0 and not args.no_cpu:
+        rate, done, el = cpu_reference_rate(H, W, x.cpu(), args.cpu_seconds)
         line["cpu_baseline"] = {"value": rate, "unit": "triplets/s", "cores": cpu_cores(),
                                 "kind": "port", "cpu_model": cpu_model(),
-                                "sample": f"{done} triplets of the workload in chunks of 16, {el:.1f} s"}
+                                "threads": torch.get_num_threads(),
+                                "sample": f"{done} triplets of rank 0's workload in chunks of 16, {el:.1f} s"}
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def latency_stats(net, cap, x, calls: int = 300) -> dict:
+    """Per-call latency (host clock, call -> result synchronised) of the batch through the
+    eager public forward (`StdaNet.forward`, plan cached, eager launches), the captured
+    graph (`CapturedForward.replay`) and the host-buffer call (`StdaNet.denoise_host`)."""
+    dev = x.device
+    x_host = x.cpu().pin_memory()
+    y_host = torch.empty((x.shape[0], 1, x.shape[2], x.shape[3]), dtype=torch.float32).pin_memory()
+
+    def measure(fn):
+        for _ in range(20):
+            fn()
+        torch.cuda.synchronize(dev)
+        ts = []
+        for _ in range(calls):
+            t0 = time.perf_counter()
+            fn()
+            torch.cuda.synchronize(dev)
+            ts.append((time.perf_counter() - t0) * 1e6)
+        ts.sort()
+        return {"p50_us": ts[len(ts) // 2], "p99_us": ts[int(len(ts) * 0.99) - 1], "min_us": ts[0]}
+
+    with torch.inference_mode():
+        out = {"batch": int(x.shape[0]), "calls": calls,
+               "eager_forward": measure(lambda: net(x)),
+               "graph_replay": measure(cap.replay),
+               "host_buffers": measure(lambda: net.denoise_host(x_host, y_host))}
+    return out
 
 
 def shard(config: str, world: int, rank: int, batch_override: int = 0):
@@ -573,12 +690,7 @@ def run_stream(args, world, rank, local):
         "warmup": max(args.warmup, 3), "ms_per_step": total_ms / steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": args.precision,
         "data": "synthetic (GPU RD-map stream generator, seeded; seeded random-init weights)",
-        "config": {"workload": f"BASELINE config {idx + 1}: 4096 frames of {H}x{W}, stride-1 windows "
-                               f"(4094 outputs) split over {world} GPU(s) with a 2-frame halo",
-                   "windows_per_gpu": n_out, "map": [H, W], "precision": args.precision,
-                   "parallelism": f"time chunks x{world} (no collective)",
-                   "l2": "flushed between timed steps (256 MiB write)",
-                   "timing": "StdaNet.forward_window per step, CUDA events"},
+        "config": workload_config(args, world),
         "gpu_launches": cap_launches(net, dev) * steps,
         "roofline": roof,
         "e2e": {"value": n_total * steps / e2e_s, "unit": "triplets/s",
@@ -586,6 +698,13 @@ def run_stream(args, world, rank, local):
                 "steps": steps, "api": "StdaNet.forward_window over 8 pipelined sub-chunks (pinned host frames in, windows out)"},
         "clocks": clocks.summary(),
     }
+    if rank == 0 and not args.no_cpu:
+        xw = torch.stack([frames[2:], frames[1:-1], frames[:-2]], dim=1)[:64].cpu()
+        rate, done, el = cpu_reference_rate(H, W, xw, args.cpu_seconds)
+        line["cpu_baseline"] = {"value": rate, "unit": "triplets/s", "cores": cpu_cores(),
+                                "kind": "port", "cpu_model": cpu_model(),
+                                "threads": torch.get_num_threads(),
+                                "sample": f"{done} windows of rank 0's chunk in chunks of 16, {el:.1f} s"}
     if rank == 0:
         print(json.dumps(line), flush=True)
 
@@ -594,6 +713,20 @@ def cap_launches(net, dev):
     from paper_2307_09063_b200.engine import _net_plan
     plan = _net_plan(net, dev)
     return plan.L.kernels_per_forward(plan.handle)
+
+
+def spawn_ranks(args) -> int:
+    """`bench.py --gpus N` (N > 1) without a torchrun environment: re-launch this command
+    as N ranks under torch.distributed.run on 127.0.0.1, one process per GPU."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           "--nproc-per-node", str(args.gpus), "--master-addr", "127.0.0.1",
+           "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
+    print(f"bench.py: spawning {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.run(cmd).returncode
 
 
 def main():
@@ -609,7 +742,13 @@ def main():
                     help="run the batch as this many concurrent slices (streams) inside the graph")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--latency", action="store_true",
+                    help="add per-call p50/p99 latency (always on for --config c1)")
     args = ap.parse_args()
+    if args.gpus < 1:
+        raise SystemExit("--gpus must be >= 1")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
     world, rank, local = dist_setup(args)
     try:
         if args.impl == "reference":

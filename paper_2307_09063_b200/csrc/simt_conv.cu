@@ -319,8 +319,11 @@ void dispatch_cob(int cob, Args a, int64_t B, int nblk, cudaStream_t st) {
 }
 
 // ---- ECA helpers ---------------------------------------------------------------
-__global__ void gate_kernel(const float* __restrict__ gap, int ntiles, const float* __restrict__ w,
-                            int k, float* __restrict__ gates, int C, int hw) {
+// `gap` and `gates` may alias (stda_eca reduces the channel sums in place: every sum is
+// read into shared memory before the __syncthreads that precedes the first gate store),
+// so neither is declared __restrict__.
+__global__ void gate_kernel(const float* gap, int ntiles, const float* __restrict__ w,
+                            int k, float* gates, int C, int hw) {
   extern __shared__ float mean[];
   const int64_t b = blockIdx.x;
   for (int c = threadIdx.x; c < C; c += blockDim.x) {

@@ -104,16 +104,9 @@ struct stda_plan {
   std::vector<EncLayers> enc;
   std::vector<DecLayers> dec;
   std::vector<void*> allocations;
-  // host-buffer pipeline resources (created on first use)
-  cudaStream_t copy_in = nullptr, copy_out = nullptr;
-  cudaEvent_t ev_start = nullptr, ev_in[2] = {}, ev_comp[2] = {}, ev_out[2] = {};
 
   ~stda_plan() {
     for (void* p : allocations) cudaFree(p);
-    if (copy_in) cudaStreamDestroy(copy_in);
-    if (copy_out) cudaStreamDestroy(copy_out);
-    for (cudaEvent_t e : {ev_start, ev_in[0], ev_in[1], ev_comp[0], ev_comp[1], ev_out[0], ev_out[1]})
-      if (e) cudaEventDestroy(e);
   }
 
   float* upload(const std::vector<float>& v) {
@@ -717,6 +710,31 @@ size_t stda_host_workspace_bytes(const stda_plan* plan, int64_t chunk) {
          plan_ws(*plan, chunk, nullptr).bytes;
 }
 
+namespace {
+struct HostPipe {
+  cudaStream_t copy_in = nullptr, copy_out = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_in[2] = {}, ev_comp[2] = {}, ev_out[2] = {};
+  HostPipe() {
+    STDA_CUDA(cudaStreamCreateWithFlags(&copy_in, cudaStreamNonBlocking));
+    STDA_CUDA(cudaStreamCreateWithFlags(&copy_out, cudaStreamNonBlocking));
+    STDA_CUDA(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));
+    for (int s = 0; s < 2; ++s) {
+      STDA_CUDA(cudaEventCreateWithFlags(&ev_in[s], cudaEventDisableTiming));
+      STDA_CUDA(cudaEventCreateWithFlags(&ev_comp[s], cudaEventDisableTiming));
+      STDA_CUDA(cudaEventCreateWithFlags(&ev_out[s], cudaEventDisableTiming));
+    }
+  }
+  ~HostPipe() {  // work already enqueued completes; handles are released afterwards
+    if (copy_in) cudaStreamDestroy(copy_in);
+    if (copy_out) cudaStreamDestroy(copy_out);
+    for (cudaEvent_t e : {ev_start, ev_in[0], ev_in[1], ev_comp[0], ev_comp[1], ev_out[0], ev_out[1]})
+      if (e) cudaEventDestroy(e);
+  }
+  HostPipe(const HostPipe&) = delete;
+  HostPipe& operator=(const HostPipe&) = delete;
+};
+}  // namespace
+
 int stda_forward_host(const stda_plan* plan, const float* x_host, float* y_host, int64_t batch,
                       int64_t chunk, void* ws, size_t ws_bytes, void* stream) {
   return guarded([&] {
@@ -727,17 +745,10 @@ int stda_forward_host(const stda_plan* plan, const float* x_host, float* y_host,
     chunk = std::min(chunk, batch);
     check_ws(plan, ws, ws_bytes, stda_host_workspace_bytes(plan, chunk));
     DeviceGuard g(plan->device);
-    stda_plan* p = const_cast<stda_plan*>(plan);
-    if (!p->copy_in) {
-      STDA_CUDA(cudaStreamCreateWithFlags(&p->copy_in, cudaStreamNonBlocking));
-      STDA_CUDA(cudaStreamCreateWithFlags(&p->copy_out, cudaStreamNonBlocking));
-      STDA_CUDA(cudaEventCreateWithFlags(&p->ev_start, cudaEventDisableTiming));
-      for (int s = 0; s < 2; ++s) {
-        STDA_CUDA(cudaEventCreateWithFlags(&p->ev_in[s], cudaEventDisableTiming));
-        STDA_CUDA(cudaEventCreateWithFlags(&p->ev_comp[s], cudaEventDisableTiming));
-        STDA_CUDA(cudaEventCreateWithFlags(&p->ev_out[s], cudaEventDisableTiming));
-      }
-    }
+    // copy streams and events belong to this call (the plan stays immutable, so concurrent
+    // calls on one plan with distinct workspaces never share a stream or an event)
+    HostPipe pipe;
+    HostPipe* p = &pipe;
     const stda_config& c = plan->cfg;
     const size_t HW = (size_t)c.map_height * c.map_width;
     const size_t in_tri = c.input_frames * HW, in_bytes = align_up(chunk * in_tri * 4),

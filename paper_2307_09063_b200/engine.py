@@ -8,6 +8,7 @@ library is missing or the tensor is not on a CUDA device.
 
 from __future__ import annotations
 
+import weakref
 from typing import Optional
 
 import numpy as np
@@ -26,7 +27,61 @@ def _stream_ptr(device: torch.device) -> int:
     return torch.cuda.current_stream(device).cuda_stream
 
 
+# ---- plan cache -------------------------------------------------------------------
+# Plans live in a module-level weak dictionary keyed by the module (not on the module:
+# a module stays deepcopy-able and picklable after a forward, and a copy never shares or
+# double-frees a plan handle).  The per-call validity check is cheap: the cached list of
+# the module's parameters/buffers, their `_version` counters (every in-place write through
+# autograd-visible ops — optimizer steps, load_state_dict, copy_ under no_grad — bumps
+# them) and a global generation counter bumped whenever any module registers a parameter
+# or buffer (attribute re-assignment, load_state_dict(assign=True)).  `.to()` / `.cuda()`
+# swap `.data` without a version bump, so the model classes drop their plans in `_apply`;
+# other `.data` swaps or writes need `invalidate_engine()`.
+_PLANS: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+_GENERATION = [0]
+
+
+def _bump_generation(*_args):
+    _GENERATION[0] += 1
+
+
+torch.nn.modules.module.register_module_parameter_registration_hook(_bump_generation)
+torch.nn.modules.module.register_module_buffer_registration_hook(_bump_generation)
+
+
+class _Entry:
+    __slots__ = ("generation", "tensors", "versions", "ptrs", "plans", "grad_anchor")
+
+    def __init__(self, module):
+        self.generation = _GENERATION[0]
+        self.tensors = list(module.parameters()) + list(module.buffers())
+        self.versions = [t._version for t in self.tensors]
+        self.ptrs = [t.data_ptr() for t in self.tensors]
+        self.plans = {}            # (precision, device) -> plan
+        params = list(module.parameters())
+        self.grad_anchor = params[0] if params else None
+
+    def valid(self) -> bool:
+        return (self.generation == _GENERATION[0]
+                and self.versions == [t._version for t in self.tensors])
+
+
+def invalidate(module) -> None:
+    """Drop the cached plans of `module` (and of its submodules' block plans)."""
+    for m in module.modules():
+        _PLANS.pop(m, None)
+
+
+def _entry(module) -> _Entry:
+    e = _PLANS.get(module)
+    if e is None or not e.valid():
+        e = _Entry(module)
+        _PLANS[module] = e
+    return e
+
+
 def _state_key(module: torch.nn.Module, precision: str, device: torch.device):
+    """Full content key (storage pointers + versions); the per-call check uses `_entry`."""
     key = [precision, str(device)]
     for t in list(module.parameters()) + list(module.buffers()):
         key.append((t.data_ptr(), t._version))
@@ -43,6 +98,19 @@ class _Plan:
         self.device = device
         self.precision = precision
         self.handle = L.plan_create(cfg, blob, _PREC_ID[precision], device.index or 0)
+        self.ws = {}               # stream -> cached workspace (small workspaces only)
+
+    def workspace(self, nbytes: int, stream: int) -> torch.Tensor:
+        """A device workspace of >= nbytes for work ordered on `stream`.  Workspaces up to
+        256 MiB are kept per stream and reused by later calls on the same stream (stream
+        order serialises them); larger ones come fresh from torch's caching allocator."""
+        if nbytes > (256 << 20):
+            return torch.empty(nbytes, device=self.device, dtype=torch.uint8)
+        ws = self.ws.get(stream)
+        if ws is None or ws.numel() < nbytes:
+            ws = torch.empty(nbytes, device=self.device, dtype=torch.uint8)
+            self.ws[stream] = ws
+        return ws
 
     def __del__(self):
         h = getattr(self, "handle", None)
@@ -62,15 +130,41 @@ def _device_of(x: torch.Tensor) -> torch.device:
 
 def _net_plan(net, device: torch.device) -> _Plan:
     from .fold import fold_state_dict
-    key = _state_key(net, net.precision, device)
-    cache = getattr(net, "_engine_cache", None)
-    if cache is not None and cache[0] == key:
-        return cache[1]
-    sd = {k: v.detach() for k, v in net.state_dict().items()}
-    blob = fold_state_dict(net.config, sd)
-    plan = _Plan(net.config, blob, net.precision, device)
-    net._engine_cache = (key, plan)
+    e = _entry(net)
+    k = (net.precision, device)
+    plan = e.plans.get(k)
+    if plan is None:
+        sd = {n: v.detach() for n, v in net.state_dict().items()}
+        blob = fold_state_dict(net.config, sd)
+        plan = _Plan(net.config, blob, net.precision, device)
+        e.plans[k] = plan
     return plan
+
+
+class _InferenceOnly(torch.autograd.Function):
+    """Autograd node on an engine output computed with grad mode on: the output keeps an
+    autograd link (like the reference's eval forward) and backward raises clearly instead
+    of the engine silently returning a detached tensor."""
+
+    @staticmethod
+    def forward(ctx, y, anchor):
+        return y
+
+    @staticmethod
+    def backward(ctx, grad):
+        raise RuntimeError(
+            "StdaNet eval-mode forwards run on the B200 inference engine, which has no "
+            "backward pass; call .train() (the module's own autograd graph) to differentiate")
+
+
+def _link_autograd(module, x: torch.Tensor, y: torch.Tensor) -> torch.Tensor:
+    if not torch.is_grad_enabled():
+        return y
+    anchor = _entry(module).grad_anchor
+    if x.requires_grad or any(p.requires_grad for p in module.parameters()):
+        a = x if x.requires_grad else anchor
+        return _InferenceOnly.apply(y, a)
+    return y
 
 
 def _as_input(x: torch.Tensor) -> torch.Tensor:
@@ -90,9 +184,9 @@ def forward(net, x: torch.Tensor) -> torch.Tensor:
     plan = _net_plan(net, device)
     with torch.cuda.device(device):
         L = plan.L
-        ws = torch.empty(L.workspace_bytes(plan.handle, B), device=device, dtype=torch.uint8)
-        L.forward(plan.handle, x.data_ptr(), y.data_ptr(), B, ws.data_ptr(), ws.numel(),
-                  _stream_ptr(device))
+        stream = _stream_ptr(device)
+        ws = plan.workspace(L.workspace_bytes(plan.handle, B), stream)
+        L.forward(plan.handle, x.data_ptr(), y.data_ptr(), B, ws.data_ptr(), ws.numel(), stream)
     return y
 
 
@@ -165,13 +259,12 @@ class _BlockPlan:
 
 def _block_plan(block, kind: str, device: torch.device) -> _BlockPlan:
     from .fold import fold_block
-    key = _state_key(block, "fp32", device)
-    cache = getattr(block, "_engine_cache", None)
-    if cache is not None and cache[0] == key:
-        return cache[1]
-    blob, cin = fold_block(block, kind)
-    plan = _BlockPlan(0 if kind == "enc" else 1, cin, blob, device)
-    block._engine_cache = (key, plan)
+    e = _entry(block)
+    plan = e.plans.get(("fp32", device))
+    if plan is None:
+        blob, cin = fold_block(block, kind)
+        plan = _BlockPlan(0 if kind == "enc" else 1, cin, blob, device)
+        e.plans[("fp32", device)] = plan
     return plan
 
 

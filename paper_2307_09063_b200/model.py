@@ -13,8 +13,11 @@ Mirrors the reference module API (`/root/reference/pkg/stda/src/stda/model.py`):
 Execution contract:
 
 * eval mode + CUDA float32 input  -> the B200 engine (C ABI `libstda_b200.so`); the
-  folded weights are cached on the module and rebuilt whenever a parameter or
-  buffer changes (tracked through tensor `_version` counters and storage pointers);
+  folded weights are cached per module (engine.py: a weak module -> plan map, so the
+  module stays picklable / deepcopy-able) and rebuilt whenever a parameter or buffer
+  changes (tensor `_version` counters, parameter registration, `.to()`); `.data`
+  writes need `invalidate_engine()`.  With grad mode on, the output keeps an autograd
+  link whose backward raises (the engine is inference-only);
 * eval mode + CPU tensor          -> `RuntimeError`: there is no CPU inference path;
 * training mode                   -> the module's own autograd graph (BatchNorm batch
   statistics, gradients); that is the training path the reference's `train()` drives
@@ -69,6 +72,21 @@ class StdaConfig:
         return tuple((c << i, c << (i + 1)) for i in range(self.stages))
 
 
+class _EngineModule(nn.Module):
+    """Base of the engine-backed modules: plan-cache invalidation hooks."""
+
+    def _apply(self, fn, *args, **kwargs):
+        # .to() / .cuda() / .double() swap parameter storage without a version bump
+        _engine.invalidate(self)
+        return super()._apply(fn, *args, **kwargs)
+
+    def invalidate_engine(self) -> None:
+        """Drop the cached folded weights / device plans.  Needed only after writes the
+        cache cannot see: `.data` assignments or in-place writes through `.data` (every
+        autograd-visible in-place write, load_state_dict and .to() are tracked)."""
+        _engine.invalidate(self)
+
+
 def _eval_cuda_input(module: nn.Module, x: torch.Tensor) -> bool:
     """True when the engine must run; raises for eval-mode CPU tensors."""
     if module.training:
@@ -89,7 +107,7 @@ def _check_4d(x: torch.Tensor, what: str) -> None:
         raise RuntimeError(f"{what}: expected 4D input (got {x.dim()}D input)")
 
 
-class MobileEncoderBlock(nn.Module):
+class MobileEncoderBlock(_EngineModule):
     """c -> 2c channels, (h, w) -> (h/2, w/2) (reference model.py:30-53).
 
     Stage 1 = relu(BN(conv1x1) + BN(conv3x3) + BN(x)); stage 2 = relu(BN(conv3x3 s2))
@@ -112,12 +130,12 @@ class MobileEncoderBlock(nn.Module):
             raise ValueError(f"spatial dims must be even, got {tuple(x.shape[-2:])}")
         if _eval_cuda_input(self, x):
             _check_4d(x, "MobileEncoderBlock")
-            return _engine.encoder_block(self, x)
+            return _engine._link_autograd(self, x, _engine.encoder_block(self, x))
         mixed = self.relu(self.branch_1x1(x) + self.branch_3x3(x) + self.branch_id(x))
         return self.relu(self.down(mixed)) + self.residual(x)
 
 
-class MobileDecoderBlock(nn.Module):
+class MobileDecoderBlock(_EngineModule):
     """2c -> c channels, (h, w) -> (2h, 2w) (reference model.py:56-79)."""
 
     def __init__(self, channels: int):
@@ -134,7 +152,7 @@ class MobileDecoderBlock(nn.Module):
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         if _eval_cuda_input(self, x):
             _check_4d(x, "MobileDecoderBlock")
-            return _engine.decoder_block(self, x)
+            return _engine._link_autograd(self, x, _engine.decoder_block(self, x))
         mixed = self.relu(self.branch_1x1(x) + self.branch_3x3(x) + self.branch_id(x))
         return self.relu(self.up(mixed)) + self.residual(x)
 
@@ -152,18 +170,18 @@ class EcaBlock(nn.Module):
         """Per-(sample, channel) gates in (0, 1) (model.py:91-94)."""
         if _eval_cuda_input(self, x):
             _check_4d(x, "EcaBlock")
-            return _engine.eca_gates(self, x)
+            return _engine._link_autograd(self, x, _engine.eca_gates(self, x))
         pooled = x.mean(dim=(-2, -1))
         return torch.sigmoid(self.conv(pooled.unsqueeze(1)).squeeze(1))
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         if _eval_cuda_input(self, x):
             _check_4d(x, "EcaBlock")
-            return _engine.eca_apply(self, x)
+            return _engine._link_autograd(self, x, _engine.eca_apply(self, x))
         return x * self.channel_weights(x).unsqueeze(-1).unsqueeze(-1)
 
 
-class StdaNet(nn.Module):
+class StdaNet(_EngineModule):
     """Spatio-temporal denoising autoencoder over map triplets (reference model.py:131-199).
 
     `precision` selects the engine arithmetic for eval forwards: "fp32" (default;
@@ -189,7 +207,6 @@ class StdaNet(nn.Module):
             self.decoder_attention.append(EcaBlock(config.eca_kernel))
         self.head = nn.Conv2d(c, 1, 3, padding=1)
         self.set_precision(precision)
-        self._engine_cache = None
         self._audit_shapes()
 
     def set_precision(self, precision: str) -> "StdaNet":
@@ -231,7 +248,7 @@ class StdaNet(nn.Module):
                 f"got {tuple(x.shape)}")
         if _eval_cuda_input(self, x):
             _check_4d(x, "StdaNet")
-            return _engine.forward(self, x)
+            return _engine._link_autograd(self, x, _engine.forward(self, x))
         skips = [self.stem(x)]
         out = skips[0]
         for encoder, attention in zip(self.encoders, self.encoder_attention):
@@ -263,14 +280,18 @@ class StdaNet(nn.Module):
         return _engine.forward_host(self, x, out)
 
 
-def load_checkpoint(path, device: str = "cuda"):
-    """Load a reference checkpoint (train.py:186-193) into the drop-in; eval mode."""
+def load_checkpoint(path, device: Optional[str] = None):
+    """Load a reference checkpoint (train.py:186-193) into the drop-in: `(model, metadata)`,
+    model in eval mode.  Like the reference the model stays on the CPU unless `device` is
+    given (eval forwards then need `.cuda()`: the engine has no CPU inference path)."""
     blob = torch.load(path, map_location="cpu", weights_only=True)
     meta = blob["metadata"]
     model = StdaNet(StdaConfig(**meta["model_config"]))
     model.load_state_dict(blob["state_dict"])
     model.eval()
-    return model.to(device), meta
+    if device is not None:
+        model = model.to(device)
+    return model, meta
 
 
 def config_dict(cfg: StdaConfig) -> dict:

@@ -1,6 +1,6 @@
 """Generate golden vectors by running the REAL reference in the build container.
 
-    PYTHONPATH=/root/reference/pkg/stda/src python tests/golden/make_golden.py
+    PYTHONPATH=/root/reference/pkg/stda/src python tests/golden/make_golden.py [case ...]
 
 For each case: seed torch, build the reference `stda.StdaNet(StdaConfig(...))`,
 optionally randomise every BatchNorm's running stats and affine (seeded), switch to
@@ -36,7 +36,12 @@ CASES = [
                                 map_height=16, map_width=16), 2, True, 3),
     ("default_128x64", dict(), 2, False, 4),
     ("default_128x128_bn", dict(map_height=128, map_width=128), 2, True, 5),
+    # BASELINE config 3 / 5 map sizes; inputs from oracle/synth.py (the generator's host
+    # restatement: scene "default" at 256^2, "dense" at 512^2)
+    ("default_256x256_bn", dict(map_height=256, map_width=256), 2, True, 6),
+    ("dense_512x512_bn", dict(map_height=512, map_width=512), 1, True, 7),
 ]
+SYNTH_SCENE = {"default_256x256_bn": 0, "dense_512x512_bn": 1}
 
 
 def rd_triplets(rng: np.random.Generator, batch: int, frames: int, h: int, w: int) -> np.ndarray:
@@ -75,21 +80,29 @@ def randomise_bn(model: torch.nn.Module, gen: torch.Generator) -> None:
                 m.bias.copy_(torch.randn(n, generator=gen) * 0.2)
 
 
-def main() -> None:
+def main(only=None) -> None:
     sys.path.insert(0, REF_SRC)
+    sys.path.insert(0, str(HERE.parents[1]))
+    from oracle import synth as osynth
     import stda  # the reference package
     from stda import StdaConfig, StdaNet, parameter_count
 
-    index = {}
+    index = json.loads((HERE / "index.json").read_text()) if only else {}
     for name, kw, batch, bn_rand, seed in CASES:
+        if only and name not in only:
+            continue
         torch.manual_seed(seed)
         cfg = StdaConfig(**kw)
         net = StdaNet(cfg)
         if bn_rand:
             randomise_bn(net, torch.Generator().manual_seed(1000 + seed))
         net.eval()                                   # before any forward
-        x = rd_triplets(np.random.default_rng(seed), batch, cfg.input_frames,
-                        cfg.map_height, cfg.map_width)
+        if name in SYNTH_SCENE:
+            x = osynth.triplets(batch, cfg.map_height, cfg.map_width, seed=seed,
+                                scene=SYNTH_SCENE[name])
+        else:
+            x = rd_triplets(np.random.default_rng(seed), batch, cfg.input_frames,
+                            cfg.map_height, cfg.map_width)
         with torch.no_grad():
             y = net(torch.from_numpy(x)).numpy()
             net64 = StdaNet(cfg)
@@ -115,4 +128,4 @@ def main() -> None:
 
 
 if __name__ == "__main__":
-    main()
+    main(sys.argv[1:] or None)   # optional case names: regenerate only those
