@@ -98,6 +98,7 @@ def test_plan_cache_sees_writes():
 
 
 @pytest.mark.gpu
+@pytest.mark.grad_mode
 def test_eval_grad_mode_output_raises_on_backward():
     torch.manual_seed(0)
     net = StdaNet(StdaConfig(map_height=64, map_width=64)).eval().cuda()
