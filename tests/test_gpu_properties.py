@@ -190,6 +190,7 @@ def test_row_band_conv_path():
     import sys
     code = (
         "import torch, numpy as np\n"
+        "torch.set_grad_enabled(False)\n"
         "from paper_2307_09063_b200 import StdaConfig, StdaNet\n"
         "from paper_2307_09063_b200.synth import synth_triplets\n"
         "for hw, b in ((128, 4), (256, 2)):\n"
@@ -218,6 +219,7 @@ def test_schedule_orders_do_not_change_results():
     import sys
     code = (
         "import torch, numpy as np, os\n"
+        "torch.set_grad_enabled(False)\n"
         "from paper_2307_09063_b200 import StdaConfig, StdaNet\n"
         "from paper_2307_09063_b200.synth import synth_triplets\n"
         "torch.manual_seed(7)\n"

@@ -4,6 +4,7 @@ from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import torch
+torch.set_grad_enabled(False)
 
 from paper_2307_09063_b200 import StdaConfig, StdaNet
 from paper_2307_09063_b200.synth import synth_triplets
