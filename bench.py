@@ -130,6 +130,26 @@ def layer_operand_bytes(cfg, precision: str) -> dict:
     return out
 
 
+def fuse_names(names, cfg, fl: dict, byt: dict, opb: dict) -> None:
+    """Entries for fused launches ("stem+enc0.s1": the stem computed inside the enc0.s1
+    tcgen05 kernel): FLOPs and operand bytes add up; the algorithmic bytes are the parts'
+    minus the intermediate the fusion keeps on chip (the stem output is still written once
+    as planes, but enc0.s1 no longer reads it)."""
+    for n in names:
+        if "+" not in n:
+            continue
+        parts = n.split("+")
+        fl[n] = sum(fl[q] for q in parts)
+        byt[n] = sum(byt[q] for q in parts)
+        if parts[:2] == ["stem", "enc0.s1"]:
+            byt[n] -= 4 * cfg.stem_channels * cfg.map_height * cfg.map_width
+        if any(q in opb for q in parts):
+            opb[n] = sum(opb.get(q, 0) for q in parts)
+        for q in parts:             # no double counting in the per-forward totals
+            for dct in (fl, byt, opb):
+                dct.pop(q, None)
+
+
 def ncu_traffic(kernel: str, batch: int, H: int, W: int, precision: str):
     """DRAM bytes per launch of `kernel` from a committed ncu --set full capture
     (profiles/ncu_traffic.json, written from the capture's raw page), or None."""
@@ -459,6 +479,7 @@ def run_engine(args, world, rank, local):
     total_flops = sum(fl.values())
     byt = layer_bytes(cfg)
     opb = layer_operand_bytes(cfg, args.precision)
+    fuse_names(names, cfg, fl, byt, opb)
     sm_ghz = (clocks.summary().get("sm_max_mhz") or 1965.0) / 1000.0
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
     floor_us = {n: b * batch / (128.0 * n_sm * sm_ghz * 1e3) for n, b in opb.items()}
@@ -630,6 +651,7 @@ def run_stream(args, world, rank, local):
     dom = max(share, key=share.get)
     hbm, bf16, _, peak_kind = peaks()
     fl, byt = layer_flops(cfg), layer_bytes(cfg)
+    fuse_names(names, cfg, fl, byt, {})
     if fl[dom]:
         ach = fl[dom] * n_out / (share[dom] * 1e-3) / 1e12
         roof = {"bound": "tensor", "kernel": dom, "achieved": ach, "peak": bf16, "unit": "TFLOP/s",

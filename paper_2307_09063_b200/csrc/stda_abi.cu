@@ -166,6 +166,7 @@ struct stda_plan {
   }
 
   bool use_tc = false;  // every encoder/decoder conv runs on the tcgen05 kernel
+  bool stem_fused = false;  // the stem runs inside the enc0.s1 tcgen05 kernel (tc_launch_stem)
   float* head_wt = nullptr;  // head weights [9][c0] for the NHWC head kernel
   std::vector<float> stem_canon;  // host copy of the stem's canonical weights + bias (constant-bank stem)
   std::vector<float> head_host;   // host copy of head_wt (constant-bank strip head)
@@ -313,19 +314,35 @@ void run_net_tc(const stda_plan& p, const Src& x, float* y, int64_t B, const Net
   // stage-1 outputs: PP for encoder stride-2 consumers, PL for decoder ConvT consumers
   const std::vector<PlBuf>& mviews = w.pl_m;
   (void)np;
-  launch_stem_planes(p.stem.w, p.stem.b, x, c.input_frames, c0, w.pl_s, w.pp_s, B, h, wd, bf, st,
-                     p.stem_canon.empty() ? nullptr : p.stem_canon.data());
-  mk.mark(st);
+  // stem: fused into the enc0.s1 kernel when the plan and this input allow it
+  tc::TcStem stem;
+  stem.x = x;
+  stem.F = c.input_frames;
+  stem.s_pl = w.pl_s;
+  stem.s_pp = w.pp_s;
+  stem.has_pl = true;
+  stem.canon = p.stem_canon.empty() ? nullptr : p.stem_canon.data();
+  const bool fuse_stem = p.stem_fused && tc::tc_stem_fusable(p.enc[0].s1_tc, stem, h, wd);
+  if (!fuse_stem) {
+    launch_stem_planes(p.stem.w, p.stem.b, x, c.input_frames, c0, w.pl_s, w.pp_s, B, h, wd, bf, st,
+                       p.stem_canon.empty() ? nullptr : p.stem_canon.data());
+    if (!p.stem_fused) mk.mark(st);  // (fused plans profile stem + enc0.s1 as one launch)
+  }
   PlBuf cur_pl = w.pl_s, cur_pp = w.pp_s;
   std::vector<PlBuf> skips{w.pl_s};
   for (int i = 0; i < S; ++i) {
     const EncLayers& E = p.enc[i];
     tc::TcLayerDesc d1 = E.s1_tc, d2 = E.s2_tc;
-    const tc::TcGeometry g1 = tc::tc_plan(d1, (int)B, h, wd);
     tc::TcOut o1;
     o1.mode = 2;  // phase planes for the stride-2 consumer
     o1.pl = mviews[i];
-    tc::tc_launch(d1, g1, cur_pl, nullptr, o1, true, st, /*rev=*/true);
+    if (i == 0 && fuse_stem) {
+      const tc::TcGeometry g1 = tc::tc_plan_stem(d1, (int)B, h, wd, c.input_frames);
+      tc::tc_launch_stem(d1, g1, stem, o1, st, /*rev=*/true);
+    } else {
+      const tc::TcGeometry g1 = tc::tc_plan(d1, (int)B, h, wd);
+      tc::tc_launch(d1, g1, d1.mode == CONV3_S1P ? cur_pp : cur_pl, nullptr, o1, true, st, /*rev=*/true);
+    }
     mk.mark(st);
     const tc::TcGeometry g2 = tc::tc_plan(d2, (int)B, h, wd);
     tc::TcOut o2;
@@ -443,11 +460,11 @@ void run_net(const stda_plan& p, const Src& x, float* y, int64_t B, const NetWs&
   mk.mark(st);
 }
 
-std::string launch_names(const stda_config& c, bool tc) {
-  std::string s = "stem";
+std::string launch_names(const stda_config& c, bool tc, bool stem_fused = false) {
+  std::string s = stem_fused ? "" : "stem;";
   for (int i = 0; i < c.stages; ++i)
-    s += ";enc" + std::to_string(i) + ".s1;enc" + std::to_string(i) + ".s2;enc" + std::to_string(i) +
-         ".gate";
+    s += std::string(i ? ";" : "") + (i == 0 && stem_fused ? "stem+" : "") + "enc" + std::to_string(i) +
+         ".s1;enc" + std::to_string(i) + ".s2;enc" + std::to_string(i) + ".gate";
   for (int j = 0; j < c.stages; ++j) {
     s += ";dec" + std::to_string(j) + ".s1;dec" + std::to_string(j) + ".s2";
     if (!tc || j + 1 < c.stages) s += ";dec" + std::to_string(j) + ".gate";  // tc: last gate fused into head
@@ -533,11 +550,23 @@ int stda_plan_create(const stda_config* cfg, const float* blob, size_t n_floats,
       E.rs = p->make_layer(CONV3_S2, ch, 2 * ch, src);
       if (p->use_tc) {
         const size_t n1 = (size_t)ch * ch * 9, n2 = (size_t)2 * ch * ch * 9;
-        E.s1_tc = p->make_tc(CONV3_S1, ch, ch, w_s1, w_s1 + n1, nullptr, nullptr, cfg->map_width >> i);
+        // encoder stage 1 reads the phase planes its stride-2 partner reads anyway (stem /
+        // encoder gate PP) and writes the 2x2 output phases of one A read per shift
+        const int m1 = tc::s1p_enabled() && tc::tc_supported(CONV3_S1P, ch, ch) ? CONV3_S1P : CONV3_S1;
+        E.s1_tc = p->make_tc(m1, ch, ch, w_s1, w_s1 + n1, nullptr, nullptr, cfg->map_width >> i);
         E.s2_tc = p->make_tc(CONV3_S2, ch, 2 * ch, w_dn, w_dn + n2, w_rs, w_rs + n2, 0);
       }
       E.eca = p->make_vec(k, src);
       p->enc.push_back(E);
+      if (i == 0 && p->use_tc) {
+        // static part of tc_stem_fusable (the input's alignment / strides are checked per call)
+        static const bool fused_on = [] {
+          const char* e = std::getenv("STDA_STEM_FUSED");
+          return !(e && e[0] == '0');
+        }();
+        p->stem_fused = fused_on && E.s1_tc.mode == CONV3_S1 && c0 == 16 && cfg->input_frames <= 4 &&
+                        cfg->map_width % 4 == 0 && cfg->map_width <= 128;
+      }
     }
     for (int j = 0; j < S; ++j) {
       const int c2 = c0 << (S - j), ch = c2 / 2;
@@ -584,7 +613,8 @@ void stda_plan_destroy(stda_plan* plan) {
 int stda_launches_per_forward(const stda_plan* plan) {
   if (!plan) return -1;
   if (plan->kind != 0) return 2;
-  return (plan->use_tc ? 1 : 2) + 6 * plan->cfg.stages;  // tensor-core path: last gate fused in head
+  // tensor-core path: last gate fused in head; the stem fused into enc0.s1 when possible
+  return (plan->use_tc ? 1 : 2) + 6 * plan->cfg.stages - (plan->stem_fused ? 1 : 0);
 }
 
 int stda_kernels_per_forward(const stda_plan* plan) {
@@ -657,7 +687,7 @@ int stda_forward_profiled(const stda_plan* plan, const float* x, float* y, int64
 
 const char* stda_launch_names(const stda_plan* plan) {
   static thread_local std::string names;
-  names = (plan && plan->kind == 0) ? launch_names(plan->cfg, plan->use_tc) : std::string();
+  names = (plan && plan->kind == 0) ? launch_names(plan->cfg, plan->use_tc, plan->stem_fused) : std::string();
   return names.c_str();
 }
 

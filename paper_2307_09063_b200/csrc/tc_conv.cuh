@@ -100,7 +100,12 @@ struct TcGeometry {
 };
 
 bool tc_supported(int mode, int cin, int cout);
-TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W);
+bool s1p_enabled();  // encoder stride-1 convs as CONV3_S1P over phase planes (env STDA_TC_S1P)
+// extra_smem: bytes a kernel variant needs besides the rings / weights (the fused stem's
+// frame-row ring); resident_only: weights must stay resident
+TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W, size_t extra_smem = 0, bool resident_only = false);
+
+
 
 // Output of one launch: either operand planes (PL over the output grid, or PP phase
 // planes of it) or NHWC fp32 with per-item channel sums gap [B][items_per_image][cout].
@@ -116,6 +121,25 @@ struct TcOut {
 // last (still in L2) the first thing stage 2 reads.
 void tc_launch(const TcLayerDesc& d, const TcGeometry& g, const PlBuf& src0, const PlBuf* src1,
                const TcOut& out, bool relu0, cudaStream_t st, bool rev = false);
+
+// ---- fused stem + first encoder stride-1 conv --------------------------------------------
+// The stem (F frames -> 16 channels, relu(conv3x3), model.py:141-144) computed by extra
+// warps of the enc0.s1 tcgen05 kernel directly into its A stages; the stem output is
+// still written once as operand planes (PP for enc0.s2's residual, PL for the head).
+struct TcStem {
+  Src x;                          // frames (NCHW or stream windows), x.xp == 1
+  int F = 3;
+  PlBuf s_pl, s_pp;               // stem output planes
+  bool has_pl = true;
+  const float* canon = nullptr;   // host: canonical stem weights [16][F][3][3] + bias [16]
+};
+// true when the fused kernel covers this layer / input (C0 = 16, F <= 4, plain S1 layer,
+// W % 4 == 0, W <= 128: the position tiles' halo recompute stays <= 1.5x); env
+// STDA_STEM_FUSED=0 disables it
+bool tc_stem_fusable(const TcLayerDesc& d1, const TcStem& s, int H, int W);
+TcGeometry tc_plan_stem(TcLayerDesc& d1, int B, int H, int W, int F);
+void tc_launch_stem(const TcLayerDesc& d1, const TcGeometry& g, const TcStem& s, const TcOut& out,
+                    cudaStream_t st, bool rev);
 
 // Debug: record a clock64 timeline of CTA 0 (see tc_kernel.cuh trace_at) into dev_buf
 // during the launch_index-th following tc_launch.

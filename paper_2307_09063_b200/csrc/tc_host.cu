@@ -29,6 +29,12 @@ struct HostTap {
 
 std::vector<HostTap> plane_taps(int mode, int pl) {
   std::vector<HostTap> t;
+  if (mode == CONV3_S1P) {
+    // the plane's 4 shift groups (dy, dx = half-resolution shift; acc = first phase of the
+    // run); only used for the staged position span (lo / hi) — packing is group-wise
+    for (int gi = 0; gi < 4; ++gi) t.push_back({s1p_p0(pl, gi), s1p_dy(pl, gi), s1p_dx(pl, gi), -1});
+    return t;
+  }
   if (mode == CONV3_S1 || mode == CONV3_ROWS) {
     for (int ky = 0; ky < 3; ++ky)
       for (int kx = 0; kx < 3; ++kx) t.push_back({0, ky - 1, kx - 1, ky * 3 + kx});
@@ -76,8 +82,17 @@ bool half_t_enabled() {  // env STDA_TC_HALF=0 keeps 3-MMA full ConvT items (A/B
 }
 
 bool tc_supported(int mode, int cin, int cout) {
-  (void)mode;
+  if (mode == CONV3_S1P && cout > 32) return false;  // fp32 concat: 4 phases x 2N <= 256 per MMA
   return cin % 16 == 0 && cin >= 16 && cin <= 64 && (cout == 16 || cout == 32 || cout == 64);
+}
+
+// env STDA_TC_S1P=0: encoder stride-1 convs on the plain S1 kernel over PL (A/B timing)
+bool s1p_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("STDA_TC_S1P");
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }
 
 // env STDA_TC_ROWS=1: stride-1 layers over 128k-wide planes as row bands (CONV3_ROWS).
@@ -95,7 +110,7 @@ bool rows_enabled() {
 void tc_pack_layer(TcLayerDesc& d, int mode, int cin, int cout, const float* w0, const float* w1,
                    bool bf16, std::vector<uint16_t>& packed, int plane_w) {
   STDA_CHECK(tc_supported(mode, cin, cout), "layer shape not supported by the tensor-core path");
-  STDA_CHECK((mode == CONV3_S1) == (w1 == nullptr), "S1 layers are single-source, S2/T dual");
+  STDA_CHECK((mode == CONV3_S1 || mode == CONV3_S1P) == (w1 == nullptr), "S1 layers are single-source, S2/T dual");
   // stride-1 layers over planes whose width is a multiple of 128 run as row bands (one A
   // read per input row serves three dy taps) when three stacked tap blocks fit one MMA
   if (mode == CONV3_S1 && rows_enabled() && plane_w > 0 && plane_w % 128 == 0 && 3 * (bf16 ? 1 : 2) * cout <= 256)
@@ -118,11 +133,12 @@ void tc_pack_layer(TcLayerDesc& d, int mode, int cin, int cout, const float* w0,
   d.n_src = w1 ? 2 : 1;
   d.cin = cin;
   d.cout = cout;
-  d.n_planes = mode == CONV3_S2 ? 4 : 1;
+  d.n_planes = n_planes_of(mode);
   d.n_acc_src = nacc_src(mode);
   d.npass = bf16 ? 1 : 3;
   const int npassB = bf16 ? 1 : 2;
   const int wk_per = tmode ? 16 : 9;
+  if (mode == CONV3_S1P) STDA_CHECK(!w1, "phase-plane conv is single-source");
   const int n_halves = mode == CONVT4_HALF ? 2 : 1;  // HALF: py = 0 taps, then py = 1 taps
   std::vector<std::vector<HostTap>> taps(d.n_planes * n_halves);
   for (int pl = 0; pl < d.n_planes * n_halves; ++pl) taps[pl] = plane_taps(mode, pl);
@@ -156,6 +172,38 @@ void tc_pack_layer(TcLayerDesc& d, int mode, int cin, int cout, const float* w0,
     const float hi = bf16_val(v);
     packed.push_back(bf16_bits(pass == 0 ? v : v - hi));
   };
+  if (mode == CONV3_S1P) {
+    // per chunk (input plane, 16-channel group), per shift group gi: the stacked tiles
+    // [kgrp 2][phase slot n][pass][cout][8]; tile j = output phase p0 + j reads input
+    // plane (qy, qx) at shift (sy, sx) through the 3x3 tap dy = 2sy + qy - py,
+    // dx = 2sx + qx - px (zero tile for a phase of the run that does not use the shift)
+    std::vector<int> seen(36, 0);
+    for (int c = 0; c < n_chunks; ++c) {
+      const int pl = c / cgroups, cgi = c % cgroups, qy = pl >> 1, qx = pl & 1;
+      for (int gi = 0; gi < 4; ++gi)
+        for (int kg = 0; kg < 2; ++kg)
+          for (int j = 0; j < s1p_n(pl, gi); ++j) {
+            const int acc = s1p_p0(pl, gi) + j, py = acc >> 1, px = acc & 1;
+            const bool used = s1p_uses(pl, gi, acc);
+            const int dy = 2 * s1p_dy(pl, gi) + qy - py, dx = 2 * s1p_dx(pl, gi) + qx - px;
+            if (used) {
+              STDA_CHECK(dy >= -1 && dy <= 1 && dx >= -1 && dx <= 1, "internal: phase-plane taps");
+              if (cgi == 0 && kg == 0) seen[acc * 9 + (dy + 1) * 3 + (dx + 1)]++;
+            }
+            for (int pass = 0; pass < npassB; ++pass)
+              for (int n = 0; n < cout; ++n)
+                for (int e = 0; e < 8; ++e) {
+                  if (used) put(ws[0], n, cgi * 16 + kg * 8 + e, (dy + 1) * 3 + (dx + 1), pass);
+                  else packed.push_back(0);
+                }
+          }
+      d.chunk_off[c + 1] = (int64_t)packed.size() * 2;
+    }
+    for (int i = 0; i < 36; ++i) STDA_CHECK(seen[i] == 1, "internal: phase-plane products");
+    d.concat = !bf16;
+    STDA_CHECK(bf16 || 4 * 2 * cout <= 256, "phase-plane conv: stacked width");
+    return;
+  }
   if (mode == CONV3_ROWS) {
     // per chunk, per dx group: [kgrp 2][block dy = -1, 0, +1][pass hi(, lo)][cout][8]
     for (int c = 0; c < n_chunks; ++c) {
@@ -239,7 +287,7 @@ int slots_cap() {  // env STDA_TC_SLOTS (A/B timing), default kMaxSlots
 }
 }  // namespace
 
-TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W) {
+TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W, size_t extra_smem, bool resident_only) {
   TcGeometry g{};
   g.B = B;
   g.H = H;
@@ -249,6 +297,11 @@ TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W) {
     g.Wp = W / 2;
     g.Ho = H / 2;
     g.Wo = W / 2;
+  } else if (d.mode == CONV3_S1P) {  // half-resolution position grid, full-resolution output
+    g.Hp = H / 2;
+    g.Wp = W / 2;
+    g.Ho = H;
+    g.Wo = W;
   } else if (d.mode == CONVT4_S2 || d.mode == CONVT4_HALF) {
     g.Hp = H;
     g.Wp = W;
@@ -319,7 +372,7 @@ TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W) {
   uint32_t b_stage = 0;
   for (int c = 0; c < d.n_planes * (d.cin / 16); ++c)
     b_stage = std::max<uint32_t>(b_stage, (uint32_t)(d.chunk_off[c + 1] - d.chunk_off[c]));
-  const size_t fixed = 1024 + 80 + kEpiWarps * 64 * sizeof(float);
+  const size_t fixed = 1024 + 80 + kEpiWarps * 64 * sizeof(float) + extra_smem;
   const uint32_t w_total = (uint32_t)d.chunk_off[d.n_planes * (d.cin / 16)];
   const size_t w_res = (w_total + 127) / 128 * 128;
   // Prefer (1) a >= 2-deep smem pipeline, (2) two TMEM slots (the epilogue of item i
@@ -335,7 +388,7 @@ TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W) {
   // per item (A/B timing of load balance vs halo reuse)
   static const char* gmax_env = std::getenv("STDA_TC_GMAX");
   int gmax = gmax_env && (int)std::strlen(gmax_env) > d.mode ? gmax_env[d.mode] - '0' : 4;
-  if (d.mode == CONV3_S1 && !gmax_env) {
+  if ((d.mode == CONV3_S1 || d.mode == CONV3_S1P) && !gmax_env) {
     // load balance: the largest G that still gives every CTA >= 6 full items (fewer,
     // larger items leave the persistent CTAs with 2-4 rounds dominated by pipeline fill
     // and the last partial round).  Measured at C2 (B=64): enc0.s1 G=4, enc1.s1 / dec1.s1
@@ -361,6 +414,7 @@ TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W) {
       const int acc_cols = G * n_acc * d.cout * (d.concat ? 2 : 1);
       if (acc_cols * want_slots > 512 || G * n_acc > 32) continue;
       for (bool resident : {true, false}) {
+        if (resident_only && !resident) continue;
         int stages = 0;
         // measured: S1/T layers are slower beyond 3 stages; S2 layers (L2-fed) may go deeper
         static const int t_stages = [] {  // env STDA_TC_TSTAGES: ring depth cap of ConvT layers
@@ -454,6 +508,102 @@ void tc_debug_trace(void* dev_buf, int launch_index) {
   g_trace_countdown = launch_index;
 }
 
+namespace {
+// frame rows one item stages: the s rows its positions [q0-L-1, q0+128G+L+1) touch (+1 each side)
+int stem_xrows(int G, int L) { return (G * 128 + 2 * L + 1) / L + 2 + 2; }
+size_t stem_extra_smem(int G, int L, int F, int W) {
+  return 2 * ((size_t)F * stem_xrows(G, L) * W * 4) + 128;
+}
+}  // namespace
+
+bool tc_stem_fusable(const TcLayerDesc& d1, const TcStem& s, int H, int W) {
+  static const bool on = [] {
+    const char* e = std::getenv("STDA_STEM_FUSED");
+    return !(e && e[0] == '0');
+  }();
+  return on && s.canon && d1.mode == CONV3_S1 && d1.cin == kStemC && d1.cout == kStemC &&
+         s.F >= 1 && s.F <= kStemMaxF && s.x.xp == 1 && W % 4 == 0 && W <= 128 && H >= 2 &&
+         (reinterpret_cast<uintptr_t>(s.x.x) & 15) == 0 && s.x.xb % 4 == 0 && s.x.xc % 4 == 0 &&
+         s.s_pp.base != nullptr && s.s_pp.C == kStemC;
+}
+
+TcGeometry tc_plan_stem(TcLayerDesc& d1, int B, int H, int W, int F) {
+  return tc_plan(d1, B, H, W, stem_extra_smem(4, W + 1, F, W), /*resident_only=*/true);
+}
+
+void tc_launch_stem(const TcLayerDesc& d, const TcGeometry& g, const TcStem& s, const TcOut& out,
+                    cudaStream_t st, bool rev) {
+  STDA_CHECK(tc_stem_fusable(d, s, g.H, g.W), "fused stem: unsupported layer / input");
+  STDA_CHECK(g.resident, "fused stem: weights must be resident");
+  STDA_CHECK(out.mode == 2, "fused stem: enc0.s1 writes phase planes");
+  Params p;
+  std::memset(&p, 0, sizeof(p));
+  p.d = d;
+  p.out = out;
+  p.H = g.H;
+  p.W = g.W;
+  p.C = d.cin;
+  p.Hp = g.Hp;
+  p.Wp = g.Wp;
+  p.L = g.L;
+  p.L_mul = (uint32_t)((((uint64_t)1 << 32) + (uint64_t)g.L - 1) / (uint64_t)g.L);
+  STDA_CHECK((uint64_t)g.items_per_image * g.G * 128 * (uint64_t)g.L < ((uint64_t)1 << 32),
+             "fused stem: map too large for the position decode");
+  p.Ho = g.Ho;
+  p.Wo = g.Wo;
+  p.G = g.G;
+  p.stages = g.stages;
+  p.slots = g.slots;
+  p.items_per_image = g.items_per_image;
+  p.total_items = g.B * g.items_per_image;
+  p.tail = g.tail;
+  static const bool rev_on = [] {
+    const char* e = std::getenv("STDA_TC_REV");
+    return !(e && e[0] == '0');
+  }();
+  p.rev = rev && rev_on ? 1 : 0;
+  p.P_max = g.P_max;
+  p.a_stage_bytes = g.a_stage_bytes;
+  p.b_stage_bytes = g.b_stage_bytes;
+  p.cps = g.cps;
+  STDA_CHECK(g.cps == 1, "fused stem: one K chunk per stage");
+  p.chunk_a_bytes = g.chunk_a_bytes;
+  p.chunk_b_bytes = g.chunk_b_bytes;
+  p.resident = 1;
+  p.w_total = g.w_total;
+  p.slot_cols = (uint32_t)(g.G * d.n_src * d.n_acc_src * d.cout * (d.concat ? 2 : 1));
+  p.tmem_cols = (uint32_t)g.tmem_cols;
+  p.relu0 = 1;
+  // the stem
+  p.sx = s.x.x;
+  p.sxb = s.x.xb;
+  p.sxc = s.x.xc;
+  p.sF = s.F;
+  p.stem_xrows = stem_xrows(g.G, g.L);
+  p.stem_xstage = (uint32_t)((size_t)s.F * p.stem_xrows * g.W * 4);
+  STDA_CHECK(stem_extra_smem(g.G, g.L, s.F, g.W) <= stem_extra_smem(4, g.L, s.F, g.W), "internal: stem ring");
+  p.s_pl = s.s_pl;
+  p.s_has_pl = s.has_pl ? 1 : 0;
+  p.s_pp = s.s_pp;
+  for (int co = 0; co < kStemC; ++co) {
+    for (int ci = 0; ci < s.F; ++ci)
+      for (int t = 0; t < 9; ++t) p.stem_w[(ci * 9 + t) * kStemC + co] = s.canon[((size_t)co * s.F + ci) * 9 + t];
+    p.stem_b[co] = s.canon[(size_t)kStemC * s.F * 9 + co];
+  }
+  if (g_trace_buf != nullptr && g_trace_countdown-- == 0) {
+    p.trace = g_trace_buf;
+    g_trace_buf = nullptr;
+    if (const char* e = std::getenv("STDA_TC_DBG")) p.dbg = std::atoi(e);
+  }
+  if (p.total_items == 0) return;
+  int dev = 0, sms = 148;
+  STDA_CUDA(cudaGetDevice(&dev));
+  STDA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int grid = std::min(p.total_items, sms);
+  const int npm = d.npass == 1 ? kNpmBf16 : (d.concat ? kNpmConcat : kNpm3);
+  dispatch_stem(npm, g.G, p, grid, g.smem_bytes, st);
+}
+
 void tc_launch(const TcLayerDesc& d, const TcGeometry& g, const PlBuf& src0, const PlBuf* src1,
                const TcOut& out, bool relu0, cudaStream_t st, bool rev) {
   Params p;
@@ -464,7 +614,9 @@ void tc_launch(const TcLayerDesc& d, const TcGeometry& g, const PlBuf& src0, con
   STDA_CHECK((src1 != nullptr) == (d.n_src == 2), "source count mismatch");
   STDA_CHECK(src0.L == g.L && (!src1 || src1->L == g.L), "operand plane geometry mismatch");
   STDA_CHECK(src0.np == (d.npass == 3 ? 2 : 1), "operand plane precision mismatch");
-  STDA_CHECK((d.mode == CONV3_S2) == (src0.planes == 4), "stride-2 convs read phase planes");
+  STDA_CHECK((d.mode == CONV3_S2 || d.mode == CONV3_S1P) == (src0.planes == 4),
+             "stride-2 and phase-plane convs read phase planes");
+  STDA_CHECK(d.mode != CONV3_S1P || out.mode == 2, "phase-plane conv writes phase planes");
   p.out = out;
   p.H = g.H;
   p.W = g.W;
@@ -525,6 +677,7 @@ void tc_launch(const TcLayerDesc& d, const TcGeometry& g, const PlBuf& src0, con
   switch (d.mode) {
     case CONV3_S1: return dispatch_s1(d.cout, npm, g.G, p, grid, g.smem_bytes, st);
     case CONV3_ROWS: return dispatch_rows(d.cout, npm, g.G, p, grid, g.smem_bytes, st);
+    case CONV3_S1P: return dispatch_s1p(d.cout, npm, g.G, p, grid, g.smem_bytes, st);
     case CONV3_S2: return dispatch_s2(d.cout, npm, g.G, p, grid, g.smem_bytes, st);
     case CONVT4_HALF:
       STDA_CHECK(out.mode == 0, "half-phase ConvT writes NHWC fp32");

@@ -22,6 +22,14 @@ constexpr int kMmaWarp = 1;    // TMEM allocator + tcgen05.mma issuer
 constexpr int kEpiWarp0 = 2;   // warps 2..9: epilogue (warp % 4 = TMEM lane quarter)
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = (kEpiWarp0 + kEpiWarps) * 32;
+// fused stem (STEM kernels, stem + first encoder stride-1 conv): warps 10.. compute the
+// stem straight into the A stages (tc_kernel.cuh stem role); warp 0 stages the frame rows
+constexpr int kStemWarp0 = kEpiWarp0 + kEpiWarps;
+constexpr int kStemWarps = 4;
+constexpr int kStemThreads = kStemWarps * 32;
+constexpr int kThreadsStem = kThreads + kStemThreads;
+constexpr int kStemC = 16, kStemMaxF = 4;
+__host__ __device__ constexpr int threads_of(int stem) { return stem ? kThreadsStem : kThreads; }
 constexpr int kMaxSmem = 227 * 1024;
 constexpr int kMaxStages = 6;  // smem ring depth cap
 constexpr int kMaxSlots = 4;   // TMEM accumulator slots cap
@@ -54,6 +62,19 @@ struct Params {
   int dbg;                    // debug ablations (env STDA_TC_DBG; 0 in normal runs):
                               // 1 no epilogue stores, 2 no TMEM loads, 4 no A copies after
                               // the first fill, 8 epilogue only releases the slot
+  // ---- fused stem (STEM kernels only) ----
+  // frames: element (b, ci, y, x) at sx[b*sxb + ci*sxc + y*W + x] (NCHW or stream windows)
+  const float* sx;
+  int64_t sxb, sxc;
+  int sF;                     // input frames (<= kStemMaxF)
+  int stem_xrows;             // frame rows staged per item (x ring stage = sF * rows * W floats)
+  uint32_t stem_xstage;       // bytes per x ring stage
+  PlBuf s_pl, s_pp;           // stem output written as operand planes (enc0.s2 / head read them)
+  int s_has_pl;
+  // relu(conv3x3(frames)) weights [ci][ky][kx][co] (co pairs = 8-byte units) and bias, read
+  // from the parameter bank by every FFMA2 (uniform across the warp)
+  alignas(16) float stem_w[kStemMaxF * 9 * kStemC];
+  alignas(16) float stem_b[kStemC];
 };
 
 // ---- debug timeline (stda_debug_trace): clock64 stamps of CTA 0, one region per role ---
@@ -140,14 +161,51 @@ __host__ __device__ constexpr bool tap_first(int mode, int t) {
 }
 // accumulators per source
 __host__ __device__ constexpr int nacc_src(int mode) {
-  return mode == CONVT4_S2 ? 4 : mode == CONVT4_HALF ? 2 : 1;
+  return mode == CONVT4_S2 || mode == CONV3_S1P ? 4 : mode == CONVT4_HALF ? 2 : 1;
 }
 // minimum shift over a plane's taps, as a*L + b
 __host__ __device__ constexpr int plane_lo_a(int mode, int pl) {
-  return mode == CONV3_S2 ? (pl >= 2 ? -1 : 0) : -1;
+  return mode == CONV3_S2 ? (pl >= 2 ? -1 : 0) : mode == CONV3_S1P ? -(pl >> 1) : -1;
 }
 __host__ __device__ constexpr int plane_lo_b(int mode, int pl) {
-  return mode == CONV3_S2 ? ((pl & 1) ? -1 : 0) : -1;
+  return mode == CONV3_S2 ? ((pl & 1) ? -1 : 0) : mode == CONV3_S1P ? -(pl & 1) : -1;
+}
+__host__ __device__ constexpr int n_planes_of(int mode) { return mode == CONV3_S2 || mode == CONV3_S1P ? 4 : 1; }
+
+// ---- phase-plane stride-1 conv (CONV3_S1P) ------------------------------------------------
+// Input: the 4 phase planes (qy, qx) of a 2Hp x 2Wp tensor (PP, planes.cuh); output: the
+// 2x2 pixel block (2y+py, 2x+px) of every half-resolution position q = y*L + x, phase
+// p = py*2 + px in accumulator p.  Output phase py reads full-resolution row 2y+py+dy =
+// 2(y+sy)+qy, i.e. input plane parity qy = (py+dy)&1 at half-resolution shift
+// sy = floor((py+dy)/2).  Per input parity the 3 taps x 2 output parities collapse onto 2
+// shifts:  qy = 0: sy = 0 -> py in {0,1}, sy = +1 -> py = 1;
+//          qy = 1: sy = -1 -> py = 0,     sy = 0  -> py in {0,1}.
+// So one A read per (input plane, shift) — 4 per plane, 16 per K chunk for 4 output pixels —
+// feeds the stacked B tiles of every output phase using that shift (9 taps x 4 phases = 36
+// products from 16 A reads, against 36 A reads for four stride-1 M-tiles).  The phases of
+// a shift group form the accumulator run p0 .. p0+n-1 (zero B tile for a phase in the run
+// that does not use the shift: 40 tiles per 36 products).  Group 0 of plane 0 is shift (0,0)
+// over all four phases (it initialises the accumulators in chunk 0).
+__host__ __device__ constexpr int s1p_shift(int q, int g) { return q == 0 ? (g == 0 ? 0 : 1) : (g == 0 ? -1 : 0); }
+__host__ __device__ constexpr int s1p_pmin(int q, int g) { return q == 0 ? (g == 0 ? 0 : 1) : 0; }
+__host__ __device__ constexpr int s1p_pmax(int q, int g) { return q == 0 ? 1 : (g == 0 ? 0 : 1); }
+__host__ __device__ constexpr int s1p_dy(int pl, int gi) { return s1p_shift(pl >> 1, gi >> 1); }
+__host__ __device__ constexpr int s1p_dx(int pl, int gi) { return s1p_shift(pl & 1, gi & 1); }
+__host__ __device__ constexpr int s1p_p0(int pl, int gi) {
+  return s1p_pmin(pl >> 1, gi >> 1) * 2 + s1p_pmin(pl & 1, gi & 1);
+}
+__host__ __device__ constexpr int s1p_n(int pl, int gi) {
+  return s1p_pmax(pl >> 1, gi >> 1) * 2 + s1p_pmax(pl & 1, gi & 1) - s1p_p0(pl, gi) + 1;
+}
+// does accumulator (phase) acc of group gi use the group's shift?
+__host__ __device__ constexpr bool s1p_uses(int pl, int gi, int acc) {
+  return (acc >> 1) >= s1p_pmin(pl >> 1, gi >> 1) && (acc >> 1) <= s1p_pmax(pl >> 1, gi >> 1) &&
+         (acc & 1) >= s1p_pmin(pl & 1, gi & 1) && (acc & 1) <= s1p_pmax(pl & 1, gi & 1);
+}
+__host__ __device__ constexpr int s1p_slot0(int pl, int gi) {
+  int s = 0;
+  for (int i = 0; i < gi; ++i) s += s1p_n(pl, i);
+  return s;
 }
 
 // ---- shift groups of the transposed conv (fp32 concat scheme) ------------------------
@@ -338,6 +396,25 @@ __device__ __forceinline__ void issue_chunk(bool leader, uint64_t a0, uint64_t b
     }
   } else {
   const int lo = plane_lo_a(MODE, PL) * L + plane_lo_b(MODE, PL);
+  if constexpr (MODE == CONV3_S1P) {
+    // one MMA (pair) per shift group over the stacked phase tiles of input plane PL
+#pragma unroll
+    for (int gi = 0; gi < 4; ++gi) {
+      const int n = s1p_n(PL, gi);
+      const uint32_t idesc = idesc_bf16(n * AW);
+      const uint64_t ad0 = a0 + (uint32_t)(s1p_dy(PL, gi) * L + s1p_dx(PL, gi) - lo);
+      const uint64_t bd = b0 + (uint32_t)s1p_slot0(PL, gi) * TAP_UNITS + ((uint64_t)((n - 1) * AW) << 16);
+      const uint32_t accum0 = (first_chunk && gi == 0) ? 0u : 1u;
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const uint64_t ad = ad0 + (uint32_t)(g * 128);
+        const uint32_t dcol = dslot + (uint32_t)((g * NACC + s1p_p0(PL, gi)) * AW);
+        tc_mma(leader, dcol, ad, bd, idesc, accum0);                                // A_hi x tiles
+        if (NPM != kNpmBf16) tc_mma(leader, dcol, ad + lo_units, bd, idesc, 1u);  // A_lo x tiles
+      }
+    }
+    return;
+  }
   if constexpr (grouped_t(MODE, NPM)) {
     // one MMA pair per shift group: A_hi x [tiles] + A_lo x [tiles], each tile [B_hi | B_lo]
     // (the A_lo x B_lo product is kept: it costs nothing extra at this width)
@@ -394,13 +471,16 @@ __device__ __forceinline__ void issue_chunk(bool leader, uint64_t a0, uint64_t b
 }
 
 // ---- the kernel ----------------------------------------------------------------------
-template <int N, int MODE, bool DUAL, int NPM, int G, int CPS>
-__global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_constant__ Params p) {
+// floor division for possibly negative positions
+__device__ __forceinline__ int floordiv(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
+
+template <int N, int MODE, bool DUAL, int NPM, int G, int CPS, int STEM = 0>
+__global__ void __launch_bounds__(threads_of(STEM), 1) tc_conv_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int NSRC = DUAL ? 2 : 1;
   constexpr int NACC_SRC = nacc_src(MODE);
   constexpr int NACC = NSRC * NACC_SRC;
-  constexpr int NPLANES = MODE == CONV3_S2 ? 4 : 1;
+  constexpr int NPLANES = n_planes_of(MODE);
   constexpr int NPASS_A = NPM == kNpmBf16 ? 1 : 2;
   constexpr int AW = NPM == kNpmConcat ? 2 * N : N;  // TMEM columns per accumulator
   const TcLayerDesc& d = p.d;
@@ -418,15 +498,25 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
   uint64_t* tfull = empty + p.stages;
   uint64_t* tempty = tfull + p.slots;
   uint64_t* wbar = tempty + p.slots;  // resident weights landed
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(wbar + 1);
+  uint64_t* xfull = wbar + 1;         // STEM: frame rows of x ring stage landed
+  uint64_t* xempty = xfull + 2;       // STEM: stem warps done with x ring stage
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(xempty + 2);
   float* red = reinterpret_cast<float*>(tmem_holder + 4);  // [kEpiWarps][N]
+  float* xring = reinterpret_cast<float*>(
+      (reinterpret_cast<uintptr_t>(red + kEpiWarps * 64) + 127) / 128 * 128);  // STEM: [2][F][rows][W]
 
   if (threadIdx.x == 0) {
     trace_at(p.trace, 4, 0);
     trace_cta(p.trace, 0);
     for (int s = 0; s < p.stages; ++s) {
-      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&full[s]), STEM ? kStemThreads : 1);  // STEM: every stem thread arrives
       mbar_init(smem_u32(&empty[s]), 1);
+    }
+    if (STEM) {
+      for (int s = 0; s < 2; ++s) {
+        mbar_init(smem_u32(&xfull[s]), 1);
+        mbar_init(smem_u32(&xempty[s]), kStemThreads);
+      }
     }
     for (int s = 0; s < p.slots; ++s) {
       mbar_init(smem_u32(&tfull[s]), 1);
@@ -465,6 +555,32 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
                p.w_total, smem_u32(wbar));
     }
     grid_dep_wait();  // weights are static; activations come from the previous kernel
+    if constexpr (STEM) {
+      // frame rows of each item's staged positions (+1 row each side), one copy per frame
+      // into the 2-stage x ring; rows outside the image are never read (the stem masks them)
+      int xs = 0;
+      uint32_t xph = 0;
+      for (int item = blockIdx.x; item < p.total_items; item += gridDim.x) {
+        int b, it;
+        item_coords(item, p, b, it);
+        const int xr0 = floordiv(it * G * 128 - p.L - 1, p.L) - 1;
+        const int r_lo = max(xr0, 0), r_hi = min(xr0 + p.stem_xrows - 1, p.H - 1);
+        mbar_wait(smem_u32(&xempty[xs]), xph ^ 1);
+        if (lane == 0) {
+          const uint32_t rb = (uint32_t)(r_hi - r_lo + 1) * p.W * 4;
+          mbar_arrive_expect_tx(smem_u32(&xfull[xs]), rb * p.sF);
+          for (int ci = 0; ci < p.sF; ++ci)
+            bulk_g2s(smem_u32(xring + ((size_t)(xs * p.sF + ci) * p.stem_xrows + (r_lo - xr0)) * p.W),
+                     p.sx + (int64_t)b * p.sxb + (int64_t)ci * p.sxc + (int64_t)r_lo * p.W, rb,
+                     smem_u32(&xfull[xs]));
+        }
+        __syncwarp();
+        if (++xs == 2) {
+          xs = 0;
+          xph ^= 1u;
+        }
+      }
+    } else {
     const PlBuf& S = p.src[lane < NCOPY ? cs : 0];
     uint32_t k = 0;
     int pstage = 0;
@@ -552,6 +668,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
       }
       }
     }
+    }  // !STEM
     __syncwarp();
   } else if (warp == kMmaWarp) {
     // ===================== MMA issuer: whole warp runs the loop, one lane issues ========
@@ -601,7 +718,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
               smem_u32(b_base + (p.resident ? (size_t)d.chunk_off[c]
                                             : (size_t)stage * p.b_stage_bytes + (size_t)cc * p.chunk_b_bytes)),
               lboB, 128);
-          if constexpr (MODE == CONV3_S2) {
+          if constexpr (MODE == CONV3_S2 || MODE == CONV3_S1P) {
             switch (c / cgroups) {
               case 0: issue_chunk<N, MODE, 0, DUAL, NPM, G>(leader, a0, b0, dslot, p.L, c == 0, src_units, lo_units); break;
               case 1: issue_chunk<N, MODE, 1, DUAL, NPM, G>(leader, a0, b0, dslot, p.L, c == 0, src_units, lo_units); break;
@@ -619,7 +736,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
       tc_commit(leader, smem_u32(&tfull[slot]));
     }
     __syncwarp();
-  } else {
+  } else if (warp < kEpiWarp0 + kEpiWarps) {
     // ===================== epilogue warps 2..9 ==========================================
     // Two warps per TMEM lane quarter; the (tile, phase, 16-channel) units of an item
     // alternate between them so each SM sub-partition has two independent epilogue
@@ -677,6 +794,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
           // column zero (planes.cuh border contract)
           if (p.out.mode == 1) {
             pl_zero_pos(p.out.pl, b, 0, y * p.out.pl.L + p.Wp);
+          } else if (MODE == CONV3_S1P) {  // the half-resolution pad column of all 4 planes
+#pragma unroll
+            for (int pz = 0; pz < 4; ++pz) pl_zero_pos(p.out.pl, b, pz, y * p.out.pl.L + p.Wp);
           } else {
             pl_zero_pos(p.out.pl, b, (y & 1) * 2, (y >> 1) * p.out.pl.L + p.Wp / 2);
             pl_zero_pos(p.out.pl, b, (y & 1) * 2 + 1, (y >> 1) * p.out.pl.L + p.Wp / 2);
@@ -685,7 +805,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
 #pragma unroll
         for (int ph = 0; ph < NACC_SRC; ++ph) {
           int oy = y, ox = x;
-          if (MODE == CONVT4_S2) {
+          if (MODE == CONVT4_S2 || MODE == CONV3_S1P) {
             oy = 2 * y + (ph >> 1);
             ox = 2 * x + (ph & 1);
           } else if (MODE == CONVT4_HALF) {
@@ -824,6 +944,134 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
         asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
       }
     }
+  } else {
+    if constexpr (STEM) {
+      // ===================== stem warps: relu(conv3x3(frames)) into the A stages ==========
+      // Every staged position of the item (its 128G positions and the 2L+2 halo) is
+      // computed from the frame rows in the x ring — the stem never makes an HBM round
+      // trip for this conv — written as bf16 hi (+ lo) core-matrix rows of the stage, and
+      // (positions the item owns) as the stem's operand planes for enc0.s2 and the head.
+      // Arithmetic is stem_const_kernel's (edge_conv.cu): FFMA2 over channel pairs in the
+      // order (frame, kx, ky), bias first, ReLU; the values are bitwise the unfused stem's.
+      constexpr int NP = NPASS_A;  // 2: hi + lo (fp32 contract), 1: bf16
+      grid_dep_wait();             // the stem planes may still be read by the previous kernel
+      const int st = threadIdx.x - kStemWarp0 * 32;
+      const int L = p.L, W = p.W, H = p.H, Lp = W / 2 + 1;
+      const int P = G * 128 + 2 * L + 2;
+      const size_t QB = (size_t)p.s_pl.Q * 8, QBp = (size_t)p.s_pp.Q * 8;
+      int stage = 0, xs = 0;
+      uint32_t phase = 0, xph = 0;
+      for (int item = blockIdx.x; item < p.total_items; item += gridDim.x) {
+        int b, it;
+        item_coords(item, p, b, it);
+        const int q0 = it * G * 128, qa = q0 - L - 1;
+        const int xr0 = floordiv(qa, L) - 1;
+        if (it == 0) {  // top / bottom margins of the stem planes, once per image
+          if (p.s_has_pl) pl_zero_margins(p.s_pl, b, st, kStemThreads);
+          pl_zero_margins(p.s_pp, b, st, kStemThreads);
+        }
+        uint16_t* plb = p.s_pl.base + (int64_t)b * p.s_pl.img_stride + (size_t)p.s_pl.off * 8;
+        uint16_t* ppb = p.s_pp.base + (int64_t)b * p.s_pp.img_stride + (size_t)p.s_pp.off * 8;
+        mbar_wait(smem_u32(&xfull[xs]), xph);
+        mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+        const float* xr = xring + (size_t)xs * p.sF * p.stem_xrows * W;
+        uint8_t* a = a_base + (size_t)stage * p.a_stage_bytes;
+        for (int i = st; i < P; i += kStemThreads) {
+          const int q = qa + i;
+          const int y = floordiv(q, L), x = q - y * L;
+          float v[kStemC];
+          if (y >= 0 && y < H && x < W) {
+            unsigned long long acc2[kStemC / 2];
+#pragma unroll
+            for (int j = 0; j < kStemC / 2; ++j)
+              acc2[j] = *reinterpret_cast<const unsigned long long*>(&p.stem_b[2 * j]);
+#pragma unroll
+            for (int ci = 0; ci < kStemMaxF; ++ci) {
+              if (ci >= p.sF) break;
+              const float* xc = xr + (size_t)ci * p.stem_xrows * W;
+#pragma unroll
+              for (int kx = 0; kx < 3; ++kx) {
+                const int ix = x + kx - 1;
+                unsigned long long v2[3];
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                  const int iy = y - 1 + k;
+                  float t = (ix >= 0 && ix < W && iy >= 0 && iy < H) ? xc[(iy - xr0) * W + ix] : 0.f;
+                  if (NP == 1) t = bf16_round(t);
+                  v2[k] = f2_pack(t, t);
+                }
+#pragma unroll
+                for (int ky = 0; ky < 3; ++ky)
+#pragma unroll
+                  for (int j = 0; j < kStemC / 2; ++j)
+                    f2_fma(acc2[j], v2[ky],
+                           *reinterpret_cast<const unsigned long long*>(
+                               &p.stem_w[((ci * 3 + ky) * 3 + kx) * kStemC + 2 * j]));
+              }
+            }
+#pragma unroll
+            for (int j = 0; j < kStemC / 2; ++j) {
+              f2_unpack(acc2[j], v[2 * j], v[2 * j + 1]);
+              v[2 * j] = fmaxf(v[2 * j], 0.f);
+              v[2 * j + 1] = fmaxf(v[2 * j + 1], 0.f);
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < kStemC; ++c) v[c] = 0.f;
+          }
+          // A stage rows: [pass][cg8][P_max][8 bf16]
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            uint32_t hw[4], lw[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const __nv_bfloat162 hb = __floats2bfloat162_rn(v[8 * h + 2 * j], v[8 * h + 2 * j + 1]);
+              hw[j] = *reinterpret_cast<const uint32_t*>(&hb);
+              if (NP == 2) {
+                const float2 hf = __bfloat1622float2(hb);
+                const __nv_bfloat162 lb =
+                    __floats2bfloat162_rn(v[8 * h + 2 * j] - hf.x, v[8 * h + 2 * j + 1] - hf.y);
+                lw[j] = *reinterpret_cast<const uint32_t*>(&lb);
+              }
+            }
+            *reinterpret_cast<uint4*>(a + ((size_t)h * p.P_max + i) * 16) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+            if (NP == 2)
+              *reinterpret_cast<uint4*>(a + ((size_t)(2 + h) * p.P_max + i) * 16) =
+                  make_uint4(lw[0], lw[1], lw[2], lw[3]);
+          }
+          // the item's own positions: the stem planes (planes.cuh layout, pads included)
+          if (q >= q0 && q < q0 + G * 128 && y < H) {
+            if (x < W) {
+              const int plane = (y & 1) * 2 + (x & 1);
+              uint16_t* pq = ppb + (int64_t)plane * p.s_pp.plane_stride + (size_t)((y >> 1) * Lp + (x >> 1)) * 8;
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                float v8[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) v8[e] = v[8 * h + e];
+                if (p.s_has_pl) store8_split<NP>(plb + (size_t)q * 8 + h * QB, 2 * QB, v8);
+                store8_split<NP>(pq + h * QBp, 2 * QBp, v8);
+              }
+            } else {  // x == W: the pad column of this row
+              if (p.s_has_pl) pl_zero_pos(p.s_pl, b, 0, q);
+              pl_zero_pos(p.s_pp, b, (y & 1) * 2, (y >> 1) * Lp + W / 2);
+              pl_zero_pos(p.s_pp, b, (y & 1) * 2 + 1, (y >> 1) * Lp + W / 2);
+            }
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // st.shared -> tcgen05.mma
+        mbar_arrive(smem_u32(&full[stage]));
+        mbar_arrive(smem_u32(&xempty[xs]));
+        if (++stage == p.stages) {
+          stage = 0;
+          phase ^= 1u;
+        }
+        if (++xs == 2) {
+          xs = 0;
+          xph ^= 1u;
+        }
+      }
+    }
   }
 
   tc_fence_before();
@@ -837,6 +1085,13 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(p.tmem_cols)
                  : "memory");
   }
+}
+
+template <int N, int NPM, int G>
+void launch_stem_k(const Params& p, int grid, size_t smem, cudaStream_t st) {
+  auto kern = tc_conv_kernel<N, CONV3_S1, false, NPM, G, 1, 1>;
+  ensure_dyn_smem(kern, kMaxSmem);
+  launch_pdl(kern, dim3(grid), dim3(kThreadsStem), smem, st, "tc_conv_kernel<stem>", p);
 }
 
 template <int N, int MODE, bool DUAL, int NPM, int G>
@@ -875,6 +1130,8 @@ void dispatch_s2(int n, int npm, int G, const Params& p, int grid, size_t smem, 
 void dispatch_t(int n, int npm, int G, const Params& p, int grid, size_t smem, cudaStream_t st);
 void dispatch_th(int n, int npm, int G, const Params& p, int grid, size_t smem, cudaStream_t st);
 void dispatch_rows(int n, int npm, int G, const Params& p, int grid, size_t smem, cudaStream_t st);
+void dispatch_s1p(int n, int npm, int G, const Params& p, int grid, size_t smem, cudaStream_t st);
+void dispatch_stem(int npm, int G, const Params& p, int grid, size_t smem, cudaStream_t st);
 
 }  // namespace detail
 }  // namespace tc
