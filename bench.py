@@ -471,15 +471,15 @@ def run_engine(args, world, rank, local):
         acc = ms if acc is None else [a + b for a, b in zip(acc, ms)]
     avg = [a / 5 for a in acc]
     fl = layer_flops(cfg)
+    byt = layer_bytes(cfg)
+    opb = layer_operand_bytes(cfg, args.precision)
+    fuse_names(names, cfg, fl, byt, opb)
     share = {n: m for n, m in zip(names, avg)}
     dom = max(share, key=share.get)
     hbm, bf16, bf16_sus, peak_kind = peaks()
     flops_per_launch = fl[dom] * batch
     achieved = flops_per_launch / (share[dom] * 1e-3) / 1e12
     total_flops = sum(fl.values())
-    byt = layer_bytes(cfg)
-    opb = layer_operand_bytes(cfg, args.precision)
-    fuse_names(names, cfg, fl, byt, opb)
     sm_ghz = (clocks.summary().get("sm_max_mhz") or 1965.0) / 1000.0
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
     floor_us = {n: b * batch / (128.0 * n_sm * sm_ghz * 1e3) for n, b in opb.items()}

@@ -8,16 +8,25 @@ namespace detail {
 
 void dispatch_stem(int npm, int G, const Params& p, int grid, size_t smem, cudaStream_t st) {
   STDA_CHECK(npm == kNpmConcat || npm == kNpmBf16, "fused stem: precision scheme");
-  auto by_g = [&](auto npm_c) {
-    constexpr int PM = decltype(npm_c)::value;
+  // G = 4 (W <= 128 keeps >= 6 full items per CTA at the C2 batch) or 2 / 1 for small batches
+  auto by_g = [&](auto npm_c, auto f_c) {
+    constexpr int PM = decltype(npm_c)::value, FF = decltype(f_c)::value;
     switch (G) {
-      case 1: return launch_stem_k<16, PM, 1>(p, grid, smem, st);
-      case 2: return launch_stem_k<16, PM, 2>(p, grid, smem, st);
-      default: return launch_stem_k<16, PM, 4>(p, grid, smem, st);
+      case 1: return launch_stem_k<16, PM, 1, FF>(p, grid, smem, st);
+      case 2: return launch_stem_k<16, PM, 2, FF>(p, grid, smem, st);
+      default: return launch_stem_k<16, PM, 4, FF>(p, grid, smem, st);
     }
   };
-  if (npm == kNpmConcat) return by_g(std::integral_constant<int, kNpmConcat>{});
-  return by_g(std::integral_constant<int, kNpmBf16>{});
+  auto by_f = [&](auto npm_c) {
+    switch (p.sF) {
+      case 1: return by_g(npm_c, std::integral_constant<int, 1>{});
+      case 2: return by_g(npm_c, std::integral_constant<int, 2>{});
+      case 3: return by_g(npm_c, std::integral_constant<int, 3>{});
+      default: return by_g(npm_c, std::integral_constant<int, 4>{});
+    }
+  };
+  if (npm == kNpmConcat) return by_f(std::integral_constant<int, kNpmConcat>{});
+  return by_f(std::integral_constant<int, kNpmBf16>{});
 }
 
 }  // namespace detail

@@ -25,7 +25,7 @@ constexpr int kThreads = (kEpiWarp0 + kEpiWarps) * 32;
 // fused stem (STEM kernels, stem + first encoder stride-1 conv): warps 10.. compute the
 // stem straight into the A stages (tc_kernel.cuh stem role); warp 0 stages the frame rows
 constexpr int kStemWarp0 = kEpiWarp0 + kEpiWarps;
-constexpr int kStemWarps = 4;
+constexpr int kStemWarps = 8;
 constexpr int kStemThreads = kStemWarps * 32;
 constexpr int kThreadsStem = kThreads + kStemThreads;
 constexpr int kStemC = 16, kStemMaxF = 4;
@@ -295,6 +295,10 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
       "l"(src), "r"(bytes), "r"(bar)
       : "memory");
 }
+__device__ __forceinline__ void bulk_s2g(void* dst, uint32_t src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src), "r"(bytes)
+               : "memory");
+}
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
@@ -512,7 +516,7 @@ __global__ void __launch_bounds__(threads_of(STEM), 1) tc_conv_kernel(const __gr
       mbar_init(smem_u32(&full[s]), STEM ? kStemThreads : 1);  // STEM: every stem thread arrives
       mbar_init(smem_u32(&empty[s]), 1);
     }
-    if (STEM) {
+    if (STEM > 0) {
       for (int s = 0; s < 2; ++s) {
         mbar_init(smem_u32(&xfull[s]), 1);
         mbar_init(smem_u32(&xempty[s]), kStemThreads);
@@ -555,7 +559,7 @@ __global__ void __launch_bounds__(threads_of(STEM), 1) tc_conv_kernel(const __gr
                p.w_total, smem_u32(wbar));
     }
     grid_dep_wait();  // weights are static; activations come from the previous kernel
-    if constexpr (STEM) {
+    if constexpr (STEM > 0) {
       // frame rows of each item's staged positions (+1 row each side), one copy per frame
       // into the 2-stage x ring; rows outside the image are never read (the stem masks them)
       int xs = 0;
@@ -945,19 +949,33 @@ __global__ void __launch_bounds__(threads_of(STEM), 1) tc_conv_kernel(const __gr
       }
     }
   } else {
-    if constexpr (STEM) {
+    if constexpr (STEM > 0) {
       // ===================== stem warps: relu(conv3x3(frames)) into the A stages ==========
       // Every staged position of the item (its 128G positions and the 2L+2 halo) is
-      // computed from the frame rows in the x ring — the stem never makes an HBM round
-      // trip for this conv — written as bf16 hi (+ lo) core-matrix rows of the stage, and
-      // (positions the item owns) as the stem's operand planes for enc0.s2 and the head.
-      // Arithmetic is stem_const_kernel's (edge_conv.cu): FFMA2 over channel pairs in the
-      // order (frame, kx, ky), bias first, ReLU; the values are bitwise the unfused stem's.
+      // computed from the frame rows in the x ring — the stem never makes an HBM round trip
+      // for this conv — and written as bf16 hi (+ lo) core-matrix rows of the A stage.
+      // Thread = (position slot, channel pair j): the pair's F*9 weight pairs live in
+      // registers, a warp covers 4 positions x 8 pairs, so each frame value is one
+      // broadcast shared-memory load for 8 lanes.  Arithmetic is stem_const_kernel's
+      // (edge_conv.cu): FFMA2 per channel pair in the order (frame, kx, ky) from the bias,
+      // then ReLU — bitwise the unfused stem.  The item's own positions then leave as the
+      // stem's operand planes: PL rows by bulk copies of the staged block ranges, PP by
+      // 16-byte copies (enc0.s2's residual source and the head's skip).
+      constexpr int F = STEM;
       constexpr int NP = NPASS_A;  // 2: hi + lo (fp32 contract), 1: bf16
       grid_dep_wait();             // the stem planes may still be read by the previous kernel
       const int st = threadIdx.x - kStemWarp0 * 32;
+      const int j = st & 7;                      // channel pair
+      const int slot = st >> 3;                  // position slot 0..31
       const int L = p.L, W = p.W, H = p.H, Lp = W / 2 + 1;
       const int P = G * 128 + 2 * L + 2;
+      unsigned long long w2[F * 9];
+#pragma unroll
+      for (int t = 0; t < F * 9; ++t)
+        w2[t] = *reinterpret_cast<const unsigned long long*>(&p.stem_w[t * kStemC + 2 * j]);
+      const unsigned long long b2 = *reinterpret_cast<const unsigned long long*>(&p.stem_b[2 * j]);
+      const uint32_t row_hi = (uint32_t)((j >> 2) * p.P_max) * 16 + (uint32_t)(j & 3) * 4;  // pass 0, cg8
+      const uint32_t row_lo = row_hi + 2u * p.P_max * 16;                                   // pass 1
       const size_t QB = (size_t)p.s_pl.Q * 8, QBp = (size_t)p.s_pp.Q * 8;
       int stage = 0, xs = 0;
       uint32_t phase = 0, xph = 0;
@@ -970,96 +988,79 @@ __global__ void __launch_bounds__(threads_of(STEM), 1) tc_conv_kernel(const __gr
           if (p.s_has_pl) pl_zero_margins(p.s_pl, b, st, kStemThreads);
           pl_zero_margins(p.s_pp, b, st, kStemThreads);
         }
-        uint16_t* plb = p.s_pl.base + (int64_t)b * p.s_pl.img_stride + (size_t)p.s_pl.off * 8;
-        uint16_t* ppb = p.s_pp.base + (int64_t)b * p.s_pp.img_stride + (size_t)p.s_pp.off * 8;
+        // the PL bulk store that last read this stage (stages >= 2 items ago) is done
+        if (st == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        asm volatile("bar.sync 2, %0;" ::"n"(kStemThreads) : "memory");
         mbar_wait(smem_u32(&xfull[xs]), xph);
         mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
-        const float* xr = xring + (size_t)xs * p.sF * p.stem_xrows * W;
+        const float* xr = xring + (size_t)xs * F * p.stem_xrows * W;
         uint8_t* a = a_base + (size_t)stage * p.a_stage_bytes;
-        for (int i = st; i < P; i += kStemThreads) {
+        for (int i = slot; i < P; i += kStemThreads / 8) {
           const int q = qa + i;
-          const int y = floordiv(q, L), x = q - y * L;
-          float v[kStemC];
+          const int y = (int)__umulhi((uint32_t)(q + 2 * L), p.L_mul) - 2;  // floor(q / L), q >= -2L
+          const int x = q - y * L;
+          float v0 = 0.f, v1 = 0.f;
           if (y >= 0 && y < H && x < W) {
-            unsigned long long acc2[kStemC / 2];
+            unsigned long long acc = b2;
 #pragma unroll
-            for (int j = 0; j < kStemC / 2; ++j)
-              acc2[j] = *reinterpret_cast<const unsigned long long*>(&p.stem_b[2 * j]);
-#pragma unroll
-            for (int ci = 0; ci < kStemMaxF; ++ci) {
-              if (ci >= p.sF) break;
+            for (int ci = 0; ci < F; ++ci) {
               const float* xc = xr + (size_t)ci * p.stem_xrows * W;
 #pragma unroll
               for (int kx = 0; kx < 3; ++kx) {
                 const int ix = x + kx - 1;
-                unsigned long long v2[3];
 #pragma unroll
-                for (int k = 0; k < 3; ++k) {
-                  const int iy = y - 1 + k;
+                for (int ky = 0; ky < 3; ++ky) {
+                  const int iy = y - 1 + ky;
                   float t = (ix >= 0 && ix < W && iy >= 0 && iy < H) ? xc[(iy - xr0) * W + ix] : 0.f;
                   if (NP == 1) t = bf16_round(t);
-                  v2[k] = f2_pack(t, t);
+                  f2_fma(acc, f2_pack(t, t), w2[(ci * 3 + ky) * 3 + kx]);
                 }
-#pragma unroll
-                for (int ky = 0; ky < 3; ++ky)
-#pragma unroll
-                  for (int j = 0; j < kStemC / 2; ++j)
-                    f2_fma(acc2[j], v2[ky],
-                           *reinterpret_cast<const unsigned long long*>(
-                               &p.stem_w[((ci * 3 + ky) * 3 + kx) * kStemC + 2 * j]));
               }
             }
-#pragma unroll
-            for (int j = 0; j < kStemC / 2; ++j) {
-              f2_unpack(acc2[j], v[2 * j], v[2 * j + 1]);
-              v[2 * j] = fmaxf(v[2 * j], 0.f);
-              v[2 * j + 1] = fmaxf(v[2 * j + 1], 0.f);
-            }
-          } else {
-#pragma unroll
-            for (int c = 0; c < kStemC; ++c) v[c] = 0.f;
+            f2_unpack(acc, v0, v1);
+            v0 = fmaxf(v0, 0.f);
+            v1 = fmaxf(v1, 0.f);
           }
-          // A stage rows: [pass][cg8][P_max][8 bf16]
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            uint32_t hw[4], lw[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const __nv_bfloat162 hb = __floats2bfloat162_rn(v[8 * h + 2 * j], v[8 * h + 2 * j + 1]);
-              hw[j] = *reinterpret_cast<const uint32_t*>(&hb);
-              if (NP == 2) {
-                const float2 hf = __bfloat1622float2(hb);
-                const __nv_bfloat162 lb =
-                    __floats2bfloat162_rn(v[8 * h + 2 * j] - hf.x, v[8 * h + 2 * j + 1] - hf.y);
-                lw[j] = *reinterpret_cast<const uint32_t*>(&lb);
-              }
-            }
-            *reinterpret_cast<uint4*>(a + ((size_t)h * p.P_max + i) * 16) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-            if (NP == 2)
-              *reinterpret_cast<uint4*>(a + ((size_t)(2 + h) * p.P_max + i) * 16) =
-                  make_uint4(lw[0], lw[1], lw[2], lw[3]);
-          }
-          // the item's own positions: the stem planes (planes.cuh layout, pads included)
-          if (q >= q0 && q < q0 + G * 128 && y < H) {
-            if (x < W) {
-              const int plane = (y & 1) * 2 + (x & 1);
-              uint16_t* pq = ppb + (int64_t)plane * p.s_pp.plane_stride + (size_t)((y >> 1) * Lp + (x >> 1)) * 8;
-#pragma unroll
-              for (int h = 0; h < 2; ++h) {
-                float v8[8];
-#pragma unroll
-                for (int e = 0; e < 8; ++e) v8[e] = v[8 * h + e];
-                if (p.s_has_pl) store8_split<NP>(plb + (size_t)q * 8 + h * QB, 2 * QB, v8);
-                store8_split<NP>(pq + h * QBp, 2 * QBp, v8);
-              }
-            } else {  // x == W: the pad column of this row
-              if (p.s_has_pl) pl_zero_pos(p.s_pl, b, 0, q);
-              pl_zero_pos(p.s_pp, b, (y & 1) * 2, (y >> 1) * Lp + W / 2);
-              pl_zero_pos(p.s_pp, b, (y & 1) * 2 + 1, (y >> 1) * Lp + W / 2);
-            }
+          const __nv_bfloat162 hb = __floats2bfloat162_rn(v0, v1);
+          *reinterpret_cast<__nv_bfloat162*>(a + row_hi + (uint32_t)i * 16) = hb;
+          if (NP == 2) {
+            const float2 hf = __bfloat1622float2(hb);
+            *reinterpret_cast<__nv_bfloat162*>(a + row_lo + (uint32_t)i * 16) = __floats2bfloat162_rn(v0 - hf.x, v1 - hf.y);
           }
         }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // st.shared -> tcgen05.mma
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // st.shared -> UMMA / bulk copies
+        asm volatile("bar.sync 2, %0;" ::"n"(kStemThreads) : "memory");
+        // the item's own positions [q0, q0 + 128G) sit at stage rows L+1 .. : PL = the staged
+        // block ranges (zeros at pad columns and past the last row, i.e. the border contract)
+        const int own = min(G * 128, p.Hp * L + L + 8 - q0);  // stay inside the bottom margin
+        if (p.s_has_pl && st == 0) {
+          uint16_t* img = p.s_pl.base + (int64_t)b * p.s_pl.img_stride;
+#pragma unroll
+          for (int blk = 0; blk < 2 * NP; ++blk)
+            bulk_s2g(img + ((size_t)blk * p.s_pl.Q + q0 + p.s_pl.off) * 8,
+                     smem_u32(a + ((size_t)blk * p.P_max + L + 1) * 16), (uint32_t)own * 16);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        // PP: 16-byte copies of the owned valid positions, pad columns zeroed
+        uint16_t* ppb = p.s_pp.base + (int64_t)b * p.s_pp.img_stride + (size_t)p.s_pp.off * 8;
+        for (int u = st; u < G * 128 * 2 * NP; u += kStemThreads) {
+          const int k = u % (G * 128), blk = u / (G * 128);  // blk = pass * 2 + cg8
+          const int q = q0 + k;
+          const int y = (int)__umulhi((uint32_t)q, p.L_mul), x = q - y * L;
+          if (y >= H) continue;
+          if (x < W) {
+            const uint4 v = *reinterpret_cast<const uint4*>(a + ((size_t)blk * p.P_max + L + 1 + k) * 16);
+            *reinterpret_cast<uint4*>(ppb + (int64_t)((y & 1) * 2 + (x & 1)) * p.s_pp.plane_stride +
+                                      (size_t)blk * QBp + (size_t)((y >> 1) * Lp + (x >> 1)) * 8) = v;
+          } else {  // x == W: the pad columns of both px planes of this plane row
+#pragma unroll
+            for (int px = 0; px < 2; ++px)
+              *reinterpret_cast<uint4*>(ppb + (int64_t)((y & 1) * 2 + px) * p.s_pp.plane_stride +
+                                        (size_t)blk * QBp + (size_t)((y >> 1) * Lp + W / 2) * 8) =
+                  make_uint4(0, 0, 0, 0);
+          }
+        }
+        (void)QB;
         mbar_arrive(smem_u32(&full[stage]));
         mbar_arrive(smem_u32(&xempty[xs]));
         if (++stage == p.stages) {
@@ -1071,6 +1072,7 @@ __global__ void __launch_bounds__(threads_of(STEM), 1) tc_conv_kernel(const __gr
           xph ^= 1u;
         }
       }
+      if (st == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // PL stores complete
     }
   }
 
@@ -1087,9 +1089,9 @@ __global__ void __launch_bounds__(threads_of(STEM), 1) tc_conv_kernel(const __gr
   }
 }
 
-template <int N, int NPM, int G>
+template <int N, int NPM, int G, int F>
 void launch_stem_k(const Params& p, int grid, size_t smem, cudaStream_t st) {
-  auto kern = tc_conv_kernel<N, CONV3_S1, false, NPM, G, 1, 1>;
+  auto kern = tc_conv_kernel<N, CONV3_S1, false, NPM, G, 1, F>;
   ensure_dyn_smem(kern, kMaxSmem);
   launch_pdl(kern, dim3(grid), dim3(kThreadsStem), smem, st, "tc_conv_kernel<stem>", p);
 }
