@@ -506,8 +506,10 @@ __global__ void __launch_bounds__(threads_of(STEM), 1) tc_conv_kernel(const __gr
   uint64_t* xempty = xfull + 2;       // STEM: stem warps done with x ring stage
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(xempty + 2);
   float* red = reinterpret_cast<float*>(tmem_holder + 4);  // [kEpiWarps][N]
+  // STEM: x ring [2][F][rows][W] (offset from the dynamic smem base: the compiler keeps
+  // the shared address space, i.e. LDS rather than generic loads)
   float* xring = reinterpret_cast<float*>(
-      (reinterpret_cast<uintptr_t>(red + kEpiWarps * 64) + 127) / 128 * 128);  // STEM: [2][F][rows][W]
+      smem + ((size_t)(reinterpret_cast<uint8_t*>(red + kEpiWarps * 64) - smem) + 127) / 128 * 128);
 
   if (threadIdx.x == 0) {
     trace_at(p.trace, 4, 0);
@@ -971,9 +973,14 @@ __global__ void __launch_bounds__(threads_of(STEM), 1) tc_conv_kernel(const __gr
       const int P = G * 128 + 2 * L + 2;
       unsigned long long w2[F * 9];
 #pragma unroll
-      for (int t = 0; t < F * 9; ++t)
-        w2[t] = *reinterpret_cast<const unsigned long long*>(&p.stem_w[t * kStemC + 2 * j]);
-      const unsigned long long b2 = *reinterpret_cast<const unsigned long long*>(&p.stem_b[2 * j]);
+      for (int t = 0; t < F * 9; ++t) {
+        // through an opaque move: the pair stays in a register for the whole kernel instead
+        // of an indexed constant-bank reload per use
+        const unsigned long long wc = *reinterpret_cast<const unsigned long long*>(&p.stem_w[t * kStemC + 2 * j]);
+        asm volatile("mov.b64 %0, %1;" : "=l"(w2[t]) : "l"(wc));
+      }
+      unsigned long long b2;
+      asm volatile("mov.b64 %0, %1;" : "=l"(b2) : "l"(*reinterpret_cast<const unsigned long long*>(&p.stem_b[2 * j])));
       const uint32_t row_hi = (uint32_t)((j >> 2) * p.P_max) * 16 + (uint32_t)(j & 3) * 4;  // pass 0, cg8
       const uint32_t row_lo = row_hi + 2u * p.P_max * 16;                                   // pass 1
       const size_t QB = (size_t)p.s_pl.Q * 8, QBp = (size_t)p.s_pp.Q * 8;
