@@ -398,7 +398,9 @@ struct alignas(16) StemConst {
   float b[kStemC];
 };
 
-template <int F, int PX, int NP>  // NP = 1: bf16 operands (inputs rounded, hi plane only)
+// NP = 1: bf16 operands (inputs rounded, hi plane only); PL = false: phase planes only (the
+// consumers of the PL copy — enc0.s1 and the head — read the phase planes instead)
+template <int F, int PX, int NP, bool PL = true>
 __global__ void __launch_bounds__(kRowThreads, 4) stem_const_kernel(const __grid_constant__ StemConst cw, Src x,
                                                                    PlBuf pl, PlBuf pp, int H, int W, int R,
                                                                    int64_t b_base) {
@@ -432,14 +434,14 @@ __global__ void __launch_bounds__(kRowThreads, 4) stem_const_kernel(const __grid
       if (y0 + R >= H) xs[((size_t)ci * (R + 2) + R + 1) * W + e] = 0.f;
     }
   if (blockIdx.x == 0) {  // top / bottom margins of the output planes, once per image
-    pl_zero_margins(pl, b, tid, kRowThreads);
+    if (PL) pl_zero_margins(pl, b, tid, kRowThreads);
     pl_zero_margins(pp, b, tid, kRowThreads);
   }
   ptx::mbar_wait(ptx::smem_u32(&bar), 0);
   __syncthreads();
   // C0 = 16: one cg16, blocks (pass, cg8) at (pass * 2 + cg8) * Q (planes.cuh)
   const size_t QB = (size_t)pl.Q * 8, QBp = (size_t)pp.Q * 8;
-  uint16_t* plb = pl.base + b * pl.img_stride + (size_t)pl.off * 8;
+  uint16_t* plb = PL ? pl.base + b * pl.img_stride + (size_t)pl.off * 8 : nullptr;
   uint16_t* ppb = pp.base + b * pp.img_stride + (size_t)pp.off * 8;
   for (int it = tid; it < (R / PX) * W; it += kRowThreads) {  // PX vertically adjacent pixels
     const int r0 = (it / W) * PX, xx = it - (it / W) * W;
@@ -490,11 +492,11 @@ __global__ void __launch_bounds__(kRowThreads, 4) stem_const_kernel(const __grid
         float v8[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) v8[i] = fmaxf(acc[o][8 * h + i], 0.f);
-        store8_split<NP>(po + h * QB, 2 * QB, v8);
+        if (PL) store8_split<NP>(po + h * QB, 2 * QB, v8);
         store8_split<NP>(pq + h * QBp, 2 * QBp, v8);
       }
       if (xx >= W - 2) {  // pad columns (planes.cuh border contract)
-        if (xx == W - 1) pl_zero_pos(pl, b, 0, oy * L + W);
+        if (PL && xx == W - 1) pl_zero_pos(pl, b, 0, oy * L + W);
         pl_zero_pos(pp, b, plane, (oy >> 1) * Lp + W / 2);
       }
     }
@@ -538,7 +540,9 @@ struct HeadConst {
   float w[9 * kHsC];  // [tap][channel]: read by the conv from the kernel-parameter bank
 };
 
-template <int W>
+// SKIP_PP: the skip (stem output) comes as phase planes: staged per row and px plane as
+// [block][row][px][W/2] (2 copies per row and block, issued by the producer warp's lanes)
+template <int W, bool SKIP_PP = false>
 __global__ void __launch_bounds__(kHsThreads, 1) head_strips_kernel(
     const __grid_constant__ HeadConst cw, const float* __restrict__ bias, const float* __restrict__ gap, int items,
     const float* __restrict__ eca_w, int k, const float* __restrict__ d, PlBuf skip, float* __restrict__ y,
@@ -570,6 +574,42 @@ __global__ void __launch_bounds__(kHsThreads, 1) head_strips_kernel(
   __syncthreads();
   grid_dep_wait();  // d, gap and skip come from the previous kernels
 
+  if (warp == kHsCompute / 32 && SKIP_PP) {
+    // ===== producer warp, phase-plane skip: lane 0 posts the bytes, lanes issue the copies
+    const int lane = tid & 31;
+    const int Lp = W / 2 + 1;
+    int i = 0;
+    for (int64_t s = s_begin; s < s_end; ++s, ++i) {
+      const int st = i & 1;
+      mbar_wait(smem_u32(&empty[st]), ((i >> 1) & 1) ^ 1);
+      const int64_t b = s / spi;
+      const int y0 = (int)(s - b * spi) * R;
+      const int r0 = y0 == 0 ? 1 : 0;
+      const int r1 = y0 + R == H ? SR - 1 : SR;
+      const int nr = r1 - r0, iy0 = y0 - 1 + r0;
+      const uint32_t bar = smem_u32(&full[st]);
+      uint8_t* base = hsm + (size_t)st * g.stage;
+      if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)(nr * W * kHsC * 4 + np * 2 * nr * W * 16));
+      __syncwarp();
+      const uint16_t* simg = skip.base + b * skip.img_stride;
+      const int ncp = 1 + nr * 2 * np * 2;
+      for (int c = lane; c < ncp; c += 32) {
+        if (c == 0) {
+          bulk_g2s(smem_u32(base + (size_t)r0 * W * kHsC * 4), d + ((size_t)b * H + iy0) * W * kHsC,
+                   (uint32_t)(nr * W * kHsC * 4), bar);
+          continue;
+        }
+        const int u = c - 1, px = u & 1, blk = (u >> 1) % (np * 2), rr = (u >> 1) / (np * 2);
+        const int r = r0 + rr, iy = iy0 + rr;
+        const int pass = blk >> 1, cg8 = blk & 1;
+        bulk_g2s(smem_u32(base + g.dbytes + (size_t)blk * g.sblk + ((size_t)(r * 2 + px) * (W / 2)) * 16),
+                 simg + (int64_t)((iy & 1) * 2 + px) * skip.plane_stride +
+                     (skip.block_index(0, pass, cg8) + skip.off + (size_t)(iy >> 1) * Lp) * 8,
+                 (uint32_t)(W / 2 * 16), bar);
+      }
+    }
+    return;
+  }
   if (warp == kHsCompute / 32) {
     // ===== producer warp: one bulk copy per tensor (and skip block) per strip =====
     if ((tid & 31) == 0) {
@@ -652,7 +692,9 @@ __global__ void __launch_bounds__(kHsThreads, 1) head_strips_kernel(
         in[j] = iy >= 0 && iy < H;
         dv[j] = *reinterpret_cast<const float4*>(ubase + p * kHsC + q * 4);
         // channels 4q..4q+3: cg8 block (q >> 1), bytes (q & 1) * 8 of position r*L + x
-        const size_t so = (size_t)(r * L + x) * 16 + (q & 1) * 8;
+        // (phase-plane skip: position (r*2 + x%2) * W/2 + x/2)
+        const size_t so = (SKIP_PP ? (size_t)((r * 2 + (x & 1)) * (W / 2) + (x >> 1)) : (size_t)(r * L + x)) * 16 +
+                          (q & 1) * 8;
         hv[j] = *reinterpret_cast<const uint2*>(sbase + (size_t)(q >> 1) * g.sblk + so);
         lv[j] = np == 2 ? *reinterpret_cast<const uint2*>(sbase + (size_t)(2 + (q >> 1)) * g.sblk + so)
                         : make_uint2(0u, 0u);
@@ -978,6 +1020,11 @@ void set_smem(K kern) {
 
 }  // namespace
 
+bool stem_pp_only_ok(int C0, int F, int H, int W) {
+  return C0 == kStemC && F >= 1 && F <= kStemMaxF && H % 4 == 0 && W % 2 == 0 && (W == 32 || W == 64 || W == 128) &&
+         head_strips_ok(C0, 1, H, W);
+}
+
 void launch_stem_planes(const float* w, const float* bias, const Src& x, int F, int C0,
                         const PlBuf& pl, const PlBuf& pp, int64_t B, int H, int W, bool bf16,
                         cudaStream_t st, const float* canon_host) {
@@ -1005,8 +1052,11 @@ void launch_stem_planes(const float* w, const float* bias, const Src& x, int F, 
     STDA_CHECK(smem <= 200 * 1024, "stem: rows do not fit shared memory");
     auto go = [&](auto fc) {
       constexpr int FF = decltype(fc)::value;
-      const auto kern = bf16 ? (PXr == 4 ? stem_const_kernel<FF, 4, 1> : stem_const_kernel<FF, 2, 1>)
-                             : (PXr == 4 ? stem_const_kernel<FF, 4, 2> : stem_const_kernel<FF, 2, 2>);
+      const bool pl_out = pl.base != nullptr;
+      const auto kern = !pl_out ? (bf16 ? stem_const_kernel<FF, 2, 1, false> : stem_const_kernel<FF, 2, 2, false>)
+                        : bf16 ? (PXr == 4 ? stem_const_kernel<FF, 4, 1> : stem_const_kernel<FF, 2, 1>)
+                               : (PXr == 4 ? stem_const_kernel<FF, 4, 2> : stem_const_kernel<FF, 2, 2>);
+      STDA_CHECK(pl_out || PXr == 2, "stem: phase-planes-only output needs 2-pixel threads");
       ensure_dyn_smem(kern, 200 * 1024);
       for (int64_t b0 = 0; b0 < B; b0 += 65535) {
         dim3 grid(H / R, (unsigned)std::min<int64_t>(65535, B - b0));
@@ -1021,6 +1071,7 @@ void launch_stem_planes(const float* w, const float* bias, const Src& x, int F, 
     }
     return;
   }
+  STDA_CHECK(pl.base != nullptr, "stem: phase-planes-only output needs the constant-bank stem");
   if (x.xp == 1 && H % 2 == 0 && W % 2 == 0 && W <= 1024) {
     // bulk-copy row-block path: R rows (even, dividing H) with R*W ~ 512 pixels
     // (256 threads x 2 vertically adjacent pixels)
@@ -1066,6 +1117,7 @@ void launch_head_fused(const float* w, const float* bias, const float* gap, int 
     int dev = 0, sms = 148;
     STDA_CUDA(cudaGetDevice(&dev));
     STDA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    STDA_CHECK(skip.planes == 1 || W <= 128, "head: phase-plane skip needs the whole-width strips");
     if (W > 128) {  // column tiles
       const HeadTiles g = head_tiles_geom(128);
       const int64_t n_strips = B * (H / g.R) * (W / 128);
@@ -1080,7 +1132,8 @@ void launch_head_fused(const float* w, const float* bias, const float* gap, int 
     const int64_t n_strips = B * (H / g.R);
     const unsigned grid = (unsigned)std::min<int64_t>(n_strips, sms);
     auto go = [&](auto wc) {
-      const auto kern = head_strips_kernel<decltype(wc)::value>;
+      const auto kern = skip.planes == 4 ? head_strips_kernel<decltype(wc)::value, true>
+                                         : head_strips_kernel<decltype(wc)::value, false>;
       ensure_dyn_smem(kern, 227 * 1024);
       launch_pdl(kern, dim3(grid), dim3(kHsThreads), g.smem, st, "head_strips_kernel", hc, bias, gap, items, eca_w,
                  k, d, skip, y, B, H, (int)bf16);
@@ -1090,6 +1143,7 @@ void launch_head_fused(const float* w, const float* bias, const float* gap, int 
     else go(std::integral_constant<int, 128>{});
     return;
   }
+  STDA_CHECK(skip.planes == 1, "head: phase-plane skip needs the strip head");
   const size_t smem = sizeof(float) * ((size_t)(kHeadTH + 2) * kIW * (C0 + 4) + 9 * C0 + 2 * C0);
   STDA_CHECK(smem <= 200 * 1024, "head kernel: stem_channels too large for the smem tile");
   set_smem(head_fused_kernel);

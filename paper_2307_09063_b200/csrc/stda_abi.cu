@@ -167,6 +167,7 @@ struct stda_plan {
 
   bool use_tc = false;  // every encoder/decoder conv runs on the tcgen05 kernel
   bool stem_fused = false;  // the stem runs inside the enc0.s1 tcgen05 kernel (tc_launch_stem)
+  bool stem_pp = false;     // the stem writes phase planes only; enc0.s1 = CONV3_S1P, head skip from PP
   float* head_wt = nullptr;  // head weights [9][c0] for the NHWC head kernel
   std::vector<float> stem_canon;  // host copy of the stem's canonical weights + bias (constant-bank stem)
   std::vector<float> head_host;   // host copy of head_wt (constant-bank strip head)
@@ -324,12 +325,14 @@ void run_net_tc(const stda_plan& p, const Src& x, float* y, int64_t B, const Net
   stem.canon = p.stem_canon.empty() ? nullptr : p.stem_canon.data();
   const bool fuse_stem = p.stem_fused && tc::tc_stem_fusable(p.enc[0].s1_tc, stem, h, wd);
   if (!fuse_stem) {
-    launch_stem_planes(p.stem.w, p.stem.b, x, c.input_frames, c0, w.pl_s, w.pp_s, B, h, wd, bf, st,
-                       p.stem_canon.empty() ? nullptr : p.stem_canon.data());
+    PlBuf no_pl = w.pl_s;
+    no_pl.base = nullptr;  // stem_pp: phase planes only
+    launch_stem_planes(p.stem.w, p.stem.b, x, c.input_frames, c0, p.stem_pp ? no_pl : w.pl_s, w.pp_s, B, h, wd,
+                       bf, st, p.stem_canon.empty() ? nullptr : p.stem_canon.data());
     if (!p.stem_fused) mk.mark(st);  // (fused plans profile stem + enc0.s1 as one launch)
   }
   PlBuf cur_pl = w.pl_s, cur_pp = w.pp_s;
-  std::vector<PlBuf> skips{w.pl_s};
+  std::vector<PlBuf> skips{p.stem_pp ? w.pp_s : w.pl_s};
   for (int i = 0; i < S; ++i) {
     const EncLayers& E = p.enc[i];
     tc::TcLayerDesc d1 = E.s1_tc, d2 = E.s2_tc;
@@ -552,7 +555,17 @@ int stda_plan_create(const stda_config* cfg, const float* blob, size_t n_floats,
         const size_t n1 = (size_t)ch * ch * 9, n2 = (size_t)2 * ch * ch * 9;
         // encoder stage 1 reads the phase planes its stride-2 partner reads anyway (stem /
         // encoder gate PP) and writes the 2x2 output phases of one A read per shift
-        const int m1 = tc::s1p_enabled() && tc::tc_supported(CONV3_S1P, ch, ch) ? CONV3_S1P : CONV3_S1;
+        // (enc0: also when the stem writes phase planes only, stem_pp)
+        static const bool stem_pp_on = [] {
+          const char* e = std::getenv("STDA_STEM_PP");
+          return !(e && e[0] == '0');
+        }();
+        if (i == 0)
+          p->stem_pp = stem_pp_on && tc::tc_supported(CONV3_S1P, ch, ch) &&
+                       stem_pp_only_ok(c0, cfg->input_frames, cfg->map_height, cfg->map_width);
+        const int m1 = (tc::s1p_enabled() || (i == 0 && p->stem_pp)) && tc::tc_supported(CONV3_S1P, ch, ch)
+                           ? CONV3_S1P
+                           : CONV3_S1;
         E.s1_tc = p->make_tc(m1, ch, ch, w_s1, w_s1 + n1, nullptr, nullptr, cfg->map_width >> i);
         E.s2_tc = p->make_tc(CONV3_S2, ch, 2 * ch, w_dn, w_dn + n2, w_rs, w_rs + n2, 0);
       }
@@ -562,9 +575,9 @@ int stda_plan_create(const stda_config* cfg, const float* blob, size_t n_floats,
         // static part of tc_stem_fusable (the input's alignment / strides are checked per call)
         static const bool fused_on = [] {
           const char* e = std::getenv("STDA_STEM_FUSED");
-          return !(e && e[0] == '0');
+          return e && e[0] == '1';
         }();
-        p->stem_fused = fused_on && E.s1_tc.mode == CONV3_S1 && c0 == 16 && cfg->input_frames <= 4 &&
+        p->stem_fused = fused_on && !p->stem_pp && E.s1_tc.mode == CONV3_S1 && c0 == 16 && cfg->input_frames <= 4 &&
                         cfg->map_width % 4 == 0 && cfg->map_width <= 128;
       }
     }

@@ -521,7 +521,7 @@ size_t stem_extra_smem(int G, int L, int F, int W) {
 bool tc_stem_fusable(const TcLayerDesc& d1, const TcStem& s, int H, int W) {
   static const bool on = [] {
     const char* e = std::getenv("STDA_STEM_FUSED");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
   }();
   return on && s.canon && d1.mode == CONV3_S1 && d1.cin == kStemC && d1.cout == kStemC &&
          s.F >= 1 && s.F <= kStemMaxF && s.x.xp == 1 && W % 4 == 0 && W <= 128 && H >= 2 &&
