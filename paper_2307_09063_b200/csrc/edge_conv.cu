@@ -528,7 +528,9 @@ __host__ __device__ constexpr HeadStrips head_strips_geom(int W) {
   g.SR = g.R + 2;
   g.L = W + 1;
   g.dbytes = g.SR * W * kHsC * 4;
-  g.sblk = g.SR * g.L * 16;
+  // (a phase-plane skip stages ceil(SR/2) rows x (W/2 + 1) positions for each of 4 planes)
+  g.sblk = g.SR * g.L * 16 > 4 * ((g.SR + 1) / 2) * (W / 2 + 1) * 16 ? g.SR * g.L * 16
+                                                                      : 4 * ((g.SR + 1) / 2) * (W / 2 + 1) * 16;
   g.stage = g.dbytes + 4 * g.sblk;
   g.smem = 2 * (size_t)g.stage + (9 * kHsC + kHsC + 16 * kHsC + kHsC) * 4 + 4 * 8;
   return g;
@@ -575,9 +577,12 @@ __global__ void __launch_bounds__(kHsThreads, 1) head_strips_kernel(
   grid_dep_wait();  // d, gap and skip come from the previous kernels
 
   if (warp == kHsCompute / 32 && SKIP_PP) {
-    // ===== producer warp, phase-plane skip: lane 0 posts the bytes, lanes issue the copies
+    // ===== producer warp, phase-plane skip: lane 0 posts the bytes, lanes issue the copies.
+    // The strip's staged rows of one parity py are consecutive rows of the py planes, so
+    // per (block, py, px) ONE copy of those plane rows (with their pad column): the stage
+    // holds [block][py*2+px][plane row][Lp] (hs_pp_row() maps a staged row to its slot)
     const int lane = tid & 31;
-    const int Lp = W / 2 + 1;
+    constexpr int Lp = W / 2 + 1;
     int i = 0;
     for (int64_t s = s_begin; s < s_end; ++s, ++i) {
       const int st = i & 1;
@@ -587,25 +592,27 @@ __global__ void __launch_bounds__(kHsThreads, 1) head_strips_kernel(
       const int r0 = y0 == 0 ? 1 : 0;
       const int r1 = y0 + R == H ? SR - 1 : SR;
       const int nr = r1 - r0, iy0 = y0 - 1 + r0;
+      const int n0 = (nr + 1 - (iy0 & 1)) / 2, n1 = nr - n0;  // staged rows of parity 0 / 1
       const uint32_t bar = smem_u32(&full[st]);
       uint8_t* base = hsm + (size_t)st * g.stage;
-      if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)(nr * W * kHsC * 4 + np * 2 * nr * W * 16));
+      if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)(nr * W * kHsC * 4 + np * 2 * 2 * nr * Lp * 16));
       __syncwarp();
       const uint16_t* simg = skip.base + b * skip.img_stride;
-      const int ncp = 1 + nr * 2 * np * 2;
+      const int ncp = 1 + np * 2 * 4;
       for (int c = lane; c < ncp; c += 32) {
         if (c == 0) {
           bulk_g2s(smem_u32(base + (size_t)r0 * W * kHsC * 4), d + ((size_t)b * H + iy0) * W * kHsC,
                    (uint32_t)(nr * W * kHsC * 4), bar);
           continue;
         }
-        const int u = c - 1, px = u & 1, blk = (u >> 1) % (np * 2), rr = (u >> 1) / (np * 2);
-        const int r = r0 + rr, iy = iy0 + rr;
+        const int u = c - 1, plane = u & 3, blk = u >> 2, py = plane >> 1;
         const int pass = blk >> 1, cg8 = blk & 1;
-        bulk_g2s(smem_u32(base + g.dbytes + (size_t)blk * g.sblk + ((size_t)(r * 2 + px) * (W / 2)) * 16),
-                 simg + (int64_t)((iy & 1) * 2 + px) * skip.plane_stride +
-                     (skip.block_index(0, pass, cg8) + skip.off + (size_t)(iy >> 1) * Lp) * 8,
-                 (uint32_t)(W / 2 * 16), bar);
+        const int iyf = iy0 + ((iy0 & 1) != py ? 1 : 0);  // first staged row of parity py
+        const int n = py ? n1 : n0;
+        bulk_g2s(smem_u32(base + g.dbytes + (size_t)blk * g.sblk + (size_t)plane * ((SR + 1) / 2) * Lp * 16),
+                 simg + (int64_t)plane * skip.plane_stride +
+                     (skip.block_index(0, pass, cg8) + skip.off + (size_t)(iyf >> 1) * Lp) * 8,
+                 (uint32_t)(n * Lp * 16), bar);
       }
     }
     return;
@@ -692,9 +699,15 @@ __global__ void __launch_bounds__(kHsThreads, 1) head_strips_kernel(
         in[j] = iy >= 0 && iy < H;
         dv[j] = *reinterpret_cast<const float4*>(ubase + p * kHsC + q * 4);
         // channels 4q..4q+3: cg8 block (q >> 1), bytes (q & 1) * 8 of position r*L + x
-        // (phase-plane skip: position (r*2 + x%2) * W/2 + x/2)
-        const size_t so = (SKIP_PP ? (size_t)((r * 2 + (x & 1)) * (W / 2) + (x >> 1)) : (size_t)(r * L + x)) * 16 +
-                          (q & 1) * 8;
+        // (phase-plane skip: plane (iy%2, x%2), plane-row slot of iy, column x/2)
+        size_t so;
+        if (SKIP_PP) {
+          const int py = iy & 1, iy0s = y0 - 1 + (y0 == 0 ? 1 : 0);
+          const int slot = (iy >> 1) - ((iy0s + ((iy0s & 1) != py ? 1 : 0)) >> 1);
+          so = ((size_t)((py * 2 + (x & 1)) * ((SR + 1) / 2) + slot) * (W / 2 + 1) + (x >> 1)) * 16 + (q & 1) * 8;
+        } else {
+          so = (size_t)(r * L + x) * 16 + (q & 1) * 8;
+        }
         hv[j] = *reinterpret_cast<const uint2*>(sbase + (size_t)(q >> 1) * g.sblk + so);
         lv[j] = np == 2 ? *reinterpret_cast<const uint2*>(sbase + (size_t)(2 + (q >> 1)) * g.sblk + so)
                         : make_uint2(0u, 0u);
