@@ -475,6 +475,41 @@ __device__ __forceinline__ void issue_chunk(bool leader, uint64_t a0, uint64_t b
 }
 
 // ---- the kernel ----------------------------------------------------------------------
+// Channel sums of one warp: v[c] of the 32 lanes summed per channel, written to out[c].
+// Reduce-scatter butterfly: at offset o = 16, 8, ... each lane sends the half of its values
+// it does not keep and adds the partner's half of the kept ones (N/2 + N/4 + ... shuffles
+// instead of 5 per channel); after the halving levels lane l holds channel(s)
+//   N = 64: 2l, 2l+1;  N = 32: l;  N = 16: l/2 (the last offset 1 is a plain add, a + b ==
+// b + a in IEEE arithmetic, so both lanes of a pair hold identical bits).  The addition
+// order per channel is fixed by the lane numbering: deterministic and batch-invariant.
+template <int N>
+__device__ __forceinline__ void gap_lane_reduce(float (&v)[N], int lane, float* out) {
+  constexpr int LV = N >= 32 ? 5 : (N == 16 ? 4 : (N == 8 ? 3 : 0));
+  static_assert(LV > 0, "gap_lane_reduce: N in {8, 16, 32, 64}");
+#pragma unroll
+  for (int lv = 0; lv < LV; ++lv) {
+    const int o = 16 >> lv;
+    const int n = N >> (lv + 1);  // values kept after this level
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < n; ++i) {
+      const float send = up ? v[i] : v[i + n];
+      const float keep = up ? v[i + n] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  if constexpr (N >= 32) {
+    constexpr int K = N / 32;  // values per lane
+#pragma unroll
+    for (int i = 0; i < K; ++i) out[lane * K + i] = v[i];
+  } else {
+    // remaining offsets: plain pairwise adds (all lanes of a group end with identical bits)
+#pragma unroll
+    for (int o = 16 >> LV; o > 0; o >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+    if ((lane & ((32 / N) - 1)) == 0) out[lane / (32 / N)] = v[0];
+  }
+}
+
 // floor division for possibly negative positions
 __device__ __forceinline__ int floordiv(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
 
@@ -932,14 +967,9 @@ __global__ void __launch_bounds__(threads_of(STEM), 1) tc_conv_kernel(const __gr
       if (et == 0) trace_cta_item(p.trace, (int)ic);
       if (p.out.mode != 0 && it == 0) pl_zero_margins(p.out.pl, b, et, kEpiWarps * 32);
       if (p.out.mode == 0 && p.out.gap) {
-        // deterministic: fixed-order sum of the 8 warp partials
-#pragma unroll
-        for (int c = 0; c < N; ++c) {
-          float s = gsum[c];
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-          if (lane == 0) red[(warp - kEpiWarp0) * N + c] = s;
-        }
+        // deterministic: a fixed butterfly over the lanes, then a fixed-order sum of the
+        // 8 warp partials
+        gap_lane_reduce<N>(gsum, lane, red + (warp - kEpiWarp0) * N);
         asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
         if (et < N) {
           float s = red[et];
