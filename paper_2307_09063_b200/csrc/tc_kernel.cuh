@@ -295,6 +295,12 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
       "l"(src), "r"(bytes), "r"(bar)
       : "memory");
 }
+// 256-bit global store (sm_100): 8 floats at a 32-byte aligned address
+__device__ __forceinline__ void st_global_v8(float* dst, const float* v) {
+  asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst), "f"(v[0]), "f"(v[1]),
+               "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+               : "memory");
+}
 __device__ __forceinline__ void bulk_s2g(void* dst, uint32_t src, uint32_t bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src), "r"(bytes)
                : "memory");
@@ -936,9 +942,10 @@ __global__ void __launch_bounds__(threads_of(STEM), 1) tc_conv_kernel(const __gr
             if (!valid || (p.dbg & 1)) continue;
             if (p.out.mode == 0) {
               float* op = p.out.f32 + (((size_t)b * p.Ho + oy) * p.Wo + ox) * N;
+              // 32-byte stores: each lane writes whole L2 sectors (the lanes' pixels are
+              // 2 apart in the ConvT phases, so a warp's stores cannot coalesce further)
 #pragma unroll
-              for (int i = 0; i < 16; i += 4)
-                *reinterpret_cast<float4*>(op + j + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+              for (int i = 0; i < 16; i += 8) st_global_v8(op + j + i, v + i);
 #pragma unroll
               for (int i = 0; i < 16; ++i) gsum[j + i] += v[i];
             } else {
