@@ -3,8 +3,11 @@ stall reasons in total and for the top instructions."""
 import csv
 import sys
 
-rows = list(csv.reader(open(sys.argv[1])))
-hdr, data = rows[1], rows[2:]
+rows = [r for r in csv.reader(open(sys.argv[1])) if r]
+# the source page may carry a preamble: the header is the first row with "Address"
+hi = next(i for i, r in enumerate(rows) if "Address" in r and "Source" in r)
+hdr = rows[hi]
+data = [r for r in rows[hi + 1:] if len(r) == len(hdr)]
 reasons = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
 col = {h: i for i, h in enumerate(hdr)}
 f = lambda r, h: float(r[col[h]] or 0)
