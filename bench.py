@@ -469,7 +469,16 @@ def run_engine(args, world, rank, local):
         flush.zero_()
         names, ms = cap.profile()
         acc = ms if acc is None else [a + b for a, b in zip(acc, ms)]
-    avg = [a / 5 for a in acc]
+    avg_evt = [a / 5 for a in acc]
+    # each launch's own duration: the slot run alone 20 times back to back after a full
+    # forward (inputs in place, CUDA events around the repeats) — the event-per-launch
+    # profile above adds each launch's drain and start-up gap to its time
+    try:
+        avg = [cap.launch_repeat(i, 20) for i in range(len(names))]
+        launch_timing = "each launch alone x20 back to back, CUDA events around the repeats"
+    except Exception:  # SIMT-path plans: the event-per-launch profile
+        avg = avg_evt
+        launch_timing = "CUDA events between the launches of eager forwards"
     fl = layer_flops(cfg)
     byt = layer_bytes(cfg)
     opb = layer_operand_bytes(cfg, args.precision)
@@ -535,6 +544,8 @@ def run_engine(args, world, rank, local):
             "whole_forward_tflops": total_flops * batch / (ms_per_step * 1e-3) / 1e12,
             "forward_operand_floor_us": sum(floor_us.values()),
             "launch_us": {n: m * 1e3 for n, m in share.items()},
+            "launch_timing": launch_timing,
+            "launch_us_event_profile": {n: m * 1e3 for n, m in zip(names, avg_evt)},
             "launch_share": {n: m / sum(avg) for n, m in share.items()},
         },
         "e2e": {"value": e2e_rate, "unit": "triplets/s",

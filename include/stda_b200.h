@@ -93,6 +93,12 @@ int stda_forward(const stda_plan* plan, const float* x, float* y, int64_t batch,
 int stda_forward_profiled(const stda_plan* plan, const float* x, float* y, int64_t batch,
                           void* workspace, size_t workspace_bytes, void* stream,
                           float* ms_per_launch, int32_t n);
+/* Measurement aid (bench.py roofline): one stda_forward (every intermediate in place), then
+ * launch slot `slot` alone `reps` times back to back; *ms_per_launch = the average device
+ * time per launch (CUDA events around the repeats).  Tensor-core plans only. */
+int stda_forward_launch_repeat(const stda_plan* plan, const float* x, float* y, int64_t batch,
+                               void* workspace, size_t workspace_bytes, void* stream, int32_t slot,
+                               int32_t reps, float* ms_per_launch);
 /* ';'-separated launch names in stda_forward order (thread-local storage). */
 const char* stda_launch_names(const stda_plan* plan);
 

@@ -37,6 +37,7 @@ SIGNATURES = {
     "stda_workspace_bytes": (_sz, [_vp, _i64]),
     "stda_forward": (C.c_int, [_vp, _vp, _vp, _i64, _vp, _sz, _vp]),
     "stda_forward_profiled": (C.c_int, [_vp, _vp, _vp, _i64, _vp, _sz, _vp, _vp, _i32]),
+    "stda_forward_launch_repeat": (C.c_int, [_vp, _vp, _vp, _i64, _vp, _sz, _vp, _i32, _i32, _vp]),
     "stda_launch_names": (C.c_char_p, [_vp]),
     "stda_forward_window": (C.c_int, [_vp, _vp, _i64, _vp, _vp, _sz, _vp]),
     "stda_host_chunk": (_i64, [_vp, _i64]),
@@ -138,6 +139,13 @@ def forward_profiled(h, x, y, batch, ws, ws_bytes, stream):
     _check(lib().stda_forward_profiled(h, x, y, batch, ws, ws_bytes, stream, ms, n),
            "stda_forward_profiled")
     return list(ms)
+
+
+def forward_launch_repeat(h, x, y, batch, ws, ws_bytes, stream, slot: int, reps: int) -> float:
+    ms = (C.c_float * 1)()
+    _check(lib().stda_forward_launch_repeat(h, x, y, batch, ws, ws_bytes, stream, slot, reps, ms),
+           "stda_forward_launch_repeat")
+    return float(ms[0])
 
 
 def launch_names(h):

@@ -168,6 +168,8 @@ struct stda_plan {
   bool use_tc = false;  // every encoder/decoder conv runs on the tcgen05 kernel
   bool stem_fused = false;  // the stem runs inside the enc0.s1 tcgen05 kernel (tc_launch_stem)
   bool stem_pp = false;     // the stem writes phase planes only; enc0.s1 = CONV3_S1P, head skip from PP
+  bool stem_tc_on = false;  // ... computed on the tensor cores (CONV_STEMT, tc_launch_stemt)
+  tc::TcLayerDesc stem_tc;
   float* head_wt = nullptr;  // head weights [9][c0] for the NHWC head kernel
   std::vector<float> stem_canon;  // host copy of the stem's canonical weights + bias (constant-bank stem)
   std::vector<float> head_host;   // host copy of head_wt (constant-bank strip head)
@@ -292,10 +294,15 @@ NetWs plan_ws(const stda_plan& p, int64_t B, char* base) {
 
 // Optional per-launch event marks (stda_forward_profiled): ev[0] before the first
 // launch, ev[i+1] after launch i.
+// `only` >= 0 launches that slot alone (stda_forward_launch_repeat; tensor-core path).
 struct Marks {
   std::vector<cudaEvent_t>* ev = nullptr;
   int i = 0;
+  int n = 0;      // marks so far: the next launch is slot n - 1
+  int only = -1;
+  bool go() const { return only < 0 || n - 1 == only; }
   void mark(cudaStream_t st) {
+    ++n;
     if (ev) STDA_CUDA(cudaEventRecord((*ev)[i++], st));
   }
 };
@@ -324,10 +331,20 @@ void run_net_tc(const stda_plan& p, const Src& x, float* y, int64_t B, const Net
   stem.has_pl = true;
   stem.canon = p.stem_canon.empty() ? nullptr : p.stem_canon.data();
   const bool fuse_stem = p.stem_fused && tc::tc_stem_fusable(p.enc[0].s1_tc, stem, h, wd);
-  if (!fuse_stem) {
+  if (!fuse_stem && p.stem_pp && p.stem_tc_on && tc::tc_stemt_ok(stem, h, wd)) {
+    // the stem as a tcgen05 GEMM per half-resolution position, writing the phase planes
+    tc::TcLayerDesc ds = p.stem_tc;
+    const tc::TcGeometry gs = tc::tc_plan_stemt(ds, (int)B, h, wd, c.input_frames);
+    tc::TcOut os;
+    os.mode = 2;
+    os.pl = w.pp_s;
+    if (mk.go()) tc::tc_launch_stemt(ds, gs, stem, os, st);
+    mk.mark(st);
+  } else if (!fuse_stem) {
     PlBuf no_pl = w.pl_s;
     no_pl.base = nullptr;  // stem_pp: phase planes only
-    launch_stem_planes(p.stem.w, p.stem.b, x, c.input_frames, c0, p.stem_pp ? no_pl : w.pl_s, w.pp_s, B, h, wd,
+    if (mk.go())
+      launch_stem_planes(p.stem.w, p.stem.b, x, c.input_frames, c0, p.stem_pp ? no_pl : w.pl_s, w.pp_s, B, h, wd,
                        bf, st, p.stem_canon.empty() ? nullptr : p.stem_canon.data());
     if (!p.stem_fused) mk.mark(st);  // (fused plans profile stem + enc0.s1 as one launch)
   }
@@ -341,17 +358,17 @@ void run_net_tc(const stda_plan& p, const Src& x, float* y, int64_t B, const Net
     o1.pl = mviews[i];
     if (i == 0 && fuse_stem) {
       const tc::TcGeometry g1 = tc::tc_plan_stem(d1, (int)B, h, wd, c.input_frames);
-      tc::tc_launch_stem(d1, g1, stem, o1, st, /*rev=*/true);
+      if (mk.go()) tc::tc_launch_stem(d1, g1, stem, o1, st, /*rev=*/true);
     } else {
       const tc::TcGeometry g1 = tc::tc_plan(d1, (int)B, h, wd);
-      tc::tc_launch(d1, g1, d1.mode == CONV3_S1P ? cur_pp : cur_pl, nullptr, o1, true, st, /*rev=*/true);
+      if (mk.go()) tc::tc_launch(d1, g1, d1.mode == CONV3_S1P ? cur_pp : cur_pl, nullptr, o1, true, st, /*rev=*/true);
     }
     mk.mark(st);
     const tc::TcGeometry g2 = tc::tc_plan(d2, (int)B, h, wd);
     tc::TcOut o2;
     o2.f32 = w.e[i];
     o2.gap = w.pe[i];
-    tc::tc_launch(d2, g2, mviews[i], &cur_pp, o2, true, st);
+    if (mk.go()) tc::tc_launch(d2, g2, mviews[i], &cur_pp, o2, true, st);
     mk.mark(st);
     h /= 2;
     wd /= 2;
@@ -360,11 +377,12 @@ void run_net_tc(const stda_plan& p, const Src& x, float* y, int64_t B, const Net
     const float* gsrc = w.pe[i];
     int gitems = g2.items_per_image;
     if (precompute_gates(gitems, d2.cout)) {
-      launch_eca_gates(gsrc, gitems, E.eca, k, w.ge[i], B, d2.cout, (int64_t)h * wd, st);
+      if (mk.go()) launch_eca_gates(gsrc, gitems, E.eca, k, w.ge[i], B, d2.cout, (int64_t)h * wd, st);
       gsrc = w.ge[i];
       gitems = kGatesReady;
     }
-    launch_gate_apply(gsrc, gitems, E.eca, k, w.e[i], nullptr, &w.pl_a[i],
+    if (mk.go())
+      launch_gate_apply(gsrc, gitems, E.eca, k, w.e[i], nullptr, &w.pl_a[i],
                       i + 1 < S ? &w.pp_a[i] : nullptr, nullptr, B, d2.cout, h, wd, st);
     mk.mark(st);
     cur_pl = w.pl_a[i];
@@ -378,13 +396,13 @@ void run_net_tc(const stda_plan& p, const Src& x, float* y, int64_t B, const Net
     tc::TcOut o1;
     o1.mode = 1;  // plane for the ConvT consumer
     o1.pl = mviews[S + j];
-    tc::tc_launch(d1, g1, cur_pl, nullptr, o1, true, st, /*rev=*/true);
+    if (mk.go()) tc::tc_launch(d1, g1, cur_pl, nullptr, o1, true, st, /*rev=*/true);
     mk.mark(st);
     const tc::TcGeometry g2 = tc::tc_plan(d2, (int)B, h, wd);
     tc::TcOut o2;
     o2.f32 = w.d[j];
     o2.gap = w.pd[j];
-    tc::tc_launch(d2, g2, mviews[S + j], &cur_pl, o2, true, st);
+    if (mk.go()) tc::tc_launch(d2, g2, mviews[S + j], &cur_pl, o2, true, st);
     mk.mark(st);
     h *= 2;
     wd *= 2;
@@ -393,17 +411,19 @@ void run_net_tc(const stda_plan& p, const Src& x, float* y, int64_t B, const Net
     const float* gsrc = w.pd[j];
     int gitems = g2.items_per_image;
     if (precompute_gates(gitems, d2.cout)) {
-      launch_eca_gates(gsrc, gitems, D.eca, k, w.gd[j], B, d2.cout, (int64_t)h * wd, st);
+      if (mk.go()) launch_eca_gates(gsrc, gitems, D.eca, k, w.gd[j], B, d2.cout, (int64_t)h * wd, st);
       gsrc = w.gd[j];
       gitems = kGatesReady;
     }
     if (j + 1 < S) {
-      launch_gate_apply(gsrc, gitems, D.eca, k, w.d[j], &sk, &w.pl_b[j], nullptr, nullptr, B, d2.cout, h, wd,
-                        st);
+      if (mk.go())
+        launch_gate_apply(gsrc, gitems, D.eca, k, w.d[j], &sk, &w.pl_b[j], nullptr, nullptr, B, d2.cout, h, wd,
+                          st);
       mk.mark(st);
       cur_pl = w.pl_b[j];
     } else {
-      launch_head_fused(p.head_wt, p.head.b, gsrc, gitems, D.eca, k, w.d[j], sk, c0, y, B, h,
+      if (mk.go())
+        launch_head_fused(p.head_wt, p.head.b, gsrc, gitems, D.eca, k, w.d[j], sk, c0, y, B, h,
                         wd, bf, st, p.head_host.empty() ? nullptr : p.head_host.data());
       mk.mark(st);
     }
@@ -541,6 +561,7 @@ int stda_plan_create(const stda_config* cfg, const float* blob, size_t n_floats,
       if (p->bf16)
         for (float& v : p->stem_canon) v = __bfloat162float(__float2bfloat16_rn(v));
     }
+    const float* stem_src = src;  // canonical stem weights [c0][F][3][3] + bias [c0]
     p->stem = p->make_layer(CONV3_S1, cfg->input_frames, c0, src);
     for (int i = 0; i < S; ++i) {
       const int ch = c0 << i;
@@ -579,6 +600,14 @@ int stda_plan_create(const stda_config* cfg, const float* blob, size_t n_floats,
         }();
         p->stem_fused = fused_on && !p->stem_pp && E.s1_tc.mode == CONV3_S1 && c0 == 16 && cfg->input_frames <= 4 &&
                         cfg->map_width % 4 == 0 && cfg->map_width <= 128;
+        // the phase-plane stem on the tensor cores (CONV_STEMT)
+        const int F = cfg->input_frames;
+        if (p->stem_pp && !p->stem_fused && F <= 4 && tc::tc_supported(CONV_STEMT, 16 * F, c0)) {
+          const float* sw = stem_src;
+          p->stem_tc = p->make_tc(CONV_STEMT, 16 * F, c0, sw, sw + (size_t)c0 * F * 9, nullptr, nullptr,
+                                  cfg->map_width);
+          p->stem_tc_on = true;
+        }
       }
     }
     for (int j = 0; j < S; ++j) {
@@ -695,6 +724,39 @@ int stda_forward_profiled(const stda_plan* plan, const float* x, float* y, int64
     STDA_CUDA(cudaEventSynchronize(ev[L]));
     for (int i = 0; i < L; ++i) STDA_CUDA(cudaEventElapsedTime(&ms_per_launch[i], ev[i], ev[i + 1]));
     for (auto& e : ev) cudaEventDestroy(e);
+  });
+}
+
+int stda_forward_launch_repeat(const stda_plan* plan, const float* x, float* y, int64_t batch, void* ws,
+                               size_t ws_bytes, void* stream, int32_t slot, int32_t reps, float* ms_per_launch) {
+  return guarded([&] {
+    STDA_CHECK(plan && plan->kind == 0 && plan->use_tc, "not a tensor-core network plan");
+    STDA_CHECK(batch > 0 && x && y && ms_per_launch && reps > 0, "bad arguments");
+    STDA_CHECK(slot >= 0 && slot < stda_launches_per_forward(plan), "launch slot out of range");
+    const NetWs need = plan_ws(*plan, batch, nullptr);
+    check_ws(plan, ws, ws_bytes, need.bytes);
+    DeviceGuard g(plan->device);
+    const stda_config& c = plan->cfg;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const Src xs = plain_src(x, c.input_frames, c.map_height, c.map_width);
+    const NetWs w = plan_ws(*plan, batch, static_cast<char*>(ws));
+    run_net(*plan, xs, y, batch, w, st);  // every intermediate of this input in place
+    cudaEvent_t e0, e1;
+    STDA_CUDA(cudaEventCreate(&e0));
+    STDA_CUDA(cudaEventCreate(&e1));
+    STDA_CUDA(cudaEventRecord(e0, st));
+    for (int r = 0; r < reps; ++r) {
+      Marks mk;
+      mk.only = slot;
+      run_net(*plan, xs, y, batch, w, st, mk);
+    }
+    STDA_CUDA(cudaEventRecord(e1, st));
+    STDA_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    STDA_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    *ms_per_launch = ms / (float)reps;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
   });
 }
 

@@ -142,6 +142,16 @@ TcGeometry tc_plan_stem(TcLayerDesc& d1, int B, int H, int W, int F);
 void tc_launch_stem(const TcLayerDesc& d1, const TcGeometry& g, const TcStem& s, const TcOut& out,
                     cudaStream_t st, bool rev);
 
+// ---- tensor-core stem (CONV_STEMT) ---------------------------------------------------------
+// The stem as a tcgen05 GEMM (simt_conv.cuh CONV_STEMT): im2col warps build each
+// position's F x 4 x 4 frame window (bf16 hi/lo) from frame rows staged by bulk copies;
+// the epilogue writes the stem output's phase planes (PP).  Layer: make_tc(CONV_STEMT,
+// 16 * F, 16, canonical stem weights [16][F][3][3], bias).  Opt-in: env STDA_STEM_TC=1.
+bool tc_stemt_ok(const TcStem& s, int H, int W);
+TcGeometry tc_plan_stemt(TcLayerDesc& d, int B, int H, int W, int F);
+void tc_launch_stemt(const TcLayerDesc& d, const TcGeometry& g, const TcStem& s, const TcOut& out,
+                     cudaStream_t st);
+
 // Debug: record a clock64 timeline of CTA 0 (see tc_kernel.cuh trace_at) into dev_buf
 // during the launch_index-th following tc_launch.
 void tc_debug_trace(void* dev_buf, int launch_index);

@@ -29,6 +29,7 @@ struct HostTap {
 
 std::vector<HostTap> plane_taps(int mode, int pl) {
   std::vector<HostTap> t;
+  if (mode == CONV_STEMT) return {{0, 0, 0, -1}};  // im2col: one unshifted A read per chunk
   if (mode == CONV3_S1P) {
     // the plane's 4 shift groups (dy, dx = half-resolution shift; acc = first phase of the
     // run); only used for the staged position span (lo / hi) — packing is group-wise
@@ -82,6 +83,7 @@ bool half_t_enabled() {  // env STDA_TC_HALF=0 keeps 3-MMA full ConvT items (A/B
 }
 
 bool tc_supported(int mode, int cin, int cout) {
+  if (mode == CONV_STEMT) return cin % 16 == 0 && cin >= 16 && cin <= 64 && cout == 16;
   if (mode == CONV3_S1P && cout > 32) return false;  // fp32 concat: 4 phases x 2N <= 256 per MMA
   return cin % 16 == 0 && cin >= 16 && cin <= 64 && (cout == 16 || cout == 32 || cout == 64);
 }
@@ -112,7 +114,8 @@ bool rows_enabled() {
 void tc_pack_layer(TcLayerDesc& d, int mode, int cin, int cout, const float* w0, const float* w1,
                    bool bf16, std::vector<uint16_t>& packed, int plane_w) {
   STDA_CHECK(tc_supported(mode, cin, cout), "layer shape not supported by the tensor-core path");
-  STDA_CHECK((mode == CONV3_S1 || mode == CONV3_S1P) == (w1 == nullptr), "S1 layers are single-source, S2/T dual");
+  STDA_CHECK((mode == CONV3_S1 || mode == CONV3_S1P || mode == CONV_STEMT) == (w1 == nullptr),
+             "S1 layers are single-source, S2/T dual");
   // stride-1 layers over planes whose width is a multiple of 128 run as row bands (one A
   // read per input row serves three dy taps) when three stacked tap blocks fit one MMA
   if (mode == CONV3_S1 && rows_enabled() && plane_w > 0 && plane_w % 128 == 0 && 3 * (bf16 ? 1 : 2) * cout <= 256)
@@ -174,6 +177,33 @@ void tc_pack_layer(TcLayerDesc& d, int mode, int cin, int cout, const float* w0,
     const float hi = bf16_val(v);
     packed.push_back(bf16_bits(pass == 0 ? v : v - hi));
   };
+  if (mode == CONV_STEMT) {
+    // canonical stem weights [co][F][3][3]; chunk f = frame f; per chunk the 4 stacked phase
+    // tiles [kgrp 2][phase 4][pass][cout][8]: K element e of group kg is window pixel
+    // (wy, wx) = (2kg + e/4, e%4), read by output phase (py, px) through tap
+    // (ky, kx) = (wy - py, wx - px) when both lie in 0..2 (else a zero weight)
+    const int F = cin / 16;
+    for (int f = 0; f < F; ++f) {
+      for (int kg = 0; kg < 2; ++kg)
+        for (int ph = 0; ph < 4; ++ph)
+          for (int pass = 0; pass < npassB; ++pass)
+            for (int n = 0; n < cout; ++n)
+              for (int e = 0; e < 8; ++e) {
+                const int wy = 2 * kg + e / 4, wx = e % 4;
+                const int ky = wy - (ph >> 1), kx = wx - (ph & 1);
+                if (ky < 0 || ky > 2 || kx < 0 || kx > 2) {
+                  packed.push_back(0);
+                  continue;
+                }
+                const float v = w0[((size_t)n * F + f) * 9 + ky * 3 + kx];
+                const float hi = bf16_val(v);
+                packed.push_back(bf16_bits(pass == 0 ? v : v - hi));
+              }
+      d.chunk_off[f + 1] = (int64_t)packed.size() * 2;
+    }
+    d.concat = !bf16;
+    return;
+  }
   if (mode == CONV3_S1P) {
     // per chunk (input plane, 16-channel group), per shift group gi: the stacked tiles
     // [kgrp 2][phase slot n][pass][cout][8]; tile j = output phase p0 + j reads input
@@ -299,7 +329,7 @@ TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W, size_t extra_smem, bool 
     g.Wp = W / 2;
     g.Ho = H / 2;
     g.Wo = W / 2;
-  } else if (d.mode == CONV3_S1P) {  // half-resolution position grid, full-resolution output
+  } else if (d.mode == CONV3_S1P || d.mode == CONV_STEMT) {  // half-res positions, full-res output
     g.Hp = H / 2;
     g.Wp = W / 2;
     g.Ho = H;
@@ -390,7 +420,7 @@ TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W, size_t extra_smem, bool 
   // per item (A/B timing of load balance vs halo reuse)
   static const char* gmax_env = std::getenv("STDA_TC_GMAX");
   int gmax = gmax_env && (int)std::strlen(gmax_env) > d.mode ? gmax_env[d.mode] - '0' : 4;
-  if ((d.mode == CONV3_S1 || d.mode == CONV3_S1P) && !gmax_env) {
+  if ((d.mode == CONV3_S1 || d.mode == CONV3_S1P || d.mode == CONV_STEMT) && !gmax_env) {
     // load balance: the largest G that still gives every CTA >= 6 full items (fewer,
     // larger items leave the persistent CTAs with 2-4 rounds dominated by pipeline fill
     // and the last partial round).  Measured at C2 (B=64): enc0.s1 G=4, enc1.s1 / dec1.s1
@@ -428,7 +458,8 @@ TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W, size_t extra_smem, bool 
           return e ? std::max(1, std::min(kMaxStages, std::atoi(e))) : 3;
         }();
         const bool tmode = d.mode == CONVT4_S2 || d.mode == CONVT4_HALF;
-        for (int st = d.mode == CONV3_S2 ? kMaxStages : tmode ? t_stages : s1_stages; st >= 1; --st) {
+        const int st_cap = d.mode == CONV3_S2 || d.mode == CONV_STEMT ? kMaxStages : tmode ? t_stages : s1_stages;
+        for (int st = st_cap; st >= 1; --st) {
           const size_t need = resident ? (size_t)st * a_stage + w_res : (size_t)st * (a_stage + b_stage);
           if (need + fixed <= (size_t)kMaxSmem) {
             stages = st;
@@ -517,6 +548,94 @@ size_t stem_extra_smem(int G, int L, int F, int W) {
   return 2 * ((size_t)F * stem_xrows(G, L) * W * 4) + 128;
 }
 }  // namespace
+
+// ---- tensor-core stem (CONV_STEMT) --------------------------------------------------------
+namespace {
+// frame rows of one item: its half-resolution rows y_lo..y_hi -> frame rows 2y_lo-1 .. 2y_hi+2
+int stemt_xrows(int G, int L) { return 2 * ((G * 128 + L - 2) / L) + 4; }
+size_t stemt_extra_smem(int G, int L, int F, int W) { return 2 * ((size_t)F * stemt_xrows(G, L) * W * 4) + 128; }
+}  // namespace
+
+bool tc_stemt_ok(const TcStem& s, int H, int W) {
+  // env STDA_STEM_TC=1 enables it.  Off by default: parity-green, but at C2 it runs 33 us
+  // (CTA median) against the SIMT stem's ~27 us.  Ablations (tools/stemt_dbg.sh): without
+  // epilogue stores 24.6 us, epilogue releasing slots only 15.7 us — the 67 MB of phase-plane
+  // output leave the 8 epilogue warps at ~14 B/clk/SM against the ~21-25 B/clk/SM store
+  // ceiling (tools/store_bench.cu), and the MMA waits on TMEM slots
+  static const bool on = [] {
+    const char* e = std::getenv("STDA_STEM_TC");
+    return e && e[0] == '1';
+  }();
+  return on && s.F >= 1 && s.F <= kStemMaxF && s.x.xp == 1 && H % 2 == 0 && W % 4 == 0 && W >= 8 &&
+         (reinterpret_cast<uintptr_t>(s.x.x) & 15) == 0 && s.x.xb % 4 == 0 && s.x.xc % 4 == 0 &&
+         s.s_pp.base != nullptr && s.s_pp.C == kStemC && s.s_pp.planes == 4 &&
+         stemt_extra_smem(2, W / 2 + 1, s.F, W) <= 96 * 1024;
+}
+
+TcGeometry tc_plan_stemt(TcLayerDesc& d, int B, int H, int W, int F) {
+  STDA_CHECK(d.mode == CONV_STEMT, "internal: tensor-core stem plan");
+  return tc_plan(d, B, H, W, stemt_extra_smem(2, W / 2 + 1, F, W), /*resident_only=*/true);
+}
+
+void tc_launch_stemt(const TcLayerDesc& d, const TcGeometry& g, const TcStem& s, const TcOut& out,
+                     cudaStream_t st) {
+  STDA_CHECK(tc_stemt_ok(s, g.H, g.W) && d.mode == CONV_STEMT, "tensor-core stem: unsupported input");
+  STDA_CHECK(g.resident && g.cps == 1 && g.G <= 2, "tensor-core stem: plan");
+  STDA_CHECK(out.mode == 2 && out.pl.L == g.L, "tensor-core stem: writes phase planes");
+  Params p;
+  std::memset(&p, 0, sizeof(p));
+  p.d = d;
+  p.out = out;
+  p.H = g.H;
+  p.W = g.W;
+  p.C = d.cin;
+  p.Hp = g.Hp;
+  p.Wp = g.Wp;
+  p.L = g.L;
+  p.L_mul = (uint32_t)((((uint64_t)1 << 32) + (uint64_t)g.L - 1) / (uint64_t)g.L);
+  STDA_CHECK((uint64_t)g.items_per_image * g.G * 128 * (uint64_t)g.L < ((uint64_t)1 << 32),
+             "tensor-core stem: map too large for the position decode");
+  p.Ho = g.Ho;
+  p.Wo = g.Wo;
+  p.G = g.G;
+  p.stages = g.stages;
+  p.slots = g.slots;
+  p.items_per_image = g.items_per_image;
+  p.total_items = g.B * g.items_per_image;
+  p.tail = g.tail;
+  p.rev = 0;
+  p.P_max = g.P_max;
+  STDA_CHECK(g.P_max == g.G * 128, "internal: tensor-core stem stages exactly its positions");
+  p.a_stage_bytes = g.a_stage_bytes;
+  p.b_stage_bytes = g.b_stage_bytes;
+  p.cps = 1;
+  p.chunk_a_bytes = g.chunk_a_bytes;
+  p.chunk_b_bytes = g.chunk_b_bytes;
+  p.resident = 1;
+  p.w_total = g.w_total;
+  p.slot_cols = (uint32_t)(g.G * 4 * d.cout * (d.concat ? 2 : 1));
+  p.tmem_cols = (uint32_t)g.tmem_cols;
+  p.relu0 = 1;
+  p.sx = s.x.x;
+  p.sxb = s.x.xb;
+  p.sxc = s.x.xc;
+  p.sF = s.F;
+  p.stem_xrows = stemt_xrows(g.G, g.L);
+  p.stem_xstage = (uint32_t)((size_t)s.F * p.stem_xrows * g.W * 4);
+  STDA_CHECK(stemt_extra_smem(g.G, g.L, s.F, g.W) <= stemt_extra_smem(2, g.L, s.F, g.W), "internal: stem ring");
+  if (g_trace_buf != nullptr && g_trace_countdown-- == 0) {
+    p.trace = g_trace_buf;
+    g_trace_buf = nullptr;
+    if (const char* e = std::getenv("STDA_TC_DBG")) p.dbg = std::atoi(e);
+  }
+  if (p.total_items == 0) return;
+  int dev = 0, sms = 148;
+  STDA_CUDA(cudaGetDevice(&dev));
+  STDA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int grid = std::min(p.total_items, sms);
+  const int npm = d.npass == 1 ? kNpmBf16 : kNpmConcat;
+  dispatch_stemt(npm, g.G, p, grid, g.smem_bytes, st);
+}
 
 bool tc_stem_fusable(const TcLayerDesc& d1, const TcStem& s, int H, int W) {
   static const bool on = [] {

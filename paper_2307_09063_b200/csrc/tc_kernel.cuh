@@ -29,7 +29,11 @@ constexpr int kStemWarps = 8;
 constexpr int kStemThreads = kStemWarps * 32;
 constexpr int kThreadsStem = kThreads + kStemThreads;
 constexpr int kStemC = 16, kStemMaxF = 4;
-__host__ __device__ constexpr int threads_of(int stem) { return stem ? kThreadsStem : kThreads; }
+// the tensor-core stem (CONV_STEMT) needs only 4 im2col warps: fewer threads leave the
+// epilogue warps the registers for batched TMEM loads
+constexpr int kStemtThreads = 128;
+__host__ __device__ constexpr int stem_threads(int mode) { return mode == CONV_STEMT ? kStemtThreads : kStemThreads; }
+__host__ __device__ constexpr int threads_of(int mode, int stem) { return stem ? kThreads + stem_threads(mode) : kThreads; }
 constexpr int kMaxSmem = 227 * 1024;
 constexpr int kMaxStages = 6;  // smem ring depth cap
 constexpr int kMaxSlots = 4;   // TMEM accumulator slots cap
@@ -161,14 +165,14 @@ __host__ __device__ constexpr bool tap_first(int mode, int t) {
 }
 // accumulators per source
 __host__ __device__ constexpr int nacc_src(int mode) {
-  return mode == CONVT4_S2 || mode == CONV3_S1P ? 4 : mode == CONVT4_HALF ? 2 : 1;
+  return mode == CONVT4_S2 || mode == CONV3_S1P || mode == CONV_STEMT ? 4 : mode == CONVT4_HALF ? 2 : 1;
 }
 // minimum shift over a plane's taps, as a*L + b
 __host__ __device__ constexpr int plane_lo_a(int mode, int pl) {
-  return mode == CONV3_S2 ? (pl >= 2 ? -1 : 0) : mode == CONV3_S1P ? -(pl >> 1) : -1;
+  return mode == CONV3_S2 ? (pl >= 2 ? -1 : 0) : mode == CONV3_S1P ? -(pl >> 1) : mode == CONV_STEMT ? 0 : -1;
 }
 __host__ __device__ constexpr int plane_lo_b(int mode, int pl) {
-  return mode == CONV3_S2 ? ((pl & 1) ? -1 : 0) : mode == CONV3_S1P ? -(pl & 1) : -1;
+  return mode == CONV3_S2 ? ((pl & 1) ? -1 : 0) : mode == CONV3_S1P ? -(pl & 1) : mode == CONV_STEMT ? 0 : -1;
 }
 __host__ __device__ constexpr int n_planes_of(int mode) { return mode == CONV3_S2 || mode == CONV3_S1P ? 4 : 1; }
 
@@ -406,6 +410,22 @@ __device__ __forceinline__ void issue_chunk(bool leader, uint64_t a0, uint64_t b
     }
   } else {
   const int lo = plane_lo_a(MODE, PL) * L + plane_lo_b(MODE, PL);
+  if constexpr (MODE == CONV_STEMT) {
+    // one chunk = one frame's 4x4 window per position: A_hi (and A_lo) x the 4 stacked
+    // phase tiles [B_hi | B_lo] (K-half stride = 4 tiles of AW rows)
+    constexpr uint32_t idesc = idesc_bf16(4 * AW);
+    const uint64_t bd = b0 + ((uint64_t)(3 * AW) << 16);
+    const uint32_t accum0 = first_chunk ? 0u : 1u;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const uint64_t ad = a0 + (uint32_t)(g * 128);
+      const uint32_t dcol = dslot + (uint32_t)(g * NACC * AW);
+      tc_mma(leader, dcol, ad, bd, idesc, accum0);
+      if (NPM != kNpmBf16) tc_mma(leader, dcol, ad + lo_units, bd, idesc, 1u);
+    }
+    (void)lo;
+    return;
+  }
   if constexpr (MODE == CONV3_S1P) {
     // one MMA (pair) per shift group over the stacked phase tiles of input plane PL
 #pragma unroll
@@ -520,7 +540,7 @@ __device__ __forceinline__ void gap_lane_reduce(float (&v)[N], int lane, float* 
 __device__ __forceinline__ int floordiv(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
 
 template <int N, int MODE, bool DUAL, int NPM, int G, int CPS, int STEM = 0>
-__global__ void __launch_bounds__(threads_of(STEM), 1) tc_conv_kernel(const __grid_constant__ Params p) {
+__global__ void __launch_bounds__(threads_of(MODE, STEM), 1) tc_conv_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int NSRC = DUAL ? 2 : 1;
   constexpr int NACC_SRC = nacc_src(MODE);
@@ -556,13 +576,13 @@ __global__ void __launch_bounds__(threads_of(STEM), 1) tc_conv_kernel(const __gr
     trace_at(p.trace, 4, 0);
     trace_cta(p.trace, 0);
     for (int s = 0; s < p.stages; ++s) {
-      mbar_init(smem_u32(&full[s]), STEM ? kStemThreads : 1);  // STEM: every stem thread arrives
+      mbar_init(smem_u32(&full[s]), STEM ? stem_threads(MODE) : 1);  // STEM: every stem thread arrives
       mbar_init(smem_u32(&empty[s]), 1);
     }
     if (STEM > 0) {
       for (int s = 0; s < 2; ++s) {
         mbar_init(smem_u32(&xfull[s]), 1);
-        mbar_init(smem_u32(&xempty[s]), kStemThreads);
+        mbar_init(smem_u32(&xempty[s]), stem_threads(MODE));
       }
     }
     for (int s = 0; s < p.slots; ++s) {
@@ -610,7 +630,9 @@ __global__ void __launch_bounds__(threads_of(STEM), 1) tc_conv_kernel(const __gr
       for (int item = blockIdx.x; item < p.total_items; item += gridDim.x) {
         int b, it;
         item_coords(item, p, b, it);
-        const int xr0 = floordiv(it * G * 128 - p.L - 1, p.L) - 1;
+        // (STEMT: the item's half-resolution rows y.. -> frame rows 2y-1 ..)
+        const int xr0 = MODE == CONV_STEMT ? 2 * (int)__umulhi((uint32_t)(it * G * 128), p.L_mul) - 1
+                                           : floordiv(it * G * 128 - p.L - 1, p.L) - 1;
         const int r_lo = max(xr0, 0), r_hi = min(xr0 + p.stem_xrows - 1, p.H - 1);
         mbar_wait(smem_u32(&xempty[xs]), xph ^ 1);
         if (lane == 0) {
@@ -841,7 +863,7 @@ __global__ void __launch_bounds__(threads_of(STEM), 1) tc_conv_kernel(const __gr
           // column zero (planes.cuh border contract)
           if (p.out.mode == 1) {
             pl_zero_pos(p.out.pl, b, 0, y * p.out.pl.L + p.Wp);
-          } else if (MODE == CONV3_S1P) {  // the half-resolution pad column of all 4 planes
+          } else if (MODE == CONV3_S1P || MODE == CONV_STEMT) {  // the half-res pad column of all 4 planes
 #pragma unroll
             for (int pz = 0; pz < 4; ++pz) pl_zero_pos(p.out.pl, b, pz, y * p.out.pl.L + p.Wp);
           } else {
@@ -852,7 +874,7 @@ __global__ void __launch_bounds__(threads_of(STEM), 1) tc_conv_kernel(const __gr
 #pragma unroll
         for (int ph = 0; ph < NACC_SRC; ++ph) {
           int oy = y, ox = x;
-          if (MODE == CONVT4_S2 || MODE == CONV3_S1P) {
+          if (MODE == CONVT4_S2 || MODE == CONV3_S1P || MODE == CONV_STEMT) {
             oy = 2 * y + (ph >> 1);
             ox = 2 * x + (ph & 1);
           } else if (MODE == CONVT4_HALF) {
@@ -988,7 +1010,92 @@ __global__ void __launch_bounds__(threads_of(STEM), 1) tc_conv_kernel(const __gr
       }
     }
   } else {
-    if constexpr (STEM > 0) {
+    if constexpr (MODE == CONV_STEMT) {
+      // ===================== im2col warps of the tensor-core stem ==========================
+      // A stage of chunk f (frame f) = the 4x4 frame window of every half-resolution
+      // position's 2x2 pixel block: K index e of 8-channel group kg is window pixel
+      // (wy, wx) = (2kg + e/4, e%4), i.e. frame pixel (2y - 1 + wy, 2x - 1 + wx), zero
+      // outside the frame, split into bf16 hi (+ lo).  Unit = (kg, position): consecutive
+      // threads write consecutive 16-byte core-matrix rows.
+      constexpr int F = STEM;
+      constexpr int NP = NPASS_A;
+      grid_dep_wait();
+      const int st = threadIdx.x - kStemWarp0 * 32;
+      const int L = p.L, W = p.W, H = p.H;
+      const int PG = G * 128;
+      int stage = 0, xs = 0;
+      uint32_t phase = 0, xph = 0;
+      for (int item = blockIdx.x; item < p.total_items; item += gridDim.x) {
+        int b, it;
+        item_coords(item, p, b, it);
+        const int q0 = it * PG;
+        const int xr0 = 2 * (int)__umulhi((uint32_t)q0, p.L_mul) - 1;
+        mbar_wait(smem_u32(&xfull[xs]), xph);
+#pragma unroll 1
+        for (int f = 0; f < F; ++f) {
+          mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+          const float* xr = xring + ((size_t)xs * F + f) * p.stem_xrows * W;
+          uint8_t* a = a_base + (size_t)stage * p.a_stage_bytes;
+          // UB units per thread and pass: all frame loads first, then the conversions and
+          // stores (one builder warp per SM sub-partition: the LDS latency must overlap)
+          constexpr int UB = 4;
+          for (int u0 = st; u0 < 2 * PG; u0 += UB * kStemtThreads) {
+            float v[UB][8];
+#pragma unroll
+            for (int k = 0; k < UB; ++k) {
+              const int u = u0 + k * kStemtThreads;
+              const int kg = u >= PG ? 1 : 0, i = u - kg * PG;
+              const int q = q0 + i;
+              const int y = (int)__umulhi((uint32_t)q, p.L_mul), x = q - y * L;
+              const bool pos_ok = u < 2 * PG && y < p.Hp && x < p.Wp;
+#pragma unroll
+              for (int r = 0; r < 2; ++r) {
+                const int iy = 2 * y - 1 + 2 * kg + r;
+                const bool row_ok = pos_ok && iy >= 0 && iy < H;
+                const float* row = xr + (size_t)(iy - xr0) * W;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                  const int ix = 2 * x - 1 + c;
+                  v[k][r * 4 + c] = (row_ok && ix >= 0 && ix < W) ? row[ix] : 0.f;
+                }
+              }
+            }
+#pragma unroll
+            for (int k = 0; k < UB; ++k) {
+              const int u = u0 + k * kStemtThreads;
+              if (u >= 2 * PG) break;
+              const int kg = u >= PG ? 1 : 0, i = u - kg * PG;
+              uint32_t hw[4], lw[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const __nv_bfloat162 h2 = __floats2bfloat162_rn(v[k][2 * e], v[k][2 * e + 1]);
+                hw[e] = *reinterpret_cast<const uint32_t*>(&h2);
+                if (NP == 2) {
+                  const float2 hf = __bfloat1622float2(h2);
+                  const __nv_bfloat162 l2 = __floats2bfloat162_rn(v[k][2 * e] - hf.x, v[k][2 * e + 1] - hf.y);
+                  lw[e] = *reinterpret_cast<const uint32_t*>(&l2);
+                }
+              }
+              *reinterpret_cast<uint4*>(a + ((size_t)kg * p.P_max + i) * 16) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+              if (NP == 2)
+                *reinterpret_cast<uint4*>(a + ((size_t)(2 + kg) * p.P_max + i) * 16) =
+                    make_uint4(lw[0], lw[1], lw[2], lw[3]);
+            }
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // st.shared -> UMMA
+          mbar_arrive(smem_u32(&full[stage]));
+          if (++stage == p.stages) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+        mbar_arrive(smem_u32(&xempty[xs]));
+        if (++xs == 2) {
+          xs = 0;
+          xph ^= 1u;
+        }
+      }
+    } else if constexpr (STEM > 0) {
       // ===================== stem warps: relu(conv3x3(frames)) into the A stages ==========
       // Every staged position of the item (its 128G positions and the 2L+2 halo) is
       // computed from the frame rows in the x ring — the stem never makes an HBM round trip
@@ -1140,6 +1247,13 @@ void launch_stem_k(const Params& p, int grid, size_t smem, cudaStream_t st) {
   launch_pdl(kern, dim3(grid), dim3(kThreadsStem), smem, st, "tc_conv_kernel<stem>", p);
 }
 
+template <int NPM, int G, int F>
+void launch_stemt_k(const Params& p, int grid, size_t smem, cudaStream_t st) {
+  auto kern = tc_conv_kernel<16, CONV_STEMT, false, NPM, G, 1, F>;
+  ensure_dyn_smem(kern, kMaxSmem);
+  launch_pdl(kern, dim3(grid), dim3(threads_of(CONV_STEMT, F)), smem, st, "tc_conv_kernel<stemt>", p);
+}
+
 template <int N, int MODE, bool DUAL, int NPM, int G>
 void launch_k(const Params& p, int grid, size_t smem, cudaStream_t st) {
   auto kern = p.cps == 2 ? tc_conv_kernel<N, MODE, DUAL, NPM, G, 2> : tc_conv_kernel<N, MODE, DUAL, NPM, G, 1>;
@@ -1178,6 +1292,7 @@ void dispatch_th(int n, int npm, int G, const Params& p, int grid, size_t smem, 
 void dispatch_rows(int n, int npm, int G, const Params& p, int grid, size_t smem, cudaStream_t st);
 void dispatch_s1p(int n, int npm, int G, const Params& p, int grid, size_t smem, cudaStream_t st);
 void dispatch_stem(int npm, int G, const Params& p, int grid, size_t smem, cudaStream_t st);
+void dispatch_stemt(int npm, int G, const Params& p, int grid, size_t smem, cudaStream_t st);
 
 }  // namespace detail
 }  // namespace tc

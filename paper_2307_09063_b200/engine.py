@@ -389,3 +389,14 @@ class CapturedForward:
             ms = L.forward_profiled(self.plan.handle, self.x.data_ptr(), self.y.data_ptr(),
                                     self.batch, ws.data_ptr(), ws.numel(), _stream_ptr(self.device))
         return L.launch_names(self.plan.handle), ms
+
+    def launch_repeat(self, slot: int, reps: int = 20) -> float:
+        """Average device time (ms) of launch slot `slot` run alone `reps` times back to back
+        after one full forward (its inputs in place): the kernel's own duration, without the
+        per-launch event records of `profile` between it and its neighbours."""
+        L = self.plan.L
+        with torch.cuda.device(self.device):
+            ws = self.ws[0] if len(self.slices) == 1 else torch.empty(
+                L.workspace_bytes(self.plan.handle, self.batch), device=self.device, dtype=torch.uint8)
+            return L.forward_launch_repeat(self.plan.handle, self.x.data_ptr(), self.y.data_ptr(), self.batch,
+                                           ws.data_ptr(), ws.numel(), _stream_ptr(self.device), slot, reps)

@@ -234,3 +234,40 @@ def test_schedule_orders_do_not_change_results():
         subprocess.run([sys.executable, "-c", code], check=True, env=env, cwd=root)
     import numpy as np
     assert np.array_equal(np.load("/tmp/sched_default.npy"), np.load("/tmp/sched_plain.npy"))
+
+
+def test_tensor_core_stem_path():
+    """STDA_STEM_TC=1 (the stem as a tcgen05 GEMM over 4x4 frame windows, off by default)
+    against the CPU oracle (fp32 tolerance) and the default SIMT stem, fp32 and bf16, at the
+    C2 map size and at 256^2 (checked in a subprocess: the switch is read once)."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import torch, numpy as np, os\n"
+        "torch.set_grad_enabled(False)\n"
+        "from paper_2307_09063_b200 import StdaConfig, StdaNet\n"
+        "from paper_2307_09063_b200.synth import synth_triplets\n"
+        "for hw, b, prec in ((128, 5, 'fp32'), (256, 2, 'fp32'), (128, 3, 'bf16')):\n"
+        "    torch.manual_seed(hw)\n"
+        "    net = StdaNet(StdaConfig(map_height=hw, map_width=hw), precision=prec).eval().cuda()\n"
+        "    x = synth_triplets(b, hw, hw, seed=9)\n"
+        "    np.save(f'/tmp/stemtc_{hw}_{prec}_' + os.environ['STDA_STEM_TC'] + '.npy', net(x).cpu().numpy())\n"
+        "    np.save(f'/tmp/stemtc_{hw}_{prec}_x.npy', x.cpu().numpy())\n"
+    )
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for flag in ("0", "1"):
+        subprocess.run([sys.executable, "-c", code], check=True, env=dict(os.environ, STDA_STEM_TC=flag), cwd=root)
+    import numpy as np
+    from oracle import port
+    from tests._helpers import CONFIG_FIELDS, nmax_err
+    for hw, prec, tol in ((128, "fp32", 1e-4), (256, "fp32", 1e-4), (128, "bf16", 3e-2)):
+        a = np.load(f"/tmp/stemtc_{hw}_{prec}_0.npy")
+        b = np.load(f"/tmp/stemtc_{hw}_{prec}_1.npy")
+        assert nmax_err(b, a) <= (2e-5 if prec == "fp32" else 2e-2)
+        torch.manual_seed(hw)
+        net = StdaNet(StdaConfig(map_height=hw, map_width=hw))
+        sd = {k: v.detach() for k, v in net.state_dict().items()}
+        cfg = {f: getattr(net.config, f) for f in CONFIG_FIELDS}
+        ref = port.forward(sd, cfg, torch.from_numpy(np.load(f"/tmp/stemtc_{hw}_{prec}_x.npy"))).numpy()
+        assert nmax_err(b, ref) <= tol
