@@ -350,6 +350,35 @@ void run_net_tc(const stda_plan& p, const Src& x, float* y, int64_t B, const Net
   }
   PlBuf cur_pl = w.pl_s, cur_pp = w.pp_s;
   std::vector<PlBuf> skips{p.stem_pp ? w.pp_s : w.pl_s};
+  // gate-on-load: an ECA gate (+ skip) whose consumer is a plain stride-1 conv is applied
+  // inside that conv (tc_launch_gatein), which also writes the gated planes; the gate slot
+  // then only forms the gates (eca_gates_kernel)
+  bool pend = false;
+  tc::TcGateIn gin;
+  auto s1_launch = [&](tc::TcLayerDesc& d1, const PlBuf& src, const tc::TcOut& o1, int hh, int ww) {
+    if (pend) {
+      const tc::TcGeometry g1 = tc::tc_plan_gatein(d1, (int)B, hh, ww, gin);
+      if (mk.go()) tc::tc_launch_gatein(d1, g1, gin, o1, st, /*rev=*/true);
+      pend = false;
+    } else {
+      const tc::TcGeometry g1 = tc::tc_plan(d1, (int)B, hh, ww);
+      if (mk.go()) tc::tc_launch(d1, g1, src, nullptr, o1, true, st, /*rev=*/true);
+    }
+  };
+  // can the next stride-1 conv take this gate on load?
+  auto gatein_next = [&](const tc::TcLayerDesc& nxt, const float* x, const float* gates, const PlBuf* skip,
+                         const PlBuf& out_pl, const PlBuf* out_pp, int hh, int ww) {
+    tc::TcGateIn g;
+    g.x = x;
+    g.gates = gates;
+    if (skip) g.skip = *skip;
+    g.out_pl = out_pl;
+    if (out_pp) g.out_pp = *out_pp;
+    if (!tc::tc_gatein_ok(nxt, g, hh, ww) || !tc::tc_gatein_fits(nxt, (int)B, hh, ww, g)) return false;
+    gin = g;
+    pend = true;
+    return true;
+  };
   for (int i = 0; i < S; ++i) {
     const EncLayers& E = p.enc[i];
     tc::TcLayerDesc d1 = E.s1_tc, d2 = E.s2_tc;
@@ -360,14 +389,18 @@ void run_net_tc(const stda_plan& p, const Src& x, float* y, int64_t B, const Net
       const tc::TcGeometry g1 = tc::tc_plan_stem(d1, (int)B, h, wd, c.input_frames);
       if (mk.go()) tc::tc_launch_stem(d1, g1, stem, o1, st, /*rev=*/true);
     } else {
-      const tc::TcGeometry g1 = tc::tc_plan(d1, (int)B, h, wd);
-      if (mk.go()) tc::tc_launch(d1, g1, d1.mode == CONV3_S1P ? cur_pp : cur_pl, nullptr, o1, true, st, /*rev=*/true);
+      s1_launch(d1, d1.mode == CONV3_S1P ? cur_pp : cur_pl, o1, h, wd);
     }
     mk.mark(st);
     const tc::TcGeometry g2 = tc::tc_plan(d2, (int)B, h, wd);
+    // gate-on-load by the next stride-1 conv: e_i goes out chunk-planar for its builder
+    const tc::TcLayerDesc& nxt = i + 1 < S ? p.enc[i + 1].s1_tc : p.dec[0].s1_tc;
+    const bool gi_on =
+        gatein_next(nxt, w.e[i], w.ge[i], nullptr, w.pl_a[i], i + 1 < S ? &w.pp_a[i] : nullptr, h / 2, wd / 2);
     tc::TcOut o2;
     o2.f32 = w.e[i];
     o2.gap = w.pe[i];
+    o2.cp = gi_on ? 1 : 0;
     if (mk.go()) tc::tc_launch(d2, g2, mviews[i], &cur_pp, o2, true, st);
     mk.mark(st);
     h /= 2;
@@ -376,14 +409,18 @@ void run_net_tc(const stda_plan& p, const Src& x, float* y, int64_t B, const Net
     // large maps: the gate once per image (planes.cuh kGatesReady), not once per CTA
     const float* gsrc = w.pe[i];
     int gitems = g2.items_per_image;
-    if (precompute_gates(gitems, d2.cout)) {
+    if (gi_on) {
       if (mk.go()) launch_eca_gates(gsrc, gitems, E.eca, k, w.ge[i], B, d2.cout, (int64_t)h * wd, st);
-      gsrc = w.ge[i];
-      gitems = kGatesReady;
+    } else {
+      if (precompute_gates(gitems, d2.cout)) {
+        if (mk.go()) launch_eca_gates(gsrc, gitems, E.eca, k, w.ge[i], B, d2.cout, (int64_t)h * wd, st);
+        gsrc = w.ge[i];
+        gitems = kGatesReady;
+      }
+      if (mk.go())
+        launch_gate_apply(gsrc, gitems, E.eca, k, w.e[i], nullptr, &w.pl_a[i],
+                          i + 1 < S ? &w.pp_a[i] : nullptr, nullptr, B, d2.cout, h, wd, st);
     }
-    if (mk.go())
-      launch_gate_apply(gsrc, gitems, E.eca, k, w.e[i], nullptr, &w.pl_a[i],
-                      i + 1 < S ? &w.pp_a[i] : nullptr, nullptr, B, d2.cout, h, wd, st);
     mk.mark(st);
     cur_pl = w.pl_a[i];
     cur_pp = w.pp_a[i];
@@ -396,20 +433,31 @@ void run_net_tc(const stda_plan& p, const Src& x, float* y, int64_t B, const Net
     tc::TcOut o1;
     o1.mode = 1;  // plane for the ConvT consumer
     o1.pl = mviews[S + j];
-    if (mk.go()) tc::tc_launch(d1, g1, cur_pl, nullptr, o1, true, st, /*rev=*/true);
+    (void)g1;
+    s1_launch(d1, cur_pl, o1, h, wd);
     mk.mark(st);
     const tc::TcGeometry g2 = tc::tc_plan(d2, (int)B, h, wd);
+    const PlBuf& sk = skips[S - 1 - j];
+    const bool gi_on = j + 1 < S && sk.planes == 1 &&
+                       gatein_next(p.dec[j + 1].s1_tc, w.d[j], w.gd[j], &sk, w.pl_b[j], nullptr, 2 * h, 2 * wd);
     tc::TcOut o2;
     o2.f32 = w.d[j];
     o2.gap = w.pd[j];
+    o2.cp = gi_on ? 1 : 0;
     if (mk.go()) tc::tc_launch(d2, g2, mviews[S + j], &cur_pl, o2, true, st);
     mk.mark(st);
     h *= 2;
     wd *= 2;
     // b_j = d_j * gate + skip  (model.py:197-198); the last one is fused into the head
-    const PlBuf& sk = skips[S - 1 - j];
     const float* gsrc = w.pd[j];
     int gitems = g2.items_per_image;
+    if (gi_on) {
+      // b_j formed inside dec_{j+1}.s1 (gate-on-load with the skip)
+      if (mk.go()) launch_eca_gates(gsrc, gitems, D.eca, k, w.gd[j], B, d2.cout, (int64_t)h * wd, st);
+      mk.mark(st);
+      cur_pl = w.pl_b[j];
+      continue;
+    }
     if (precompute_gates(gitems, d2.cout)) {
       if (mk.go()) launch_eca_gates(gsrc, gitems, D.eca, k, w.gd[j], B, d2.cout, (int64_t)h * wd, st);
       gsrc = w.gd[j];

@@ -95,6 +95,7 @@ struct TcGeometry {
   int cps;                // K chunks per ring stage (one barrier round trip per cps chunks)
   uint32_t chunk_a_bytes, chunk_b_bytes;
   bool resident;          // packed weights stay in smem for the whole launch
+  int gx_nst = 0;         // gate-in plans: x ring stages
   uint32_t w_total;       // packed weight bytes
   size_t smem_bytes;
 };
@@ -111,6 +112,7 @@ TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W, size_t extra_smem = 0, b
 // planes of it) or NHWC fp32 with per-item channel sums gap [B][items_per_image][cout].
 struct TcOut {
   int mode = 0;  // 0 = NHWC fp32 (+gap), 1 = PL, 2 = PP
+  int cp = 0;    // mode 0: chunk-planar fp32 [B][C/16][Ho*Wo][16] instead of NHWC (gate-in input)
   float* f32 = nullptr;
   float* gap = nullptr;
   PlBuf pl;
@@ -151,6 +153,26 @@ bool tc_stemt_ok(const TcStem& s, int H, int W);
 TcGeometry tc_plan_stemt(TcLayerDesc& d, int B, int H, int W, int F);
 void tc_launch_stemt(const TcLayerDesc& d, const TcGeometry& g, const TcStem& s, const TcOut& out,
                      cudaStream_t st);
+
+// ---- gate-on-load stride-1 conv -------------------------------------------------------------
+// The ECA gate (and skip add) of the previous block applied while the A stages of the next
+// stride-1 conv are formed (tc_kernel.cuh gate-in role): x = that block's NHWC fp32 output,
+// gates = its ECA gates [B][C] (eca_gates_kernel), optional skip planes (PL); the gated
+// tensor is also written as PL (+ PP) operand planes for its other consumers — bitwise the
+// planes gate_apply writes.  Opt-in (env STDA_GATEIN=1): slower than the gate kernels at C2.
+struct TcGateIn {
+  const float* x = nullptr;  // chunk-planar fp32 [B][C/16][H*W][16] (TcOut::cp of its producer)
+  const float* gates = nullptr;
+  PlBuf skip;    // base null: no skip
+  PlBuf out_pl;  // the gated tensor as PL
+  PlBuf out_pp;  // ... and PP (base null: none)
+};
+bool gatein_enabled();
+bool tc_gatein_ok(const TcLayerDesc& d, const TcGateIn& gi, int H, int W);
+TcGeometry tc_plan_gatein(TcLayerDesc& d, int B, int H, int W, const TcGateIn& gi);
+bool tc_gatein_fits(const TcLayerDesc& d, int B, int H, int W, const TcGateIn& gi);
+void tc_launch_gatein(const TcLayerDesc& d, const TcGeometry& g, const TcGateIn& gi, const TcOut& out,
+                      cudaStream_t st, bool rev);
 
 // Debug: record a clock64 timeline of CTA 0 (see tc_kernel.cuh trace_at) into dev_buf
 // during the launch_index-th following tc_launch.

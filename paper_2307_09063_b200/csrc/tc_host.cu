@@ -310,6 +310,7 @@ void tc_pack_layer(TcLayerDesc& d, int mode, int cin, int cout, const float* w0,
 }
 
 namespace {
+bool s1_env_set() { return std::getenv("STDA_TC_S1STAGES") != nullptr; }
 int slots_cap() {  // env STDA_TC_SLOTS (A/B timing), default kMaxSlots
   static const int v = [] {
     const char* e = std::getenv("STDA_TC_SLOTS");
@@ -458,7 +459,10 @@ TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W, size_t extra_smem, bool 
           return e ? std::max(1, std::min(kMaxStages, std::atoi(e))) : 3;
         }();
         const bool tmode = d.mode == CONVT4_S2 || d.mode == CONVT4_HALF;
-        const int st_cap = d.mode == CONV3_S2 || d.mode == CONV_STEMT ? kMaxStages : tmode ? t_stages : s1_stages;
+        // the phase-plane stride-1 conv (small resident weights) takes a 4th stage: enc0.s1
+        // 39.2 -> 38.2 us at C2 (round 2); plain stride-1 layers stay at 3
+        const int s1_cap = d.mode == CONV3_S1P && !s1_env_set() ? 4 : s1_stages;
+        const int st_cap = d.mode == CONV3_S2 || d.mode == CONV_STEMT ? kMaxStages : tmode ? t_stages : s1_cap;
         for (int st = st_cap; st >= 1; --st) {
           const size_t need = resident ? (size_t)st * a_stage + w_res : (size_t)st * (a_stage + b_stage);
           if (need + fixed <= (size_t)kMaxSmem) {
@@ -635,6 +639,141 @@ void tc_launch_stemt(const TcLayerDesc& d, const TcGeometry& g, const TcStem& s,
   const int grid = std::min(p.total_items, sms);
   const int npm = d.npass == 1 ? kNpmBf16 : kNpmConcat;
   dispatch_stemt(npm, g.G, p, grid, g.smem_bytes, st);
+}
+
+// ---- gate-on-load stride-1 conv ---------------------------------------------------------------
+// env STDA_GATEIN=1 enables it.  Off by default: bitwise-identical outputs, but at C2 the
+// builder warps (6 warps beside the MMA / epilogue roles, 1.5x halo positions per item)
+// form a K chunk every ~6k cycles against 1.6k of MMA: enc1.s1 62 us vs enc0.gate + enc1.s1
+// 47.8 us, dec1.s1 57 us vs 37.5 us
+bool gatein_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("STDA_GATEIN");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+bool tc_gatein_ok(const TcLayerDesc& d, const TcGateIn& gi, int H, int W) {
+  return gatein_enabled() && d.mode == CONV3_S1 && d.n_src == 1 && d.cin % 16 == 0 && gi.x && gi.gates &&
+         (reinterpret_cast<uintptr_t>(gi.x) & 15) == 0 && (reinterpret_cast<uintptr_t>(gi.gates) & 15) == 0 &&
+         gi.out_pl.base && gi.out_pl.planes == 1 && gi.out_pl.L == W + 1 && gi.out_pl.C == d.cin &&
+         (!gi.skip.base || (gi.skip.planes == 1 && gi.skip.L == W + 1 && gi.skip.C == d.cin)) &&
+         (!gi.out_pp.base || (gi.out_pp.planes == 4 && H % 2 == 0 && W % 2 == 0 && gi.out_pp.C == d.cin));
+}
+
+namespace {
+// x ring stage of a gate-in item: the staged rows of one chunk plane (64 B per pixel) and the
+// skip's staged positions per (pass, cg8) block
+int gatein_xrows(int G, int L) { return (G * 128 + 2 * L + 1) / L + 2; }
+uint32_t gatein_skip_off(int G, int L, int W) { return ((uint32_t)gatein_xrows(G, L) * W * 64 + 127) / 128 * 128; }
+uint32_t gatein_xstage(int G, int L, int W, bool skip, int np) {
+  const uint32_t P = (uint32_t)(G * 128 + 2 * L + 2);
+  return gatein_skip_off(G, L, W) + (skip ? (uint32_t)np * 2 * P * 16 : 0u);
+}
+}  // namespace
+
+TcGeometry tc_plan_gatein(TcLayerDesc& d, int B, int H, int W, const TcGateIn& gi) {
+  const int np = d.npass == 3 ? 2 : 1, L = W + 1;
+  const bool skip = gi.skip.base != nullptr;
+  // reserve the x ring for the tile count the plain plan picks; accept when the plan with the
+  // reservation does not pick more tiles per item than reserved for
+  const TcGeometry g0 = tc_plan(d, B, H, W, 0, true);
+  // the deepest x ring (4..2 stages) that leaves the plain plan's tile count and ring
+  for (int nx = 4; nx >= 2; --nx) {
+    const size_t extra = nx * (size_t)gatein_xstage(g0.G, L, W, skip, np) + 128;
+    TcLayerDesc dd = d;
+    TcGeometry g;
+    try {
+      g = tc_plan(dd, B, H, W, extra, true);
+    } catch (const Error&) {
+      continue;
+    }
+    if (g.G == g0.G && (g.stages >= std::min(g0.stages, 3) || nx == 2)) {
+      d = dd;
+      g.gx_nst = nx;
+      return g;
+    }
+  }
+  STDA_CHECK(false, "gate-in conv: no tiling fits shared memory");
+  return g0;
+}
+
+bool tc_gatein_fits(const TcLayerDesc& d, int B, int H, int W, const TcGateIn& gi) {
+  try {
+    TcLayerDesc dd = d;
+    tc_plan_gatein(dd, B, H, W, gi);
+    return true;
+  } catch (const Error&) {
+    return false;
+  }
+}
+
+void tc_launch_gatein(const TcLayerDesc& d, const TcGeometry& g, const TcGateIn& gi, const TcOut& out,
+                      cudaStream_t st, bool rev) {
+  STDA_CHECK(tc_gatein_ok(d, gi, g.H, g.W), "gate-in conv: unsupported layer / input");
+  STDA_CHECK(g.resident && g.cps == 1, "gate-in conv: plan");
+  STDA_CHECK(g.P_max >= g.G * 128 + 2 * g.L + 2, "internal: gate-in staged span");
+  STDA_CHECK(gi.out_pl.np == (d.npass == 3 ? 2 : 1), "gate-in conv: plane precision");
+  Params p;
+  std::memset(&p, 0, sizeof(p));
+  p.d = d;
+  p.out = out;
+  p.H = g.H;
+  p.W = g.W;
+  p.C = d.cin;
+  p.Hp = g.Hp;
+  p.Wp = g.Wp;
+  p.L = g.L;
+  p.L_mul = (uint32_t)((((uint64_t)1 << 32) + (uint64_t)g.L - 1) / (uint64_t)g.L);
+  STDA_CHECK((uint64_t)(g.items_per_image * g.G * 128 + 2 * g.L) * (uint64_t)g.L < ((uint64_t)1 << 32),
+             "gate-in conv: map too large for the position decode");
+  p.Ho = g.Ho;
+  p.Wo = g.Wo;
+  p.G = g.G;
+  p.stages = g.stages;
+  p.slots = g.slots;
+  p.items_per_image = g.items_per_image;
+  p.total_items = g.B * g.items_per_image;
+  p.tail = g.tail;
+  static const bool rev_on = [] {
+    const char* e = std::getenv("STDA_TC_REV");
+    return !(e && e[0] == '0');
+  }();
+  p.rev = rev && rev_on ? 1 : 0;
+  p.P_max = g.P_max;
+  p.a_stage_bytes = g.a_stage_bytes;
+  p.b_stage_bytes = g.b_stage_bytes;
+  p.cps = 1;
+  p.chunk_a_bytes = g.chunk_a_bytes;
+  p.chunk_b_bytes = g.chunk_b_bytes;
+  p.resident = 1;
+  p.w_total = g.w_total;
+  p.slot_cols = (uint32_t)(g.G * d.cout * (d.concat ? 2 : 1));
+  p.tmem_cols = (uint32_t)g.tmem_cols;
+  p.relu0 = 1;
+  p.gx = gi.x;
+  p.gates = gi.gates;
+  p.stem_xstage = gatein_xstage(g.G, g.L, g.W, gi.skip.base != nullptr, gi.out_pl.np);
+  p.gx_skip_off = gatein_skip_off(g.G, g.L, g.W);
+  p.gx_nst = g.gx_nst;
+  STDA_CHECK(p.gx_nst >= 2 && p.gx_nst <= 4, "internal: gate-in x ring");
+  p.gskip = gi.skip;
+  p.gpl = gi.out_pl;
+  p.gpp = gi.out_pp;
+  if (g_trace_buf != nullptr && g_trace_countdown-- == 0) {
+    p.trace = g_trace_buf;
+    g_trace_buf = nullptr;
+    if (const char* e = std::getenv("STDA_TC_DBG")) p.dbg = std::atoi(e);
+  }
+  if (p.total_items == 0) return;
+  int dev = 0, sms = 148;
+  STDA_CUDA(cudaGetDevice(&dev));
+  STDA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int grid = std::min(p.total_items, sms);
+  const int npm = d.npass == 1 ? kNpmBf16 : (d.concat ? kNpmConcat : kNpm3);
+  STDA_CHECK(npm != kNpm3, "gate-in conv: 3-MMA scheme not instantiated");
+  dispatch_gatein(d.cout, npm, g.G, p, grid, g.smem_bytes, st);
 }
 
 bool tc_stem_fusable(const TcLayerDesc& d1, const TcStem& s, int H, int W) {

@@ -32,8 +32,15 @@ constexpr int kStemC = 16, kStemMaxF = 4;
 // the tensor-core stem (CONV_STEMT) needs only 4 im2col warps: fewer threads leave the
 // epilogue warps the registers for batched TMEM loads
 constexpr int kStemtThreads = 128;
-__host__ __device__ constexpr int stem_threads(int mode) { return mode == CONV_STEMT ? kStemtThreads : kStemThreads; }
-__host__ __device__ constexpr int threads_of(int mode, int stem) { return stem ? kThreads + stem_threads(mode) : kThreads; }
+// gate-on-load stride-1 conv (STEM template value kGateIn, MODE CONV3_S1): 6 builder warps
+// form the A stages from the previous block's NHWC fp32 output x gate (+ skip), and write the
+// gated tensor's operand planes as a side output (tc_kernel.cuh gate-in role)
+constexpr int kGateIn = 8;
+constexpr int kGateInThreads = 192;
+__host__ __device__ constexpr int stem_threads(int mode, int stem = 0) {
+  return stem == kGateIn ? kGateInThreads : mode == CONV_STEMT ? kStemtThreads : kStemThreads;
+}
+__host__ __device__ constexpr int threads_of(int mode, int stem) { return stem ? kThreads + stem_threads(mode, stem) : kThreads; }
 constexpr int kMaxSmem = 227 * 1024;
 constexpr int kMaxStages = 6;  // smem ring depth cap
 constexpr int kMaxSlots = 4;   // TMEM accumulator slots cap
@@ -79,6 +86,13 @@ struct Params {
   // from the parameter bank by every FFMA2 (uniform across the warp)
   alignas(16) float stem_w[kStemMaxF * 9 * kStemC];
   alignas(16) float stem_b[kStemC];
+  // ---- gate-on-load (STEM == kGateIn) ----
+  const float* gx;      // the block input before its ECA gate: NHWC fp32 [B][H][W][C]
+  const float* gates;   // ECA gates [B][C] (eca_gates_kernel)
+  PlBuf gskip;          // optional skip added after the gate (base null: none), PL planes
+  PlBuf gpl, gpp;       // side outputs: the gated tensor as PL (always) and PP (base null: none)
+  uint32_t gx_skip_off; // x ring stage: skip ranges after the rows (bytes)
+  int gx_nst;           // x ring stages (2..4)
 };
 
 // ---- debug timeline (stda_debug_trace): clock64 stamps of CTA 0, one region per role ---
@@ -564,7 +578,7 @@ __global__ void __launch_bounds__(threads_of(MODE, STEM), 1) tc_conv_kernel(cons
   uint64_t* tempty = tfull + p.slots;
   uint64_t* wbar = tempty + p.slots;  // resident weights landed
   uint64_t* xfull = wbar + 1;         // STEM: frame rows of x ring stage landed
-  uint64_t* xempty = xfull + 2;       // STEM: stem warps done with x ring stage
+  uint64_t* xempty = xfull + 4;       // STEM: stem warps done with x ring stage (<= 4 stages)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(xempty + 2);
   float* red = reinterpret_cast<float*>(tmem_holder + 4);  // [kEpiWarps][N]
   // STEM: x ring [2][F][rows][W] (offset from the dynamic smem base: the compiler keeps
@@ -576,13 +590,13 @@ __global__ void __launch_bounds__(threads_of(MODE, STEM), 1) tc_conv_kernel(cons
     trace_at(p.trace, 4, 0);
     trace_cta(p.trace, 0);
     for (int s = 0; s < p.stages; ++s) {
-      mbar_init(smem_u32(&full[s]), STEM ? stem_threads(MODE) : 1);  // STEM: every stem thread arrives
+      mbar_init(smem_u32(&full[s]), STEM ? stem_threads(MODE, STEM) : 1);  // STEM: every stem thread arrives
       mbar_init(smem_u32(&empty[s]), 1);
     }
     if (STEM > 0) {
-      for (int s = 0; s < 2; ++s) {
+      for (int s = 0; s < 4; ++s) {
         mbar_init(smem_u32(&xfull[s]), 1);
-        mbar_init(smem_u32(&xempty[s]), stem_threads(MODE));
+        mbar_init(smem_u32(&xempty[s]), stem_threads(MODE, STEM));
       }
     }
     for (int s = 0; s < p.slots; ++s) {
@@ -622,7 +636,48 @@ __global__ void __launch_bounds__(threads_of(MODE, STEM), 1) tc_conv_kernel(cons
                p.w_total, smem_u32(wbar));
     }
     grid_dep_wait();  // weights are static; activations come from the previous kernel
-    if constexpr (STEM > 0) {
+    if constexpr (STEM == kGateIn) {
+      // gate-in: per item and 16-channel chunk, the staged rows of the input's chunk plane
+      // (chunk-planar fp32, one contiguous range) and the skip's staged positions (one range
+      // per (pass, cg8) block) into the 2-stage x ring
+      constexpr int NP = NPASS_A;
+      const bool has_skip = p.gskip.base != nullptr;
+      const int L = p.L, W = p.W, H = p.H, C = p.C;
+      const int P = G * 128 + 2 * L + 2;
+      int xs = 0;
+      uint32_t xph = 0;
+      for (int item = blockIdx.x; item < p.total_items; item += gridDim.x) {
+        int b, it;
+        item_coords(item, p, b, it);
+        const int qa = it * G * 128 - L - 1;
+        const int y_lo = max(floordiv(qa, L), 0);
+        const int y_hi = min(floordiv(qa + P - 1, L), H - 1);
+        for (int c = 0; c < C / 16; ++c) {
+          mbar_wait(smem_u32(&xempty[xs]), xph ^ 1);
+          if (lane == 0) {
+            const uint32_t xb = (uint32_t)max(y_hi - y_lo + 1, 0) * W * 64;
+            const uint32_t sb = has_skip ? (uint32_t)NP * 2 * P * 16 : 0u;
+            const uint32_t bar = smem_u32(&xfull[xs]);
+            mbar_arrive_expect_tx(bar, xb + sb);
+            uint8_t* dst = reinterpret_cast<uint8_t*>(xring) + (size_t)xs * p.stem_xstage;
+            if (xb)
+              bulk_g2s(smem_u32(dst), p.gx + (((size_t)b * (C / 16) + c) * H * W + (size_t)y_lo * W) * 16, xb, bar);
+            if (has_skip) {
+              const uint16_t* skb = p.gskip.base + (int64_t)b * p.gskip.img_stride;
+              for (int blk = 0; blk < NP * 2; ++blk)
+                bulk_g2s(smem_u32(dst + p.gx_skip_off + (size_t)blk * P * 16),
+                         skb + (p.gskip.block_index(c, blk >> 1, blk & 1) + qa + p.gskip.off) * 8, (uint32_t)P * 16,
+                         bar);
+            }
+          }
+          __syncwarp();
+          if (++xs == p.gx_nst) {
+            xs = 0;
+            xph ^= 1u;
+          }
+        }
+      }
+    } else if constexpr (STEM > 0) {
       // frame rows of each item's staged positions (+1 row each side), one copy per frame
       // into the 2-stage x ring; rows outside the image are never read (the stem masks them)
       int xs = 0;
@@ -955,19 +1010,23 @@ __global__ void __launch_bounds__(threads_of(MODE, STEM), 1) tc_conv_kernel(cons
                   const int yc = (int)__umulhi((uint32_t)qc, p.L_mul);
                   const int xc = qc - yc * p.L;
                   if (yc >= p.Hp || xc >= p.Wp) continue;
-                  *reinterpret_cast<float4*>(p.out.f32 + (((size_t)b * p.Ho + yc) * p.Wo + xc) * N + j + 4 * r) =
-                      c4[c];
+                  float* dst = p.out.cp ? p.out.f32 + (((size_t)b * (N / 16) + j / 16) * p.Ho * p.Wo +
+                                                       (size_t)yc * p.Wo + xc) * 16 + 4 * r
+                                        : p.out.f32 + (((size_t)b * p.Ho + yc) * p.Wo + xc) * N + j + 4 * r;
+                  *reinterpret_cast<float4*>(dst) = c4[c];
                 }
               }
               continue;
             }
             if (!valid || (p.dbg & 1)) continue;
             if (p.out.mode == 0) {
-              float* op = p.out.f32 + (((size_t)b * p.Ho + oy) * p.Wo + ox) * N;
+              float* op = p.out.cp ? p.out.f32 + (((size_t)b * (N / 16) + j / 16) * p.Ho * p.Wo +
+                                                  (size_t)oy * p.Wo + ox) * 16
+                                   : p.out.f32 + (((size_t)b * p.Ho + oy) * p.Wo + ox) * N + j;
               // 32-byte stores: each lane writes whole L2 sectors (the lanes' pixels are
               // 2 apart in the ConvT phases, so a warp's stores cannot coalesce further)
 #pragma unroll
-              for (int i = 0; i < 16; i += 8) st_global_v8(op + j + i, v + i);
+              for (int i = 0; i < 16; i += 8) st_global_v8(op + i, v + i);
 #pragma unroll
               for (int i = 0; i < 16; ++i) gsum[j + i] += v[i];
             } else {
@@ -1095,6 +1154,164 @@ __global__ void __launch_bounds__(threads_of(MODE, STEM), 1) tc_conv_kernel(cons
           xph ^= 1u;
         }
       }
+    } else if constexpr (STEM == kGateIn) {
+      // ===================== gate-in builder warps ======================================
+      // A stage of K chunk c (16 channels): staged positions i = 0..P-1 at q = q0 - L - 1 + i
+      // (P = 128G + 2L + 2, the S1 taps' span); unit (i, quad j) = channels c*16 + 4j..+3 of
+      // that pixel of the previous block's NHWC fp32 output: v = x * gate (+ skip hi + lo),
+      // the gate kernels' arithmetic (planes.cuh gate_mul / gate_fma) so every plane value is
+      // bitwise the one gate_apply writes, split into bf16 hi (+ lo): 8 bytes per pass at
+      // core-matrix row i, byte (j & 1) * 8 of cg8 block j >> 1.  Zero outside the image and
+      // at the pad column.  The item's own positions [q0, q0 + 128G) leave as the gated
+      // tensor's operand planes (planes.cuh border contract kept): PL by one bulk copy per
+      // (pass, cg8) block range of the stage, PP by 8-byte stores.
+      constexpr int NP = NPASS_A;
+      constexpr int NT = kGateInThreads;
+      constexpr int UB = 4;  // units per thread in flight
+      grid_dep_wait();       // x, the gates and the skip come from the previous kernels
+      const int st = threadIdx.x - kStemWarp0 * 32;
+      const int L = p.L, W = p.W, H = p.H, C = p.C;
+      const int P = G * 128 + 2 * L + 2;
+      const int Lp = W / 2 + 1;
+      const bool has_skip = p.gskip.base != nullptr, has_pp = p.gpp.base != nullptr;
+      int stage = 0, xs = 0;
+      uint32_t phase = 0, xph = 0;
+      for (int item = blockIdx.x; item < p.total_items; item += gridDim.x) {
+        int b, it;
+        item_coords(item, p, b, it);
+        const int q0 = it * G * 128, qa = q0 - L - 1;
+        const int y_lo = max(floordiv(qa, L), 0);  // first staged row (as the producer)
+        if (it == 0) {  // top / bottom margins of the side-output planes, once per image
+          pl_zero_margins(p.gpl, b, st, NT);
+          if (has_pp) pl_zero_margins(p.gpp, b, st, NT);
+        }
+        for (int c = 0; c < C / 16; ++c) {
+          // the PL bulk stores that last read this stage (>= 2 chunks ago) are done
+          if (st == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          asm volatile("bar.sync 3, %0;" ::"n"(NT) : "memory");
+          mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+          uint8_t* a = a_base + (size_t)stage * p.a_stage_bytes;
+          const int j = st & 3;  // NT % 4 == 0: a thread keeps its channel quad
+          const float4 g4 = *reinterpret_cast<const float4*>(p.gates + (size_t)b * C + c * 16 + 4 * j);
+          mbar_wait(smem_u32(&xfull[xs]), xph);
+          const uint8_t* xr = reinterpret_cast<const uint8_t*>(xring) + (size_t)xs * p.stem_xstage;
+          const uint8_t* skr = xr + p.gx_skip_off + (size_t)(j >> 1) * P * 16 + (j & 1) * 8;  // pass 0 block
+          for (int u0 = st; u0 < 4 * P; u0 += UB * NT) {
+            float4 xv[UB];
+            uint2 sh[UB], sl[UB];
+            bool ok[UB];
+#pragma unroll
+            for (int k = 0; k < UB; ++k) {
+              const int u = u0 + k * NT, i = u >> 2;
+              const int q = qa + i;
+              const int y = (int)__umulhi((uint32_t)(q + 2 * L), p.L_mul) - 2;  // floor(q / L), q >= -2L
+              const int x = q - y * L;
+              ok[k] = u < 4 * P && y >= 0 && y < H && x < W;
+              xv[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+              sh[k] = sl[k] = make_uint2(0u, 0u);
+              if (ok[k]) {
+                xv[k] = *reinterpret_cast<const float4*>(xr + ((size_t)(y - y_lo) * W + x) * 64 + j * 16);
+                if (has_skip) {
+                  sh[k] = *reinterpret_cast<const uint2*>(skr + (size_t)i * 16);
+                  if (NP == 2) sl[k] = *reinterpret_cast<const uint2*>(skr + (size_t)(2 * P + i) * 16);
+                }
+              }
+            }
+#pragma unroll
+            for (int k = 0; k < UB; ++k) {
+              const int u = u0 + k * NT, i = u >> 2;
+              if (u >= 4 * P) break;
+              float v[4] = {0.f, 0.f, 0.f, 0.f};
+              if (ok[k]) {
+                const float xs4[4] = {xv[k].x, xv[k].y, xv[k].z, xv[k].w};
+                const float gs4[4] = {g4.x, g4.y, g4.z, g4.w};
+                if (has_skip) {
+                  float s4[4];
+                  s4[0] = __uint_as_float(sh[k].x << 16);
+                  s4[1] = __uint_as_float(sh[k].x & 0xFFFF0000u);
+                  s4[2] = __uint_as_float(sh[k].y << 16);
+                  s4[3] = __uint_as_float(sh[k].y & 0xFFFF0000u);
+                  if (NP == 2) {
+                    s4[0] += __uint_as_float(sl[k].x << 16);
+                    s4[1] += __uint_as_float(sl[k].x & 0xFFFF0000u);
+                    s4[2] += __uint_as_float(sl[k].y << 16);
+                    s4[3] += __uint_as_float(sl[k].y & 0xFFFF0000u);
+                  }
+#pragma unroll
+                  for (int e = 0; e < 4; ++e) v[e] = gate_fma(xs4[e], gs4[e], s4[e]);
+                } else {
+#pragma unroll
+                  for (int e = 0; e < 4; ++e) v[e] = gate_mul(xs4[e], gs4[e]);
+                }
+              }
+              float hi[4], lo[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                hi[e] = bf16_round(v[e]);
+                lo[e] = v[e] - hi[e];
+              }
+              const uint2 hw = make_uint2(pack_bf16x2(hi[0], hi[1]), pack_bf16x2(hi[2], hi[3]));
+              const uint32_t off = ((uint32_t)(j >> 1) * p.P_max + i) * 16 + (j & 1) * 8;
+              *reinterpret_cast<uint2*>(a + off) = hw;
+              uint2 lw = make_uint2(0u, 0u);
+              if (NP == 2) {
+                lw = make_uint2(pack_bf16x2(lo[0], lo[1]), pack_bf16x2(lo[2], lo[3]));
+                *reinterpret_cast<uint2*>(a + off + 2u * p.P_max * 16) = lw;
+              }
+              // phase-plane side output of own positions (pad column: both px planes' pad)
+              if (has_pp && i >= L + 1 && i < L + 1 + G * 128) {
+                const int q = qa + i;
+                const int y = (int)__umulhi((uint32_t)q, p.L_mul), x = q - y * L;
+                if (y < H) {
+                  uint16_t* ppb = p.gpp.base + (int64_t)b * p.gpp.img_stride +
+                                  (p.gpp.block_index(c, 0, j >> 1) + p.gpp.off) * 8 + (j & 1) * 4;
+                  const size_t lod = (size_t)(NP == 2 ? 2 : 0) * p.gpp.Q * 8;
+                  if (x < W) {
+                    uint16_t* d = ppb + (int64_t)((y & 1) * 2 + (x & 1)) * p.gpp.plane_stride +
+                                  (size_t)((y >> 1) * Lp + (x >> 1)) * 8;
+                    *reinterpret_cast<uint2*>(d) = hw;
+                    if (NP == 2) *reinterpret_cast<uint2*>(d + lod) = lw;
+                  } else {
+#pragma unroll
+                    for (int px = 0; px < 2; ++px) {
+                      uint16_t* d = ppb + (int64_t)((y & 1) * 2 + px) * p.gpp.plane_stride +
+                                    (size_t)((y >> 1) * Lp + W / 2) * 8;
+                      *reinterpret_cast<uint2*>(d) = make_uint2(0u, 0u);
+                      if (NP == 2) *reinterpret_cast<uint2*>(d + lod) = make_uint2(0u, 0u);
+                    }
+                  }
+                }
+              }
+            }
+          }
+          mbar_arrive(smem_u32(&xempty[xs]));  // this thread is done reading the x stage
+          if (++xs == p.gx_nst) {
+            xs = 0;
+            xph ^= 1u;
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // st.shared -> UMMA / bulk copies
+          asm volatile("bar.sync 3, %0;" ::"n"(NT) : "memory");
+          if (st == 0) {
+            // PL side output: the own positions of each (pass, cg8) block, one range each
+            // (zeros at pad columns and past the last row: the border contract)
+            const int own = min(G * 128, p.Hp * L + L + 8 - q0);  // stay inside the bottom margin
+            uint16_t* img = p.gpl.base + (int64_t)b * p.gpl.img_stride;
+#pragma unroll
+            for (int pass = 0; pass < NP; ++pass)
+#pragma unroll
+              for (int cg8 = 0; cg8 < 2; ++cg8)
+                bulk_s2g(img + (p.gpl.block_index(c, pass, cg8) + q0 + p.gpl.off) * 8,
+                         smem_u32(a + ((size_t)(pass * 2 + cg8) * p.P_max + L + 1) * 16), (uint32_t)own * 16);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+          mbar_arrive(smem_u32(&full[stage]));
+          if (++stage == p.stages) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+      if (st == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // PL stores complete
     } else if constexpr (STEM > 0) {
       // ===================== stem warps: relu(conv3x3(frames)) into the A stages ==========
       // Every staged position of the item (its 128G positions and the 2L+2 halo) is
@@ -1293,6 +1510,7 @@ void dispatch_rows(int n, int npm, int G, const Params& p, int grid, size_t smem
 void dispatch_s1p(int n, int npm, int G, const Params& p, int grid, size_t smem, cudaStream_t st);
 void dispatch_stem(int npm, int G, const Params& p, int grid, size_t smem, cudaStream_t st);
 void dispatch_stemt(int npm, int G, const Params& p, int grid, size_t smem, cudaStream_t st);
+void dispatch_gatein(int n, int npm, int G, const Params& p, int grid, size_t smem, cudaStream_t st);
 
 }  // namespace detail
 }  // namespace tc

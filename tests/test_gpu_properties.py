@@ -271,3 +271,31 @@ def test_tensor_core_stem_path():
         cfg = {f: getattr(net.config, f) for f in CONFIG_FIELDS}
         ref = port.forward(sd, cfg, torch.from_numpy(np.load(f"/tmp/stemtc_{hw}_{prec}_x.npy"))).numpy()
         assert nmax_err(b, ref) <= tol
+
+
+def test_gate_on_load_path_is_bitwise():
+    """STDA_GATEIN=1 (ECA gate + skip applied by the next stride-1 conv's builder warps, off
+    by default) forms every operand plane with the gate kernels' arithmetic, so the forward is
+    bitwise the default one — fp32 and bf16, C2 and 256^2 (subprocesses: switches read once)."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import torch, numpy as np, os\n"
+        "torch.set_grad_enabled(False)\n"
+        "from paper_2307_09063_b200 import StdaConfig, StdaNet\n"
+        "from paper_2307_09063_b200.synth import synth_triplets\n"
+        "for hw, b, prec in ((128, 6, 'fp32'), (256, 2, 'fp32'), (128, 3, 'bf16')):\n"
+        "    torch.manual_seed(hw)\n"
+        "    net = StdaNet(StdaConfig(map_height=hw, map_width=hw), precision=prec).eval().cuda()\n"
+        "    x = synth_triplets(b, hw, hw, seed=21)\n"
+        "    np.save(f'/tmp/gatein_{hw}_{prec}_' + os.environ['STDA_GATEIN'] + '.npy', net(x).cpu().numpy())\n"
+    )
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for flag in ("0", "1"):
+        subprocess.run([sys.executable, "-c", code], check=True, env=dict(os.environ, STDA_GATEIN=flag), cwd=root)
+    import numpy as np
+    for hw, prec in ((128, "fp32"), (256, "fp32"), (128, "bf16")):
+        a = np.load(f"/tmp/gatein_{hw}_{prec}_0.npy")
+        b = np.load(f"/tmp/gatein_{hw}_{prec}_1.npy")
+        assert np.array_equal(a, b), (hw, prec, float(np.abs(a - b).max()))
