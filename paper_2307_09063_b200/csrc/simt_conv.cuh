@@ -18,8 +18,10 @@ namespace stda {
 // CONV_STEMT: tensor-core only — the stem (F frames -> 16 channels, 3x3) as one GEMM per
 //            half-resolution position: K = the F x 4 x 4 frame window of the position's 2x2
 //            pixel block (one 16-value chunk per frame), N = 4 phases x 16 channels
+// CONVT4_SP: tensor-core only — ConvT 4x4/s2 with each output phase's tile origin shifted
+//            so that all four phases read the same four A windows (tc_kernel.cuh)
 enum ConvMode : int { CONV3_S1 = 0, CONV3_S2 = 1, CONVT4_S2 = 2, CONVT4_HALF = 3, CONV3_ROWS = 4,
-                      CONV3_S1P = 5, CONV_STEMT = 6 };
+                      CONV3_S1P = 5, CONV_STEMT = 6, CONVT4_SP = 7 };
 
 // A logical input tensor [B][C][H][W]: value = x*gx[b][c] (+ s*gs[b][c]).
 // Element (b, c, pixel p = y*W + x) of x lives at x[b*xb + c*xc + p*xp] (NCHW: xp = 1,

@@ -254,7 +254,8 @@ NetWs plan_ws(const stda_plan& p, int64_t B, char* base) {
     const int h = c.map_height >> lvl, wd = c.map_width >> lvl;
     w.d.push_back(take(B * ch * (size_t)h * wd));
     const size_t tiles =
-        std::max<size_t>(conv_tiles(CONVT4_S2, h, wd), 2 * cdiv((h / 2) * (wd / 2 + 1), 128));  // x2: half-phase items
+        std::max<size_t>(conv_tiles(CONVT4_S2, h, wd),
+                         2 * cdiv((h / 2) * (wd / 2 + 1) + wd / 2 + 2, 128));  // x2: half-phase items; +1 row: SP
     w.pd.push_back(take(B * ch * tiles));
     w.gd.push_back(take(B * ch));
   }

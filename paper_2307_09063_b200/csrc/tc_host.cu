@@ -30,6 +30,7 @@ struct HostTap {
 std::vector<HostTap> plane_taps(int mode, int pl) {
   std::vector<HostTap> t;
   if (mode == CONV_STEMT) return {{0, 0, 0, -1}};  // im2col: one unshifted A read per chunk
+  if (mode == CONVT4_SP) return {{0, 0, 0, -1}, {0, 0, 1, -1}, {0, 1, 0, -1}, {0, 1, 1, -1}};  // the 4 windows
   if (mode == CONV3_S1P) {
     // the plane's 4 shift groups (dy, dx = half-resolution shift; acc = first phase of the
     // run); only used for the staged position span (lo / hi) — packing is group-wise
@@ -73,6 +74,14 @@ std::vector<HostTap> plane_taps(int mode, int pl) {
 }
 
 }  // namespace
+
+bool sp_enabled() {  // env STDA_TC_SP=0: the 9-shift-group transposed conv (A/B timing)
+  static const bool on = [] {
+    const char* e = std::getenv("STDA_TC_SP");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 bool half_t_enabled() {  // env STDA_TC_HALF=0 keeps 3-MMA full ConvT items (A/B timing)
   static const bool on = [] {
@@ -133,7 +142,10 @@ void tc_pack_layer(TcLayerDesc& d, int mode, int cin, int cout, const float* w0,
   // chunk (three input rows), so at 256-wide planes the ring drops to one stage; half-phase
   // items stage 128 + L + 2 (measured C5 dec1.s2: 4.10 -> 3.04 ms)
   if (mode == CONVT4_S2 && !bf16 && half_t_enabled() && (wide_t || half_all || plane_w >= 256)) mode = CONVT4_HALF;
-  const bool tmode = mode == CONVT4_S2 || mode == CONVT4_HALF;
+  // full transposed convs whose hi/lo-concatenated accumulators fit run with shifted phase
+  // origins: 4 A windows per source and K chunk instead of 9 shift groups
+  if (mode == CONVT4_S2 && !bf16 && sp_enabled() && (w1 ? 2 : 1) * 4 * 2 * cout * 2 <= 512) mode = CONVT4_SP;
+  const bool tmode = mode == CONVT4_S2 || mode == CONVT4_HALF || mode == CONVT4_SP;
   d.mode = mode;
   d.n_src = w1 ? 2 : 1;
   d.cin = cin;
@@ -202,6 +214,23 @@ void tc_pack_layer(TcLayerDesc& d, int mode, int cin, int cout, const float* w0,
       d.chunk_off[f + 1] = (int64_t)packed.size() * 2;
     }
     d.concat = !bf16;
+    return;
+  }
+  if (mode == CONVT4_SP) {
+    // per chunk, per source and window (a, b): the 4 stacked phase tiles [kgrp 2][phase 4]
+    // [pass 2][cout][8]; phase (py, px) reads window (a, b) through its sub-kernel tap (a, b)
+    STDA_CHECK(d.concat, "internal: shifted-phase ConvT needs the hi/lo concat");
+    for (int c = 0; c < n_chunks; ++c) {
+      const int cgi = c % cgroups;
+      for (int s = 0; s < d.n_src; ++s)
+        for (int w = 0; w < 4; ++w)
+          for (int kg = 0; kg < 2; ++kg)
+            for (int ph = 0; ph < 4; ++ph)
+              for (int pass = 0; pass < 2; ++pass)
+                for (int n = 0; n < cout; ++n)
+                  for (int e = 0; e < 8; ++e) put(ws[s], n, cgi * 16 + kg * 8 + e, ph * 4 + (w >> 1) * 2 + (w & 1), pass);
+      d.chunk_off[c + 1] = (int64_t)packed.size() * 2;
+    }
     return;
   }
   if (mode == CONV3_S1P) {
@@ -335,7 +364,7 @@ TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W, size_t extra_smem, bool 
     g.Wp = W / 2;
     g.Ho = H;
     g.Wo = W;
-  } else if (d.mode == CONVT4_S2 || d.mode == CONVT4_HALF) {
+  } else if (d.mode == CONVT4_S2 || d.mode == CONVT4_HALF || d.mode == CONVT4_SP) {
     g.Hp = H;
     g.Wp = W;
     g.Ho = 2 * H;
@@ -369,7 +398,7 @@ TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W, size_t extra_smem, bool 
     STDA_CHECK(g.Wp % 128 == 0, "row-band conv: plane width must be a multiple of 128");
     const int AW = d.cout * (d.concat ? 2 : 1);
     const uint32_t w_total = (uint32_t)d.chunk_off[d.cin / 16];
-    const size_t fixed = 1024 + 80 + kEpiWarps * 64 * sizeof(float);
+    const size_t fixed = 1024 + 80 + kEpiWarpsMax * 64 * sizeof(float);
     bool found = false;
     static const int t_cap = [] {  // env STDA_TC_ROWS_T: largest rows per item (A/B timing)
       const char* e = std::getenv("STDA_TC_ROWS_T");
@@ -405,7 +434,7 @@ TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W, size_t extra_smem, bool 
   uint32_t b_stage = 0;
   for (int c = 0; c < d.n_planes * (d.cin / 16); ++c)
     b_stage = std::max<uint32_t>(b_stage, (uint32_t)(d.chunk_off[c + 1] - d.chunk_off[c]));
-  const size_t fixed = 1024 + 80 + kEpiWarps * 64 * sizeof(float) + extra_smem;
+  const size_t fixed = 1024 + 80 + kEpiWarpsMax * 64 * sizeof(float) + extra_smem;
   const uint32_t w_total = (uint32_t)d.chunk_off[d.n_planes * (d.cin / 16)];
   const size_t w_res = (w_total + 127) / 128 * 128;
   // Prefer (1) a >= 2-deep smem pipeline, (2) two TMEM slots (the epilogue of item i
@@ -458,7 +487,7 @@ TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W, size_t extra_smem, bool 
           const char* e = std::getenv("STDA_TC_S1STAGES");
           return e ? std::max(1, std::min(kMaxStages, std::atoi(e))) : 3;
         }();
-        const bool tmode = d.mode == CONVT4_S2 || d.mode == CONVT4_HALF;
+        const bool tmode = d.mode == CONVT4_S2 || d.mode == CONVT4_HALF || d.mode == CONVT4_SP;
         // the phase-plane stride-1 conv (small resident weights) takes a 4th stage: enc0.s1
         // 39.2 -> 38.2 us at C2 (round 2); plain stride-1 layers stay at 3
         const int s1_cap = d.mode == CONV3_S1P && !s1_env_set() ? 4 : s1_stages;
@@ -506,7 +535,7 @@ TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W, size_t extra_smem, bool 
     }();
     const int n_chunks = d.n_planes * (d.cin / 16);
     // measured: helps the transposed convs (dec0.s2 -4 %, dec1.s2 -1.5 %), not S1/S2
-    const bool tmode = d.mode == CONVT4_S2 || d.mode == CONVT4_HALF;
+    const bool tmode = d.mode == CONVT4_S2 || d.mode == CONVT4_HALF || d.mode == CONVT4_SP;
     if (cps_cap >= 2 && tmode && n_chunks % 2 == 0) {
       const size_t per = 2 * (size_t)g.a_stage_bytes + (g.resident ? 0 : 2 * (size_t)g.b_stage_bytes);
       const size_t base = (g.resident ? (size_t)((g.w_total + 127) / 128 * 128) : 0) + fixed;
@@ -520,7 +549,8 @@ TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W, size_t extra_smem, bool 
       }
     }
   }
-  const int positions = g.Hp * g.L;
+  // SP: tile origins run from one row and column above the image (phase (0,0) at +L+1)
+  const int positions = g.Hp * g.L + (d.mode == CONVT4_SP ? g.L + 1 : 0);
   g.items_per_image = cdiv(positions, g.G * 128) * (d.mode == CONVT4_HALF ? 2 : 1);
   static const bool planlog = std::getenv("STDA_TC_PLANLOG") != nullptr;  // debug: print plans
   if (planlog)
@@ -942,6 +972,7 @@ void tc_launch(const TcLayerDesc& d, const TcGeometry& g, const PlBuf& src0, con
     case CONVT4_HALF:
       STDA_CHECK(out.mode == 0, "half-phase ConvT writes NHWC fp32");
       return dispatch_th(d.cout, npm, g.G, p, grid, g.smem_bytes, st);
+    case CONVT4_SP: return dispatch_sp(d.cout, npm, g.G, p, grid, g.smem_bytes, st);
     default: return dispatch_t(d.cout, npm, g.G, p, grid, g.smem_bytes, st);
   }
 }

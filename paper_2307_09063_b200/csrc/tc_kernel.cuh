@@ -40,7 +40,17 @@ constexpr int kGateInThreads = 192;
 __host__ __device__ constexpr int stem_threads(int mode, int stem = 0) {
   return stem == kGateIn ? kGateInThreads : mode == CONV_STEMT ? kStemtThreads : kStemThreads;
 }
-__host__ __device__ constexpr int threads_of(int mode, int stem) { return stem ? kThreads + stem_threads(mode, stem) : kThreads; }
+// epilogue warps: 8.  A build with -DSTDA_EPI16_SP=1 gives the shifted-phase transposed
+// conv 16 (its epilogue binds once the MMA stream is 4 windows per chunk); measured slower
+// at C2 (dec1.s2 48.4 vs 41.1 us: 113 registers per thread, spills), so off.
+#ifndef STDA_EPI16_SP
+#define STDA_EPI16_SP 0
+#endif
+constexpr int kEpiWarpsMax = STDA_EPI16_SP ? 16 : kEpiWarps;
+__host__ __device__ constexpr int epi_warps(int mode) { return mode == CONVT4_SP && STDA_EPI16_SP ? 16 : kEpiWarps; }
+__host__ __device__ constexpr int threads_of(int mode, int stem) {
+  return stem ? kThreads + stem_threads(mode, stem) : (kEpiWarp0 + epi_warps(mode)) * 32;
+}
 constexpr int kMaxSmem = 227 * 1024;
 constexpr int kMaxStages = 6;  // smem ring depth cap
 constexpr int kMaxSlots = 4;   // TMEM accumulator slots cap
@@ -149,13 +159,15 @@ __device__ __forceinline__ void item_coords(int n, const Params& p, int& b, int&
 // HALF (ConvT, one output-row parity py per work item): t = px*4 + a*2 + b, accumulator px,
 //      shift (a - 1, px + b - 1) relative to the item's origin shifted down by py rows
 __host__ __device__ constexpr int ntaps(int mode, int pl) {
-  return mode == CONV3_S1 || mode == CONV3_ROWS ? 9
+  return mode == CONVT4_SP ? 4
+         : mode == CONV3_S1 || mode == CONV3_ROWS ? 9
          : mode == CONVT4_S2   ? 16
          : mode == CONVT4_HALF ? 8
                                : (pl == 0 ? 1 : pl == 3 ? 4 : 2);
 }
 __host__ __device__ constexpr int tap_dy(int mode, int pl, int t) {
-  return mode == CONV3_S1 || mode == CONV3_ROWS ? t / 3 - 1
+  return mode == CONVT4_SP ? t >> 1
+         : mode == CONV3_S1 || mode == CONV3_ROWS ? t / 3 - 1
          : mode == CONVT4_S2   ? (t / 4 >> 1) + ((t >> 1) & 1) - 1
          : mode == CONVT4_HALF ? ((t >> 1) & 1) - 1
          : pl == 2             ? (t == 0 ? -1 : 0)
@@ -163,7 +175,8 @@ __host__ __device__ constexpr int tap_dy(int mode, int pl, int t) {
                                : 0;
 }
 __host__ __device__ constexpr int tap_dx(int mode, int pl, int t) {
-  return mode == CONV3_S1 || mode == CONV3_ROWS ? t % 3 - 1
+  return mode == CONVT4_SP ? t & 1
+         : mode == CONV3_S1 || mode == CONV3_ROWS ? t % 3 - 1
          : mode == CONVT4_S2   ? ((t / 4) & 1) + (t & 1) - 1
          : mode == CONVT4_HALF ? (t >> 2) + (t & 1) - 1
          : pl == 1             ? (t == 0 ? -1 : 0)
@@ -179,14 +192,15 @@ __host__ __device__ constexpr bool tap_first(int mode, int t) {
 }
 // accumulators per source
 __host__ __device__ constexpr int nacc_src(int mode) {
-  return mode == CONVT4_S2 || mode == CONV3_S1P || mode == CONV_STEMT ? 4 : mode == CONVT4_HALF ? 2 : 1;
+  return mode == CONVT4_S2 || mode == CONV3_S1P || mode == CONV_STEMT || mode == CONVT4_SP ? 4
+         : mode == CONVT4_HALF ? 2 : 1;
 }
 // minimum shift over a plane's taps, as a*L + b
 __host__ __device__ constexpr int plane_lo_a(int mode, int pl) {
-  return mode == CONV3_S2 ? (pl >= 2 ? -1 : 0) : mode == CONV3_S1P ? -(pl >> 1) : mode == CONV_STEMT ? 0 : -1;
+  return mode == CONV3_S2 ? (pl >= 2 ? -1 : 0) : mode == CONV3_S1P ? -(pl >> 1) : mode == CONV_STEMT || mode == CONVT4_SP ? 0 : -1;
 }
 __host__ __device__ constexpr int plane_lo_b(int mode, int pl) {
-  return mode == CONV3_S2 ? ((pl & 1) ? -1 : 0) : mode == CONV3_S1P ? -(pl & 1) : mode == CONV_STEMT ? 0 : -1;
+  return mode == CONV3_S2 ? ((pl & 1) ? -1 : 0) : mode == CONV3_S1P ? -(pl & 1) : mode == CONV_STEMT || mode == CONVT4_SP ? 0 : -1;
 }
 __host__ __device__ constexpr int n_planes_of(int mode) { return mode == CONV3_S2 || mode == CONV3_S1P ? 4 : 1; }
 
@@ -424,6 +438,31 @@ __device__ __forceinline__ void issue_chunk(bool leader, uint64_t a0, uint64_t b
     }
   } else {
   const int lo = plane_lo_a(MODE, PL) * L + plane_lo_b(MODE, PL);
+  if constexpr (MODE == CONVT4_SP) {
+    // shifted-phase ConvT: output phase (py, px) of accumulator row m is the half-resolution
+    // position q0 + m + (1-py)*L + (1-px), so its 2x2 sub-kernel tap (a, b) reads input
+    // position q0 + m + a*L + b for every phase: four A windows per source, each one MMA
+    // pair over the four stacked phase tiles [B_hi | B_lo] (N = 4 * AW)
+    constexpr uint32_t idesc = idesc_bf16(4 * AW);
+#pragma unroll
+    for (int s = 0; s < (DUAL ? 2 : 1); ++s) {
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const uint64_t ad0 = a0 + (uint32_t)s * src_units + (uint32_t)((w >> 1) * L + (w & 1));
+        const uint64_t bd = b0 + (uint32_t)((s * 4 + w) * 4) * TAP_UNITS + ((uint64_t)(3 * AW) << 16);
+        const uint32_t accum0 = (first_chunk && w == 0) ? 0u : 1u;
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const uint64_t ad = ad0 + (uint32_t)(g * 128);
+          const uint32_t dcol = dslot + (uint32_t)((g * NACC + s * NACC_SRC) * AW);
+          tc_mma(leader, dcol, ad, bd, idesc, accum0);
+          if (NPM != kNpmBf16) tc_mma(leader, dcol, ad + lo_units, bd, idesc, 1u);
+        }
+      }
+    }
+    (void)lo;
+    return;
+  }
   if constexpr (MODE == CONV_STEMT) {
     // one chunk = one frame's 4x4 window per position: A_hi (and A_lo) x the 4 stacked
     // phase tiles [B_hi | B_lo] (K-half stride = 4 tiles of AW rows)
@@ -562,6 +601,7 @@ __global__ void __launch_bounds__(threads_of(MODE, STEM), 1) tc_conv_kernel(cons
   constexpr int NPLANES = n_planes_of(MODE);
   constexpr int NPASS_A = NPM == kNpmBf16 ? 1 : 2;
   constexpr int AW = NPM == kNpmConcat ? 2 * N : N;  // TMEM columns per accumulator
+  constexpr int EPW = STEM ? kEpiWarps : epi_warps(MODE);  // epilogue warps
   const TcLayerDesc& d = p.d;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cgroups = d.cin / 16;
@@ -580,11 +620,11 @@ __global__ void __launch_bounds__(threads_of(MODE, STEM), 1) tc_conv_kernel(cons
   uint64_t* xfull = wbar + 1;         // STEM: frame rows of x ring stage landed
   uint64_t* xempty = xfull + 4;       // STEM: stem warps done with x ring stage (<= 4 stages)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(xempty + 2);
-  float* red = reinterpret_cast<float*>(tmem_holder + 4);  // [kEpiWarps][N]
+  float* red = reinterpret_cast<float*>(tmem_holder + 4);  // [EPW][N]
   // STEM: x ring [2][F][rows][W] (offset from the dynamic smem base: the compiler keeps
   // the shared address space, i.e. LDS rather than generic loads)
   float* xring = reinterpret_cast<float*>(
-      smem + ((size_t)(reinterpret_cast<uint8_t*>(red + kEpiWarps * 64) - smem) + 127) / 128 * 128);
+      smem + ((size_t)(reinterpret_cast<uint8_t*>(red + kEpiWarpsMax * 64) - smem) + 127) / 128 * 128);
 
   if (threadIdx.x == 0) {
     trace_at(p.trace, 4, 0);
@@ -601,7 +641,7 @@ __global__ void __launch_bounds__(threads_of(MODE, STEM), 1) tc_conv_kernel(cons
     }
     for (int s = 0; s < p.slots; ++s) {
       mbar_init(smem_u32(&tfull[s]), 1);
-      mbar_init(smem_u32(&tempty[s]), kEpiWarps * 32);
+      mbar_init(smem_u32(&tempty[s]), EPW * 32);
     }
     mbar_init(smem_u32(wbar), 1);
     fence_barrier_init();
@@ -713,7 +753,10 @@ __global__ void __launch_bounds__(threads_of(MODE, STEM), 1) tc_conv_kernel(cons
       int b, it;
       item_coords(item, p, b, it);
       // HALF: items (tile, py) interleaved; the tile origin moves down py rows
-      const int q0 = MODE == CONVT4_HALF ? (it >> 1) * p.G * 128 + (it & 1) * p.L : it * p.G * 128;
+      // (SP: tile origins start one row and column above the image: phase (0,0) at q0 + L + 1)
+      const int q0 = MODE == CONVT4_HALF ? (it >> 1) * p.G * 128 + (it & 1) * p.L
+                     : MODE == CONVT4_SP ? it * p.G * 128 - p.L - 1
+                                         : it * p.G * 128;
       const uint16_t* img = S.base + (int64_t)b * S.img_stride;
       if constexpr (MODE == CONV3_ROWS) {
         // per staged row and (pass, cg8) block one copy of kRowsSL positions (weights resident)
@@ -860,7 +903,7 @@ __global__ void __launch_bounds__(threads_of(MODE, STEM), 1) tc_conv_kernel(cons
       tc_commit(leader, smem_u32(&tfull[slot]));
     }
     __syncwarp();
-  } else if (warp < kEpiWarp0 + kEpiWarps) {
+  } else if (warp < kEpiWarp0 + EPW) {
     // ===================== epilogue warps 2..9 ==========================================
     // Two warps per TMEM lane quarter; the (tile, phase, 16-channel) units of an item
     // alternate between them so each SM sub-partition has two independent epilogue
@@ -868,7 +911,8 @@ __global__ void __launch_bounds__(threads_of(MODE, STEM), 1) tc_conv_kernel(cons
     // store chain).
     constexpr int NJ = N / 16;
     const int ew = warp & 3;                               // TMEM lane quarter of this warp
-    const int half = (warp - kEpiWarp0) / 4;               // which units of the item
+    constexpr int NH = EPW / 4;                            // warps per TMEM lane quarter
+    const int half = (warp - kEpiWarp0) / 4;               // which units of the item (u % NH)
     const int et = threadIdx.x - kEpiWarp0 * 32;
     grid_dep_wait();  // outputs may still be read by the previous kernel
     uint32_t ic = 0;
@@ -877,7 +921,7 @@ __global__ void __launch_bounds__(threads_of(MODE, STEM), 1) tc_conv_kernel(cons
       const uint32_t sphase = (ic / p.slots) & 1;
       int b, it;
       item_coords(item, p, b, it);
-      const int q0 = (MODE == CONVT4_HALF ? it >> 1 : it) * p.G * 128;
+      const int q0 = (MODE == CONVT4_HALF ? it >> 1 : it) * p.G * 128 - (MODE == CONVT4_SP ? p.L + 1 : 0);
       const int py = MODE == CONVT4_HALF ? (it & 1) : 0;  // output row parity of a HALF item
       int ry0 = 0, rx0 = 0;  // ROWS: the item's first output row / column
       if (MODE == CONV3_ROWS) {
@@ -913,7 +957,7 @@ __global__ void __launch_bounds__(threads_of(MODE, STEM), 1) tc_conv_kernel(cons
         // row's last tile clears it
         const bool padpos = MODE == CONV3_ROWS ? (rx0 + 128 == p.Wp && ew == 3 && lane == 31)
                                                : (y < p.Hp && x == p.Wp);
-        if (p.out.mode != 0 && ((g * NACC_SRC * NJ) & 1) == half && padpos) {
+        if (p.out.mode != 0 && ((g * NACC_SRC * NJ) % NH) == half && padpos) {
           // this position is a pad of the output grid: keep the operand plane's pad
           // column zero (planes.cuh border contract)
           if (p.out.mode == 1) {
@@ -929,7 +973,15 @@ __global__ void __launch_bounds__(threads_of(MODE, STEM), 1) tc_conv_kernel(cons
 #pragma unroll
         for (int ph = 0; ph < NACC_SRC; ++ph) {
           int oy = y, ox = x;
-          if (MODE == CONVT4_S2 || MODE == CONV3_S1P || MODE == CONV_STEMT) {
+          bool pvalid = true;  // SP: this phase's row of the tile is an output position
+          if constexpr (MODE == CONVT4_SP) {
+            const int qp = q0 + g * 128 + ew * 32 + lane + (1 - (ph >> 1)) * p.L + (1 - (ph & 1));
+            const int yy = (int)__umulhi((uint32_t)(qp + 2 * p.L), p.L_mul) - 2;  // floor(qp / L)
+            const int xx = qp - yy * p.L;
+            pvalid = yy >= 0 && yy < p.Hp && xx < p.Wp;
+            oy = 2 * yy + (ph >> 1);
+            ox = 2 * xx + (ph & 1);
+          } else if (MODE == CONVT4_S2 || MODE == CONV3_S1P || MODE == CONV_STEMT) {
             oy = 2 * y + (ph >> 1);
             ox = 2 * x + (ph & 1);
           } else if (MODE == CONVT4_HALF) {
@@ -938,7 +990,7 @@ __global__ void __launch_bounds__(threads_of(MODE, STEM), 1) tc_conv_kernel(cons
           }
 #pragma unroll
           for (int j = 0; j < N; j += 16) {
-            if ((((g * NACC_SRC + ph) * NJ + j / 16) & 1) != half) continue;  // warp-uniform
+            if ((((g * NACC_SRC + ph) * NJ + j / 16) % NH) != half) continue;  // warp-uniform
             float a0[16], a1[16];
             const int gt = MODE == CONV3_ROWS ? G - 1 - g : g;  // ROWS: row j at column (T-1-j)*AW
             const uint32_t c0 = (uint32_t)((gt * NACC + ph) * AW + j);
@@ -1018,7 +1070,7 @@ __global__ void __launch_bounds__(threads_of(MODE, STEM), 1) tc_conv_kernel(cons
               }
               continue;
             }
-            if (!valid || (p.dbg & 1)) continue;
+            if (!(MODE == CONVT4_SP ? pvalid : valid) || (p.dbg & 1)) continue;
             if (p.out.mode == 0) {
               float* op = p.out.cp ? p.out.f32 + (((size_t)b * (N / 16) + j / 16) * p.Ho * p.Wo +
                                                   (size_t)oy * p.Wo + ox) * 16
@@ -1053,19 +1105,19 @@ __global__ void __launch_bounds__(threads_of(MODE, STEM), 1) tc_conv_kernel(cons
       mbar_arrive(smem_u32(&tempty[slot]));
       if (et == 0) trace_at(p.trace, 3, 2 * ic + 1);
       if (et == 0) trace_cta_item(p.trace, (int)ic);
-      if (p.out.mode != 0 && it == 0) pl_zero_margins(p.out.pl, b, et, kEpiWarps * 32);
+      if (p.out.mode != 0 && it == 0) pl_zero_margins(p.out.pl, b, et, EPW * 32);
       if (p.out.mode == 0 && p.out.gap) {
         // deterministic: a fixed butterfly over the lanes, then a fixed-order sum of the
         // 8 warp partials
         gap_lane_reduce<N>(gsum, lane, red + (warp - kEpiWarp0) * N);
-        asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+        asm volatile("bar.sync 1, %0;" ::"n"(EPW * 32) : "memory");
         if (et < N) {
           float s = red[et];
 #pragma unroll
-          for (int w = 1; w < kEpiWarps; ++w) s += red[w * N + et];
+          for (int w = 1; w < EPW; ++w) s += red[w * N + et];
           p.out.gap[((size_t)b * p.items_per_image + it) * N + et] = s;
         }
-        asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+        asm volatile("bar.sync 1, %0;" ::"n"(EPW * 32) : "memory");
       }
     }
   } else {
@@ -1475,7 +1527,7 @@ template <int N, int MODE, bool DUAL, int NPM, int G>
 void launch_k(const Params& p, int grid, size_t smem, cudaStream_t st) {
   auto kern = p.cps == 2 ? tc_conv_kernel<N, MODE, DUAL, NPM, G, 2> : tc_conv_kernel<N, MODE, DUAL, NPM, G, 1>;
   ensure_dyn_smem(kern, kMaxSmem);
-  launch_pdl(kern, dim3(grid), dim3(kThreads), smem, st, "tc_conv_kernel", p);
+  launch_pdl(kern, dim3(grid), dim3(threads_of(MODE, 0)), smem, st, "tc_conv_kernel", p);
 }
 
 template <int MODE, bool DUAL>
@@ -1510,6 +1562,7 @@ void dispatch_rows(int n, int npm, int G, const Params& p, int grid, size_t smem
 void dispatch_s1p(int n, int npm, int G, const Params& p, int grid, size_t smem, cudaStream_t st);
 void dispatch_stem(int npm, int G, const Params& p, int grid, size_t smem, cudaStream_t st);
 void dispatch_stemt(int npm, int G, const Params& p, int grid, size_t smem, cudaStream_t st);
+void dispatch_sp(int n, int npm, int G, const Params& p, int grid, size_t smem, cudaStream_t st);
 void dispatch_gatein(int n, int npm, int G, const Params& p, int grid, size_t smem, cudaStream_t st);
 
 }  // namespace detail
