@@ -21,7 +21,7 @@ namespace stda {
 // CONVT4_SP: tensor-core only — ConvT 4x4/s2 with each output phase's tile origin shifted
 //            so that all four phases read the same four A windows (tc_kernel.cuh)
 enum ConvMode : int { CONV3_S1 = 0, CONV3_S2 = 1, CONVT4_S2 = 2, CONVT4_HALF = 3, CONV3_ROWS = 4,
-                      CONV3_S1P = 5, CONV_STEMT = 6, CONVT4_SP = 7 };
+                      CONV3_S1P = 5, CONV_STEMT = 6, CONVT4_SP = 7, CONVT4_SPH = 8 };
 
 // A logical input tensor [B][C][H][W]: value = x*gx[b][c] (+ s*gs[b][c]).
 // Element (b, c, pixel p = y*W + x) of x lives at x[b*xb + c*xc + p*xp] (NCHW: xp = 1,

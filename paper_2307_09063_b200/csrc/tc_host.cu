@@ -30,7 +30,8 @@ struct HostTap {
 std::vector<HostTap> plane_taps(int mode, int pl) {
   std::vector<HostTap> t;
   if (mode == CONV_STEMT) return {{0, 0, 0, -1}};  // im2col: one unshifted A read per chunk
-  if (mode == CONVT4_SP) return {{0, 0, 0, -1}, {0, 0, 1, -1}, {0, 1, 0, -1}, {0, 1, 1, -1}};  // the 4 windows
+  if (mode == CONVT4_SP || mode == CONVT4_SPH)
+    return {{0, 0, 0, -1}, {0, 0, 1, -1}, {0, 1, 0, -1}, {0, 1, 1, -1}};  // the 4 windows
   if (mode == CONV3_S1P) {
     // the plane's 4 shift groups (dy, dx = half-resolution shift; acc = first phase of the
     // run); only used for the staged position span (lo / hi) — packing is group-wise
@@ -145,7 +146,9 @@ void tc_pack_layer(TcLayerDesc& d, int mode, int cin, int cout, const float* w0,
   // full transposed convs whose hi/lo-concatenated accumulators fit run with shifted phase
   // origins: 4 A windows per source and K chunk instead of 9 shift groups
   if (mode == CONVT4_S2 && !bf16 && sp_enabled() && (w1 ? 2 : 1) * 4 * 2 * cout * 2 <= 512) mode = CONVT4_SP;
-  const bool tmode = mode == CONVT4_S2 || mode == CONVT4_HALF || mode == CONVT4_SP;
+  // ... and the half-phase items likewise (two px phases of one row parity per item)
+  if (mode == CONVT4_HALF && sp_enabled() && (w1 ? 2 : 1) * 2 * 2 * cout * 2 <= 512) mode = CONVT4_SPH;
+  const bool tmode = mode == CONVT4_S2 || mode == CONVT4_HALF || mode == CONVT4_SP || mode == CONVT4_SPH;
   d.mode = mode;
   d.n_src = w1 ? 2 : 1;
   d.cin = cin;
@@ -214,6 +217,27 @@ void tc_pack_layer(TcLayerDesc& d, int mode, int cin, int cout, const float* w0,
       d.chunk_off[f + 1] = (int64_t)packed.size() * 2;
     }
     d.concat = !bf16;
+    return;
+  }
+  if (mode == CONVT4_SPH) {
+    // per output-row parity py (a block of its own, TcLayerDesc::half_bytes), chunk, source and
+    // window (a, b): the 2 stacked px tiles [kgrp 2][px 2][pass 2][cout][8]
+    STDA_CHECK(d.concat, "internal: shifted half-phase ConvT needs the hi/lo concat");
+    for (int hv = 0; hv < 2; ++hv) {
+      for (int c = 0; c < n_chunks; ++c) {
+        const int cgi = c % cgroups;
+        for (int s = 0; s < d.n_src; ++s)
+          for (int w = 0; w < 4; ++w)
+            for (int kg = 0; kg < 2; ++kg)
+              for (int px = 0; px < 2; ++px)
+                for (int pass = 0; pass < 2; ++pass)
+                  for (int n = 0; n < cout; ++n)
+                    for (int e = 0; e < 8; ++e)
+                      put(ws[s], n, cgi * 16 + kg * 8 + e, (hv * 2 + px) * 4 + (w >> 1) * 2 + (w & 1), pass);
+        if (hv == 0) d.chunk_off[c + 1] = (int64_t)packed.size() * 2;
+      }
+    }
+    d.half_bytes = d.chunk_off[n_chunks];
     return;
   }
   if (mode == CONVT4_SP) {
@@ -364,7 +388,7 @@ TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W, size_t extra_smem, bool 
     g.Wp = W / 2;
     g.Ho = H;
     g.Wo = W;
-  } else if (d.mode == CONVT4_S2 || d.mode == CONVT4_HALF || d.mode == CONVT4_SP) {
+  } else if (d.mode == CONVT4_S2 || d.mode == CONVT4_HALF || d.mode == CONVT4_SP || d.mode == CONVT4_SPH) {
     g.Hp = H;
     g.Wp = W;
     g.Ho = 2 * H;
@@ -487,7 +511,7 @@ TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W, size_t extra_smem, bool 
           const char* e = std::getenv("STDA_TC_S1STAGES");
           return e ? std::max(1, std::min(kMaxStages, std::atoi(e))) : 3;
         }();
-        const bool tmode = d.mode == CONVT4_S2 || d.mode == CONVT4_HALF || d.mode == CONVT4_SP;
+        const bool tmode = d.mode == CONVT4_S2 || d.mode == CONVT4_HALF || d.mode == CONVT4_SP || d.mode == CONVT4_SPH;
         // the phase-plane stride-1 conv (small resident weights) takes a 4th stage: enc0.s1
         // 39.2 -> 38.2 us at C2 (round 2); plain stride-1 layers stay at 3
         const int s1_cap = d.mode == CONV3_S1P && !s1_env_set() ? 4 : s1_stages;
@@ -535,7 +559,7 @@ TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W, size_t extra_smem, bool 
     }();
     const int n_chunks = d.n_planes * (d.cin / 16);
     // measured: helps the transposed convs (dec0.s2 -4 %, dec1.s2 -1.5 %), not S1/S2
-    const bool tmode = d.mode == CONVT4_S2 || d.mode == CONVT4_HALF || d.mode == CONVT4_SP;
+    const bool tmode = d.mode == CONVT4_S2 || d.mode == CONVT4_HALF || d.mode == CONVT4_SP || d.mode == CONVT4_SPH;
     if (cps_cap >= 2 && tmode && n_chunks % 2 == 0) {
       const size_t per = 2 * (size_t)g.a_stage_bytes + (g.resident ? 0 : 2 * (size_t)g.b_stage_bytes);
       const size_t base = (g.resident ? (size_t)((g.w_total + 127) / 128 * 128) : 0) + fixed;
@@ -550,8 +574,9 @@ TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W, size_t extra_smem, bool 
     }
   }
   // SP: tile origins run from one row and column above the image (phase (0,0) at +L+1)
-  const int positions = g.Hp * g.L + (d.mode == CONVT4_SP ? g.L + 1 : 0);
-  g.items_per_image = cdiv(positions, g.G * 128) * (d.mode == CONVT4_HALF ? 2 : 1);
+  const int positions = g.Hp * g.L + (d.mode == CONVT4_SP || d.mode == CONVT4_SPH ? g.L + 1 : 0);
+  const bool halfm = d.mode == CONVT4_HALF || d.mode == CONVT4_SPH;
+  g.items_per_image = cdiv(positions, g.G * 128) * (halfm ? 2 : 1);
   static const bool planlog = std::getenv("STDA_TC_PLANLOG") != nullptr;  // debug: print plans
   if (planlog)
     std::fprintf(stderr, "tc_plan mode %d cin %d cout %d grid %dx%d B %d: G %d stages %d cps %d slots %d resident %d "
@@ -561,7 +586,7 @@ TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W, size_t extra_smem, bool 
     const char* e = std::getenv("STDA_TC_TAIL");
     return !(e && e[0] == '0');
   }();
-  g.tail = tail_last && positions % (g.G * 128) != 0 ? (d.mode == CONVT4_HALF ? 2 : 1) : 0;
+  g.tail = tail_last && positions % (g.G * 128) != 0 ? (halfm ? 2 : 1) : 0;
   return g;
 }
 
@@ -960,7 +985,7 @@ void tc_launch(const TcLayerDesc& d, const TcGeometry& g, const PlBuf& src0, con
   int grid = std::min(p.total_items, sms);
   // HALF: an even grid keeps every CTA on items of one py (items alternate py), so each
   // CTA loads one weight block (TcLayerDesc::half_bytes)
-  if (d.mode == CONVT4_HALF) grid &= ~1;
+  if (d.mode == CONVT4_HALF || d.mode == CONVT4_SPH) grid &= ~1;
   const int npm = d.npass == 1 ? kNpmBf16 : (d.concat ? kNpmConcat : kNpm3);
   STDA_CHECK(d.cout == 16 || d.cout == 32 || d.cout == 64, "unsupported cout for the tensor-core path");
   STDA_CHECK(g.G == 1 || g.G == 2 || g.G == 4 || (d.mode == CONV3_ROWS && g.G == 8), "unsupported tile count per item");
@@ -973,6 +998,7 @@ void tc_launch(const TcLayerDesc& d, const TcGeometry& g, const PlBuf& src0, con
       STDA_CHECK(out.mode == 0, "half-phase ConvT writes NHWC fp32");
       return dispatch_th(d.cout, npm, g.G, p, grid, g.smem_bytes, st);
     case CONVT4_SP: return dispatch_sp(d.cout, npm, g.G, p, grid, g.smem_bytes, st);
+    case CONVT4_SPH: return dispatch_sph(d.cout, npm, g.G, p, grid, g.smem_bytes, st);
     default: return dispatch_t(d.cout, npm, g.G, p, grid, g.smem_bytes, st);
   }
 }

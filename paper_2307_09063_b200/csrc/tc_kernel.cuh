@@ -159,14 +159,14 @@ __device__ __forceinline__ void item_coords(int n, const Params& p, int& b, int&
 // HALF (ConvT, one output-row parity py per work item): t = px*4 + a*2 + b, accumulator px,
 //      shift (a - 1, px + b - 1) relative to the item's origin shifted down by py rows
 __host__ __device__ constexpr int ntaps(int mode, int pl) {
-  return mode == CONVT4_SP ? 4
+  return mode == CONVT4_SP || mode == CONVT4_SPH ? 4
          : mode == CONV3_S1 || mode == CONV3_ROWS ? 9
          : mode == CONVT4_S2   ? 16
          : mode == CONVT4_HALF ? 8
                                : (pl == 0 ? 1 : pl == 3 ? 4 : 2);
 }
 __host__ __device__ constexpr int tap_dy(int mode, int pl, int t) {
-  return mode == CONVT4_SP ? t >> 1
+  return mode == CONVT4_SP || mode == CONVT4_SPH ? t >> 1
          : mode == CONV3_S1 || mode == CONV3_ROWS ? t / 3 - 1
          : mode == CONVT4_S2   ? (t / 4 >> 1) + ((t >> 1) & 1) - 1
          : mode == CONVT4_HALF ? ((t >> 1) & 1) - 1
@@ -175,7 +175,7 @@ __host__ __device__ constexpr int tap_dy(int mode, int pl, int t) {
                                : 0;
 }
 __host__ __device__ constexpr int tap_dx(int mode, int pl, int t) {
-  return mode == CONVT4_SP ? t & 1
+  return mode == CONVT4_SP || mode == CONVT4_SPH ? t & 1
          : mode == CONV3_S1 || mode == CONV3_ROWS ? t % 3 - 1
          : mode == CONVT4_S2   ? ((t / 4) & 1) + (t & 1) - 1
          : mode == CONVT4_HALF ? (t >> 2) + (t & 1) - 1
@@ -193,14 +193,14 @@ __host__ __device__ constexpr bool tap_first(int mode, int t) {
 // accumulators per source
 __host__ __device__ constexpr int nacc_src(int mode) {
   return mode == CONVT4_S2 || mode == CONV3_S1P || mode == CONV_STEMT || mode == CONVT4_SP ? 4
-         : mode == CONVT4_HALF ? 2 : 1;
+         : mode == CONVT4_HALF || mode == CONVT4_SPH ? 2 : 1;
 }
 // minimum shift over a plane's taps, as a*L + b
 __host__ __device__ constexpr int plane_lo_a(int mode, int pl) {
-  return mode == CONV3_S2 ? (pl >= 2 ? -1 : 0) : mode == CONV3_S1P ? -(pl >> 1) : mode == CONV_STEMT || mode == CONVT4_SP ? 0 : -1;
+  return mode == CONV3_S2 ? (pl >= 2 ? -1 : 0) : mode == CONV3_S1P ? -(pl >> 1) : mode == CONV_STEMT || mode == CONVT4_SP || mode == CONVT4_SPH ? 0 : -1;
 }
 __host__ __device__ constexpr int plane_lo_b(int mode, int pl) {
-  return mode == CONV3_S2 ? ((pl & 1) ? -1 : 0) : mode == CONV3_S1P ? -(pl & 1) : mode == CONV_STEMT || mode == CONVT4_SP ? 0 : -1;
+  return mode == CONV3_S2 ? ((pl & 1) ? -1 : 0) : mode == CONV3_S1P ? -(pl & 1) : mode == CONV_STEMT || mode == CONVT4_SP || mode == CONVT4_SPH ? 0 : -1;
 }
 __host__ __device__ constexpr int n_planes_of(int mode) { return mode == CONV3_S2 || mode == CONV3_S1P ? 4 : 1; }
 
@@ -438,18 +438,20 @@ __device__ __forceinline__ void issue_chunk(bool leader, uint64_t a0, uint64_t b
     }
   } else {
   const int lo = plane_lo_a(MODE, PL) * L + plane_lo_b(MODE, PL);
-  if constexpr (MODE == CONVT4_SP) {
+  if constexpr (MODE == CONVT4_SP || MODE == CONVT4_SPH) {
     // shifted-phase ConvT: output phase (py, px) of accumulator row m is the half-resolution
     // position q0 + m + (1-py)*L + (1-px), so its 2x2 sub-kernel tap (a, b) reads input
     // position q0 + m + a*L + b for every phase: four A windows per source, each one MMA
     // pair over the four stacked phase tiles [B_hi | B_lo] (N = 4 * AW)
-    constexpr uint32_t idesc = idesc_bf16(4 * AW);
+    // (SPH: the item's two px phases of one output-row parity, the same four windows)
+    constexpr int NPH = NACC_SRC;
+    constexpr uint32_t idesc = idesc_bf16(NPH * AW);
 #pragma unroll
     for (int s = 0; s < (DUAL ? 2 : 1); ++s) {
 #pragma unroll
       for (int w = 0; w < 4; ++w) {
         const uint64_t ad0 = a0 + (uint32_t)s * src_units + (uint32_t)((w >> 1) * L + (w & 1));
-        const uint64_t bd = b0 + (uint32_t)((s * 4 + w) * 4) * TAP_UNITS + ((uint64_t)(3 * AW) << 16);
+        const uint64_t bd = b0 + (uint32_t)((s * 4 + w) * NPH) * TAP_UNITS + ((uint64_t)((NPH - 1) * AW) << 16);
         const uint32_t accum0 = (first_chunk && w == 0) ? 0u : 1u;
 #pragma unroll
         for (int g = 0; g < G; ++g) {
@@ -672,7 +674,8 @@ __global__ void __launch_bounds__(threads_of(MODE, STEM), 1) tc_conv_kernel(cons
       mbar_arrive_expect_tx(smem_u32(wbar), p.w_total);
       // HALF: this CTA's py block only (even grid: item parity == blockIdx.x parity)
       bulk_g2s(smem_u32(b_base),
-               reinterpret_cast<const uint8_t*>(d.w) + (MODE == CONVT4_HALF ? (blockIdx.x & 1) * d.half_bytes : 0),
+               reinterpret_cast<const uint8_t*>(d.w) +
+                   (MODE == CONVT4_HALF || MODE == CONVT4_SPH ? (blockIdx.x & 1) * d.half_bytes : 0),
                p.w_total, smem_u32(wbar));
     }
     grid_dep_wait();  // weights are static; activations come from the previous kernel
@@ -756,7 +759,8 @@ __global__ void __launch_bounds__(threads_of(MODE, STEM), 1) tc_conv_kernel(cons
       // (SP: tile origins start one row and column above the image: phase (0,0) at q0 + L + 1)
       const int q0 = MODE == CONVT4_HALF ? (it >> 1) * p.G * 128 + (it & 1) * p.L
                      : MODE == CONVT4_SP ? it * p.G * 128 - p.L - 1
-                                         : it * p.G * 128;
+                     : MODE == CONVT4_SPH ? (it >> 1) * p.G * 128 - p.L - 1
+                                          : it * p.G * 128;
       const uint16_t* img = S.base + (int64_t)b * S.img_stride;
       if constexpr (MODE == CONV3_ROWS) {
         // per staged row and (pass, cg8) block one copy of kRowsSL positions (weights resident)
@@ -820,7 +824,8 @@ __global__ void __launch_bounds__(threads_of(MODE, STEM), 1) tc_conv_kernel(cons
           const uint32_t a_bytes = (uint32_t)(p.G * 128 + pt.hi - pt.lo) * 16;
           if (lane == NCOPY && !p.resident)
             bulk_g2s(smem_u32(b_base + (size_t)stage * p.b_stage_bytes + (size_t)cc * p.chunk_b_bytes),
-                     reinterpret_cast<const uint8_t*>(d.w) + (MODE == CONVT4_HALF ? (it & 1) * d.half_bytes : 0) +
+                     reinterpret_cast<const uint8_t*>(d.w) +
+                         (MODE == CONVT4_HALF || MODE == CONVT4_SPH ? (it & 1) * d.half_bytes : 0) +
                          d.chunk_off[c],
                      (uint32_t)(d.chunk_off[c + 1] - d.chunk_off[c]), fb);
           if (lane < NCOPY) {
@@ -921,8 +926,9 @@ __global__ void __launch_bounds__(threads_of(MODE, STEM), 1) tc_conv_kernel(cons
       const uint32_t sphase = (ic / p.slots) & 1;
       int b, it;
       item_coords(item, p, b, it);
-      const int q0 = (MODE == CONVT4_HALF ? it >> 1 : it) * p.G * 128 - (MODE == CONVT4_SP ? p.L + 1 : 0);
-      const int py = MODE == CONVT4_HALF ? (it & 1) : 0;  // output row parity of a HALF item
+      const int q0 = (MODE == CONVT4_HALF || MODE == CONVT4_SPH ? it >> 1 : it) * p.G * 128 -
+                     (MODE == CONVT4_SP || MODE == CONVT4_SPH ? p.L + 1 : 0);
+      const int py = MODE == CONVT4_HALF || MODE == CONVT4_SPH ? (it & 1) : 0;  // output row parity
       int ry0 = 0, rx0 = 0;  // ROWS: the item's first output row / column
       if (MODE == CONV3_ROWS) {
         const int tpr = p.Wp / 128, band = it / tpr;
@@ -974,13 +980,14 @@ __global__ void __launch_bounds__(threads_of(MODE, STEM), 1) tc_conv_kernel(cons
         for (int ph = 0; ph < NACC_SRC; ++ph) {
           int oy = y, ox = x;
           bool pvalid = true;  // SP: this phase's row of the tile is an output position
-          if constexpr (MODE == CONVT4_SP) {
-            const int qp = q0 + g * 128 + ew * 32 + lane + (1 - (ph >> 1)) * p.L + (1 - (ph & 1));
+          if constexpr (MODE == CONVT4_SP || MODE == CONVT4_SPH) {
+            const int ppy = MODE == CONVT4_SP ? ph >> 1 : py, ppx = MODE == CONVT4_SP ? ph & 1 : ph;
+            const int qp = q0 + g * 128 + ew * 32 + lane + (1 - ppy) * p.L + (1 - ppx);
             const int yy = (int)__umulhi((uint32_t)(qp + 2 * p.L), p.L_mul) - 2;  // floor(qp / L)
             const int xx = qp - yy * p.L;
             pvalid = yy >= 0 && yy < p.Hp && xx < p.Wp;
-            oy = 2 * yy + (ph >> 1);
-            ox = 2 * xx + (ph & 1);
+            oy = 2 * yy + ppy;
+            ox = 2 * xx + ppx;
           } else if (MODE == CONVT4_S2 || MODE == CONV3_S1P || MODE == CONV_STEMT) {
             oy = 2 * y + (ph >> 1);
             ox = 2 * x + (ph & 1);
@@ -1070,7 +1077,7 @@ __global__ void __launch_bounds__(threads_of(MODE, STEM), 1) tc_conv_kernel(cons
               }
               continue;
             }
-            if (!(MODE == CONVT4_SP ? pvalid : valid) || (p.dbg & 1)) continue;
+            if (!(MODE == CONVT4_SP || MODE == CONVT4_SPH ? pvalid : valid) || (p.dbg & 1)) continue;
             if (p.out.mode == 0) {
               float* op = p.out.cp ? p.out.f32 + (((size_t)b * (N / 16) + j / 16) * p.Ho * p.Wo +
                                                   (size_t)oy * p.Wo + ox) * 16
@@ -1563,6 +1570,7 @@ void dispatch_s1p(int n, int npm, int G, const Params& p, int grid, size_t smem,
 void dispatch_stem(int npm, int G, const Params& p, int grid, size_t smem, cudaStream_t st);
 void dispatch_stemt(int npm, int G, const Params& p, int grid, size_t smem, cudaStream_t st);
 void dispatch_sp(int n, int npm, int G, const Params& p, int grid, size_t smem, cudaStream_t st);
+void dispatch_sph(int n, int npm, int G, const Params& p, int grid, size_t smem, cudaStream_t st);
 void dispatch_gatein(int n, int npm, int G, const Params& p, int grid, size_t smem, cudaStream_t st);
 
 }  // namespace detail
