@@ -84,6 +84,27 @@ bool sp_enabled() {  // env STDA_TC_SP=0: the 9-shift-group transposed conv (A/B
   return on;
 }
 
+// Shifted-phase convs: 3 MMAs of width N per window (hi*hi, lo*hi, hi*lo into one
+// accumulator) or the hi/lo concatenation (2 MMAs of width 2N, twice the TMEM columns).
+// Measured at C2 (round 2): the full-phase conv (dec1.s2) 41.1 -> 32.8 us with 3 MMAs — half
+// the accumulator columns give G = 2 tiles per item and half the epilogue's TMEM loads, which
+// bound it — while the half-phase conv (dec0.s2) is faster with the concat (30.7 vs 35.6 us).
+// env STDA_TC_SP3=0 / STDA_TC_SPH3=1 flip them (A/B timing).
+bool sp3_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("STDA_TC_SP3");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+bool sph3_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("STDA_TC_SPH3");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 bool half_t_enabled() {  // env STDA_TC_HALF=0 keeps 3-MMA full ConvT items (A/B timing)
   static const bool on = [] {
     const char* e = std::getenv("STDA_TC_HALF");
@@ -222,18 +243,19 @@ void tc_pack_layer(TcLayerDesc& d, int mode, int cin, int cout, const float* w0,
   if (mode == CONVT4_SPH) {
     // per output-row parity py (a block of its own, TcLayerDesc::half_bytes), chunk, source and
     // window (a, b): the 2 stacked px tiles [kgrp 2][px 2][pass 2][cout][8]
-    STDA_CHECK(d.concat, "internal: shifted half-phase ConvT needs the hi/lo concat");
+    if (sph3_enabled()) d.concat = 0;
     for (int hv = 0; hv < 2; ++hv) {
       for (int c = 0; c < n_chunks; ++c) {
         const int cgi = c % cgroups;
         for (int s = 0; s < d.n_src; ++s)
           for (int w = 0; w < 4; ++w)
-            for (int kg = 0; kg < 2; ++kg)
-              for (int px = 0; px < 2; ++px)
-                for (int pass = 0; pass < 2; ++pass)
-                  for (int n = 0; n < cout; ++n)
-                    for (int e = 0; e < 8; ++e)
-                      put(ws[s], n, cgi * 16 + kg * 8 + e, (hv * 2 + px) * 4 + (w >> 1) * 2 + (w & 1), pass);
+            for (int o = 0; o < 2 * 2 * 2; ++o) {  // concat: (kg, px, pass); 3-MMA: (pass, kg, px)
+              const int kg = d.concat ? o >> 2 : (o >> 1) & 1, px = d.concat ? (o >> 1) & 1 : o & 1;
+              const int pass = d.concat ? o & 1 : o >> 2;
+              for (int n = 0; n < cout; ++n)
+                for (int e = 0; e < 8; ++e)
+                  put(ws[s], n, cgi * 16 + kg * 8 + e, (hv * 2 + px) * 4 + (w >> 1) * 2 + (w & 1), pass);
+            }
         if (hv == 0) d.chunk_off[c + 1] = (int64_t)packed.size() * 2;
       }
     }
@@ -243,16 +265,17 @@ void tc_pack_layer(TcLayerDesc& d, int mode, int cin, int cout, const float* w0,
   if (mode == CONVT4_SP) {
     // per chunk, per source and window (a, b): the 4 stacked phase tiles [kgrp 2][phase 4]
     // [pass 2][cout][8]; phase (py, px) reads window (a, b) through its sub-kernel tap (a, b)
-    STDA_CHECK(d.concat, "internal: shifted-phase ConvT needs the hi/lo concat");
+    if (sp3_enabled()) d.concat = 0;
     for (int c = 0; c < n_chunks; ++c) {
       const int cgi = c % cgroups;
       for (int s = 0; s < d.n_src; ++s)
         for (int w = 0; w < 4; ++w)
-          for (int kg = 0; kg < 2; ++kg)
-            for (int ph = 0; ph < 4; ++ph)
-              for (int pass = 0; pass < 2; ++pass)
-                for (int n = 0; n < cout; ++n)
-                  for (int e = 0; e < 8; ++e) put(ws[s], n, cgi * 16 + kg * 8 + e, ph * 4 + (w >> 1) * 2 + (w & 1), pass);
+          for (int o = 0; o < 2 * 4 * 2; ++o) {  // concat: (kg, ph, pass); 3-MMA: (pass, kg, ph)
+            const int kg = d.concat ? o >> 3 : (o >> 2) & 1, ph = d.concat ? (o >> 1) & 3 : o & 3;
+            const int pass = d.concat ? o & 1 : o >> 3;
+            for (int n = 0; n < cout; ++n)
+              for (int e = 0; e < 8; ++e) put(ws[s], n, cgi * 16 + kg * 8 + e, ph * 4 + (w >> 1) * 2 + (w & 1), pass);
+          }
       d.chunk_off[c + 1] = (int64_t)packed.size() * 2;
     }
     return;

@@ -459,6 +459,8 @@ __device__ __forceinline__ void issue_chunk(bool leader, uint64_t a0, uint64_t b
           const uint32_t dcol = dslot + (uint32_t)((g * NACC + s * NACC_SRC) * AW);
           tc_mma(leader, dcol, ad, bd, idesc, accum0);
           if (NPM != kNpmBf16) tc_mma(leader, dcol, ad + lo_units, bd, idesc, 1u);
+          // 3-MMA scheme (no concat): [pass][kgrp][phase][N] blocks, + A_hi x B_lo
+          if (NPM == kNpm3) tc_mma(leader, dcol, ad, bd + (uint32_t)(2 * NPH * N), idesc, 1u);
         }
       }
     }
