@@ -17,7 +17,12 @@ void dispatch_s1p(int n, int npm, int G, const Params& p, int grid, size_t smem,
     }
   };
   using std::integral_constant;
-  STDA_CHECK(npm == kNpmConcat || npm == kNpmBf16, "phase-plane conv: precision scheme");
+  STDA_CHECK(npm == kNpmConcat || npm == kNpmBf16 || npm == kNpm3, "phase-plane conv: precision scheme");
+  if (npm == kNpm3) {
+    STDA_CHECK(n == 16 || n == 32, "phase-plane conv: 3-MMA N");
+    if (n == 16) return by_g(integral_constant<int, 16>{}, integral_constant<int, kNpm3>{});
+    return by_g(integral_constant<int, 32>{}, integral_constant<int, kNpm3>{});
+  }
   if (npm == kNpmConcat) {
     STDA_CHECK(n == 16 || n == 32, "phase-plane conv: fp32 needs cout <= 32");
     if (n == 16) return by_g(integral_constant<int, 16>{}, integral_constant<int, kNpmConcat>{});

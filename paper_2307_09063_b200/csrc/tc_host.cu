@@ -205,7 +205,9 @@ void tc_pack_layer(TcLayerDesc& d, int mode, int cin, int cout, const float* w0,
     const char* e = std::getenv("STDA_TC_S2_NOCONCAT");
     return e && e[0] == '1';
   }();
-  d.concat = !bf16 && n_acc * 2 * cout * 2 <= 512 && !(mode == CONV3_S2 && s2_noconcat);
+  static const char* noconcat_env = std::getenv("STDA_TC_NOCONCAT");  // mode digits without concat (A/B)
+  const bool noconcat_mode = noconcat_env && std::strchr(noconcat_env, '0' + mode) != nullptr;
+  d.concat = !bf16 && n_acc * 2 * cout * 2 <= 512 && !(mode == CONV3_S2 && s2_noconcat) && !noconcat_mode;
   // per (src, tap): concat -> [kgrp 2][pass 2][n][8] (kgrp row block = [B_hi; B_lo], 2N rows)
   //                 else   -> [pass][kgrp 2][n][8]
   auto put = [&](const float* w, int n, int ci, int wk, int pass) {
@@ -285,30 +287,38 @@ void tc_pack_layer(TcLayerDesc& d, int mode, int cin, int cout, const float* w0,
     // [kgrp 2][phase slot n][pass][cout][8]; tile j = output phase p0 + j reads input
     // plane (qy, qx) at shift (sy, sx) through the 3x3 tap dy = 2sy + qy - py,
     // dx = 2sx + qx - px (zero tile for a phase of the run that does not use the shift)
+    // 3-MMA scheme (env STDA_TC_S1P3=1, A/B): per group [pass][kgrp 2][phase slot n][cout][8]
+    static const bool s1p3 = [] {
+      const char* e = std::getenv("STDA_TC_S1P3");
+      return e && e[0] == '1';
+    }();
+    d.concat = !bf16 && !s1p3;
     std::vector<int> seen(36, 0);
     for (int c = 0; c < n_chunks; ++c) {
       const int pl = c / cgroups, cgi = c % cgroups, qy = pl >> 1, qx = pl & 1;
       for (int gi = 0; gi < 4; ++gi)
-        for (int kg = 0; kg < 2; ++kg)
-          for (int j = 0; j < s1p_n(pl, gi); ++j) {
-            const int acc = s1p_p0(pl, gi) + j, py = acc >> 1, px = acc & 1;
-            const bool used = s1p_uses(pl, gi, acc);
-            const int dy = 2 * s1p_dy(pl, gi) + qy - py, dx = 2 * s1p_dx(pl, gi) + qx - px;
-            if (used) {
-              STDA_CHECK(dy >= -1 && dy <= 1 && dx >= -1 && dx <= 1, "internal: phase-plane taps");
-              if (cgi == 0 && kg == 0) seen[acc * 9 + (dy + 1) * 3 + (dx + 1)]++;
-            }
-            for (int pass = 0; pass < npassB; ++pass)
-              for (int n = 0; n < cout; ++n)
-                for (int e = 0; e < 8; ++e) {
-                  if (used) put(ws[0], n, cgi * 16 + kg * 8 + e, (dy + 1) * 3 + (dx + 1), pass);
-                  else packed.push_back(0);
-                }
+        for (int o = 0; o < 2 * s1p_n(pl, gi) * npassB; ++o) {
+          const int nn = s1p_n(pl, gi);
+          // concat: (kg, j, pass); 3-MMA: (pass, kg, j)
+          const int kg = d.concat ? o / (nn * npassB) : (o / nn) % 2;
+          const int j = d.concat ? (o / npassB) % nn : o % nn;
+          const int pass = d.concat ? o % npassB : o / (2 * nn);
+          const int acc = s1p_p0(pl, gi) + j, py = acc >> 1, px = acc & 1;
+          const bool used = s1p_uses(pl, gi, acc);
+          const int dy = 2 * s1p_dy(pl, gi) + qy - py, dx = 2 * s1p_dx(pl, gi) + qx - px;
+          if (used) {
+            STDA_CHECK(dy >= -1 && dy <= 1 && dx >= -1 && dx <= 1, "internal: phase-plane taps");
+            if (cgi == 0 && kg == 0 && pass == 0) seen[acc * 9 + (dy + 1) * 3 + (dx + 1)]++;
           }
+          for (int n = 0; n < cout; ++n)
+            for (int e = 0; e < 8; ++e) {
+              if (used) put(ws[0], n, cgi * 16 + kg * 8 + e, (dy + 1) * 3 + (dx + 1), pass);
+              else packed.push_back(0);
+            }
+        }
       d.chunk_off[c + 1] = (int64_t)packed.size() * 2;
     }
     for (int i = 0; i < 36; ++i) STDA_CHECK(seen[i] == 1, "internal: phase-plane products");
-    d.concat = !bf16;
     STDA_CHECK(bf16 || 4 * 2 * cout <= 256, "phase-plane conv: stacked width");
     return;
   }

@@ -498,6 +498,7 @@ __device__ __forceinline__ void issue_chunk(bool leader, uint64_t a0, uint64_t b
         const uint32_t dcol = dslot + (uint32_t)((g * NACC + s1p_p0(PL, gi)) * AW);
         tc_mma(leader, dcol, ad, bd, idesc, accum0);                                // A_hi x tiles
         if (NPM != kNpmBf16) tc_mma(leader, dcol, ad + lo_units, bd, idesc, 1u);  // A_lo x tiles
+        if (NPM == kNpm3) tc_mma(leader, dcol, ad, bd + (uint32_t)(2 * n * N), idesc, 1u);  // A_hi x B_lo
       }
     }
     return;
