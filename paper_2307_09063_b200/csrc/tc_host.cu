@@ -166,7 +166,10 @@ void tc_pack_layer(TcLayerDesc& d, int mode, int cin, int cout, const float* w0,
   if (mode == CONVT4_S2 && !bf16 && half_t_enabled() && (wide_t || half_all || plane_w >= 256)) mode = CONVT4_HALF;
   // full transposed convs whose hi/lo-concatenated accumulators fit run with shifted phase
   // origins: 4 A windows per source and K chunk instead of 9 shift groups
-  if (mode == CONVT4_S2 && !bf16 && sp_enabled() && (w1 ? 2 : 1) * 4 * 2 * cout * 2 <= 512) mode = CONVT4_SP;
+  // (bf16: one pass, the four phase tiles of N columns; two TMEM slots need 2 x 4 x N <= 256)
+  if (mode == CONVT4_S2 && sp_enabled() &&
+      (bf16 ? (w1 ? 2 : 1) * 4 * cout <= 256 : (w1 ? 2 : 1) * 4 * 2 * cout * 2 <= 512))
+    mode = CONVT4_SP;
   // ... and the half-phase items likewise (two px phases of one row parity per item)
   if (mode == CONVT4_HALF && sp_enabled() && (w1 ? 2 : 1) * 2 * 2 * cout * 2 <= 512) mode = CONVT4_SPH;
   const bool tmode = mode == CONVT4_S2 || mode == CONVT4_HALF || mode == CONVT4_SP || mode == CONVT4_SPH;
@@ -251,7 +254,7 @@ void tc_pack_layer(TcLayerDesc& d, int mode, int cin, int cout, const float* w0,
         const int cgi = c % cgroups;
         for (int s = 0; s < d.n_src; ++s)
           for (int w = 0; w < 4; ++w)
-            for (int o = 0; o < 2 * 2 * 2; ++o) {  // concat: (kg, px, pass); 3-MMA: (pass, kg, px)
+            for (int o = 0; o < 2 * 2 * npassB; ++o) {  // concat: (kg, px, pass); else (pass, kg, px)
               const int kg = d.concat ? o >> 2 : (o >> 1) & 1, px = d.concat ? (o >> 1) & 1 : o & 1;
               const int pass = d.concat ? o & 1 : o >> 2;
               for (int n = 0; n < cout; ++n)
@@ -267,12 +270,12 @@ void tc_pack_layer(TcLayerDesc& d, int mode, int cin, int cout, const float* w0,
   if (mode == CONVT4_SP) {
     // per chunk, per source and window (a, b): the 4 stacked phase tiles [kgrp 2][phase 4]
     // [pass 2][cout][8]; phase (py, px) reads window (a, b) through its sub-kernel tap (a, b)
-    if (sp3_enabled()) d.concat = 0;
+    if (sp3_enabled() || bf16) d.concat = 0;
     for (int c = 0; c < n_chunks; ++c) {
       const int cgi = c % cgroups;
       for (int s = 0; s < d.n_src; ++s)
         for (int w = 0; w < 4; ++w)
-          for (int o = 0; o < 2 * 4 * 2; ++o) {  // concat: (kg, ph, pass); 3-MMA: (pass, kg, ph)
+          for (int o = 0; o < 2 * 4 * npassB; ++o) {  // concat: (kg, ph, pass); else (pass, kg, ph)
             const int kg = d.concat ? o >> 3 : (o >> 2) & 1, ph = d.concat ? (o >> 1) & 3 : o & 3;
             const int pass = d.concat ? o & 1 : o >> 3;
             for (int n = 0; n < cout; ++n)
