@@ -299,3 +299,44 @@ def test_gate_on_load_path_is_bitwise():
         a = np.load(f"/tmp/gatein_{hw}_{prec}_0.npy")
         b = np.load(f"/tmp/gatein_{hw}_{prec}_1.npy")
         assert np.array_equal(a, b), (hw, prec, float(np.abs(a - b).max()))
+
+
+def test_transposed_conv_forms_agree():
+    """The transposed-conv forms — shifted-phase with 3 MMAs (default), shifted-phase with the
+    hi/lo concat (STDA_TC_SP3=0), the nine shift groups (STDA_TC_SP=0) — stay within the fp32
+    tolerance of the oracle and of each other; C2 shapes (full-phase dec1.s2, half-phase
+    dec0.s2) and 256^2 (half-phase items), fp32 and bf16 (subprocesses: switches read once)."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import torch, numpy as np, os\n"
+        "torch.set_grad_enabled(False)\n"
+        "from paper_2307_09063_b200 import StdaConfig, StdaNet\n"
+        "from paper_2307_09063_b200.synth import synth_triplets\n"
+        "for hw, b, prec in ((128, 6, 'fp32'), (256, 2, 'fp32'), (128, 4, 'bf16')):\n"
+        "    torch.manual_seed(hw)\n"
+        "    net = StdaNet(StdaConfig(map_height=hw, map_width=hw), precision=prec).eval().cuda()\n"
+        "    x = synth_triplets(b, hw, hw, seed=31)\n"
+        "    np.save(f'/tmp/tform_{hw}_{prec}_' + os.environ['TAG'] + '.npy', net(x).cpu().numpy())\n"
+        "    np.save(f'/tmp/tform_{hw}_{prec}_x.npy', x.cpu().numpy())\n"
+    )
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    runs = {"default": {}, "concat": {"STDA_TC_SP3": "0"}, "groups": {"STDA_TC_SP": "0"}}
+    for tag, extra in runs.items():
+        subprocess.run([sys.executable, "-c", code], check=True, env=dict(os.environ, TAG=tag, **extra), cwd=root)
+    import numpy as np
+    from oracle import port
+    from tests._helpers import CONFIG_FIELDS, nmax_err
+    for hw, prec, tol in ((128, "fp32", 1e-4), (256, "fp32", 1e-4), (128, "bf16", 3e-2)):
+        torch.manual_seed(hw)
+        net = StdaNet(StdaConfig(map_height=hw, map_width=hw))
+        sd = {k: v.detach() for k, v in net.state_dict().items()}
+        cfg = {f: getattr(net.config, f) for f in CONFIG_FIELDS}
+        ref = port.forward(sd, cfg, torch.from_numpy(np.load(f"/tmp/tform_{hw}_{prec}_x.npy"))).numpy()
+        outs = {t: np.load(f"/tmp/tform_{hw}_{prec}_{t}.npy") for t in runs}
+        for t, y in outs.items():
+            assert nmax_err(y, ref) <= tol, (hw, prec, t, nmax_err(y, ref))
+        if prec == "fp32":
+            assert nmax_err(outs["concat"], outs["default"]) <= 2e-5
+            assert nmax_err(outs["groups"], outs["default"]) <= 2e-5
