@@ -916,10 +916,19 @@ int stda_forward_host(const stda_plan* plan, const float* x_host, float* y_host,
     STDA_CUDA(cudaEventRecord(p->ev_start, st));
     STDA_CUDA(cudaStreamWaitEvent(p->copy_in, p->ev_start, 0));
     STDA_CUDA(cudaStreamWaitEvent(p->copy_out, p->ev_start, 0));
-    const int64_t n_chunks = (batch + chunk - 1) / chunk;
+    // chunk sequence: a short first chunk (a quarter) when the call spans several, so the
+    // first copy-in the forwards cannot overlap is short; then full chunks (env
+    // STDA_HOST_RAMP=0: equal chunks, A/B timing)
+    static const bool ramp_on = [] {
+      const char* e = std::getenv("STDA_HOST_RAMP");
+      return !(e && e[0] == '0');
+    }();
+    const int64_t first = ramp_on && batch > 2 * chunk ? std::max<int64_t>(1, chunk / 4) : chunk;
+    const int64_t n_chunks = 1 + (batch - std::min(first, batch) + chunk - 1) / chunk;
+    int64_t b0 = 0;
     for (int64_t k = 0; k < n_chunks; ++k) {
       const int s = (int)(k & 1);
-      const int64_t b0 = k * chunk, nb = std::min(chunk, batch - b0);
+      const int64_t nb = std::min(k == 0 ? first : chunk, batch - b0);
       if (k >= 2) STDA_CUDA(cudaStreamWaitEvent(p->copy_in, p->ev_comp[s], 0));
       STDA_CUDA(cudaMemcpyAsync(d_in[s], x_host + b0 * in_tri, nb * in_tri * 4,
                                 cudaMemcpyHostToDevice, p->copy_in));
@@ -933,6 +942,7 @@ int stda_forward_host(const stda_plan* plan, const float* x_host, float* y_host,
       STDA_CUDA(cudaMemcpyAsync(y_host + b0 * HW, d_out[s], nb * HW * 4, cudaMemcpyDeviceToHost,
                                 p->copy_out));
       STDA_CUDA(cudaEventRecord(p->ev_out[s], p->copy_out));
+      b0 += nb;
     }
     for (int s = 0; s < 2 && s < n_chunks; ++s) STDA_CUDA(cudaStreamWaitEvent(st, p->ev_out[s], 0));
     STDA_CUDA(cudaStreamSynchronize(p->copy_out));
