@@ -538,13 +538,34 @@ __host__ __device__ constexpr HeadStrips head_strips_geom(int W) {
 
 __device__ __forceinline__ int hs_swz(int p) { return (p >> 1) & 3; }
 
+// d / u values of a head stage: fp32, or bf16 (DBF: the bf16 variant's d, and u — which that
+// variant rounds to bf16 before the conv — stored in place at the same value index)
+template <bool DBF>
+__device__ __forceinline__ float4 hd_load(const float* base, size_t idx) {
+  if constexpr (DBF) {
+    const uint2 r = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(base) + idx);
+    return make_float4(__uint_as_float(r.x << 16), __uint_as_float(r.x & 0xFFFF0000u), __uint_as_float(r.y << 16),
+                       __uint_as_float(r.y & 0xFFFF0000u));
+  } else {
+    return *reinterpret_cast<const float4*>(base + idx);
+  }
+}
+template <bool DBF>
+__device__ __forceinline__ void hd_store(float* base, size_t idx, float4 u) {
+  if constexpr (DBF)
+    *reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(base) + idx) =
+        make_uint2(pack_bf16x2(u.x, u.y), pack_bf16x2(u.z, u.w));
+  else
+    *reinterpret_cast<float4*>(base + idx) = u;
+}
+
 struct HeadConst {
   float w[9 * kHsC];  // [tap][channel]: read by the conv from the kernel-parameter bank
 };
 
 // SKIP_PP: the skip (stem output) comes as phase planes: staged per row and px plane as
 // [block][row][px][W/2] (2 copies per row and block, issued by the producer warp's lanes)
-template <int W, bool SKIP_PP = false>
+template <int W, bool SKIP_PP = false, bool DBF = false>
 __global__ void __launch_bounds__(kHsThreads, 1) head_strips_kernel(
     const __grid_constant__ HeadConst cw, const float* __restrict__ bias, const float* __restrict__ gap, int items,
     const float* __restrict__ eca_w, int k, const float* __restrict__ d, PlBuf skip, float* __restrict__ y,
@@ -595,14 +616,15 @@ __global__ void __launch_bounds__(kHsThreads, 1) head_strips_kernel(
       const int n0 = (nr + 1 - (iy0 & 1)) / 2, n1 = nr - n0;  // staged rows of parity 0 / 1
       const uint32_t bar = smem_u32(&full[st]);
       uint8_t* base = hsm + (size_t)st * g.stage;
-      if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)(nr * W * kHsC * 4 + np * 2 * 2 * nr * Lp * 16));
+      if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)(nr * W * kHsC * (DBF ? 2 : 4) + np * 2 * 2 * nr * Lp * 16));
       __syncwarp();
       const uint16_t* simg = skip.base + b * skip.img_stride;
       const int ncp = 1 + np * 2 * 4;
       for (int c = lane; c < ncp; c += 32) {
         if (c == 0) {
-          bulk_g2s(smem_u32(base + (size_t)r0 * W * kHsC * 4), d + ((size_t)b * H + iy0) * W * kHsC,
-                   (uint32_t)(nr * W * kHsC * 4), bar);
+          bulk_g2s(smem_u32(base + (size_t)r0 * W * kHsC * (DBF ? 2 : 4)),
+                   reinterpret_cast<const uint8_t*>(d) + ((size_t)b * H + iy0) * W * kHsC * (DBF ? 2 : 4),
+                   (uint32_t)(nr * W * kHsC * (DBF ? 2 : 4)), bar);
           continue;
         }
         const int u = c - 1, plane = u & 3, blk = u >> 2, py = plane >> 1;
@@ -631,9 +653,10 @@ __global__ void __launch_bounds__(kHsThreads, 1) head_strips_kernel(
         const int nr = r1 - r0, iy0 = y0 - 1 + r0;
         const uint32_t bar = smem_u32(&full[st]);
         uint8_t* base = hsm + (size_t)st * g.stage;
-        mbar_arrive_expect_tx(bar, (uint32_t)(nr * W * kHsC * 4 + np * 2 * nr * L * 16));
-        bulk_g2s(smem_u32(base + (size_t)r0 * W * kHsC * 4), d + ((size_t)b * H + iy0) * W * kHsC,
-                 (uint32_t)(nr * W * kHsC * 4), bar);
+        mbar_arrive_expect_tx(bar, (uint32_t)(nr * W * kHsC * (DBF ? 2 : 4) + np * 2 * nr * L * 16));
+        bulk_g2s(smem_u32(base + (size_t)r0 * W * kHsC * (DBF ? 2 : 4)),
+                 reinterpret_cast<const uint8_t*>(d) + ((size_t)b * H + iy0) * W * kHsC * (DBF ? 2 : 4),
+                 (uint32_t)(nr * W * kHsC * (DBF ? 2 : 4)), bar);
         const uint16_t* simg = skip.base + b * skip.img_stride;
         for (int pass = 0; pass < np; ++pass)
           for (int cg8 = 0; cg8 < 2; ++cg8)
@@ -697,7 +720,7 @@ __global__ void __launch_bounds__(kHsThreads, 1) head_strips_kernel(
         const int r = p / W, x = p - r * W;
         const int iy = y0 - 1 + r;
         in[j] = iy >= 0 && iy < H;
-        dv[j] = *reinterpret_cast<const float4*>(ubase + p * kHsC + q * 4);
+        dv[j] = hd_load<DBF>(ubase, (size_t)p * kHsC + q * 4);
         // channels 4q..4q+3: cg8 block (q >> 1), bytes (q & 1) * 8 of position r*L + x
         // (phase-plane skip: plane (iy%2, x%2), plane-row slot of iy, column x/2)
         size_t so;
@@ -740,7 +763,7 @@ __global__ void __launch_bounds__(kHsThreads, 1) head_strips_kernel(
             u.w = bf16_round(u.w);
           }
         }
-        *reinterpret_cast<float4*>(ubase + p * kHsC + (q ^ hs_swz(p)) * 4) = u;
+        hd_store<DBF>(ubase, (size_t)p * kHsC + (q ^ hs_swz(p)) * 4, u);
       }
     }
     fence_proxy_async();  // generic writes of this stage before its next async refill
@@ -758,7 +781,7 @@ __global__ void __launch_bounds__(kHsThreads, 1) head_strips_kernel(
 #pragma unroll
         for (int rr = 0; rr < 4; ++rr) {
           const int p = (2 * rp + rr) * W + (in ? xx : 0);
-          u[j][rr] = *reinterpret_cast<const float4*>(ubase + p * kHsC + (j ^ hs_swz(p)) * 4);
+          u[j][rr] = hd_load<DBF>(ubase, (size_t)p * kHsC + (j ^ hs_swz(p)) * 4);
           if (!in) u[j][rr] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
@@ -813,7 +836,7 @@ __host__ __device__ constexpr HeadTiles head_tiles_geom(int TW) {
   return g;
 }
 
-template <int TW>
+template <int TW, bool DBF = false>
 __global__ void __launch_bounds__(kHsThreads, 1) head_tiles_kernel(
     const __grid_constant__ HeadConst cw, const float* __restrict__ bias, const float* __restrict__ gap, int items,
     const float* __restrict__ eca_w, int k, const float* __restrict__ d, PlBuf skip, float* __restrict__ y,
@@ -865,13 +888,14 @@ __global__ void __launch_bounds__(kHsThreads, 1) head_tiles_kernel(
       const uint32_t bar = smem_u32(&full[st]);
       uint8_t* base = hsm + (size_t)st * g.stage;
       if (lane == 0)
-        mbar_arrive_expect_tx(bar, (uint32_t)((r1 - r0) * ((cr - cl) * kHsC * 4 + np * 2 * SW * 16)));
+        mbar_arrive_expect_tx(bar, (uint32_t)((r1 - r0) * ((cr - cl) * kHsC * (DBF ? 2 : 4) + np * 2 * SW * 16)));
       __syncwarp();
       for (int c = lane; c < (r1 - r0) * nk; c += 32) {
         const int r = r0 + c / nk, kk = c % nk, iy = y0 - 1 + r;
         if (kk == 0) {
-          bulk_g2s(smem_u32(base + ((size_t)r * SW + (cl - (x0 - 1))) * kHsC * 4),
-                   d + (((size_t)b * H + iy) * W + cl) * kHsC, (uint32_t)((cr - cl) * kHsC * 4), bar);
+          bulk_g2s(smem_u32(base + ((size_t)r * SW + (cl - (x0 - 1))) * kHsC * (DBF ? 2 : 4)),
+                   reinterpret_cast<const uint8_t*>(d) + (((size_t)b * H + iy) * W + cl) * kHsC * (DBF ? 2 : 4),
+                   (uint32_t)((cr - cl) * kHsC * (DBF ? 2 : 4)), bar);
         } else {
           const int blk = kk - 1;  // (pass, cg8)
           bulk_g2s(smem_u32(base + g.dbytes + (size_t)blk * g.sblk + (size_t)r * SW * 16),
@@ -937,7 +961,7 @@ __global__ void __launch_bounds__(kHsThreads, 1) head_tiles_kernel(
         const int r = p / SW, xs = p - r * SW;
         const int iy = y0 - 1 + r, ix = x0 - 1 + xs;
         in[j] = u < NU && iy >= 0 && iy < H && ix >= 0 && ix < W;
-        dv[j] = *reinterpret_cast<const float4*>(ubase + p * kHsC + q * 4);
+        dv[j] = hd_load<DBF>(ubase, (size_t)p * kHsC + q * 4);
         // channels 4q..4q+3: cg8 block (q >> 1), bytes (q & 1) * 8 of stage position p
         const size_t so = (size_t)p * 16 + (q & 1) * 8;
         hv[j] = *reinterpret_cast<const uint2*>(sbase + (size_t)(q >> 1) * g.sblk + so);
@@ -974,7 +998,7 @@ __global__ void __launch_bounds__(kHsThreads, 1) head_tiles_kernel(
             uu.w = bf16_round(uu.w);
           }
         }
-        *reinterpret_cast<float4*>(ubase + p * kHsC + (q ^ hs_swz(p)) * 4) = uu;
+        hd_store<DBF>(ubase, (size_t)p * kHsC + (q ^ hs_swz(p)) * 4, uu);
       }
     }
     fence_proxy_async();  // generic writes of this stage before its next async refill
@@ -991,7 +1015,7 @@ __global__ void __launch_bounds__(kHsThreads, 1) head_tiles_kernel(
 #pragma unroll
         for (int rr = 0; rr < 4; ++rr) {
           const int p = (2 * rp + rr) * SW + cx + kx;
-          u[j][rr] = *reinterpret_cast<const float4*>(ubase + p * kHsC + (j ^ hs_swz(p)) * 4);
+          u[j][rr] = hd_load<DBF>(ubase, (size_t)p * kHsC + (j ^ hs_swz(p)) * 4);
         }
 #pragma unroll
       for (int j = 0; j < 4; ++j)
@@ -1116,9 +1140,18 @@ void launch_stem_planes(const float* w, const float* bias, const Src& x, int F, 
   }
 }
 
+bool head_bf16_ok(int C0, int64_t B, int H, int W, const PlBuf& skip) {
+  static const bool strips_off = [] {
+    const char* e = std::getenv("STDA_HEAD");
+    return e && std::string(e) == "tiles";
+  }();
+  return !strips_off && head_strips_ok(C0, B, H, W) && (skip.planes == 1 || W <= 128);
+}
+
 void launch_head_fused(const float* w, const float* bias, const float* gap, int items,
                        const float* eca_w, int k, const float* d, const PlBuf& skip, int C0, float* y,
-                       int64_t B, int H, int W, bool bf16, cudaStream_t st, const float* w_host) {
+                       int64_t B, int H, int W, bool bf16, cudaStream_t st, const float* w_host, bool d_bf16) {
+  STDA_CHECK(!d_bf16 || (w_host != nullptr && head_bf16_ok(C0, B, H, W, skip)), "head: bf16 d needs the strip head");
   STDA_CHECK(C0 % 8 == 0, "head kernel needs stem_channels % 8 == 0");
   static const bool strips_off = [] {
     const char* e = std::getenv("STDA_HEAD");
@@ -1135,7 +1168,7 @@ void launch_head_fused(const float* w, const float* bias, const float* gap, int 
       const HeadTiles g = head_tiles_geom(128);
       const int64_t n_strips = B * (H / g.R) * (W / 128);
       const unsigned grid = (unsigned)std::min<int64_t>(n_strips, sms);
-      const auto kern = head_tiles_kernel<128>;
+      const auto kern = d_bf16 ? head_tiles_kernel<128, true> : head_tiles_kernel<128, false>;
       ensure_dyn_smem(kern, 227 * 1024);
       launch_pdl(kern, dim3(grid), dim3(kHsThreads), g.smem, st, "head_tiles_kernel", hc, bias, gap, items, eca_w, k,
                  d, skip, y, B, H, W, (int)bf16);
@@ -1145,8 +1178,9 @@ void launch_head_fused(const float* w, const float* bias, const float* gap, int 
     const int64_t n_strips = B * (H / g.R);
     const unsigned grid = (unsigned)std::min<int64_t>(n_strips, sms);
     auto go = [&](auto wc) {
-      const auto kern = skip.planes == 4 ? head_strips_kernel<decltype(wc)::value, true>
-                                         : head_strips_kernel<decltype(wc)::value, false>;
+      constexpr int WW = decltype(wc)::value;
+      const auto kern = skip.planes == 4 ? (d_bf16 ? head_strips_kernel<WW, true, true> : head_strips_kernel<WW, true, false>)
+                                         : (d_bf16 ? head_strips_kernel<WW, false, true> : head_strips_kernel<WW, false, false>);
       ensure_dyn_smem(kern, 227 * 1024);
       launch_pdl(kern, dim3(grid), dim3(kHsThreads), g.smem, st, "head_strips_kernel", hc, bias, gap, items, eca_w,
                  k, d, skip, y, B, H, (int)bf16);

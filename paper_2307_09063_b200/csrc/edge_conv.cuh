@@ -29,6 +29,9 @@ void launch_stem_planes(const float* w, const float* bias, const Src& x, int F, 
 // the kernel-parameter bank instead of shared memory.
 void launch_head_fused(const float* w, const float* bias, const float* gap, int items,
                        const float* eca_w, int k, const float* d, const PlBuf& skip, int C0, float* y,
-                       int64_t B, int H, int W, bool bf16, cudaStream_t st, const float* w_host = nullptr);
+                       int64_t B, int H, int W, bool bf16, cudaStream_t st, const float* w_host = nullptr,
+                       bool d_bf16 = false);
+// d_bf16 (the bf16 variant's last stage-2 output stored as bf16): strip / tile heads only
+bool head_bf16_ok(int C0, int64_t B, int H, int W, const PlBuf& skip);
 
 }  // namespace stda

@@ -252,12 +252,14 @@ constexpr int kGsStages = 4;
 // Compile-time channel count / passes / skip / phase-plane output: the unit loop has no
 // runtime division and each thread keeps one 8-channel group (kGsCompute % (C / 8) == 0),
 // so its plane block offsets are loop-invariant.
-template <int C, int NP, bool SKIP, bool PP, bool WHOLE>
+// XBF: x holds bf16 values (the bf16 variant's stage-2 outputs), else fp32
+template <int C, int NP, bool SKIP, bool PP, bool WHOLE, bool XBF>
 __global__ void __launch_bounds__(kGsThreads, 1) gate_strips_kernel(
     const float* __restrict__ gap, int items, const float* __restrict__ eca_w, int k,
-    const float* __restrict__ x, PlBuf skip, PlBuf out_pl, PlBuf out_pp, int H, int W, int TW, uint32_t TW_mul,
+    const void* __restrict__ x, PlBuf skip, PlBuf out_pl, PlBuf out_pp, int H, int W, int TW, uint32_t TW_mul,
     int R, int64_t B, uint32_t x_bytes, uint32_t stage_bytes) {
   constexpr int stages = kGsStages;
+  constexpr int XB = XBF ? 2 : 4;  // bytes per x value
   using namespace ptx;
   constexpr int G8 = C / 8;
   constexpr int nblk = (C / 16) * NP * 2;
@@ -309,8 +311,9 @@ __global__ void __launch_bounds__(kGsThreads, 1) gate_strips_kernel(
         const int r = whole ? 0 : c / nk, kk = whole ? c : c - r * nk;
         const int nr = whole ? R : 1;
         if (kk == 0)
-          bulk_g2s(smem_u32(base + (size_t)r * TW * C * 4), x + (((size_t)b * H + y0 + r) * W + x0) * C,
-                   (uint32_t)nr * TW * C * 4, bar);
+          bulk_g2s(smem_u32(base + (size_t)r * TW * C * XB),
+                   static_cast<const uint8_t*>(x) + ((((size_t)b * H + y0 + r) * W + x0) * C) * XB,
+                   (uint32_t)nr * TW * C * XB, bar);
         else
           bulk_g2s(smem_u32(base + x_bytes + (size_t)(kk - 1) * sk_blk + (size_t)r * Ls * 16),
                    skip.base + b * skip.img_stride +
@@ -375,9 +378,21 @@ __global__ void __launch_bounds__(kGsThreads, 1) gate_strips_kernel(
 #pragma unroll 2
     for (int pix = tid / G8; pix < R * TW; pix += kGsCompute / G8) {
       const int r = (int)__umulhi((uint32_t)pix, TW_mul), xl = pix - r * TW, xx = x0 + xl;
-      const float4 a0 = *reinterpret_cast<const float4*>(xs + (size_t)pix * C + c8 * 8);
-      const float4 a1 = *reinterpret_cast<const float4*>(xs + (size_t)pix * C + c8 * 8 + 4);
-      const float xv[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      float xv[8];
+      if (XBF) {
+        const uint4 h = *reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(xs) + (size_t)pix * C + c8 * 8);
+        const uint32_t hw[4] = {h.x, h.y, h.z, h.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          xv[2 * j] = __uint_as_float(hw[j] << 16);
+          xv[2 * j + 1] = __uint_as_float(hw[j] & 0xFFFF0000u);
+        }
+      } else {
+        const float4 a0 = *reinterpret_cast<const float4*>(xs + (size_t)pix * C + c8 * 8);
+        const float4 a1 = *reinterpret_cast<const float4*>(xs + (size_t)pix * C + c8 * 8 + 4);
+        xv[0] = a0.x; xv[1] = a0.y; xv[2] = a0.z; xv[3] = a0.w;
+        xv[4] = a1.x; xv[5] = a1.y; xv[6] = a1.z; xv[7] = a1.w;
+      }
       float v[8];
       if (SKIP) {  // + skip (model.py:197-198), exact hi + lo of its plane
         const size_t so = (size_t)(r * Ls + xl) * 16;
@@ -466,53 +481,88 @@ void launch_eca_gates(const float* gap, int items, const float* eca_w, int k, fl
              "eca_gates_kernel", gap, items, eca_w, k, gates, C, hw);
 }
 
-void launch_gate_apply(const float* gap, int items, const float* eca_w, int k, const float* x,
-                       const PlBuf* skip, const PlBuf* out_pl, const PlBuf* out_pp, float* out_f32,
-                       int64_t B, int C, int H, int W, cudaStream_t st) {
-  STDA_CHECK(C % 8 == 0 && C <= 1024, "gate_apply: channel count");
+namespace {
+// the persistent strip plan of gate_apply (valid = the strip kernel runs)
+struct GateStripPlan {
+  bool valid = false;
+  int TW = 0, R = 0;
+  size_t stage_bytes = 0, smem = 0;
+  unsigned grid = 0;
+};
+GateStripPlan gate_strip_plan(bool has_skip, const PlBuf* out_pl, bool f32_out, int64_t B, int C, int H, int W,
+                              int xb) {
+  GateStripPlan sp;
   static const bool strips_off = [] {
     const char* e = std::getenv("STDA_GATE");
     return e && std::string(e) == "rows";
   }();
-  if (!strips_off && out_f32 == nullptr && out_pl != nullptr && C % 16 == 0 && C <= 128 && H % 2 == 0 &&
-      W % 2 == 0 && B > 0) {
-    // persistent strips: R rows (even, dividing H) x TW columns; whole-width strips unless
-    // kGsStages of them do not fit shared memory (large maps: column tiles, per-row copies)
-    const int np = out_pl->np, nblk = (C / 16) * np * 2, L = W + 1;
-    auto stage = [&](int r, int tw) {
-      return (size_t)r * tw * C * 4 + (skip ? (size_t)nblk * r * (tw == W ? L : tw) * 16 : 0);
-    };
-    static const size_t stage_cap = [] {  // env STDA_GATE_STAGE_KB (A/B timing), default 16
-      const char* e = std::getenv("STDA_GATE_STAGE_KB");
-      return (size_t)(e ? std::max(8, std::atoi(e)) : 16) * 1024;  // measured best of 16/32/48
-    }();
-    const size_t fixed = (size_t)(kEcaGroups + 2) * C * 4 + 2 * kGsStages * 8;
-    auto smem_of = [&](size_t sb) { return kGsStages * ((sb + 127) / 128 * 128) + fixed; };
-    int TW = W;
-    while (smem_of(stage(2, TW)) > 227 * 1024 && TW % 2 == 0 && TW / 2 >= 16) TW /= 2;
-    int R = 2;
-    while (R * 2 <= 16 && H % (R * 2) == 0 && stage(R * 2, TW) <= stage_cap) R *= 2;
-    const size_t stage_bytes = (stage(R, TW) + 127) / 128 * 128;
-    const size_t smem = smem_of(stage(R, TW));
-    int dev = 0, sms = 148;
-    STDA_CUDA(cudaGetDevice(&dev));
-    STDA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const int64_t n_strips = B * (H / R) * (W / TW);
-    // measured: with fewer than ~4 strips per SM the per-CTA fill (first loads + gate)
-    // dominates and the one-shot row-block kernel is faster
-    if (H % R == 0 && smem <= 227 * 1024 && n_strips >= 4 * (int64_t)sms) {
-      const unsigned grid = (unsigned)std::min<int64_t>(n_strips, sms);
+  if (strips_off || f32_out || out_pl == nullptr || C % 16 != 0 || C > 128 || H % 2 || W % 2 || B <= 0) return sp;
+  const int np = out_pl->np, nblk = (C / 16) * np * 2, L = W + 1;
+  auto stage = [&](int r, int tw) {
+    return (size_t)r * tw * C * xb + (has_skip ? (size_t)nblk * r * (tw == W ? L : tw) * 16 : 0);
+  };
+  static const size_t stage_cap = [] {  // env STDA_GATE_STAGE_KB (A/B timing), default 16
+    const char* e = std::getenv("STDA_GATE_STAGE_KB");
+    return (size_t)(e ? std::max(8, std::atoi(e)) : 16) * 1024;  // measured best of 16/32/48
+  }();
+  const size_t fixed = (size_t)(kEcaGroups + 2) * C * 4 + 2 * kGsStages * 8;
+  auto smem_of = [&](size_t sb) { return kGsStages * ((sb + 127) / 128 * 128) + fixed; };
+  int TW = W;
+  while (smem_of(stage(2, TW)) > 227 * 1024 && TW % 2 == 0 && TW / 2 >= 16) TW /= 2;
+  int R = 2;
+  while (R * 2 <= 16 && H % (R * 2) == 0 && stage(R * 2, TW) <= stage_cap) R *= 2;
+  int dev = 0, sms = 148;
+  STDA_CUDA(cudaGetDevice(&dev));
+  STDA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int64_t n_strips = B * (H / R) * (W / TW);
+  sp.smem = smem_of(stage(R, TW));
+  // measured: with fewer than ~4 strips per SM the per-CTA fill (first loads + gate)
+  // dominates and the one-shot row-block kernel is faster.  bf16 inputs (xb == 2) only
+  // the strip kernel reads, so for them the choice must not depend on the batch (the
+  // bf16 storage decision, and with it the rounding, is per plan shape, not per B).
+  sp.valid = H % R == 0 && sp.smem <= 227 * 1024 && (xb == 2 || n_strips >= 4 * (int64_t)sms);
+  sp.TW = TW;
+  sp.R = R;
+  sp.stage_bytes = (stage(R, TW) + 127) / 128 * 128;
+  sp.grid = (unsigned)std::min<int64_t>(n_strips, sms);
+  return sp;
+}
+}  // namespace
+
+bool gate_apply_bf16_ok(bool has_skip, const PlBuf* out_pl, int64_t B, int C, int H, int W) {
+  return gate_strip_plan(has_skip, out_pl, false, B, C, H, W, 2).valid;
+}
+
+void launch_gate_apply(const float* gap, int items, const float* eca_w, int k, const float* x,
+                       const PlBuf* skip, const PlBuf* out_pl, const PlBuf* out_pp, float* out_f32,
+                       int64_t B, int C, int H, int W, cudaStream_t st, bool x_bf16) {
+  STDA_CHECK(C % 8 == 0 && C <= 1024, "gate_apply: channel count");
+  const GateStripPlan sp = gate_strip_plan(skip != nullptr, out_pl, out_f32 != nullptr, B, C, H, W, x_bf16 ? 2 : 4);
+  STDA_CHECK(!x_bf16 || sp.valid, "gate_apply: bf16 input needs the strip kernel");
+  if (sp.valid) {
+    const int np = out_pl->np, TW = sp.TW, R = sp.R;
+    const size_t stage_bytes = sp.stage_bytes, smem = sp.smem;
+    {
+      const unsigned grid = sp.grid;
       const uint32_t TW_mul = (uint32_t)((((uint64_t)1 << 32) + (uint64_t)TW - 1) / (uint64_t)TW);
       STDA_CHECK((uint64_t)R * TW * TW < ((uint64_t)1 << 32), "gate strips: row index");
       auto go = [&](auto cc, auto npc, auto skc, auto ppc) {
-        const auto kern = TW == W ? gate_strips_kernel<decltype(cc)::value, decltype(npc)::value,
-                                                       decltype(skc)::value, decltype(ppc)::value, true>
-                                  : gate_strips_kernel<decltype(cc)::value, decltype(npc)::value,
-                                                       decltype(skc)::value, decltype(ppc)::value, false>;
+        constexpr int CC = decltype(cc)::value, NPC = decltype(npc)::value;
+        constexpr bool SKC = decltype(skc)::value, PPC = decltype(ppc)::value;
+        auto kern = TW == W ? gate_strips_kernel<CC, NPC, SKC, PPC, true, false>
+                            : gate_strips_kernel<CC, NPC, SKC, PPC, false, false>;
+        if constexpr (NPC == 1) {  // bf16 inputs only in the bf16 variant (one pass)
+          if (x_bf16)
+            kern = TW == W ? gate_strips_kernel<CC, NPC, SKC, PPC, true, true>
+                           : gate_strips_kernel<CC, NPC, SKC, PPC, false, true>;
+        } else {
+          STDA_CHECK(!x_bf16, "gate_apply: bf16 input with hi/lo planes");
+        }
         ensure_dyn_smem(kern, 227 * 1024);
-        launch_pdl(kern, dim3(grid), dim3(kGsThreads), smem, st, "gate_strips_kernel", gap, items, eca_w, k, x,
-                   skip ? *skip : PlBuf{}, *out_pl, out_pp ? *out_pp : PlBuf{}, H, W, TW, TW_mul, R, B,
-                   (uint32_t)((size_t)R * TW * C * 4), (uint32_t)stage_bytes);
+        launch_pdl(kern, dim3(grid), dim3(kGsThreads), smem, st, "gate_strips_kernel", gap, items, eca_w, k,
+                   static_cast<const void*>(x), skip ? *skip : PlBuf{}, *out_pl, out_pp ? *out_pp : PlBuf{}, H,
+                   W, TW, TW_mul, R, B, (uint32_t)((size_t)R * TW * C * (x_bf16 ? 2 : 4)),
+                   (uint32_t)stage_bytes);
       };
       using std::integral_constant;
       auto g3 = [&](auto cc, auto npc) {

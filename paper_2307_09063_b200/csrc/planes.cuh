@@ -213,6 +213,8 @@ __device__ __forceinline__ float eca_gate_of(const float* mean, int C, int c, co
 // written to any of: PL over H x W, PP over (H/2 x W/2) planes, NHWC fp32.
 void launch_gate_apply(const float* gap, int items, const float* eca_w, int k, const float* x,
                        const PlBuf* skip, const PlBuf* out_pl, const PlBuf* out_pp, float* out_f32,
-                       int64_t B, int C, int H, int W, cudaStream_t st);
+                       int64_t B, int C, int H, int W, cudaStream_t st, bool x_bf16 = false);
+// x_bf16 (the bf16 variant's stage-2 outputs stored as bf16) is taken by the strip kernel only
+bool gate_apply_bf16_ok(bool has_skip, const PlBuf* out_pl, int64_t B, int C, int H, int W);
 
 }  // namespace stda

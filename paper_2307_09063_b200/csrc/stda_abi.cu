@@ -50,6 +50,26 @@ void set_error(const std::string& msg) { g_last_error = msg; }
 // launch buys nothing), while eager launches (the host-buffer path) are 7 % faster with
 // the edges (they hide the kernel-to-kernel launch gap).  So: on unless the stream is
 // being captured.  env STDA_PDL=1 / 0 forces them on / off.
+// bf16 variant: stage-2 outputs (ECA inputs) stored as bf16 NHWC — the variant rounds the
+// gated values to bf16 anyway; halves their HBM round trip.  env STDA_BF_NHWC=0 keeps fp32.
+bool bf_nhwc_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("STDA_BF_NHWC");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// ... except the head's input: the strip head rewrites d in place as u, and bf16 u costs the
+// conv an unpack per value (measured +3 us head vs -3 us dec1.s2: a wash).  env STDA_HEAD_BF=1.
+bool head_bf_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("STDA_HEAD_BF");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 bool pdl_enabled(cudaStream_t st) {
   static const int mode = [] {
     const char* e = std::getenv("STDA_PDL");
@@ -402,6 +422,8 @@ void run_net_tc(const stda_plan& p, const Src& x, float* y, int64_t B, const Net
     o2.f32 = w.e[i];
     o2.gap = w.pe[i];
     o2.cp = gi_on ? 1 : 0;
+    // bf16 variant: e_i stored as bf16 for the strip gate kernel
+    o2.bf = bf && !gi_on && bf_nhwc_enabled() && gate_apply_bf16_ok(false, &w.pl_a[i], B, d2.cout, h / 2, wd / 2);
     if (mk.go()) tc::tc_launch(d2, g2, mviews[i], &cur_pp, o2, true, st);
     mk.mark(st);
     h /= 2;
@@ -420,7 +442,7 @@ void run_net_tc(const stda_plan& p, const Src& x, float* y, int64_t B, const Net
       }
       if (mk.go())
         launch_gate_apply(gsrc, gitems, E.eca, k, w.e[i], nullptr, &w.pl_a[i],
-                          i + 1 < S ? &w.pp_a[i] : nullptr, nullptr, B, d2.cout, h, wd, st);
+                          i + 1 < S ? &w.pp_a[i] : nullptr, nullptr, B, d2.cout, h, wd, st, o2.bf != 0);
     }
     mk.mark(st);
     cur_pl = w.pl_a[i];
@@ -445,6 +467,10 @@ void run_net_tc(const stda_plan& p, const Src& x, float* y, int64_t B, const Net
     o2.f32 = w.d[j];
     o2.gap = w.pd[j];
     o2.cp = gi_on ? 1 : 0;
+    // bf16 variant: d_j stored as bf16 for the strip gate kernel / the strip or tile head
+    o2.bf = bf && !gi_on && bf_nhwc_enabled() &&
+            (j + 1 < S ? gate_apply_bf16_ok(true, &w.pl_b[j], B, d2.cout, 2 * h, 2 * wd)
+                       : head_bf_enabled() && !p.head_host.empty() && head_bf16_ok(c0, B, 2 * h, 2 * wd, sk));
     if (mk.go()) tc::tc_launch(d2, g2, mviews[S + j], &cur_pl, o2, true, st);
     mk.mark(st);
     h *= 2;
@@ -467,13 +493,13 @@ void run_net_tc(const stda_plan& p, const Src& x, float* y, int64_t B, const Net
     if (j + 1 < S) {
       if (mk.go())
         launch_gate_apply(gsrc, gitems, D.eca, k, w.d[j], &sk, &w.pl_b[j], nullptr, nullptr, B, d2.cout, h, wd,
-                          st);
+                          st, o2.bf != 0);
       mk.mark(st);
       cur_pl = w.pl_b[j];
     } else {
       if (mk.go())
         launch_head_fused(p.head_wt, p.head.b, gsrc, gitems, D.eca, k, w.d[j], sk, c0, y, B, h,
-                        wd, bf, st, p.head_host.empty() ? nullptr : p.head_host.data());
+                        wd, bf, st, p.head_host.empty() ? nullptr : p.head_host.data(), o2.bf != 0);
       mk.mark(st);
     }
   }

@@ -113,6 +113,7 @@ TcGeometry tc_plan(TcLayerDesc& d, int B, int H, int W, size_t extra_smem = 0, b
 struct TcOut {
   int mode = 0;  // 0 = NHWC fp32 (+gap), 1 = PL, 2 = PP
   int cp = 0;    // mode 0: chunk-planar fp32 [B][C/16][Ho*Wo][16] instead of NHWC (gate-in input)
+  int bf = 0;    // mode 0: the NHWC / chunk-planar values stored as bf16 (bf16 variant)
   float* f32 = nullptr;
   float* gap = nullptr;
   PlBuf pl;

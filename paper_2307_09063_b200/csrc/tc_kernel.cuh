@@ -1072,23 +1072,34 @@ __global__ void __launch_bounds__(threads_of(MODE, STEM), 1) tc_conv_kernel(cons
                   const int yc = (int)__umulhi((uint32_t)qc, p.L_mul);
                   const int xc = qc - yc * p.L;
                   if (yc >= p.Hp || xc >= p.Wp) continue;
-                  float* dst = p.out.cp ? p.out.f32 + (((size_t)b * (N / 16) + j / 16) * p.Ho * p.Wo +
-                                                       (size_t)yc * p.Wo + xc) * 16 + 4 * r
-                                        : p.out.f32 + (((size_t)b * p.Ho + yc) * p.Wo + xc) * N + j + 4 * r;
-                  *reinterpret_cast<float4*>(dst) = c4[c];
+                  const size_t e = p.out.cp ? (((size_t)b * (N / 16) + j / 16) * p.Ho * p.Wo +
+                                               (size_t)yc * p.Wo + xc) * 16 + 4 * r
+                                            : (((size_t)b * p.Ho + yc) * p.Wo + xc) * N + j + 4 * r;
+                  if (p.out.bf)  // bf16 variant: 4 values as 8 bytes
+                    *reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(p.out.f32) + e) =
+                        make_uint2(pack_bf16x2(c4[c].x, c4[c].y), pack_bf16x2(c4[c].z, c4[c].w));
+                  else
+                    *reinterpret_cast<float4*>(p.out.f32 + e) = c4[c];
                 }
               }
               continue;
             }
             if (!(MODE == CONVT4_SP || MODE == CONVT4_SPH ? pvalid : valid) || (p.dbg & 1)) continue;
             if (p.out.mode == 0) {
-              float* op = p.out.cp ? p.out.f32 + (((size_t)b * (N / 16) + j / 16) * p.Ho * p.Wo +
-                                                  (size_t)oy * p.Wo + ox) * 16
-                                   : p.out.f32 + (((size_t)b * p.Ho + oy) * p.Wo + ox) * N + j;
-              // 32-byte stores: each lane writes whole L2 sectors (the lanes' pixels are
-              // 2 apart in the ConvT phases, so a warp's stores cannot coalesce further)
+              const size_t e = p.out.cp ? (((size_t)b * (N / 16) + j / 16) * p.Ho * p.Wo + (size_t)oy * p.Wo + ox) * 16
+                                        : (((size_t)b * p.Ho + oy) * p.Wo + ox) * N + j;
+              if (p.out.bf) {  // bf16 variant: 16 values as one 32-byte store
+                uint32_t w8[8];
 #pragma unroll
-              for (int i = 0; i < 16; i += 8) st_global_v8(op + i, v + i);
+                for (int i = 0; i < 8; ++i) w8[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
+                st_global_v8(reinterpret_cast<float*>(reinterpret_cast<uint16_t*>(p.out.f32) + e),
+                             reinterpret_cast<const float*>(w8));
+              } else {
+                // 32-byte stores: each lane writes whole L2 sectors (the lanes' pixels are
+                // 2 apart in the ConvT phases, so a warp's stores cannot coalesce further)
+#pragma unroll
+                for (int i = 0; i < 16; i += 8) st_global_v8(p.out.f32 + e + i, v + i);
+              }
 #pragma unroll
               for (int i = 0; i < 16; ++i) gsum[j + i] += v[i];
             } else {

@@ -111,10 +111,12 @@ def test_simt_path_poisoned(monkeypatch):
     assert torch.equal(y0, y1)
 
 
-def test_batch_plans_agree_per_triplet():
+@pytest.mark.parametrize("prec", ["fp32", "bf16"])
+def test_batch_plans_agree_per_triplet(prec):
     """Different batch sizes pick different tiling plans and schedules; each triplet's
-    output must not depend on them (no cross-image reads, per-image ECA order)."""
-    net = _net(128)
+    output must not depend on them (no cross-image reads, per-image ECA order, and in
+    the bf16 variant the same storage precision of the stage-2 outputs at every B)."""
+    net = _net(128, prec)
     x = synth_triplets(64, 128, 128, seed=13)
     y64 = _run_forward(net, x, 0xFF)
     for b0, b1 in ((0, 1), (5, 8), (17, 50)):

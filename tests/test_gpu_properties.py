@@ -293,7 +293,10 @@ def test_gate_on_load_path_is_bitwise():
     )
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     for flag in ("0", "1"):
-        subprocess.run([sys.executable, "-c", code], check=True, env=dict(os.environ, STDA_GATEIN=flag), cwd=root)
+        # bf16 stage-2 storage (bf16 variant default) rounds before the gate; the gate-in
+        # path keeps fp32 stage-2 outputs, so compare it with STDA_BF_NHWC=0
+        subprocess.run([sys.executable, "-c", code], check=True,
+                       env=dict(os.environ, STDA_GATEIN=flag, STDA_BF_NHWC="0"), cwd=root)
     import numpy as np
     for hw, prec in ((128, "fp32"), (256, "fp32"), (128, "bf16")):
         a = np.load(f"/tmp/gatein_{hw}_{prec}_0.npy")
@@ -340,3 +343,41 @@ def test_transposed_conv_forms_agree():
         if prec == "fp32":
             assert nmax_err(outs["concat"], outs["default"]) <= 2e-5
             assert nmax_err(outs["groups"], outs["default"]) <= 2e-5
+
+
+def test_bf16_stage2_storage_forms():
+    """bf16 variant: stage-2 outputs stored as bf16 (default), as fp32 (STDA_BF_NHWC=0) and
+    the bf16 head input (STDA_HEAD_BF=1) all stay within the bf16 tolerance of the fp32
+    oracle; C2 and 256^2 shapes (256^2: column-tiled gate strips, head tiles)."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import torch, numpy as np, os\n"
+        "torch.set_grad_enabled(False)\n"
+        "from paper_2307_09063_b200 import StdaConfig, StdaNet\n"
+        "from paper_2307_09063_b200.synth import synth_triplets\n"
+        "for hw, b in ((128, 5), (256, 2)):\n"
+        "    torch.manual_seed(hw)\n"
+        "    net = StdaNet(StdaConfig(map_height=hw, map_width=hw), precision='bf16').eval().cuda()\n"
+        "    x = synth_triplets(b, hw, hw, seed=41)\n"
+        "    np.save(f'/tmp/bfst_{hw}_' + os.environ['TAG'] + '.npy', net(x).cpu().numpy())\n"
+        "    np.save(f'/tmp/bfst_{hw}_x.npy', x.cpu().numpy())\n"
+    )
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    runs = {"default": {}, "f32": {"STDA_BF_NHWC": "0"}, "headbf": {"STDA_HEAD_BF": "1"}}
+    for tag, extra in runs.items():
+        subprocess.run([sys.executable, "-c", code], check=True, env=dict(os.environ, TAG=tag, **extra), cwd=root)
+    import numpy as np
+    from oracle import port
+    from tests._helpers import CONFIG_FIELDS, nmax_err
+    for hw in (128, 256):
+        torch.manual_seed(hw)
+        net = StdaNet(StdaConfig(map_height=hw, map_width=hw))
+        sd = {k: v.detach() for k, v in net.state_dict().items()}
+        cfg = {f: getattr(net.config, f) for f in CONFIG_FIELDS}
+        ref = port.forward(sd, cfg, torch.from_numpy(np.load(f"/tmp/bfst_{hw}_x.npy"))).numpy()
+        for t in runs:
+            y = np.load(f"/tmp/bfst_{hw}_{t}.npy")
+            assert np.isfinite(y).all()
+            assert nmax_err(y, ref) <= 3e-2, (hw, t, nmax_err(y, ref))
