@@ -150,6 +150,47 @@ def fuse_names(names, cfg, fl: dict, byt: dict, opb: dict) -> None:
                 dct.pop(q, None)
 
 
+def kernel_roofline(name: str, flops: float, nbytes: float, launch_ms: float, precision: str,
+                    operand_floor_us) -> dict:
+    """Roofline of one launch from its ALGORITHMIC flops and bytes (folded conv FLOPs; every
+    operand tensor read once and every result written once in its fp32 / bf16 contract form).
+    The launch is bound by whichever roof gives the longer floor time: tensor floor = the MMA
+    passes actually executed (3 for the fp32-contract 3xBF16 split, 1 for bf16) x algorithmic
+    FLOPs / the measured dense-bf16 peak; HBM floor = algorithmic bytes / the measured copy
+    bandwidth.  Every conv of this network has an arithmetic intensity below the ridge
+    (<= 192 executed FLOP/B against ~251), so layer by layer the forward is HBM-bound; the
+    tensor-side figures are kept under "tensor"."""
+    hbm, bf16, _, peak_kind = peaks()
+    t_s = launch_ms * 1e-3
+    passes = 3 if precision == "fp32" else 1
+    hbm_floor_us = nbytes / (hbm * 1e3)
+    tensor_floor_us = passes * flops / (bf16 * 1e6)
+    tflops = flops / t_s / 1e12
+    gbs = nbytes / t_s / 1e9
+    tensor = None
+    if flops:
+        tensor = {"achieved": tflops, "peak": bf16, "unit": "TFLOP/s", "frac": tflops / bf16,
+                  "peak_kind": f"{peak_kind} dense bf16", "flops_per_launch": flops,
+                  "mma_passes": passes, "floor_us": tensor_floor_us}
+        if operand_floor_us:
+            tensor["operand_floor_us"] = operand_floor_us
+            tensor["frac_of_operand_floor"] = operand_floor_us / (launch_ms * 1e3)
+    if flops and tensor_floor_us > hbm_floor_us:
+        roof = {"bound": "tensor", "kernel": name, "achieved": tflops, "peak": bf16, "unit": "TFLOP/s",
+                "frac": tflops / bf16, "peak_kind": f"{peak_kind} dense bf16"}
+    else:
+        roof = {"bound": "hbm", "kernel": name, "achieved": gbs, "peak": hbm, "unit": "GB/s",
+                "frac": gbs / hbm, "peak_kind": f"{peak_kind} HBM copy bandwidth"}
+    roof["bytes_per_launch"] = nbytes
+    roof["hbm_floor_us"] = hbm_floor_us
+    roof["bound_rule"] = ("longer of: executed MMA passes x algorithmic FLOPs / measured dense-bf16 peak; "
+                          "algorithmic bytes / measured HBM copy bandwidth")
+    if tensor:
+        roof["tensor"] = tensor
+        roof["frac_of_binding_floor"] = max(hbm_floor_us, tensor_floor_us, operand_floor_us or 0.0) / (launch_ms * 1e3)
+    return roof
+
+
 def ncu_traffic(kernel: str, batch: int, H: int, W: int, precision: str):
     """DRAM bytes per launch of `kernel` from a committed ncu --set full capture
     (profiles/ncu_traffic.json, written from the capture's raw page), or None."""
@@ -486,25 +527,12 @@ def run_engine(args, world, rank, local):
     share = {n: m for n, m in zip(names, avg)}
     dom = max(share, key=share.get)
     hbm, bf16, bf16_sus, peak_kind = peaks()
-    flops_per_launch = fl[dom] * batch
-    achieved = flops_per_launch / (share[dom] * 1e-3) / 1e12
     total_flops = sum(fl.values())
     sm_ghz = (clocks.summary().get("sm_max_mhz") or 1965.0) / 1000.0
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
     floor_us = {n: b * batch / (128.0 * n_sm * sm_ghz * 1e3) for n, b in opb.items()}
-    if dom in opb:   # tcgen05 conv: FLOP roofline + the operand-feed floor that binds it
-        roof = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": bf16, "unit": "TFLOP/s",
-                "frac": achieved / bf16, "peak_kind": f"{peak_kind} dense bf16",
-                "flops_per_launch": flops_per_launch,
-                "operand_floor_us": floor_us[dom],
-                "frac_of_operand_floor": floor_us[dom] / (share[dom] * 1e3),
-                "hbm_floor_us": byt[dom] * batch / (hbm * 1e3),
-                "frac_of_binding_floor": max(floor_us[dom], byt[dom] * batch / (hbm * 1e3)) / (share[dom] * 1e3)}
-    else:            # SIMT edge / gate kernel: HBM roofline on algorithmic bytes
-        gbs = byt[dom] * batch / (share[dom] * 1e-3) / 1e9
-        roof = {"bound": "hbm", "kernel": dom, "achieved": gbs, "peak": hbm, "unit": "GB/s",
-                "frac": gbs / hbm, "peak_kind": f"{peak_kind} HBM copy bandwidth",
-                "bytes_per_launch": byt[dom] * batch}
+    roof = kernel_roofline(dom, fl[dom] * batch, byt[dom] * batch, share[dom], args.precision,
+                           floor_us.get(dom))
     roof["traffic"] = ncu_traffic(dom, batch, H, W, args.precision)
 
     # end-to-end through the public host-buffer API: a fixed stream of batches in pinned host
@@ -542,6 +570,11 @@ def run_engine(args, world, rank, local):
             "executed": ("tcgen05 kind::f16, 3xBF16 split (A_hi x [B_hi|B_lo] + A_lo x B_hi), fp32 accumulate in TMEM"
                          if args.precision == "fp32" else "tcgen05 kind::f16, bf16 operands, fp32 accumulate"),
             "whole_forward_tflops": total_flops * batch / (ms_per_step * 1e-3) / 1e12,
+            # the fused ideal: 16 B per pixel in + out, folded FLOPs at the executed passes
+            "whole_forward_frac_of_tensor_roof": (3 if args.precision == "fp32" else 1) * total_flops * batch
+                                                 / (ms_per_step * 1e-3) / 1e12 / bf16,
+            "whole_forward_hbm_frac": 16.0 * H * W * batch / (ms_per_step * 1e-3) / 1e9 / hbm,
+            "layerwise_hbm_frac": sum(byt[n] for n in share) * batch / (ms_per_step * 1e-3) / 1e9 / hbm,
             "forward_operand_floor_us": sum(floor_us.values()),
             "launch_us": {n: m * 1e3 for n, m in share.items()},
             "launch_timing": launch_timing,
@@ -663,14 +696,7 @@ def run_stream(args, world, rank, local):
     hbm, bf16, _, peak_kind = peaks()
     fl, byt = layer_flops(cfg), layer_bytes(cfg)
     fuse_names(names, cfg, fl, byt, {})
-    if fl[dom]:
-        ach = fl[dom] * n_out / (share[dom] * 1e-3) / 1e12
-        roof = {"bound": "tensor", "kernel": dom, "achieved": ach, "peak": bf16, "unit": "TFLOP/s",
-                "frac": ach / bf16, "peak_kind": f"{peak_kind} dense bf16"}
-    else:
-        gbs = byt[dom] * n_out / (share[dom] * 1e-3) / 1e9
-        roof = {"bound": "hbm", "kernel": dom, "achieved": gbs, "peak": hbm, "unit": "GB/s",
-                "frac": gbs / hbm, "peak_kind": f"{peak_kind} HBM copy bandwidth"}
+    roof = kernel_roofline(dom, fl[dom] * n_out, byt[dom] * n_out, share[dom], args.precision, None)
     roof["traffic"] = None
     roof["launch_ms"] = share[dom]
     roof["launch_us"] = {n: m * 1e3 for n, m in share.items()}
