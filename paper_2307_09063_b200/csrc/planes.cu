@@ -19,12 +19,17 @@ __global__ void __launch_bounds__(kGateThreads) gate_apply_kernel(
   grid_dep_wait();  // PDL: previous kernel complete (common.cuh)
   __shared__ float mean[1024];
   __shared__ float gate[1024];
+  __shared__ float part[kEcaGroups * kEcaParallelMaxC];
   const int64_t b = blockIdx.y;
   // gate for this image: fixed-order reduction of the producer's per-item partial sums
   if (items == kGatesReady) {
     for (int c = threadIdx.x; c < C; c += blockDim.x) gate[c] = __ldg(gap + b * C + c);
   } else {
-    for (int c = threadIdx.x; c < C; c += blockDim.x) mean[c] = eca_channel_sum(gap, items, C, b, c) / (float)(H * W);
+    if (C <= kEcaParallelMaxC) {
+      eca_means_block(gap, items, C, b, (float)(H * W), part, mean);
+    } else {
+      for (int c = threadIdx.x; c < C; c += blockDim.x) mean[c] = eca_channel_sum(gap, items, C, b, c) / (float)(H * W);
+    }
     __syncthreads();
     for (int c = threadIdx.x; c < C; c += blockDim.x) gate[c] = eca_gate_of(mean, C, c, eca_w, k);
   }
@@ -95,6 +100,7 @@ __global__ void __launch_bounds__(kGateThreads) gate_apply_rows_kernel(
   extern __shared__ __align__(128) uint8_t smem_raw[];
   __shared__ float gate[1024];
   __shared__ float mean[1024];
+  __shared__ float part[kEcaGroups * kEcaParallelMaxC];
   __shared__ __align__(8) uint64_t bar;
   const int tid = threadIdx.x;
   const int64_t b = blockIdx.y;
@@ -133,7 +139,11 @@ __global__ void __launch_bounds__(kGateThreads) gate_apply_rows_kernel(
   if (items == kGatesReady) {
     for (int c = tid; c < C; c += blockDim.x) gate[c] = __ldg(gap + b * C + c);
   } else {
-    for (int c = tid; c < C; c += blockDim.x) mean[c] = eca_channel_sum(gap, items, C, b, c) / (float)(H * W);
+    if (C <= kEcaParallelMaxC) {
+      eca_means_block(gap, items, C, b, (float)(H * W), part, mean);
+    } else {
+      for (int c = tid; c < C; c += blockDim.x) mean[c] = eca_channel_sum(gap, items, C, b, c) / (float)(H * W);
+    }
     __syncthreads();
     for (int c = tid; c < C; c += blockDim.x) gate[c] = eca_gate_of(mean, C, c, eca_w, k);
   }
@@ -594,7 +604,10 @@ void launch_gate_apply(const float* gap, int items, const float* eca_w, int k, c
       return al((size_t)r * W * C * 4) + (skip ? al((size_t)nblk * r * L * 16) : 0) +
              al((size_t)nblk * r * L * 16) + (out_pp ? al((size_t)4 * nblk * (r / 2) * Lp * 16) : 0);
     };
-    while (R * 2 <= 8 && H % (R * 2) == 0 && (size_t)R * 2 * W <= 512 && bytes(R * 2) <= 96 * 1024) R *= 2;
+    // (small batches: keep >= one CTA per SM before growing the row block)
+    while (R * 2 <= 8 && H % (R * 2) == 0 && (size_t)R * 2 * W <= 512 && bytes(R * 2) <= 96 * 1024 &&
+           (int64_t)(H / (R * 2)) * B >= 148)
+      R *= 2;
     const size_t smem = bytes(R);
     STDA_CHECK(smem <= 200 * 1024, "gate_apply: rows do not fit shared memory");
     ensure_dyn_smem(gate_apply_rows_kernel, 200 * 1024);

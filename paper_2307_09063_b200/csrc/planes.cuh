@@ -191,6 +191,24 @@ __device__ __forceinline__ float eca_channel_sum(const float* gap, int items, in
   for (int g = 0; g < kEcaGroups; ++g) s += eca_group_sum(gap, items, C, b, c, g);
   return s;
 }
+// block-parallel form of eca_channel_sum for every channel of image b: thread u forms the
+// group sum (c = u % C, g = u / C) — one batch of loads in flight per thread instead of
+// kEcaGroups dependent round trips — then the groups are added in increasing g: the same
+// float operations as eca_channel_sum, so the same bits.  mean[c] = sum / hw.
+// part: kEcaGroups * C floats of shared memory; every thread of the block calls this.
+constexpr int kEcaParallelMaxC = 128;
+__device__ __forceinline__ void eca_means_block(const float* gap, int items, int C, int64_t b, float hw,
+                                                float* part, float* mean) {
+  for (int u = threadIdx.x; u < kEcaGroups * C; u += blockDim.x)
+    part[u] = eca_group_sum(gap, items, C, b, u % C, u / C);
+  __syncthreads();
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    float s = 0.f;
+#pragma unroll
+    for (int g = 0; g < kEcaGroups; ++g) s += part[g * C + c];
+    mean[c] = s / hw;
+  }
+}
 // eca(x) (+ skip) (model.py:95-98, 197-198) in ONE rounding order for every kernel that
 // applies a gate: skip = hi + lo of its operand plane (exact in fp32), then one fused
 // multiply-add; without a skip one multiply.  Explicit intrinsics: no kernel may differ
