@@ -1009,6 +1009,21 @@ void tc_launch(const TcLayerDesc& d, const TcGeometry& g, const PlBuf& src0, con
     }();
     p.early_trigger = early;
   }
+  {
+    // second producer warp (tc_kernel.cuh kProd2), measured on B200: C2 enc1.s2 32.7 -> 28.2 us
+    // with it, every other C2 layer 0.2-1.8 us slower; C3 (B = 1024, 256^2) enc1.s2 1880 ->
+    // 1567 us, dec0.s2 2120 -> 1898 us, enc0.s2 1955 -> 1857 us, stride-1 layers +-3 %; C5
+    // neutral.  So: the stride-2 conv with 64 output channels always, the other stride-2 /
+    // half-phase transposed convs on long launches (>= 32 items per CTA).
+    // env STDA_TC_PROD2=1 / 0 forces it on / off everywhere
+    static const int prod2 = [] {
+      const char* e = std::getenv("STDA_TC_PROD2");
+      return e ? std::atoi(e) : -1;
+    }();
+    const bool s2_like = d.mode == CONV3_S2 || d.mode == CONVT4_SPH;
+    p.prod2 = prod2 >= 0 ? prod2
+                         : ((d.mode == CONV3_S2 && d.cout == 64) || (s2_like && p.total_items >= 32 * 148) ? 1 : 0);
+  }
   if (g_trace_buf != nullptr && g_trace_countdown-- == 0) {
     p.trace = g_trace_buf;
     g_trace_buf = nullptr;

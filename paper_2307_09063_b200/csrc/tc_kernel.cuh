@@ -48,8 +48,14 @@ __host__ __device__ constexpr int stem_threads(int mode, int stem = 0) {
 #endif
 constexpr int kEpiWarpsMax = STDA_EPI16_SP ? 16 : kEpiWarps;
 __host__ __device__ constexpr int epi_warps(int mode) { return mode == CONVT4_SP && STDA_EPI16_SP ? 16 : kEpiWarps; }
+// Kernels without STEM warps run a second producer warp (the warp after the epilogue warps):
+// the two take alternate ring stages.  One warp needs ~1000 cycles to post a stage of the
+// stride-2 convs (wait, byte count, address arithmetic, one bulk copy per lane) against
+// ~800-1200 cycles of MMA issue per stage, and the MMA warp waited on it
+// (profiles/r2_cta_trace_v2.txt: enc1.s2 MMA wait-full 604 cycles per chunk).
+constexpr int kProd2 = 1;
 __host__ __device__ constexpr int threads_of(int mode, int stem) {
-  return stem ? kThreads + stem_threads(mode, stem) : (kEpiWarp0 + epi_warps(mode)) * 32;
+  return stem ? kThreads + stem_threads(mode, stem) : (kEpiWarp0 + epi_warps(mode) + kProd2) * 32;
 }
 constexpr int kMaxSmem = 227 * 1024;
 constexpr int kMaxStages = 6;  // smem ring depth cap
@@ -80,6 +86,7 @@ struct Params {
   int relu0;
   unsigned long long* trace;  // debug timeline of CTA 0 (null in normal runs)
   int early_trigger;          // griddepcontrol.launch_dependents at kernel start
+  int prod2;                  // the second producer warp takes every other ring stage (else it idles)
   int dbg;                    // debug ablations (env STDA_TC_DBG; 0 in normal runs):
                               // 1 no epilogue stores, 2 no TMEM loads, 4 no A copies after
                               // the first fill, 8 epilogue only releases the slot
@@ -666,14 +673,17 @@ __global__ void __launch_bounds__(threads_of(MODE, STEM), 1) tc_conv_kernel(cons
   // single-wave persistent grid: let the next kernel's CTAs take SMs as ours retire
   if (p.early_trigger) grid_dep_launch();
 
-  if (warp == kProdWarp) {
+  constexpr int NPW = STEM == 0 ? 1 + kProd2 : 1;  // producer warps
+  const bool two_prod = NPW == 2 && p.prod2 != 0;
+  if (warp == kProdWarp || (two_prod && warp == kEpiWarp0 + EPW)) {
+    const uint32_t pw = warp == kProdWarp ? 0u : 1u;  // takes ring-stage steps k with k % NPW == pw
     // ===================== producer: cp.async.bulk of A ranges + packed weights =========
     // The whole warp runs the loop; lane 0 posts the stage's byte count, then lane l
     // issues copy l (source, pass, 8-channel group) — the per-copy address arithmetic runs
     // in parallel instead of ~130 serial cycles per copy on one thread.
     constexpr int NCOPY = NSRC * NPASS_A * 2;
     const int cs = lane / (NPASS_A * 2), cpass = (lane >> 1) % NPASS_A, ccg8 = lane & 1;
-    if (lane == 0 && p.resident) {
+    if (lane == 0 && p.resident && pw == 0) {
       mbar_arrive_expect_tx(smem_u32(wbar), p.w_total);
       // HALF: this CTA's py block only (even grid: item parity == blockIdx.x parity)
       bulk_g2s(smem_u32(b_base),
@@ -777,6 +787,7 @@ __global__ void __launch_bounds__(threads_of(MODE, STEM), 1) tc_conv_kernel(cons
             pstage = 0;
             pphase ^= 1u;
           }
+          if (two_prod && (k & 1u) != pw) continue;  // the other producer warp's stage
           mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
           const uint32_t fb = smem_u32(&full[stage]);
           if (lane == 0) mbar_arrive_expect_tx(fb, (uint32_t)(CPS * (p.G + 2) * NCP * kRowsSL * 16));
@@ -802,6 +813,7 @@ __global__ void __launch_bounds__(threads_of(MODE, STEM), 1) tc_conv_kernel(cons
           pstage = 0;
           pphase ^= 1u;
         }
+        if (two_prod && (k & 1u) != pw) continue;  // the other producer warp's stage
         mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
         if (lane == 0) trace_at(p.trace, 0, 2 * k);
         const uint32_t fb = smem_u32(&full[stage]);
