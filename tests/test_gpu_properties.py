@@ -228,12 +228,15 @@ def test_schedule_orders_do_not_change_results():
         "np.save('/tmp/sched_' + os.environ['TAG'] + '.npy', net(x).cpu().numpy())\n"
     )
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    runs = {"default": {}, "plain": {"STDA_TC_TAIL": "0", "STDA_TC_REV": "0", "STDA_TC_GMAX": "4444"}}
+    # ... and so does the second producer warp (on for some launches by default): everywhere / nowhere
+    runs = {"default": {}, "plain": {"STDA_TC_TAIL": "0", "STDA_TC_REV": "0", "STDA_TC_GMAX": "4444"},
+            "prod2": {"STDA_TC_PROD2": "1"}, "prod1": {"STDA_TC_PROD2": "0"}}
     for tag, extra in runs.items():
         env = dict(os.environ, TAG=tag, **extra)
         subprocess.run([sys.executable, "-c", code], check=True, env=env, cwd=root)
     import numpy as np
-    assert np.array_equal(np.load("/tmp/sched_default.npy"), np.load("/tmp/sched_plain.npy"))
+    for tag in ("plain", "prod2", "prod1"):
+        assert np.array_equal(np.load("/tmp/sched_default.npy"), np.load(f"/tmp/sched_{tag}.npy")), tag
 
 
 def test_tensor_core_stem_path():
