@@ -559,6 +559,25 @@ __device__ __forceinline__ void hd_store(float* base, size_t idx, float4 u) {
     *reinterpret_cast<float4*>(base + idx) = u;
 }
 
+// the same by byte address inside a stage
+template <bool DBF>
+__device__ __forceinline__ float4 hd_load_b(const uint8_t* p) {
+  if constexpr (DBF) {
+    const uint2 r = *reinterpret_cast<const uint2*>(p);
+    return make_float4(__uint_as_float(r.x << 16), __uint_as_float(r.x & 0xFFFF0000u), __uint_as_float(r.y << 16),
+                       __uint_as_float(r.y & 0xFFFF0000u));
+  } else {
+    return *reinterpret_cast<const float4*>(p);
+  }
+}
+template <bool DBF>
+__device__ __forceinline__ void hd_store_b(uint8_t* p, float4 u) {
+  if constexpr (DBF)
+    *reinterpret_cast<uint2*>(p) = make_uint2(pack_bf16x2(u.x, u.y), pack_bf16x2(u.z, u.w));
+  else
+    *reinterpret_cast<float4*>(p) = u;
+}
+
 struct HeadConst {
   float w[9 * kHsC];  // [tap][channel]: read by the conv from the kernel-parameter bank
 };
@@ -671,6 +690,28 @@ __global__ void __launch_bounds__(kHsThreads, 1) head_strips_kernel(
   // ===== 8 compute warps =====
   const float bv = __ldg(bias);
   const int cx = tid % W, rp = tid / W;  // conv: column, row pair
+  // Index arithmetic hoisted out of the strip loop (the kernel is issue-bound: 2 warps per
+  // scheduler, and integer address math was ~60 % of its instructions).  Transform step `it`
+  // of a thread touches stage pixel p = it * 64 + tid / 4; for W >= 64 its row (it * 64) / W
+  // is a compile-time constant of the unrolled loop and its column is a per-thread constant
+  // plus (it * 64) % W, so every shared-memory address is base register + immediate.
+  const int q = tid & 3, t4 = tid >> 2;
+  constexpr bool kCtRows = W >= 64;
+  // byte offsets inside a stage: d / u value quad q of pixel t4, skip bytes of pixel t4, the
+  // swizzled quad of the u store (hs_swz(p) = (column >> 1) & 3: W % 8 == 0)
+  const uint32_t t_d = (uint32_t)t4 * (kHsC * (DBF ? 2 : 4)) + (uint32_t)q * (DBF ? 8 : 16);
+  const uint32_t t_u = (uint32_t)t4 * (kHsC * (DBF ? 2 : 4)) + (uint32_t)(q ^ ((t4 >> 1) & 3)) * (DBF ? 8 : 16);
+  constexpr int SH = (SR + 1) / 2, LP = W / 2 + 1;
+  const uint32_t t_s = (uint32_t)(q >> 1) * g.sblk + (uint32_t)(q & 1) * 8 +
+                       (SKIP_PP ? (uint32_t)((t4 & 1) * SH * LP + (t4 >> 1)) * 16 : (uint32_t)t4 * 16);
+  // conv: column cx + kx - 1 of rows 2rp .. 2rp + 3: pixel byte offset and swizzle per kx
+  uint32_t c_px[3], c_sw[3];
+#pragma unroll
+  for (int kx = 0; kx < 3; ++kx) {
+    const int xx = min(max(cx + kx - 1, 0), W - 1);
+    c_px[kx] = (uint32_t)((2 * rp) * W + xx) * (kHsC * (DBF ? 2 : 4));
+    c_sw[kx] = (uint32_t)((xx >> 1) & 3) * (DBF ? 8 : 16);
+  }
   int64_t cur_b = -1;
   int i = 0;
   for (int64_t s = s_begin; s < s_end; ++s, ++i) {
@@ -707,8 +748,12 @@ __global__ void __launch_bounds__(kHsThreads, 1) head_strips_kernel(
     static_assert(NIT * kHsCompute == SR * W * 4, "transform steps");
     constexpr int NB = NIT % 4 == 0 ? 4 : NIT % 3 == 0 ? 3 : 2;
     static_assert(NIT % NB == 0, "transform batches");
-    const int q = tid & 3;
     const float4 g4 = *reinterpret_cast<const float4*>(gate + q * 4);
+    const bool top = y0 == 0, bot = y0 + R == H;  // staged row 0 / SR - 1 lies outside the image
+    // phase-plane skip: staged row r sits in plane row slot r >> 1 of its parity's planes,
+    // one slot earlier for even r in an image's first strip (no row above the image is staged)
+    const uint32_t zoff = SKIP_PP && top ? (uint32_t)LP * 16 : 0u;
+    uint8_t* ub = reinterpret_cast<uint8_t*>(ubase);
 #pragma unroll
     for (int it0 = 0; it0 < NIT; it0 += NB) {
       float4 dv[NB];
@@ -716,29 +761,43 @@ __global__ void __launch_bounds__(kHsThreads, 1) head_strips_kernel(
       bool in[NB];
 #pragma unroll
       for (int j = 0; j < NB; ++j) {
-        const int p = ((it0 + j) * kHsCompute + tid) >> 2;
-        const int r = p / W, x = p - r * W;
-        const int iy = y0 - 1 + r;
-        in[j] = iy >= 0 && iy < H;
-        dv[j] = hd_load<DBF>(ubase, (size_t)p * kHsC + q * 4);
-        // channels 4q..4q+3: cg8 block (q >> 1), bytes (q & 1) * 8 of position r*L + x
-        // (phase-plane skip: plane (iy%2, x%2), plane-row slot of iy, column x/2)
-        size_t so;
-        if (SKIP_PP) {
-          const int py = iy & 1, iy0s = y0 - 1 + (y0 == 0 ? 1 : 0);
-          const int slot = (iy >> 1) - ((iy0s + ((iy0s & 1) != py ? 1 : 0)) >> 1);
-          so = ((size_t)((py * 2 + (x & 1)) * ((SR + 1) / 2) + slot) * (W / 2 + 1) + (x >> 1)) * 16 + (q & 1) * 8;
+        if constexpr (kCtRows) {
+          constexpr int VB = kHsC * (DBF ? 2 : 4);  // bytes per stage pixel
+          const int it = it0 + j;
+          const int r = (it * 64) / W, xc = (it * 64) % W;  // compile-time under the unroll
+          in[j] = !(r == 0 && top) && !(r == SR - 1 && bot);
+          dv[j] = hd_load_b<DBF>(ub + t_d + (uint32_t)(r * W + xc) * VB);
+          uint32_t so;
+          if (SKIP_PP)  // plane ((r + 1) & 1, column & 1), slot r >> 1 (y0 is a multiple of R, R even)
+            so = (uint32_t)(((((r + 1) & 1) * 2) * SH + (r >> 1)) * LP + xc / 2) * 16 - ((r & 1) == 0 ? zoff : 0u);
+          else
+            so = (uint32_t)(r * L + xc) * 16;
+          hv[j] = *reinterpret_cast<const uint2*>(sbase + t_s + so);
+          lv[j] = np == 2 ? *reinterpret_cast<const uint2*>(sbase + t_s + so + 2 * g.sblk) : make_uint2(0u, 0u);
         } else {
-          so = (size_t)(r * L + x) * 16 + (q & 1) * 8;
+          const int p = ((it0 + j) * kHsCompute + tid) >> 2;
+          const int r = p / W, x = p - r * W;
+          const int iy = y0 - 1 + r;
+          in[j] = iy >= 0 && iy < H;
+          dv[j] = hd_load<DBF>(ubase, (size_t)p * kHsC + q * 4);
+          // channels 4q..4q+3: cg8 block (q >> 1), bytes (q & 1) * 8 of position r*L + x
+          // (phase-plane skip: plane (iy%2, x%2), plane-row slot of iy, column x/2)
+          size_t so;
+          if (SKIP_PP) {
+            const int py = iy & 1, iy0s = y0 - 1 + (y0 == 0 ? 1 : 0);
+            const int slot = (iy >> 1) - ((iy0s + ((iy0s & 1) != py ? 1 : 0)) >> 1);
+            so = ((size_t)((py * 2 + (x & 1)) * ((SR + 1) / 2) + slot) * (W / 2 + 1) + (x >> 1)) * 16 + (q & 1) * 8;
+          } else {
+            so = (size_t)(r * L + x) * 16 + (q & 1) * 8;
+          }
+          hv[j] = *reinterpret_cast<const uint2*>(sbase + (size_t)(q >> 1) * g.sblk + so);
+          lv[j] = np == 2 ? *reinterpret_cast<const uint2*>(sbase + (size_t)(2 + (q >> 1)) * g.sblk + so)
+                          : make_uint2(0u, 0u);
         }
-        hv[j] = *reinterpret_cast<const uint2*>(sbase + (size_t)(q >> 1) * g.sblk + so);
-        lv[j] = np == 2 ? *reinterpret_cast<const uint2*>(sbase + (size_t)(2 + (q >> 1)) * g.sblk + so)
-                        : make_uint2(0u, 0u);
       }
       __syncwarp();
 #pragma unroll
       for (int j = 0; j < NB; ++j) {
-        const int p = ((it0 + j) * kHsCompute + tid) >> 2;
         float4 u = make_float4(0.f, 0.f, 0.f, 0.f);
         if (in[j]) {
           float s4[4];
@@ -763,7 +822,13 @@ __global__ void __launch_bounds__(kHsThreads, 1) head_strips_kernel(
             u.w = bf16_round(u.w);
           }
         }
-        hd_store<DBF>(ubase, (size_t)p * kHsC + (q ^ hs_swz(p)) * 4, u);
+        if constexpr (kCtRows) {
+          const int it = it0 + j;
+          hd_store_b<DBF>(ub + t_u + (uint32_t)(((it * 64) / W) * W + (it * 64) % W) * (kHsC * (DBF ? 2 : 4)), u);
+        } else {
+          const int p = ((it0 + j) * kHsCompute + tid) >> 2;
+          hd_store<DBF>(ubase, (size_t)p * kHsC + (q ^ hs_swz(p)) * 4, u);
+        }
       }
     }
     fence_proxy_async();  // generic writes of this stage before its next async refill
@@ -773,17 +838,15 @@ __global__ void __launch_bounds__(kHsThreads, 1) head_strips_kernel(
     float acc0[4] = {0.f, 0.f, 0.f, 0.f}, acc1[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
     for (int kx = 0; kx < 3; ++kx) {
-      const int xx = cx + kx - 1;
-      const bool in = xx >= 0 && xx < W;
+      // a column outside the image contributes exact zeros: skip it (the border lane idles)
+      if ((kx == 0 && cx == 0) || (kx == 2 && cx == W - 1)) continue;
       float4 u[4][4];  // [channel quad][row]: all loads of this column first
 #pragma unroll
       for (int j = 0; j < 4; ++j)
 #pragma unroll
-        for (int rr = 0; rr < 4; ++rr) {
-          const int p = (2 * rp + rr) * W + (in ? xx : 0);
-          u[j][rr] = hd_load<DBF>(ubase, (size_t)p * kHsC + (j ^ hs_swz(p)) * 4);
-          if (!in) u[j][rr] = make_float4(0.f, 0.f, 0.f, 0.f);
-        }
+        for (int rr = 0; rr < 4; ++rr)
+          u[j][rr] = hd_load_b<DBF>(ub + c_px[kx] + (((uint32_t)j * (DBF ? 8 : 16)) ^ c_sw[kx]) +
+                                    (uint32_t)(rr * W) * (kHsC * (DBF ? 2 : 4)));
 #pragma unroll
       for (int j = 0; j < 4; ++j)
 #pragma unroll
