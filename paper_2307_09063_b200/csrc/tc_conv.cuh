@@ -21,10 +21,11 @@
 // Data movement: the operand planes already hold bf16 hi/lo core matrices in HBM, so the
 // producer is ONE thread issuing cp.async.bulk copies (A: one contiguous range per
 // source/pass/8-channel group; B: one packed weight chunk) completing on an mbarrier
-// transaction count.  Roles (192 threads): warp 0 lane 0 = bulk-copy producer; warp 1
-// = TMEM allocator + single-thread tcgen05.mma issuer; warps 2-5 = epilogue (warp % 4 =
-// TMEM lane quarter): tcgen05.ld -> bias/relu/dual -> operand-plane (hi/lo) or NHWC fp32
-// stores + per-item channel sums for ECA.  smem stage ring (full/empty) and TMEM
+// transaction count.  Roles (352 threads): warp 0 = bulk-copy producer (lane l issues copy
+// l); warp 1 = TMEM allocator + single-thread tcgen05.mma issuer; warps 2-9 = epilogue
+// (warp % 4 = TMEM lane quarter): tcgen05.ld -> bias/relu/dual -> operand-plane (hi/lo) or
+// NHWC fp32 stores + per-item channel sums for ECA; warp 10 = second producer on the
+// launches that take it (every other ring stage, tc_kernel.cuh kProd2).  smem stage ring (full/empty) and TMEM
 // accumulator slots (full/empty); persistent CTAs.
 #pragma once
 
