@@ -14,6 +14,22 @@ __global__ void stg_kernel(uint4* out, size_t n_per_cta, int iters) {
     for (size_t i = threadIdx.x; i < n_per_cta; i += blockDim.x) base[i] = v;
 }
 
+// one warp store instruction = 32 / LPR runs of LPR consecutive 16-byte lanes, the runs in
+// 32 / LPR regions of the CTA's range far apart (the gate kernels' plane stores: a warp's 8
+// pixels x 4 channel groups go to 4 plane blocks as 128-byte runs, LPR = 8; phase planes: 64-byte
+// runs, LPR = 4)
+template <int LPR>
+__global__ void stg_runs_kernel(uint4* out, size_t n_per_cta, int iters) {
+  constexpr int NR = 32 / LPR;
+  uint4* base = out + blockIdx.x * n_per_cta;
+  const size_t region = n_per_cta / NR;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int run = lane / LPR, w = lane % LPR;
+  const uint4 v = make_uint4(threadIdx.x, blockIdx.x, 1, 2);
+  for (int it = 0; it < iters; ++it)
+    for (size_t i = (size_t)warp * LPR; i < region; i += (size_t)nw * LPR) base[run * region + i + w] = v;
+}
+
 __global__ void bulk_kernel(uint8_t* out, size_t bytes_per_cta, int chunk, int iters) {
   extern __shared__ __align__(128) uint8_t sm[];
   for (int i = threadIdx.x; i < chunk / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = i;
@@ -56,6 +72,19 @@ int main() {
       const double bytes = (double)sms * pc * iters;
       printf("STG.128  %4zu KB/CTA warps %2d: %7.1f GB/s  %5.1f B/clk/SM (at 1.965 GHz)\n", pc >> 10, warps,
              bytes / ms / 1e6, bytes / ms / 1e-3 / sms / 1.965e9);
+    }
+    for (int lpr : {8, 4, 2}) {
+      auto kern = lpr == 8 ? stg_runs_kernel<8> : lpr == 4 ? stg_runs_kernel<4> : stg_runs_kernel<2>;
+      kern<<<sms, 512>>>((uint4*)buf, pc / 16, 1);
+      cudaEventRecord(a);
+      kern<<<sms, 512>>>((uint4*)buf, pc / 16, iters);
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+      float ms;
+      cudaEventElapsedTime(&ms, a, b);
+      const double bytes = (double)sms * pc * iters;
+      printf("STG.128  %4zu KB/CTA 16 warps, %3d-byte runs in %2d regions: %7.1f GB/s  %5.1f B/clk/SM\n", pc >> 10,
+             lpr * 16, 32 / lpr, bytes / ms / 1e6, bytes / ms / 1e-3 / sms / 1.965e9);
     }
     for (int chunk : {4096, 16384, 32768}) {
       cudaFuncSetAttribute(bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 << 10);
