@@ -712,31 +712,49 @@ __global__ void __launch_bounds__(kHsThreads, 1) head_strips_kernel(
     c_px[kx] = (uint32_t)((2 * rp) * W + xx) * (kHsC * (DBF ? 2 : 4));
     c_sw[kx] = (uint32_t)((xx >> 1) & 3) * (DBF ? 8 : 16);
   }
-  int64_t cur_b = -1;
+  int64_t cur_b = -1, pre_b = -1;  // image of gate slot 0 / of slot 1 (formed ahead)
+  int gsel = 0;
   int i = 0;
   for (int64_t s = s_begin; s < s_end; ++s, ++i) {
     const int st = i & 1;
     const int64_t b = s / spi;
     const int y0 = (int)(s - b * spi) * R;
-    if (b != cur_b && items == kGatesReady) {
-      asm volatile("bar.sync 1, %0;" ::"n"(kHsCompute) : "memory");  // previous image's gate readers
-      if (tid < kHsC) gate[tid] = __ldg(gap + b * kHsC + tid);
-      asm volatile("bar.sync 1, %0;" ::"n"(kHsCompute) : "memory");
+    if (b != cur_b && b == pre_b) {
+      gsel = 1;  // formed together with the previous image
       cur_b = b;
     } else if (b != cur_b) {
-      // ECA gate of image b (model.py:128-135): kEcaGroups group sums in parallel, added
-      // in group order (planes.cuh: the one reduction order of every gate)
-      if (tid < kEcaGroups * kHsC) part[tid] = eca_group_sum(gap, items, kHsC, b, tid % kHsC, tid / kHsC);
-      asm volatile("bar.sync 1, %0;" ::"n"(kHsCompute) : "memory");
-      if (tid < kHsC) {
-        float a = 0.f;
-        for (int grp = 0; grp < kEcaGroups; ++grp) a += part[grp * kHsC + tid];
-        mean[tid] = a / (float)(H * W);
+      // ECA gates (model.py:128-135) of image b and — when this CTA's strips reach it — of
+      // image b + 1 in the same pass: the second image's loads fly with the first's, so the
+      // CTAs whose strips span two images stop once (2-3 us) instead of twice.  Per image:
+      // kEcaGroups group sums in parallel, added in group order (planes.cuh: the one
+      // reduction order of every gate).  Threads 0..127 take image b, 128..255 image b + 1.
+      const bool two = b + 1 <= (s_end - 1) / spi;
+      const int im = tid >> 7, t7 = tid & 127;
+      static_assert(kHsCompute == 2 * kEcaGroups * kHsC, "one (image, group, channel) per thread");
+      float* gate2 = ws;              // [2][16] (the weight slots are unused: weights sit in the parameter bank)
+      float* mean2 = ws + 2 * kHsC;   // [2][16]
+      asm volatile("bar.sync 1, %0;" ::"n"(kHsCompute) : "memory");  // previous images' gate readers
+      if (items == kGatesReady) {
+        if (tid < kHsC * (two ? 2 : 1)) gate2[tid] = __ldg(gap + b * kHsC + tid);
+      } else {
+        if (im == 0 || two) part[tid] = eca_group_sum(gap, items, kHsC, b + im, t7 % kHsC, t7 / kHsC);
+        asm volatile("bar.sync 1, %0;" ::"n"(kHsCompute) : "memory");
+        if (tid < kHsC * (two ? 2 : 1)) {
+          const int mi = tid / kHsC, c = tid % kHsC;
+          float a = 0.f;
+          for (int grp = 0; grp < kEcaGroups; ++grp) a += part[mi * 128 + grp * kHsC + c];
+          mean2[tid] = a / (float)(H * W);
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kHsCompute) : "memory");
+        if (tid < kHsC * (two ? 2 : 1)) {
+          const int mi = tid / kHsC, c = tid % kHsC;
+          gate2[tid] = eca_gate_of(mean2 + mi * kHsC, kHsC, c, eca_w, k);
+        }
       }
       asm volatile("bar.sync 1, %0;" ::"n"(kHsCompute) : "memory");
-      if (tid < kHsC) gate[tid] = eca_gate_of(mean, kHsC, tid, eca_w, k);
-      asm volatile("bar.sync 1, %0;" ::"n"(kHsCompute) : "memory");
+      gsel = 0;
       cur_b = b;
+      pre_b = two ? b + 1 : -1;
     }
     mbar_wait(smem_u32(&full[st]), (i >> 1) & 1);
     float* ubase = reinterpret_cast<float*>(hsm + (size_t)st * g.stage);
@@ -748,7 +766,7 @@ __global__ void __launch_bounds__(kHsThreads, 1) head_strips_kernel(
     static_assert(NIT * kHsCompute == SR * W * 4, "transform steps");
     constexpr int NB = NIT % 4 == 0 ? 4 : NIT % 3 == 0 ? 3 : 2;
     static_assert(NIT % NB == 0, "transform batches");
-    const float4 g4 = *reinterpret_cast<const float4*>(gate + q * 4);
+    const float4 g4 = *reinterpret_cast<const float4*>(ws + gsel * kHsC + q * 4);
     const bool top = y0 == 0, bot = y0 + R == H;  // staged row 0 / SR - 1 lies outside the image
     // phase-plane skip: staged row r sits in plane row slot r >> 1 of its parity's planes,
     // one slot earlier for even r in an image's first strip (no row above the image is staged)
