@@ -275,9 +275,10 @@ __global__ void __launch_bounds__(kGsThreads, 1) gate_strips_kernel(
   constexpr int nblk = (C / 16) * NP * 2;
   static_assert(kGsCompute % G8 == 0, "one channel group per thread");
   extern __shared__ __align__(128) uint8_t gsm[];
-  float* gate = reinterpret_cast<float*>(gsm + (size_t)stages * stage_bytes);  // [C]
-  float* part = gate + C;  // [kEcaGroups][C] group sums, then [C] means
-  uint64_t* full = reinterpret_cast<uint64_t*>(part + (kEcaGroups + 1) * C);
+  float* gate2 = reinterpret_cast<float*>(gsm + (size_t)stages * stage_bytes);  // [2][C]: current image, next image
+  float* part = gate2 + 2 * C;                  // [2][kEcaGroups][C] group sums
+  float* mean2 = part + 2 * kEcaGroups * C;     // [2][C]
+  uint64_t* full = reinterpret_cast<uint64_t*>(mean2 + 2 * C);
   uint64_t* empty = full + stages;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int L = W + 1, Lp = W / 2 + 1;
@@ -344,7 +345,7 @@ __global__ void __launch_bounds__(kGsThreads, 1) gate_strips_kernel(
   const size_t pl_blk = ((size_t)kh * out_pl.Q + out_pl.off) * 8;
   const size_t pp_blk = PP ? ((size_t)kh * out_pp.Q + out_pp.off) * 8 : 0;
   const size_t pl_lo = (size_t)2 * out_pl.Q * 8, pp_lo = PP ? (size_t)2 * out_pp.Q * 8 : 0;
-  int64_t cur_b = -1;
+  int64_t cur_b = -1, pre_b = -1;  // image of gate slot 0 / of slot 1 (formed ahead)
   int st = 0;
   uint32_t ph = 0;
   float g8[8];
@@ -352,29 +353,44 @@ __global__ void __launch_bounds__(kGsThreads, 1) gate_strips_kernel(
     const int64_t b = s / spi;
     const int rem = (int)(s - b * spi);
     const int y0 = (rem / tpr) * R, x0 = WHOLE ? 0 : (rem - (rem / tpr) * tpr) * TW;
-    if (b != cur_b) {
+    if (b != cur_b && b == pre_b) {
+      // formed together with the previous image
+#pragma unroll
+      for (int j = 0; j < 8; ++j) g8[j] = gate2[C + c8 * 8 + j];
+      cur_b = b;
+    } else if (b != cur_b) {
+      // ECA gates (model.py:128-135) of image b and — when this CTA's strips reach it — of
+      // image b + 1 in the same pass (the second image's loads fly with the first's: the
+      // CTAs whose strips span two images stop once instead of twice).  Per image: the
+      // kEcaGroups group sums in parallel, then added in group order (planes.cuh: the one
+      // reduction order of every gate).
+      const int ni = b + 1 <= (s_end - 1) / spi ? 2 : 1;
+      asm volatile("bar.sync 1, %0;" ::"n"(kGsCompute) : "memory");  // previous images' gate readers
       if (items == kGatesReady) {
-        asm volatile("bar.sync 1, %0;" ::"n"(kGsCompute) : "memory");  // previous image's gate readers
-        if (tid < C) gate[tid] = __ldg(gap + b * C + tid);
+        for (int u = tid; u < ni * C; u += kGsCompute) gate2[u] = __ldg(gap + b * C + u);
       } else {
-        // ECA gate of image b (model.py:128-135): the kEcaGroups group sums in parallel,
-        // then added in group order (planes.cuh: the one reduction order of every gate)
-        for (int u = tid; u < kEcaGroups * C; u += kGsCompute)
-          part[u] = eca_group_sum(gap, items, C, b, u % C, u / C);
-        asm volatile("bar.sync 1, %0;" ::"n"(kGsCompute) : "memory");
-        float* mean = part + kEcaGroups * C;  // [C]
-        if (tid < C) {
-          float a = 0.f;
-          for (int g = 0; g < kEcaGroups; ++g) a += part[g * C + tid];
-          mean[tid] = a / (float)(H * W);
+        for (int u = tid; u < ni * kEcaGroups * C; u += kGsCompute) {
+          const int im = u / (kEcaGroups * C), v = u - im * (kEcaGroups * C);
+          part[u] = eca_group_sum(gap, items, C, b + im, v % C, v / C);
         }
         asm volatile("bar.sync 1, %0;" ::"n"(kGsCompute) : "memory");
-        if (tid < C) gate[tid] = eca_gate_of(mean, C, tid, eca_w, k);
+        for (int u = tid; u < ni * C; u += kGsCompute) {
+          const int im = u / C, c = u - im * C;
+          float a = 0.f;
+          for (int g = 0; g < kEcaGroups; ++g) a += part[im * (kEcaGroups * C) + g * C + c];
+          mean2[u] = a / (float)(H * W);
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kGsCompute) : "memory");
+        for (int u = tid; u < ni * C; u += kGsCompute) {
+          const int im = u / C, c = u - im * C;
+          gate2[u] = eca_gate_of(mean2 + im * C, C, c, eca_w, k);
+        }
       }
       asm volatile("bar.sync 1, %0;" ::"n"(kGsCompute) : "memory");
 #pragma unroll
-      for (int j = 0; j < 8; ++j) g8[j] = gate[c8 * 8 + j];
+      for (int j = 0; j < 8; ++j) g8[j] = gate2[c8 * 8 + j];
       cur_b = b;
+      pre_b = ni == 2 ? b + 1 : -1;
     }
     if (y0 == 0 && x0 == 0) {  // top / bottom margins of the output planes, once per image
       pl_zero_margins(out_pl, b, tid, kGsCompute);
@@ -515,7 +531,7 @@ GateStripPlan gate_strip_plan(bool has_skip, const PlBuf* out_pl, bool f32_out, 
     const char* e = std::getenv("STDA_GATE_STAGE_KB");
     return (size_t)(e ? std::max(8, std::atoi(e)) : 16) * 1024;  // measured best of 16/32/48
   }();
-  const size_t fixed = (size_t)(kEcaGroups + 2) * C * 4 + 2 * kGsStages * 8;
+  const size_t fixed = (size_t)2 * (kEcaGroups + 2) * C * 4 + 2 * kGsStages * 8;
   auto smem_of = [&](size_t sb) { return kGsStages * ((sb + 127) / 128 * 128) + fixed; };
   int TW = W;
   while (smem_of(stage(2, TW)) > 227 * 1024 && TW % 2 == 0 && TW / 2 >= 16) TW /= 2;
