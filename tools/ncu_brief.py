@@ -11,7 +11,15 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
         "l1tex__throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
         "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
-        "smsp__inst_executed.sum", "launch__registers_per_thread"]
+        "smsp__inst_executed.sum", "launch__registers_per_thread",
+        # tensor cores: tcgen05 pipe busy, executed UTCHMMA bf16 ops against the dense peak (the
+        # 3xBF16 split executes 3x the algorithmic FLOPs), shared-memory wavefronts of the
+        # operand reads, TMEM instructions
+        "sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_elapsed",
+        "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+        "sm__ops_path_tensor_op_utchmma_src_bf16_dst_fp32_sparsity_off.avg.pct_of_peak_sustained_elapsed",
+        "l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+        "sm__inst_executed_pipe_tmem.avg.pct_of_peak_sustained_active"]
 for r in rows[2:]:
     print("==", r[col["Kernel Name"]][:90])
     for k in KEYS:
