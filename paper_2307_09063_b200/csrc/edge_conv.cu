@@ -1024,63 +1024,86 @@ __global__ void __launch_bounds__(kHsThreads, 1) head_tiles_kernel(
     const uint8_t* sbase = hsm + (size_t)st * g.stage + g.dbytes;
     // transform: one (stage pixel, channel quad) per thread step, NB steps per batch: all
     // loads of a batch, one __syncwarp (the 4 quads of a pixel are lanes of one warp and
-    // are rewritten in place; steps touch disjoint pixels), then all stores
-    constexpr int NU = SR * SW * 4;
-    constexpr int NIT = (NU + kHsCompute - 1) / kHsCompute;
-    constexpr int NB = 4;
-    const int q = tid & 3;
+    // are rewritten in place; steps touch disjoint pixels), then all stores.
+    // Step `it` of the unrolled loop covers stage row it / 2, columns (it & 1) * 64 + tid / 4:
+    // the row is a compile-time constant and every shared-memory address is a per-thread
+    // byte offset plus an immediate (the kernel spent more cycles here than in the conv on
+    // index arithmetic: divisions by SW, bounds checks); the two halo columns 128, 129 of
+    // the SR rows (48 units) follow in one extra step of warps 0 and 1.
+    static_assert(TW == 128 && SW == 130 && kHsCompute == 256, "transform step mapping");
+    constexpr int VB = kHsC * (DBF ? 2 : 4), QB = DBF ? 8 : 16;  // bytes per stage pixel / value quad
+    const int q = tid & 3, t4 = tid >> 2;
     const float4 g4 = *reinterpret_cast<const float4*>(gate + q * 4);
+    const bool top = y0 == 0, bot = y0 + R == H, left = x0 == 0, right = x0 + TW == W;
+    uint8_t* ub = reinterpret_cast<uint8_t*>(ubase);
+    const uint32_t t_d = (uint32_t)t4 * VB + (uint32_t)q * QB;
+    const uint32_t t_s = (uint32_t)(q >> 1) * g.sblk + (uint32_t)(q & 1) * 8 + (uint32_t)t4 * 16;
+    // u = d * gate + skip (model.py:197-198) of one unit, zero outside the image
+    auto unit = [&](float4 dvv, uint2 hvv, uint2 lvv, bool inside) {
+      float4 uu = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (inside) {
+        float s4[4];
+        s4[0] = __uint_as_float(hvv.x << 16);
+        s4[1] = __uint_as_float(hvv.x & 0xFFFF0000u);
+        s4[2] = __uint_as_float(hvv.y << 16);
+        s4[3] = __uint_as_float(hvv.y & 0xFFFF0000u);
+        if (np == 2) {
+          s4[0] += __uint_as_float(lvv.x << 16);
+          s4[1] += __uint_as_float(lvv.x & 0xFFFF0000u);
+          s4[2] += __uint_as_float(lvv.y << 16);
+          s4[3] += __uint_as_float(lvv.y & 0xFFFF0000u);
+        }
+        uu.x = gate_fma(dvv.x, g4.x, s4[0]);
+        uu.y = gate_fma(dvv.y, g4.y, s4[1]);
+        uu.z = gate_fma(dvv.z, g4.z, s4[2]);
+        uu.w = gate_fma(dvv.w, g4.w, s4[3]);
+        if (bf16) {
+          uu.x = bf16_round(uu.x);
+          uu.y = bf16_round(uu.y);
+          uu.z = bf16_round(uu.z);
+          uu.w = bf16_round(uu.w);
+        }
+      }
+      return uu;
+    };
+    constexpr int NIT = 2 * SR, NB = 4;
+    static_assert(NIT % NB == 0, "transform batches");
 #pragma unroll
     for (int it0 = 0; it0 < NIT; it0 += NB) {
       float4 dv[NB];
       uint2 hv[NB], lv[NB];
-      bool in[NB];
 #pragma unroll
       for (int j = 0; j < NB; ++j) {
-        const int u = (it0 + j) * kHsCompute + tid;
-        const int p = min(u, NU - 1) >> 2;
-        const int r = p / SW, xs = p - r * SW;
-        const int iy = y0 - 1 + r, ix = x0 - 1 + xs;
-        in[j] = u < NU && iy >= 0 && iy < H && ix >= 0 && ix < W;
-        dv[j] = hd_load<DBF>(ubase, (size_t)p * kHsC + q * 4);
-        // channels 4q..4q+3: cg8 block (q >> 1), bytes (q & 1) * 8 of stage position p
-        const size_t so = (size_t)p * 16 + (q & 1) * 8;
-        hv[j] = *reinterpret_cast<const uint2*>(sbase + (size_t)(q >> 1) * g.sblk + so);
-        lv[j] = np == 2 ? *reinterpret_cast<const uint2*>(sbase + (size_t)(2 + (q >> 1)) * g.sblk + so)
-                        : make_uint2(0u, 0u);
+        const int it = it0 + j;
+        const uint32_t pofs = (uint32_t)((it >> 1) * SW + (it & 1) * 64);  // compile-time
+        dv[j] = hd_load_b<DBF>(ub + t_d + pofs * VB);
+        // channels 4q..4q+3: cg8 block (q >> 1), bytes (q & 1) * 8 of the stage position
+        hv[j] = *reinterpret_cast<const uint2*>(sbase + t_s + pofs * 16);
+        lv[j] = np == 2 ? *reinterpret_cast<const uint2*>(sbase + t_s + pofs * 16 + 2 * g.sblk) : make_uint2(0u, 0u);
       }
       __syncwarp();
 #pragma unroll
       for (int j = 0; j < NB; ++j) {
-        const int u = (it0 + j) * kHsCompute + tid;
-        if (u >= NU) continue;
-        const int p = u >> 2;
-        float4 uu = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (in[j]) {
-          float s4[4];
-          s4[0] = __uint_as_float(hv[j].x << 16);
-          s4[1] = __uint_as_float(hv[j].x & 0xFFFF0000u);
-          s4[2] = __uint_as_float(hv[j].y << 16);
-          s4[3] = __uint_as_float(hv[j].y & 0xFFFF0000u);
-          if (np == 2) {
-            s4[0] += __uint_as_float(lv[j].x << 16);
-            s4[1] += __uint_as_float(lv[j].x & 0xFFFF0000u);
-            s4[2] += __uint_as_float(lv[j].y << 16);
-            s4[3] += __uint_as_float(lv[j].y & 0xFFFF0000u);
-          }
-          uu.x = gate_fma(dv[j].x, g4.x, s4[0]);  // eca(d) + skip (model.py:197-198)
-          uu.y = gate_fma(dv[j].y, g4.y, s4[1]);
-          uu.z = gate_fma(dv[j].z, g4.z, s4[2]);
-          uu.w = gate_fma(dv[j].w, g4.w, s4[3]);
-          if (bf16) {
-            uu.x = bf16_round(uu.x);
-            uu.y = bf16_round(uu.y);
-            uu.z = bf16_round(uu.z);
-            uu.w = bf16_round(uu.w);
-          }
-        }
-        hd_store<DBF>(ubase, (size_t)p * kHsC + (q ^ hs_swz(p)) * 4, uu);
+        const int it = it0 + j, r = it >> 1;
+        const uint32_t pofs = (uint32_t)(r * SW + (it & 1) * 64);
+        const bool inside = !(r == 0 && top) && !(r == SR - 1 && bot) && !((it & 1) == 0 && left && t4 == 0);
+        // hs_swz(p) = (p >> 1) & 3 with p = r * 130 + column: (r + (column >> 1)) & 3
+        const uint32_t sw = (uint32_t)((r + (t4 >> 1)) & 3);
+        hd_store_b<DBF>(ub + (uint32_t)t4 * VB + pofs * VB + ((uint32_t)q ^ sw) * QB, unit(dv[j], hv[j], lv[j], inside));
       }
+    }
+    if (tid < 64) {  // the halo columns 128, 129: unit (row, column, quad) = (tid / 8, 128 + (tid / 4) % 2, tid % 4)
+      const int r = min(tid >> 3, SR - 1), xs = 128 + (t4 & 1);
+      const uint32_t pp = (uint32_t)(r * SW + xs);
+      const bool act = tid < 8 * SR;
+      const int iy = y0 - 1 + r;
+      const bool inside = act && iy >= 0 && iy < H && !(xs == SW - 1 && right);
+      const float4 dv1 = hd_load_b<DBF>(ub + pp * VB + (uint32_t)q * QB);
+      const uint32_t so = (uint32_t)(q >> 1) * g.sblk + (uint32_t)(q & 1) * 8 + pp * 16;
+      const uint2 hv1 = *reinterpret_cast<const uint2*>(sbase + so);
+      const uint2 lv1 = np == 2 ? *reinterpret_cast<const uint2*>(sbase + so + 2 * g.sblk) : make_uint2(0u, 0u);
+      __syncwarp();
+      if (act) hd_store_b<DBF>(ub + pp * VB + ((uint32_t)q ^ (uint32_t)hs_swz((int)pp)) * QB, unit(dv1, hv1, lv1, inside));
     }
     fence_proxy_async();  // generic writes of this stage before its next async refill
     asm volatile("bar.sync 1, %0;" ::"n"(kHsCompute) : "memory");
@@ -1091,13 +1114,17 @@ __global__ void __launch_bounds__(kHsThreads, 1) head_tiles_kernel(
 #pragma unroll
     for (int kx = 0; kx < 3; ++kx) {
       float4 u[4][4];  // [channel quad][row]: all loads of this column first
+      // stage pixel (2rp + rr) * SW + cx + kx: byte offset = per-thread base + rr * SW * VB,
+      // swizzle (2rp + rr + ((cx + kx) >> 1)) & 3
+      const uint32_t cb = (uint32_t)((2 * rp) * SW + cx + kx) * VB;
+      const int s0 = 2 * rp + ((cx + kx) >> 1);
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int rr = 0; rr < 4; ++rr) {
+        const uint32_t sw = (uint32_t)((s0 + rr) & 3) * QB;
 #pragma unroll
-        for (int rr = 0; rr < 4; ++rr) {
-          const int p = (2 * rp + rr) * SW + cx + kx;
-          u[j][rr] = hd_load<DBF>(ubase, (size_t)p * kHsC + (j ^ hs_swz(p)) * 4);
-        }
+        for (int j = 0; j < 4; ++j)
+          u[j][rr] = hd_load_b<DBF>(ub + cb + (uint32_t)(rr * SW) * VB + (((uint32_t)j * QB) ^ sw));
+      }
 #pragma unroll
       for (int j = 0; j < 4; ++j)
 #pragma unroll
