@@ -913,6 +913,20 @@ struct HostPipe {
   HostPipe(const HostPipe&) = delete;
   HostPipe& operator=(const HostPipe&) = delete;
 };
+
+// One pipe per (host thread, device), created on the thread's first host-buffer call and
+// reused by its later ones: creating and destroying two streams and seven events costs
+// ~150-200 us per call, more than a batch-1 forward.  Calls of one thread are sequential and
+// each ends with the copy-out stream drained, so a pipe is idle whenever its thread starts a
+// new call; threads never share one (the plan stays immutable, concurrent calls on one plan
+// with distinct workspaces never share a stream or an event).
+HostPipe& thread_pipe(int device) {
+  thread_local std::vector<std::pair<int, std::unique_ptr<HostPipe>>> pipes;
+  for (auto& e : pipes)
+    if (e.first == device) return *e.second;
+  pipes.emplace_back(device, std::make_unique<HostPipe>());
+  return *pipes.back().second;
+}
 }  // namespace
 
 int stda_forward_host(const stda_plan* plan, const float* x_host, float* y_host, int64_t batch,
@@ -925,10 +939,8 @@ int stda_forward_host(const stda_plan* plan, const float* x_host, float* y_host,
     chunk = std::min(chunk, batch);
     check_ws(plan, ws, ws_bytes, stda_host_workspace_bytes(plan, chunk));
     DeviceGuard g(plan->device);
-    // copy streams and events belong to this call (the plan stays immutable, so concurrent
-    // calls on one plan with distinct workspaces never share a stream or an event)
-    HostPipe pipe;
-    HostPipe* p = &pipe;
+    // copy streams and events belong to the calling thread (thread_pipe)
+    HostPipe* p = &thread_pipe(plan->device);
     const stda_config& c = plan->cfg;
     const size_t HW = (size_t)c.map_height * c.map_width;
     const size_t in_tri = c.input_frames * HW, in_bytes = align_up(chunk * in_tri * 4),
